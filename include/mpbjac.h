@@ -1,0 +1,214 @@
+/*
+ * mpbjac.h — C-ABI of libmpbjac.so, the B200 (sm_100a) hot path of the
+ * mixed-precision block-Jacobi preconditioned CG of arXiv 2407.15973.
+ *
+ * Every pointer argument is a DEVICE pointer unless its name starts with h_
+ * (host).  All calls are stream-ordered on the handle's stream and never
+ * allocate on the solve path: the caller owns matrix, vector, trace and
+ * workspace buffers; the handle owns only small per-plan tables and a scratch
+ * area for the standalone (non-solve) entry points.  Return value: 0 ok,
+ * negative = invalid argument (the reference raises ValueError there),
+ * positive = a cudaError_t.  mpb_status_string() names both kinds.
+ *
+ * Reference interface each entry point replaces (paths relative to the
+ * reference's pkg/src/mpcg/):
+ *   mpb_csr_matvec_f64/_f32        kernels_numba.py:37-45  csr_matvec
+ *                                  (via sparse.py:175-183  spmv)
+ *   mpb_block_jacobi_sweeps_*      kernels_numba.py:48-70  block_jacobi_sweeps
+ *   mpb_dot_f64 / mpb_dot_f32      kernels_numba.py:18-24  dot_seq
+ *                                  (via sparse.py:186-192  dot)
+ *   mpb_norm_sq_f64 / _f32         kernels_numba.py:27-34  norm_sq_f64
+ *                                  (via sparse.py:195-199  norm2)
+ *   mpb_narrow_f64_f32             sparse.py:202-230       convert_precision(.., F32)
+ *   mpb_widen_f32_f64              sparse.py:202-230       convert_precision(.., F64)
+ *   mpb_setup_diag_f64/_f32        bjac.py:171-185         setup (diag checks)
+ *   mpb_convert_values_f32         bjac.py:175 / sparse.py:202-214 (matrix values)
+ *   mpb_plan_create                bjac.py:29-75           BlockPartition
+ *   mpb_bjac_apply_f64/_f32        bjac.py:127-149         BjacPreconditioner.apply
+ *   mpb_bjac_inner_apply_*         bjac.py:106-125         BjacPreconditioner.inner_apply
+ *   mpb_fmp_apply                  policies.py:154-160     fmp_apply
+ *   mpb_pcg_solve                  solver.py:101-184       pcg_solve (whole loop,
+ *                                  with policies.py:102-183 apply_policy on device)
+ *   mpb_true_relres                solver.py:93-98         true_relres
+ */
+#ifndef MPBJAC_H
+#define MPBJAC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MPB_VERSION 100
+
+/* status codes (negative: argument errors) */
+#define MPB_OK 0
+#define MPB_ERR_ARG (-1)        /* null pointer / bad size                */
+#define MPB_ERR_SHAPE (-2)      /* inconsistent lengths                   */
+#define MPB_ERR_PARTITION (-3)  /* partition does not cover the matrix    */
+#define MPB_ERR_SWEEPS (-4)     /* k < 1 or t < 1                          */
+#define MPB_ERR_INDEX32 (-5)    /* nnz or n does not fit int32 indexing    */
+#define MPB_ERR_POLICY (-6)     /* unknown policy kind / missing instance  */
+#define MPB_ERR_WORKSPACE (-7)  /* workspace too small                     */
+
+/* policy kinds (policies.py:30-37) */
+#define MPB_UNIFORM 0
+#define MPB_FIXED_LOW 1
+#define MPB_ADAPTIVE_HL 2
+#define MPB_ADAPTIVE_LH 3
+
+/* numerical outcomes of a solve (solver.py:31-44, sparse.py:23-24) */
+#define MPB_SOLVE_OK 0
+#define MPB_SOLVE_BREAKDOWN 1        /* r'z == 0            -> BreakdownError */
+#define MPB_SOLVE_INDEF_PRECOND 2    /* r'z < 0             -> IndefiniteOperatorError */
+#define MPB_SOLVE_INDEF_MATRIX 3     /* p'Ap <= 0           -> IndefiniteOperatorError */
+#define MPB_SOLVE_NONFINITE 4        /* ||r|| not finite    -> NonFiniteResidualError */
+#define MPB_SOLVE_NARROW_OVERFLOW 5  /* fp32 narrowing     -> NarrowingOverflowError */
+
+typedef struct mpb_handle mpb_handle;
+typedef struct mpb_plan mpb_plan;
+
+/* CSR matrix on the device.  int32 row_ptr/col_idx (n and nnz < 2^31),
+ * columns strictly ascending within each row (sparse.py:59-104). */
+typedef struct mpb_csr {
+  int64_t n;
+  int64_t nnz;
+  const int32_t *row_ptr; /* n+1 */
+  const int32_t *col_idx; /* nnz */
+  const double *val64;    /* nnz, A.values (also the fp64 instance's values) */
+  const float *val32;     /* nnz, fp32 instance's values, NULL if unused     */
+} mpb_csr;
+
+typedef struct mpb_solve_options {
+  int kind;            /* MPB_UNIFORM ...                                  */
+  double adp_tol;      /* adaptive threshold (policies.py:40-43 defaults)  */
+  int k, t;            /* outer passes, inner sweeps                       */
+  double res_tol;      /* SolveConfig.res_tol                              */
+  int64_t max_iter;    /* iteration cap (SolveConfig.iteration_cap)        */
+  int64_t true_stride; /* record_true_residual_every (0: off)              */
+  int has_x0;          /* x holds x0 on entry; else x is zeroed            */
+  int graph_iters;     /* iterations per CUDA-graph replay (0: default)    */
+} mpb_solve_options;
+
+typedef struct mpb_solve_result {
+  int converged;
+  int error;              /* MPB_SOLVE_*                                   */
+  int64_t iterations;
+  int64_t err_iteration;
+  double err_value;
+  double r0_norm;
+  double final_true_relres;
+  int64_t overflow_count; /* narrowing overflow details                    */
+  int64_t overflow_index;
+  double device_seconds;  /* CUDA-event time of the iteration loop         */
+  int64_t kernel_launches;
+} mpb_solve_result;
+
+/* ---- library / handle ---------------------------------------------------- */
+int mpb_version(void);
+const char *mpb_status_string(int status);
+int mpb_create(int device, void *stream, mpb_handle **out);
+int mpb_destroy(mpb_handle *h);
+int mpb_set_stream(mpb_handle *h, void *stream);
+int mpb_synchronize(mpb_handle *h);
+/* Number of kernels this handle launched so far (for bench accounting). */
+int64_t mpb_launch_count(const mpb_handle *h);
+
+/* ---- partition / tile plan (host-only math, include/mpbjac_order.h) ---- */
+/* h_tile_lo must hold nb + n/512 + 2 entries; returns ntiles. No GPU needed. */
+int64_t mpb_plan_tiles_host(int64_t nb, const int64_t *h_offsets,
+                            const int64_t *h_row_ptr, int64_t *h_tile_lo,
+                            int *h_large);
+int mpb_plan_create(mpb_handle *h, int64_t n, int64_t nb,
+                    const int64_t *h_offsets, const int64_t *h_row_ptr,
+                    mpb_plan **out);
+int mpb_plan_destroy(mpb_plan *p);
+int mpb_plan_info(const mpb_plan *p, int64_t *h_ntiles, int *h_large,
+                  int64_t *h_max_tile_nnz);
+
+/* ---- reference backend kernels (kernels_numba.py) ------------------------ */
+int mpb_csr_matvec_f64(mpb_handle *h, int64_t n, const int32_t *row_ptr,
+                       const int32_t *col_idx, const double *val,
+                       const double *x, double *y);
+int mpb_csr_matvec_f32(mpb_handle *h, int64_t n, const int32_t *row_ptr,
+                       const int32_t *col_idx, const float *val,
+                       const float *x, float *y);
+/* in_block: one byte per nonzero (bjac.py:187-188); tmp: n entries */
+int mpb_block_jacobi_sweeps_f64(mpb_handle *h, const int32_t *row_ptr,
+                                const int32_t *col_idx, const double *val,
+                                const uint8_t *in_block, const double *diag,
+                                int t, const double *r, double *y, double *tmp,
+                                int64_t row_start, int64_t row_end);
+int mpb_block_jacobi_sweeps_f32(mpb_handle *h, const int32_t *row_ptr,
+                                const int32_t *col_idx, const float *val,
+                                const uint8_t *in_block, const float *diag,
+                                int t, const float *r, float *y, float *tmp,
+                                int64_t row_start, int64_t row_end);
+/* Device-order sums (mpbjac_order.h).  plan may be NULL: then 512-row
+ * tiles.  Result is written to h_out after a stream synchronize. */
+int mpb_dot_f64(mpb_handle *h, const mpb_plan *plan, int64_t n,
+                const double *x, const double *y, double *h_out);
+int mpb_dot_f32(mpb_handle *h, const mpb_plan *plan, int64_t n, const float *x,
+                const float *y, float *h_out);
+int mpb_norm_sq_f64(mpb_handle *h, const mpb_plan *plan, int64_t n,
+                    const double *x, double *h_out);
+int mpb_norm_sq_f32(mpb_handle *h, const mpb_plan *plan, int64_t n,
+                    const float *x, double *h_out);
+
+/* ---- conversions and setup (sparse.py:202-230, bjac.py:152-190) -------- */
+/* RN-even narrowing; counts finite values that land on +-inf.  Synchronous. */
+int mpb_narrow_f64_f32(mpb_handle *h, int64_t n, const double *src, float *dst,
+                       int64_t *h_overflow_count, int64_t *h_first_index);
+int mpb_widen_f32_f64(mpb_handle *h, int64_t n, const float *src, double *dst);
+/* Extract diag (the stored a_ii) and report the first row with no stored
+ * diagonal (h_missing) and the first row whose diagonal is zero (h_zero);
+ * -1 when none.  For the fp32 variant val32 is checked and val64 tells an
+ * underflow (nonzero fp64 diag) from a true zero.  Synchronous. */
+int mpb_setup_diag_f64(mpb_handle *h, int64_t n, const int32_t *row_ptr,
+                       const int32_t *col_idx, const double *val64,
+                       double *diag, int64_t *h_missing, int64_t *h_zero);
+int mpb_setup_diag_f32(mpb_handle *h, int64_t n, const int32_t *row_ptr,
+                       const int32_t *col_idx, const float *val32,
+                       float *diag, int64_t *h_missing, int64_t *h_zero);
+int mpb_convert_values_f32(mpb_handle *h, int64_t nnz, const double *val64,
+                           float *val32, int64_t *h_overflow_count,
+                           int64_t *h_first_index);
+
+/* ---- the preconditioner (bjac.py:106-149, policies.py:154-160) --------- */
+int mpb_bjac_apply_f64(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A,
+                       int k, int t, const double *r, double *z);
+int mpb_bjac_apply_f32(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A,
+                       int k, int t, const float *r, float *z);
+/* narrow(r) -> fp32 apply -> widen, fused; overflow reported like
+ * mpb_narrow_f64_f32 (z is not written when it overflows).  Synchronous. */
+int mpb_fmp_apply(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, int k,
+                  int t, const double *r, double *z,
+                  int64_t *h_overflow_count, int64_t *h_first_index);
+/* t sweeps on block b alone: r_b/y_b hold the block's rows. */
+int mpb_bjac_inner_apply_f64(mpb_handle *h, const mpb_csr *A, int64_t row_lo,
+                             int64_t row_hi, int t, const double *r_b,
+                             double *y_b);
+int mpb_bjac_inner_apply_f32(mpb_handle *h, const mpb_csr *A, int64_t row_lo,
+                             int64_t row_hi, int t, const float *r_b,
+                             float *y_b);
+
+/* ---- the whole PCG loop on the device (solver.py:101-184) -------------- */
+int64_t mpb_solve_workspace_bytes(const mpb_plan *plan, int64_t n);
+/* b, x: n fp64 (x: in x0 if has_x0, out solution).  Trace arrays hold
+ * max_iter entries: implicit relres, true relres (NaN = not recorded),
+ * branch (0 high / 1 low), wall time since the loop started (s). */
+int mpb_pcg_solve(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A,
+                  const mpb_solve_options *opt, const double *b, double *x,
+                  double *tr_relres, double *tr_true, int32_t *tr_branch,
+                  double *tr_time, void *workspace, int64_t workspace_bytes,
+                  mpb_solve_result *res);
+/* ||b - A x|| / r0_norm in device order.  Synchronous. */
+int mpb_true_relres(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A,
+                    const double *x, const double *b, double r0_norm,
+                    double *h_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

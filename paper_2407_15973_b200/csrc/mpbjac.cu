@@ -1,0 +1,930 @@
+// mpbjac.cu — C-ABI of libmpbjac.so (declared in include/mpbjac.h).
+//
+// Host side of the B200 hot path: tile plans, launch sequences for the fused
+// preconditioner passes, and the device-resident PCG loop replayed as a CUDA
+// graph.  Each entry point cites the reference function it replaces in
+// include/mpbjac.h.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "../../include/mpbjac.h"
+#include "mpbjac_kernels.cuh"
+
+using namespace mpb;
+
+namespace {
+
+constexpr int kCapMaxE32 = 8192;  // staged entries per tile, fp32 values
+constexpr int kCapMaxE64 = 6144;  // staged entries per tile, fp64 values
+constexpr int kDefaultGraphIters = 8;
+constexpr int kEltThreads = 256;
+
+inline int status_of(cudaError_t e) { return e == cudaSuccess ? MPB_OK : static_cast<int>(e); }
+
+#define MPB_CUDA(expr)                       \
+  do {                                       \
+    cudaError_t e_ = (expr);                 \
+    if (e_ != cudaSuccess) return status_of(e_); \
+  } while (0)
+
+#define MPB_LAUNCHED(h)                               \
+  do {                                                \
+    (h)->launches++;                                  \
+    cudaError_t e_ = cudaGetLastError();              \
+    if (e_ != cudaSuccess) return status_of(e_);      \
+  } while (0)
+
+struct GraphKey {
+  const void *plan, *rp, *ci, *v64, *v32, *b, *x, *trr, *trt, *trb, *trw, *ws;
+  int kind, k, t, iters;
+  long long stride, n;
+  bool operator==(const GraphKey &o) const { return std::memcmp(this, &o, sizeof(GraphKey)) == 0; }
+};
+
+}  // namespace
+
+struct mpb_plan {
+  int device;
+  int64_t n, nb, ntiles, max_tile_nnz;
+  int large;
+  int *d_tile_lo, *d_tile_bf, *d_tile_bl, *d_boff;
+};
+
+struct mpb_handle {
+  int device;
+  cudaStream_t user;    // caller's stream (may be the legacy default stream)
+  cudaStream_t solve;   // private stream for graph capture
+  cudaEvent_t ev_in, ev_out, ev_t0, ev_t1;
+  void *scratch;
+  size_t scratch_bytes;
+  SolverState *h_state;  // pinned
+  int64_t launches;
+  cudaGraphExec_t gexec;
+  GraphKey gkey;
+  int64_t graph_kernels;
+  bool have_graph;
+};
+
+namespace {
+
+int elt_blocks(long long n) {
+  long long b = (n + kEltThreads - 1) / kEltThreads;
+  return static_cast<int>(std::max(1LL, std::min(b, 148LL * 16)));
+}
+
+int ensure_scratch(mpb_handle *h, size_t bytes) {
+  if (h->scratch_bytes >= bytes) return MPB_OK;
+  if (h->scratch) {
+    MPB_CUDA(cudaStreamSynchronize(h->user));
+    MPB_CUDA(cudaFree(h->scratch));
+    h->scratch = nullptr;
+    h->scratch_bytes = 0;
+  }
+  bytes = std::max(bytes, size_t(1) << 20);
+  MPB_CUDA(cudaMalloc(&h->scratch, bytes));
+  h->scratch_bytes = bytes;
+  return MPB_OK;
+}
+
+inline size_t al256(size_t b) { return (b + 255) & ~size_t(255); }
+
+template <typename T>
+int cap_for(const mpb_plan *p) {
+  const int capmax = sizeof(T) == 4 ? kCapMaxE32 : kCapMaxE64;
+  return static_cast<int>(std::min<int64_t>(p->max_tile_nnz + 8, capmax));
+}
+
+template <typename T, bool F, bool L>
+int smem_optin() {
+  static bool done = false;
+  if (!done) {
+    MPB_CUDA(cudaFuncSetAttribute(k_bjac_tile<T, F, L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(tile_smem_bytes(sizeof(T) == 4 ? kCapMaxE32 : kCapMaxE64,
+                                                                   sizeof(T)))));
+    done = true;
+  }
+  return MPB_OK;
+}
+
+int spmv_optin() {
+  static bool done = false;
+  if (!done) {
+    MPB_CUDA(cudaFuncSetAttribute(k_spmv_pq, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(region_bytes(kCapMaxE64, 8) + region_bytes(kCapMaxE64, 4))));
+    done = true;
+  }
+  return MPB_OK;
+}
+
+// Buffers one preconditioner application needs besides r and z.
+template <typename T>
+struct ApplyBufs {
+  T *zA, *zB;            // intermediate pass outputs (k > 1)
+  T *res, *dg, *wA, *wB; // large-block path (plan->large)
+};
+
+template <typename T, bool F, bool L>
+int launch_pass(mpb_handle *h, cudaStream_t s, const mpb_plan *p, PassArgs<T> a, const ApplyBufs<T> &bufs) {
+  const int nt = static_cast<int>(p->ntiles);
+  if (!p->large) {
+    int st = smem_optin<T, F, L>();
+    if (st) return st;
+    const uint32_t smem = tile_smem_bytes(a.cap_e, sizeof(T));
+    k_bjac_tile<T, F, L><<<nt, kTileThreads, smem, s>>>(a);
+    MPB_LAUNCHED(h);
+    return MPB_OK;
+  }
+  a.resbuf = bufs.res;
+  a.dbuf = bufs.dg;
+  k_big_resid<T, F><<<nt, kTileThreads, 0, s>>>(a, bufs.wA);
+  MPB_LAUNCHED(h);
+  T *cur = bufs.wA, *nxt = bufs.wB;
+  for (int sweep = 1; sweep < a.t; sweep++) {
+    k_big_sweep<T><<<nt, kTileThreads, 0, s>>>(a, cur, nxt);
+    MPB_LAUNCHED(h);
+    std::swap(cur, nxt);
+  }
+  k_big_finish<T, F, L><<<nt, kTileThreads, 0, s>>>(a, cur);
+  MPB_LAUNCHED(h);
+  return MPB_OK;
+}
+
+// k outer passes (bjac.py:127-149).  Residual from r64 (narrowed on load) or
+// rT; final output to zout (T) and/or zout64; r.z partials when part != null.
+template <typename T>
+int launch_apply(mpb_handle *h, cudaStream_t s, const mpb_plan *p, const int *rp, const int *ci, const T *val,
+                 int k, int t, const double *r64, const T *rT, T *zout, double *zout64, double *part,
+                 unsigned long long *ovf_count, long long *ovf_first, const SolverState *st, int want_branch,
+                 const ApplyBufs<T> &bufs) {
+  PassArgs<T> a{};
+  a.rp = rp;
+  a.ci = ci;
+  a.val = val;
+  a.tile_lo = p->d_tile_lo;
+  a.tile_bf = p->d_tile_bf;
+  a.tile_bl = p->d_tile_bl;
+  a.boff = p->d_boff;
+  a.t = t;
+  a.cap_e = cap_for<T>(p);
+  a.r64 = r64;
+  a.rT = rT;
+  a.ovf_count = ovf_count;
+  a.ovf_first = ovf_first;
+  a.st = st;
+  a.want_branch = want_branch;
+  for (int pass = 0; pass < k; pass++) {
+    const bool first = pass == 0, last = pass == k - 1;
+    a.zin = first ? nullptr : ((pass - 1) & 1 ? bufs.zB : bufs.zA);
+    a.zout = last ? zout : (pass & 1 ? bufs.zB : bufs.zA);
+    a.zout64 = last ? zout64 : nullptr;
+    a.part = last ? part : nullptr;
+    int rc;
+    if (first && last) rc = launch_pass<T, true, true>(h, s, p, a, bufs);
+    else if (first) rc = launch_pass<T, true, false>(h, s, p, a, bufs);
+    else if (last) rc = launch_pass<T, false, true>(h, s, p, a, bufs);
+    else rc = launch_pass<T, false, false>(h, s, p, a, bufs);
+    if (rc) return rc;
+  }
+  return MPB_OK;
+}
+
+int check_csr(const mpb_csr *A) {
+  if (!A || !A->row_ptr || !A->col_idx || A->n < 1) return MPB_ERR_ARG;
+  if (A->n >= (int64_t(1) << 31) - 1 || A->nnz >= (int64_t(1) << 31)) return MPB_ERR_INDEX32;
+  return MPB_OK;
+}
+
+// partition/tile plan, same rule as include/mpbjac_order.h (and the oracle)
+int64_t plan_tiles(int64_t nb, const int64_t *offs, const int64_t *rp, int64_t *tile_lo, int *large) {
+  int64_t nt = 0, cur_lo = 0, cur_rows = 0, cur_nnz = 0;
+  *large = 0;
+  for (int64_t b = 0; b < nb; b++) {
+    const int64_t lo = offs[b], hi = offs[b + 1];
+    const int64_t br = hi - lo, bz = rp[hi] - rp[lo];
+    if (br > MPB_TILE_MAX_ROWS) {
+      if (cur_rows > 0) tile_lo[nt++] = cur_lo;
+      for (int64_t s = lo; s < hi; s += MPB_TILE_MAX_ROWS) tile_lo[nt++] = s;
+      cur_lo = hi;
+      cur_rows = cur_nnz = 0;
+      *large = 1;
+      continue;
+    }
+    if (cur_rows > 0 && (cur_rows + br > MPB_TILE_MAX_ROWS || cur_nnz + bz > MPB_TILE_PACK_NNZ)) {
+      tile_lo[nt++] = cur_lo;
+      cur_lo = lo;
+      cur_rows = cur_nnz = 0;
+    }
+    cur_rows += br;
+    cur_nnz += bz;
+  }
+  if (cur_rows > 0) tile_lo[nt++] = cur_lo;
+  tile_lo[nt] = offs[nb];
+  return nt;
+}
+
+// Solve-time workspace layout
+struct SolveWs {
+  double *r, *q, *p0, *p1, *z64, *zA64, *zB64;
+  float *z32, *zA32, *zB32;
+  double *res64, *dg64, *wA64, *wB64;
+  float *res32, *dg32, *wA32, *wB32;
+  double *part;
+  SolverState *st;
+  size_t bytes;
+};
+
+SolveWs carve(const mpb_plan *p, int64_t n, char *base) {
+  SolveWs w{};
+  size_t off = 0;
+  auto take = [&](size_t bytes) -> char * {
+    char *q = base ? base + off : nullptr;
+    off += al256(bytes);
+    return q;
+  };
+  const size_t d = sizeof(double) * (n + 2), f = sizeof(float) * (n + 4);
+  w.r = (double *)take(d);
+  w.q = (double *)take(d);
+  w.p0 = (double *)take(d);
+  w.p1 = (double *)take(d);
+  w.z64 = (double *)take(d);
+  w.zA64 = (double *)take(d);
+  w.zB64 = (double *)take(d);
+  w.z32 = (float *)take(f);
+  w.zA32 = (float *)take(f);
+  w.zB32 = (float *)take(f);
+  if (p->large) {
+    w.res64 = (double *)take(d);
+    w.dg64 = (double *)take(d);
+    w.wA64 = (double *)take(d);
+    w.wB64 = (double *)take(d);
+    w.res32 = (float *)take(f);
+    w.dg32 = (float *)take(f);
+    w.wA32 = (float *)take(f);
+    w.wB32 = (float *)take(f);
+  }
+  w.part = (double *)take(sizeof(double) * (p->ntiles + 1));
+  w.st = (SolverState *)take(sizeof(SolverState));
+  w.bytes = off;
+  return w;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C-ABI (C linkage comes from the declarations in include/mpbjac.h)
+// ===========================================================================
+
+int mpb_version(void) { return MPB_VERSION; }
+
+const char *mpb_status_string(int status) {
+  switch (status) {
+    case MPB_OK: return "ok";
+    case MPB_ERR_ARG: return "invalid argument";
+    case MPB_ERR_SHAPE: return "inconsistent shapes";
+    case MPB_ERR_PARTITION: return "partition does not match the matrix";
+    case MPB_ERR_SWEEPS: return "sweep counts k and t must be at least 1";
+    case MPB_ERR_INDEX32: return "matrix too large for int32 indexing";
+    case MPB_ERR_POLICY: return "policy needs a preconditioner instance that was not set up";
+    case MPB_ERR_WORKSPACE: return "workspace too small";
+    default: break;
+  }
+  if (status > 0) return cudaGetErrorString(static_cast<cudaError_t>(status));
+  return "unknown status";
+}
+
+int mpb_create(int device, void *stream, mpb_handle **out) {
+  if (!out) return MPB_ERR_ARG;
+  *out = nullptr;
+  MPB_CUDA(cudaSetDevice(device));
+  mpb_handle *h = new mpb_handle();
+  h->device = device;
+  h->user = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaStreamCreateWithFlags(&h->solve, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_in, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_out, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreate(&h->ev_t0);
+  if (e == cudaSuccess) e = cudaEventCreate(&h->ev_t1);
+  if (e == cudaSuccess) e = cudaMallocHost(&h->h_state, sizeof(SolverState));
+  if (e != cudaSuccess) {
+    delete h;
+    return status_of(e);
+  }
+  *out = h;
+  return MPB_OK;
+}
+
+int mpb_destroy(mpb_handle *h) {
+  if (!h) return MPB_OK;
+  cudaStreamSynchronize(h->user);
+  cudaStreamSynchronize(h->solve);
+  if (h->have_graph) cudaGraphExecDestroy(h->gexec);
+  if (h->scratch) cudaFree(h->scratch);
+  cudaFreeHost(h->h_state);
+  cudaEventDestroy(h->ev_in);
+  cudaEventDestroy(h->ev_out);
+  cudaEventDestroy(h->ev_t0);
+  cudaEventDestroy(h->ev_t1);
+  cudaStreamDestroy(h->solve);
+  delete h;
+  return MPB_OK;
+}
+
+int mpb_set_stream(mpb_handle *h, void *stream) {
+  if (!h) return MPB_ERR_ARG;
+  h->user = static_cast<cudaStream_t>(stream);
+  return MPB_OK;
+}
+
+int mpb_synchronize(mpb_handle *h) {
+  if (!h) return MPB_ERR_ARG;
+  MPB_CUDA(cudaStreamSynchronize(h->user));
+  MPB_CUDA(cudaStreamSynchronize(h->solve));
+  return MPB_OK;
+}
+
+int64_t mpb_launch_count(const mpb_handle *h) { return h ? h->launches : 0; }
+
+// ---- plans -----------------------------------------------------------------
+int64_t mpb_plan_tiles_host(int64_t nb, const int64_t *h_offsets, const int64_t *h_row_ptr, int64_t *h_tile_lo,
+                            int *h_large) {
+  if (nb < 1 || !h_offsets || !h_row_ptr || !h_tile_lo || !h_large) return MPB_ERR_ARG;
+  return plan_tiles(nb, h_offsets, h_row_ptr, h_tile_lo, h_large);
+}
+
+int mpb_plan_create(mpb_handle *h, int64_t n, int64_t nb, const int64_t *h_offsets, const int64_t *h_row_ptr,
+                    mpb_plan **out) {
+  if (!h || !out || !h_offsets || !h_row_ptr || nb < 1 || n < 1) return MPB_ERR_ARG;
+  *out = nullptr;
+  if (h_offsets[0] != 0 || h_offsets[nb] != n) return MPB_ERR_PARTITION;
+  for (int64_t b = 0; b < nb; b++)
+    if (h_offsets[b + 1] <= h_offsets[b]) return MPB_ERR_PARTITION;
+  if (n >= (int64_t(1) << 31) - 1 || h_row_ptr[n] >= (int64_t(1) << 31)) return MPB_ERR_INDEX32;
+  std::vector<int64_t> tlo(nb + n / MPB_TILE_MAX_ROWS + 2);
+  int large = 0;
+  const int64_t nt = plan_tiles(nb, h_offsets, h_row_ptr, tlo.data(), &large);
+  std::vector<int> tl(nt + 1), bfv(nt), blv(nt), boff(nb + 1);
+  int64_t max_nnz = 0;
+  int64_t b = 0;
+  for (int64_t i = 0; i <= nt; i++) tl[i] = static_cast<int>(tlo[i]);
+  for (int64_t i = 0; i <= nb; i++) boff[i] = static_cast<int>(h_offsets[i]);
+  for (int64_t i = 0; i < nt; i++) {
+    const int64_t lo = tlo[i], hi = tlo[i + 1];
+    while (h_offsets[b + 1] <= lo) b++;
+    bfv[i] = static_cast<int>(b);
+    int64_t e = b;
+    while (h_offsets[e + 1] < hi) e++;
+    blv[i] = static_cast<int>(e);
+    max_nnz = std::max(max_nnz, h_row_ptr[hi] - h_row_ptr[lo]);
+  }
+  MPB_CUDA(cudaSetDevice(h->device));
+  mpb_plan *p = new mpb_plan();
+  p->device = h->device;
+  p->n = n;
+  p->nb = nb;
+  p->ntiles = nt;
+  p->large = large;
+  p->max_tile_nnz = max_nnz;
+  cudaError_t e = cudaMalloc(&p->d_tile_lo, sizeof(int) * (nt + 1));
+  if (e == cudaSuccess) e = cudaMalloc(&p->d_tile_bf, sizeof(int) * nt);
+  if (e == cudaSuccess) e = cudaMalloc(&p->d_tile_bl, sizeof(int) * nt);
+  if (e == cudaSuccess) e = cudaMalloc(&p->d_boff, sizeof(int) * (nb + 1));
+  if (e == cudaSuccess) e = cudaMemcpy(p->d_tile_lo, tl.data(), sizeof(int) * (nt + 1), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(p->d_tile_bf, bfv.data(), sizeof(int) * nt, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(p->d_tile_bl, blv.data(), sizeof(int) * nt, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(p->d_boff, boff.data(), sizeof(int) * (nb + 1), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    mpb_plan_destroy(p);
+    return status_of(e);
+  }
+  *out = p;
+  return MPB_OK;
+}
+
+int mpb_plan_destroy(mpb_plan *p) {
+  if (!p) return MPB_OK;
+  cudaFree(p->d_tile_lo);
+  cudaFree(p->d_tile_bf);
+  cudaFree(p->d_tile_bl);
+  cudaFree(p->d_boff);
+  delete p;
+  return MPB_OK;
+}
+
+int mpb_plan_info(const mpb_plan *p, int64_t *h_ntiles, int *h_large, int64_t *h_max_tile_nnz) {
+  if (!p) return MPB_ERR_ARG;
+  if (h_ntiles) *h_ntiles = p->ntiles;
+  if (h_large) *h_large = p->large;
+  if (h_max_tile_nnz) *h_max_tile_nnz = p->max_tile_nnz;
+  return MPB_OK;
+}
+
+// ---- backend kernels -------------------------------------------------------
+int mpb_csr_matvec_f64(mpb_handle *h, int64_t n, const int32_t *row_ptr, const int32_t *col_idx, const double *val,
+                       const double *x, double *y) {
+  if (!h || n < 0 || (n > 0 && (!row_ptr || !y))) return MPB_ERR_ARG;
+  if (n == 0) return MPB_OK;
+  k_matvec<double><<<elt_blocks(n), kEltThreads, 0, h->user>>>(n, row_ptr, col_idx, val, x, y);
+  MPB_LAUNCHED(h);
+  return MPB_OK;
+}
+
+int mpb_csr_matvec_f32(mpb_handle *h, int64_t n, const int32_t *row_ptr, const int32_t *col_idx, const float *val,
+                       const float *x, float *y) {
+  if (!h || n < 0 || (n > 0 && (!row_ptr || !y))) return MPB_ERR_ARG;
+  if (n == 0) return MPB_OK;
+  k_matvec<float><<<elt_blocks(n), kEltThreads, 0, h->user>>>(n, row_ptr, col_idx, val, x, y);
+  MPB_LAUNCHED(h);
+  return MPB_OK;
+}
+
+template <typename T>
+static int sweeps_impl(mpb_handle *h, const int32_t *rp, const int32_t *ci, const T *val, const uint8_t *mask,
+                       const T *diag, int t, const T *r, T *y, T *tmp, int64_t rs, int64_t re) {
+  if (!h || !rp || !diag || !r || !y || !tmp || rs < 0 || re < rs) return MPB_ERR_ARG;
+  if (re == rs) return MPB_OK;
+  const int g = elt_blocks(re - rs);
+  k_msweep_init<T><<<g, kEltThreads, 0, h->user>>>(rs, re, r, diag, y);
+  MPB_LAUNCHED(h);
+  for (int s = 0; s < t - 1; s++) {
+    k_msweep_tmp<T><<<g, kEltThreads, 0, h->user>>>(rs, re, rp, ci, val, mask, y, tmp);
+    MPB_LAUNCHED(h);
+    k_msweep_upd<T><<<g, kEltThreads, 0, h->user>>>(rs, re, r, diag, tmp, y);
+    MPB_LAUNCHED(h);
+  }
+  return MPB_OK;
+}
+
+int mpb_block_jacobi_sweeps_f64(mpb_handle *h, const int32_t *row_ptr, const int32_t *col_idx, const double *val,
+                                const uint8_t *in_block, const double *diag, int t, const double *r, double *y,
+                                double *tmp, int64_t row_start, int64_t row_end) {
+  return sweeps_impl<double>(h, row_ptr, col_idx, val, in_block, diag, t, r, y, tmp, row_start, row_end);
+}
+
+int mpb_block_jacobi_sweeps_f32(mpb_handle *h, const int32_t *row_ptr, const int32_t *col_idx, const float *val,
+                                const uint8_t *in_block, const float *diag, int t, const float *r, float *y,
+                                float *tmp, int64_t row_start, int64_t row_end) {
+  return sweeps_impl<float>(h, row_ptr, col_idx, val, in_block, diag, t, r, y, tmp, row_start, row_end);
+}
+
+template <typename T, typename ACC, bool SQ>
+static int tile_reduce(mpb_handle *h, const mpb_plan *plan, int64_t n, const T *x, const T *y, ACC *h_out) {
+  if (!h || !h_out || n < 0) return MPB_ERR_ARG;
+  if (n == 0) {
+    *h_out = ACC(0);
+    return MPB_OK;
+  }
+  if (plan && plan->n != n) return MPB_ERR_SHAPE;
+  const int64_t nt = plan ? plan->ntiles : (n + kTileRows - 1) / kTileRows;
+  int rc = ensure_scratch(h, al256(sizeof(ACC) * (nt + 1)) + 256);
+  if (rc) return rc;
+  ACC *part = static_cast<ACC *>(h->scratch);
+  ACC *res = reinterpret_cast<ACC *>(static_cast<char *>(h->scratch) + al256(sizeof(ACC) * (nt + 1)));
+  k_tile_dot<T, ACC, SQ><<<static_cast<unsigned>(nt), kTileThreads, 0, h->user>>>(n, plan ? plan->d_tile_lo : nullptr,
+                                                                                 x, y, part);
+  MPB_LAUNCHED(h);
+  k_fin<ACC><<<1, kFinThreads, 0, h->user>>>(part, nt, res);
+  MPB_LAUNCHED(h);
+  MPB_CUDA(cudaMemcpyAsync(h_out, res, sizeof(ACC), cudaMemcpyDeviceToHost, h->user));
+  MPB_CUDA(cudaStreamSynchronize(h->user));
+  return MPB_OK;
+}
+
+int mpb_dot_f64(mpb_handle *h, const mpb_plan *plan, int64_t n, const double *x, const double *y, double *h_out) {
+  return tile_reduce<double, double, false>(h, plan, n, x, y, h_out);
+}
+int mpb_dot_f32(mpb_handle *h, const mpb_plan *plan, int64_t n, const float *x, const float *y, float *h_out) {
+  return tile_reduce<float, float, false>(h, plan, n, x, y, h_out);
+}
+int mpb_norm_sq_f64(mpb_handle *h, const mpb_plan *plan, int64_t n, const double *x, double *h_out) {
+  return tile_reduce<double, double, true>(h, plan, n, x, x, h_out);
+}
+int mpb_norm_sq_f32(mpb_handle *h, const mpb_plan *plan, int64_t n, const float *x, double *h_out) {
+  return tile_reduce<float, double, true>(h, plan, n, x, x, h_out);
+}
+
+// ---- conversions / setup -----------------------------------------------------
+static int narrow_impl(mpb_handle *h, int64_t n, const double *src, float *dst, int64_t *h_cnt, int64_t *h_first) {
+  if (!h || n < 0) return MPB_ERR_ARG;
+  int rc = ensure_scratch(h, 256);
+  if (rc) return rc;
+  unsigned long long *cnt = static_cast<unsigned long long *>(h->scratch);
+  long long *first = reinterpret_cast<long long *>(cnt + 1);
+  const long long init[2] = {0, (long long)INT64_MAX};
+  MPB_CUDA(cudaMemcpyAsync(cnt, init, sizeof(init), cudaMemcpyHostToDevice, h->user));
+  if (n > 0) {
+    k_narrow<<<elt_blocks(n), kEltThreads, 0, h->user>>>(n, src, dst, cnt, first);
+    MPB_LAUNCHED(h);
+  }
+  long long out[2];
+  MPB_CUDA(cudaMemcpyAsync(out, cnt, sizeof(out), cudaMemcpyDeviceToHost, h->user));
+  MPB_CUDA(cudaStreamSynchronize(h->user));
+  if (h_cnt) *h_cnt = out[0];
+  if (h_first) *h_first = out[0] ? out[1] : -1;
+  return MPB_OK;
+}
+
+int mpb_narrow_f64_f32(mpb_handle *h, int64_t n, const double *src, float *dst, int64_t *h_overflow_count,
+                       int64_t *h_first_index) {
+  return narrow_impl(h, n, src, dst, h_overflow_count, h_first_index);
+}
+
+int mpb_convert_values_f32(mpb_handle *h, int64_t nnz, const double *val64, float *val32, int64_t *h_overflow_count,
+                           int64_t *h_first_index) {
+  return narrow_impl(h, nnz, val64, val32, h_overflow_count, h_first_index);
+}
+
+int mpb_widen_f32_f64(mpb_handle *h, int64_t n, const float *src, double *dst) {
+  if (!h || n < 0) return MPB_ERR_ARG;
+  if (n == 0) return MPB_OK;
+  k_widen<<<elt_blocks(n), kEltThreads, 0, h->user>>>(n, src, dst);
+  MPB_LAUNCHED(h);
+  return MPB_OK;
+}
+
+template <typename T>
+static int diag_impl(mpb_handle *h, int64_t n, const int32_t *rp, const int32_t *ci, const T *val, T *diag,
+                     int64_t *h_missing, int64_t *h_zero) {
+  if (!h || n < 1 || !rp || !ci || !val || !diag) return MPB_ERR_ARG;
+  int rc = ensure_scratch(h, 256);
+  if (rc) return rc;
+  long long *flags = static_cast<long long *>(h->scratch);
+  const long long init[2] = {(long long)INT64_MAX, (long long)INT64_MAX};
+  MPB_CUDA(cudaMemcpyAsync(flags, init, sizeof(init), cudaMemcpyHostToDevice, h->user));
+  k_setup_diag<T><<<elt_blocks(n), kEltThreads, 0, h->user>>>(n, rp, ci, val, diag, flags, flags + 1);
+  MPB_LAUNCHED(h);
+  long long out[2];
+  MPB_CUDA(cudaMemcpyAsync(out, flags, sizeof(out), cudaMemcpyDeviceToHost, h->user));
+  MPB_CUDA(cudaStreamSynchronize(h->user));
+  if (h_missing) *h_missing = out[0] == (long long)INT64_MAX ? -1 : out[0];
+  if (h_zero) *h_zero = out[1] == (long long)INT64_MAX ? -1 : out[1];
+  return MPB_OK;
+}
+
+int mpb_setup_diag_f64(mpb_handle *h, int64_t n, const int32_t *row_ptr, const int32_t *col_idx, const double *val64,
+                       double *diag, int64_t *h_missing, int64_t *h_zero) {
+  return diag_impl<double>(h, n, row_ptr, col_idx, val64, diag, h_missing, h_zero);
+}
+
+int mpb_setup_diag_f32(mpb_handle *h, int64_t n, const int32_t *row_ptr, const int32_t *col_idx, const float *val32,
+                       float *diag, int64_t *h_missing, int64_t *h_zero) {
+  return diag_impl<float>(h, n, row_ptr, col_idx, val32, diag, h_missing, h_zero);
+}
+
+// ---- preconditioner ----------------------------------------------------------
+template <typename T>
+static int apply_bufs_scratch(mpb_handle *h, const mpb_plan *p, int64_t n, size_t extra, ApplyBufs<T> &b,
+                              char **extra_ptr) {
+  const size_t v = al256(sizeof(T) * (n + 4));
+  const size_t need = 2 * v + (p->large ? 4 * v : 0) + al256(extra);
+  int rc = ensure_scratch(h, need);
+  if (rc) return rc;
+  char *base = static_cast<char *>(h->scratch);
+  b.zA = (T *)base;
+  b.zB = (T *)(base + v);
+  size_t off = 2 * v;
+  if (p->large) {
+    b.res = (T *)(base + off);
+    b.dg = (T *)(base + off + v);
+    b.wA = (T *)(base + off + 2 * v);
+    b.wB = (T *)(base + off + 3 * v);
+    off += 4 * v;
+  } else {
+    b.res = b.dg = b.wA = b.wB = nullptr;
+  }
+  if (extra_ptr) *extra_ptr = base + off;
+  return MPB_OK;
+}
+
+template <typename T>
+static int apply_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, const T *val, int k, int t,
+                      const T *r, T *z) {
+  int rc = check_csr(A);
+  if (rc) return rc;
+  if (!h || !plan || !r || !z || !val) return MPB_ERR_ARG;
+  if (plan->n != A->n) return MPB_ERR_PARTITION;
+  if (k < 1 || t < 1) return MPB_ERR_SWEEPS;
+  ApplyBufs<T> b;
+  rc = apply_bufs_scratch<T>(h, plan, A->n, 0, b, nullptr);
+  if (rc) return rc;
+  return launch_apply<T>(h, h->user, plan, A->row_ptr, A->col_idx, val, k, t, nullptr, r, z, nullptr, nullptr,
+                         nullptr, nullptr, nullptr, 0, b);
+}
+
+int mpb_bjac_apply_f64(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, int k, int t, const double *r,
+                       double *z) {
+  return apply_impl<double>(h, plan, A, A ? A->val64 : nullptr, k, t, r, z);
+}
+
+int mpb_bjac_apply_f32(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, int k, int t, const float *r,
+                       float *z) {
+  return apply_impl<float>(h, plan, A, A ? A->val32 : nullptr, k, t, r, z);
+}
+
+int mpb_fmp_apply(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, int k, int t, const double *r, double *z,
+                  int64_t *h_overflow_count, int64_t *h_first_index) {
+  int rc = check_csr(A);
+  if (rc) return rc;
+  if (!h || !plan || !r || !z) return MPB_ERR_ARG;
+  if (!A->val32) return MPB_ERR_POLICY;
+  if (plan->n != A->n) return MPB_ERR_PARTITION;
+  if (k < 1 || t < 1) return MPB_ERR_SWEEPS;
+  ApplyBufs<float> b;
+  char *extra;
+  rc = apply_bufs_scratch<float>(h, plan, A->n, 256, b, &extra);
+  if (rc) return rc;
+  unsigned long long *cnt = reinterpret_cast<unsigned long long *>(extra);
+  long long *first = reinterpret_cast<long long *>(extra + 8);
+  const long long init[2] = {0, (long long)INT64_MAX};
+  MPB_CUDA(cudaMemcpyAsync(cnt, init, sizeof(init), cudaMemcpyHostToDevice, h->user));
+  rc = launch_apply<float>(h, h->user, plan, A->row_ptr, A->col_idx, A->val32, k, t, r, nullptr, nullptr, z, nullptr,
+                           cnt, first, nullptr, 0, b);
+  if (rc) return rc;
+  long long out[2];
+  MPB_CUDA(cudaMemcpyAsync(out, cnt, sizeof(out), cudaMemcpyDeviceToHost, h->user));
+  MPB_CUDA(cudaStreamSynchronize(h->user));
+  if (h_overflow_count) *h_overflow_count = out[0];
+  if (h_first_index) *h_first_index = out[0] ? out[1] : -1;
+  return MPB_OK;
+}
+
+template <typename T>
+static int inner_impl(mpb_handle *h, const mpb_csr *A, const T *val, int64_t lo, int64_t hi, int t, const T *rb,
+                      T *yb) {
+  int rc = check_csr(A);
+  if (rc) return rc;
+  if (!h || !val || !rb || !yb || lo < 0 || hi > A->n || hi <= lo) return MPB_ERR_ARG;
+  if (t < 1) return MPB_ERR_SWEEPS;
+  const int64_t m = hi - lo;
+  const size_t v = al256(sizeof(T) * (m + 4));
+  rc = ensure_scratch(h, 2 * v);
+  if (rc) return rc;
+  T *db = static_cast<T *>(h->scratch);
+  T *tmp = reinterpret_cast<T *>(static_cast<char *>(h->scratch) + v);
+  const int g = elt_blocks(m);
+  k_inner_init<T><<<g, kEltThreads, 0, h->user>>>((int)lo, (int)hi, A->row_ptr, A->col_idx, val, rb, db, yb);
+  MPB_LAUNCHED(h);
+  for (int s = 1; s < t; s++) {
+    k_inner_sweep<T><<<g, kEltThreads, 0, h->user>>>((int)lo, (int)hi, A->row_ptr, A->col_idx, val, rb, db, yb, tmp);
+    MPB_LAUNCHED(h);
+    MPB_CUDA(cudaMemcpyAsync(yb, tmp, sizeof(T) * m, cudaMemcpyDeviceToDevice, h->user));
+  }
+  return MPB_OK;
+}
+
+int mpb_bjac_inner_apply_f64(mpb_handle *h, const mpb_csr *A, int64_t row_lo, int64_t row_hi, int t,
+                             const double *r_b, double *y_b) {
+  return inner_impl<double>(h, A, A ? A->val64 : nullptr, row_lo, row_hi, t, r_b, y_b);
+}
+
+int mpb_bjac_inner_apply_f32(mpb_handle *h, const mpb_csr *A, int64_t row_lo, int64_t row_hi, int t,
+                             const float *r_b, float *y_b) {
+  return inner_impl<float>(h, A, A ? A->val32 : nullptr, row_lo, row_hi, t, r_b, y_b);
+}
+
+// ---- the PCG loop ------------------------------------------------------------
+int64_t mpb_solve_workspace_bytes(const mpb_plan *plan, int64_t n) {
+  if (!plan || n != plan->n) return MPB_ERR_ARG;
+  return static_cast<int64_t>(carve(plan, n, nullptr).bytes);
+}
+
+static int enqueue_iteration(mpb_handle *h, cudaStream_t s, const mpb_plan *p, const mpb_csr *A,
+                             const mpb_solve_options *o, const SolveWs &w, double *tr_relres, double *tr_true,
+                             int32_t *tr_branch, double *tr_time) {
+  const bool high = o->kind != MPB_FIXED_LOW, low = o->kind != MPB_UNIFORM;
+  if (high) {
+    ApplyBufs<double> b{w.zA64, w.zB64, w.res64, w.dg64, w.wA64, w.wB64};
+    int rc = launch_apply<double>(h, s, p, A->row_ptr, A->col_idx, A->val64, o->k, o->t, w.r, nullptr, w.z64,
+                                  nullptr, w.part, nullptr, nullptr, w.st, 0, b);
+    if (rc) return rc;
+  }
+  if (low) {
+    ApplyBufs<float> b{w.zA32, w.zB32, w.res32, w.dg32, w.wA32, w.wB32};
+    int rc = launch_apply<float>(h, s, p, A->row_ptr, A->col_idx, A->val32, o->k, o->t, w.r, nullptr, w.z32,
+                                 nullptr, w.part, &w.st->ovf_count, &w.st->ovf_first, w.st, 1, b);
+    if (rc) return rc;
+  }
+  const unsigned nt = static_cast<unsigned>(p->ntiles);
+  k_scalar<<<1, kFinThreads, 0, s>>>(kStepRho, w.part, p->ntiles, w.st, tr_relres, tr_true, (int *)tr_branch, tr_time);
+  MPB_LAUNCHED(h);
+  int rc = spmv_optin();
+  if (rc) return rc;
+  SpmvArgs sa{};
+  sa.rp = A->row_ptr;
+  sa.ci = A->col_idx;
+  sa.val = A->val64;
+  sa.tile_lo = p->d_tile_lo;
+  sa.cap_e = cap_for<double>(p);
+  sa.z32 = w.z32;
+  sa.z64 = w.z64;
+  sa.p0 = w.p0;
+  sa.p1 = w.p1;
+  sa.q = w.q;
+  sa.part = w.part;
+  sa.st = w.st;
+  const uint32_t smem = region_bytes(sa.cap_e, 8) + region_bytes(sa.cap_e, 4);
+  k_spmv_pq<<<nt, kTileThreads, smem, s>>>(sa);
+  MPB_LAUNCHED(h);
+  k_scalar<<<1, kFinThreads, 0, s>>>(kStepPq, w.part, p->ntiles, w.st, tr_relres, tr_true, (int *)tr_branch, tr_time);
+  MPB_LAUNCHED(h);
+  return MPB_OK;
+}
+
+static int enqueue_tail(mpb_handle *h, cudaStream_t s, const mpb_plan *p, const mpb_csr *A,
+                        const mpb_solve_options *o, const SolveWs &w, const double *b, double *x, double *tr_relres,
+                        double *tr_true, int32_t *tr_branch, double *tr_time) {
+  const unsigned nt = static_cast<unsigned>(p->ntiles);
+  k_update<<<nt, kTileThreads, 0, s>>>(p->d_tile_lo, x, w.p0, w.p1, w.q, w.r, w.part, w.st);
+  MPB_LAUNCHED(h);
+  k_scalar<<<1, kFinThreads, 0, s>>>(kStepRr, w.part, p->ntiles, w.st, tr_relres, tr_true, (int *)tr_branch, tr_time);
+  MPB_LAUNCHED(h);
+  if (o->true_stride > 0) {
+    k_resid<true><<<nt, kTileThreads, 0, s>>>(A->row_ptr, A->col_idx, A->val64, p->d_tile_lo, b, x, nullptr,
+                                              w.part, w.st, 1);
+    MPB_LAUNCHED(h);
+    k_scalar<<<1, kFinThreads, 0, s>>>(kStepTrue, w.part, p->ntiles, w.st, tr_relres, tr_true, (int *)tr_branch,
+                                       tr_time);
+    MPB_LAUNCHED(h);
+  }
+  return MPB_OK;
+}
+
+int mpb_pcg_solve(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, const mpb_solve_options *opt,
+                  const double *b, double *x, double *tr_relres, double *tr_true, int32_t *tr_branch,
+                  double *tr_time, void *workspace, int64_t workspace_bytes, mpb_solve_result *res) {
+  int rc = check_csr(A);
+  if (rc) return rc;
+  if (!h || !plan || !opt || !b || !x || !tr_relres || !tr_true || !tr_branch || !tr_time || !res || !workspace)
+    return MPB_ERR_ARG;
+  if (plan->n != A->n) return MPB_ERR_PARTITION;
+  if (opt->k < 1 || opt->t < 1) return MPB_ERR_SWEEPS;
+  if (opt->kind < MPB_UNIFORM || opt->kind > MPB_ADAPTIVE_LH) return MPB_ERR_POLICY;
+  if ((opt->kind != MPB_FIXED_LOW && !A->val64) || (opt->kind != MPB_UNIFORM && !A->val32) || !A->val64)
+    return MPB_ERR_POLICY;
+  if (opt->max_iter < 1) return MPB_ERR_ARG;
+  SolveWs w = carve(plan, A->n, static_cast<char *>(workspace));
+  if (workspace_bytes < static_cast<int64_t>(w.bytes)) return MPB_ERR_WORKSPACE;
+  std::memset(res, 0, sizeof(*res));
+  res->overflow_index = -1;
+  const int64_t launches0 = h->launches;
+  MPB_CUDA(cudaSetDevice(h->device));
+  cudaStream_t s = h->solve;
+  // order after the caller's pending work
+  MPB_CUDA(cudaEventRecord(h->ev_in, h->user));
+  MPB_CUDA(cudaStreamWaitEvent(s, h->ev_in, 0));
+
+  SolverState init{};
+  init.res_tol = opt->res_tol;
+  init.adp_tol = opt->adp_tol;
+  init.cap = opt->max_iter;
+  init.stride = opt->true_stride;
+  init.kind = opt->kind;
+  init.ovf_first = INT64_MAX;
+  *h->h_state = init;
+  MPB_CUDA(cudaMemcpyAsync(w.st, h->h_state, sizeof(SolverState), cudaMemcpyHostToDevice, s));
+  k_fill<<<elt_blocks(opt->max_iter), kEltThreads, 0, s>>>(tr_true, opt->max_iter, NAN);
+  MPB_LAUNCHED(h);
+  if (!opt->has_x0) MPB_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * A->n, s));
+  const unsigned nt = static_cast<unsigned>(plan->ntiles);
+  if (opt->has_x0) {
+    k_resid<true><<<nt, kTileThreads, 0, s>>>(A->row_ptr, A->col_idx, A->val64, plan->d_tile_lo, b, x, w.r, w.part,
+                                              w.st, 0);
+  } else {
+    k_resid<false><<<nt, kTileThreads, 0, s>>>(A->row_ptr, A->col_idx, A->val64, plan->d_tile_lo, b, nullptr, w.r,
+                                               w.part, w.st, 0);
+  }
+  MPB_LAUNCHED(h);
+  k_scalar<<<1, kFinThreads, 0, s>>>(kStepR0, w.part, plan->ntiles, w.st, tr_relres, tr_true, (int *)tr_branch,
+                                     tr_time);
+  MPB_LAUNCHED(h);
+  MPB_CUDA(cudaMemcpyAsync(h->h_state, w.st, sizeof(SolverState), cudaMemcpyDeviceToHost, s));
+  MPB_CUDA(cudaStreamSynchronize(s));
+  res->r0_norm = h->h_state->r0;
+  if (h->h_state->done) {  // ||r0|| == 0 (solver.py:128-130)
+    res->converged = 1;
+    MPB_CUDA(cudaEventRecord(h->ev_out, s));
+    MPB_CUDA(cudaStreamWaitEvent(h->user, h->ev_out, 0));
+    res->kernel_launches = h->launches - launches0;
+    return MPB_OK;
+  }
+
+  // capture G iterations once (cached across solves with the same buffers)
+  const int G = opt->graph_iters > 0 ? opt->graph_iters : kDefaultGraphIters;
+  GraphKey key;
+  std::memset(&key, 0, sizeof(key));
+  key.plan = plan;
+  key.rp = A->row_ptr;
+  key.ci = A->col_idx;
+  key.v64 = A->val64;
+  key.v32 = A->val32;
+  key.b = b;
+  key.x = x;
+  key.trr = tr_relres;
+  key.trt = tr_true;
+  key.trb = tr_branch;
+  key.trw = tr_time;
+  key.ws = workspace;
+  key.kind = opt->kind;
+  key.k = opt->k;
+  key.t = opt->t;
+  key.iters = G;
+  key.stride = opt->true_stride;
+  key.n = A->n;
+  if (!(h->have_graph && h->gkey == key)) {
+    if (h->have_graph) {
+      cudaGraphExecDestroy(h->gexec);
+      h->have_graph = false;
+    }
+    const int64_t l0 = h->launches;
+    MPB_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    int crc = MPB_OK;
+    for (int i = 0; i < G && crc == MPB_OK; i++) {
+      crc = enqueue_iteration(h, s, plan, A, opt, w, tr_relres, tr_true, tr_branch, tr_time);
+      if (crc == MPB_OK) crc = enqueue_tail(h, s, plan, A, opt, w, b, x, tr_relres, tr_true, tr_branch, tr_time);
+    }
+    cudaGraph_t graph = nullptr;
+    cudaError_t ce = cudaStreamEndCapture(s, &graph);
+    if (crc != MPB_OK) {
+      if (graph) cudaGraphDestroy(graph);
+      return crc;
+    }
+    MPB_CUDA(ce);
+    ce = cudaGraphInstantiate(&h->gexec, graph, 0);
+    cudaGraphDestroy(graph);
+    MPB_CUDA(ce);
+    h->graph_kernels = h->launches - l0;
+    h->launches = l0;  // captured, not launched
+    h->have_graph = true;
+    h->gkey = key;
+  }
+  k_scalar<<<1, kFinThreads, 0, s>>>(kStepStart, w.part, 0, w.st, tr_relres, tr_true, (int *)tr_branch, tr_time);
+  MPB_LAUNCHED(h);
+  MPB_CUDA(cudaEventRecord(h->ev_t0, s));
+  for (;;) {
+    MPB_CUDA(cudaGraphLaunch(h->gexec, s));
+    h->launches += h->graph_kernels;
+    MPB_CUDA(cudaMemcpyAsync(h->h_state, w.st, sizeof(SolverState), cudaMemcpyDeviceToHost, s));
+    MPB_CUDA(cudaStreamSynchronize(s));
+    if (h->h_state->done) break;
+  }
+  MPB_CUDA(cudaEventRecord(h->ev_t1, s));
+  const SolverState st = *h->h_state;
+  if (st.error == kOk) {
+    k_resid<true><<<nt, kTileThreads, 0, s>>>(A->row_ptr, A->col_idx, A->val64, plan->d_tile_lo, b, x, nullptr,
+                                              w.part, w.st, 0);
+    MPB_LAUNCHED(h);
+    k_scalar<<<1, kFinThreads, 0, s>>>(kStepFinal, w.part, plan->ntiles, w.st, tr_relres, tr_true,
+                                       (int *)tr_branch, tr_time);
+    MPB_LAUNCHED(h);
+    MPB_CUDA(cudaMemcpyAsync(h->h_state, w.st, sizeof(SolverState), cudaMemcpyDeviceToHost, s));
+  }
+  MPB_CUDA(cudaStreamSynchronize(s));
+  float ms = 0.f;
+  MPB_CUDA(cudaEventElapsedTime(&ms, h->ev_t0, h->ev_t1));
+  const SolverState fin = *h->h_state;
+  res->converged = fin.converged;
+  res->error = fin.error;
+  res->iterations = fin.error ? fin.err_it : fin.last_it;
+  res->err_iteration = fin.error ? fin.err_it : 0;
+  res->err_value = fin.err_val;
+  res->final_true_relres = fin.error ? NAN : fin.final_true;
+  res->overflow_count = static_cast<int64_t>(fin.ovf_count);
+  res->overflow_index = fin.ovf_count ? fin.ovf_first : -1;
+  if (fin.error == kNarrowOverflow && fin.ovf_count) {  // the offending r entry
+    MPB_CUDA(cudaMemcpy(&res->err_value, w.r + fin.ovf_first, sizeof(double), cudaMemcpyDeviceToHost));
+  }
+  res->device_seconds = 1e-3 * ms;
+  res->kernel_launches = h->launches - launches0;
+  MPB_CUDA(cudaEventRecord(h->ev_out, s));
+  MPB_CUDA(cudaStreamWaitEvent(h->user, h->ev_out, 0));
+  return MPB_OK;
+}
+
+int mpb_true_relres(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, const double *x, const double *b,
+                    double r0_norm, double *h_out) {
+  int rc = check_csr(A);
+  if (rc) return rc;
+  if (!h || !plan || !x || !b || !h_out || !A->val64) return MPB_ERR_ARG;
+  if (plan->n != A->n) return MPB_ERR_PARTITION;
+  const int64_t nt = plan->ntiles;
+  rc = ensure_scratch(h, al256(sizeof(double) * (nt + 1)) + 256);
+  if (rc) return rc;
+  double *part = static_cast<double *>(h->scratch);
+  double *out = reinterpret_cast<double *>(static_cast<char *>(h->scratch) + al256(sizeof(double) * (nt + 1)));
+  k_resid<true><<<static_cast<unsigned>(nt), kTileThreads, 0, h->user>>>(A->row_ptr, A->col_idx, A->val64,
+                                                                       plan->d_tile_lo, b, x, nullptr, part,
+                                                                       nullptr, 0);
+  MPB_LAUNCHED(h);
+  k_fin<double><<<1, kFinThreads, 0, h->user>>>(part, nt, out);
+  MPB_LAUNCHED(h);
+  double v;
+  MPB_CUDA(cudaMemcpyAsync(&v, out, sizeof(double), cudaMemcpyDeviceToHost, h->user));
+  MPB_CUDA(cudaStreamSynchronize(h->user));
+  *h_out = std::sqrt(v) / r0_norm;
+  return MPB_OK;
+}
+

@@ -1,0 +1,186 @@
+// mpbjac_device.cuh — device helpers shared by the libmpbjac kernels.
+//
+// Built with --fmad=false (see Makefile): every a*b+c below is two IEEE
+// roundings, exactly like the reference's numba/numpy arithmetic
+// (pkg/src/mpcg/kernels_numba.py:1-13: fastmath off).  Division and sqrt are
+// the IEEE-rounded defaults (no -use_fast_math).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/mpbjac_order.h"
+
+namespace mpb {
+
+constexpr int kTileThreads = MPB_TILE_THREADS;
+constexpr int kTileRows = MPB_TILE_MAX_ROWS;
+constexpr int kRowsPerThread = kTileRows / kTileThreads;
+constexpr int kFinThreads = MPB_FIN_THREADS;
+static_assert(kTileRows % kTileThreads == 0, "tile rows must be a multiple of threads");
+
+// ---------------------------------------------------------------------------
+// solver state (device resident; one per solve)
+// ---------------------------------------------------------------------------
+enum SolveError {
+  kOk = 0,
+  kBreakdown = 1,
+  kIndefPrecond = 2,
+  kIndefMatrix = 3,
+  kNonFinite = 4,
+  kNarrowOverflow = 5
+};
+
+struct SolverState {
+  // scalars of the recurrence (solver.py:133-169)
+  double rho, rho_prev, pq, alpha, beta, rnorm, relres, r0;
+  double res_tol, adp_tol;
+  double final_true;
+  double err_val;
+  long long it;       // iteration in progress (1-based)
+  long long last_it;  // iteration whose trace entry was written last
+  long long cap;
+  long long stride;
+  long long err_it;
+  unsigned long long t0_ns;
+  unsigned long long ovf_count;
+  long long ovf_first;
+  int kind;
+  int branch;  // 0 high (fp64 instance), 1 low (fp32 instance)
+  int first;   // p is None (solver.py:150-151)
+  int done;
+  int converged;
+  int error;
+  int true_pending;
+  int pad;
+};
+
+// ---------------------------------------------------------------------------
+// reductions in the order fixed by include/mpbjac_order.h
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double warp_bfly(double v) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ float warp_bfly(float v) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Steps 2-3: per-warp butterfly then warp 0 butterflies the warp sums padded
+// with +0 to 32 lanes.  Result valid in thread 0.  ws: 32 entries of smem.
+template <int NT, typename R>
+__device__ __forceinline__ R block_tree(R v, R *ws) {
+  static_assert(NT % 32 == 0 && NT <= 1024, "block size");
+  v = warp_bfly(v);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) ws[warp] = v;
+  __syncthreads();
+  R r = R(0);
+  if (warp == 0) {
+    r = lane < NT / 32 ? ws[lane] : R(0);
+    r = warp_bfly(r);
+  }
+  return r;
+}
+
+// Global sum of tile partials, steps 1-3 with kFinThreads lanes.  Must be
+// called by all kFinThreads threads; result valid in thread 0.
+__device__ __forceinline__ double fin_sum(const double *part, long long count, double *ws) {
+  double acc = 0.0;
+  for (long long i = threadIdx.x; i < count; i += kFinThreads) acc = __dadd_rn(acc, part[i]);
+  return block_tree<kFinThreads>(acc, ws);
+}
+
+// ---------------------------------------------------------------------------
+// TMA bulk copies (cp.async.bulk, 1-D) + mbarrier
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+// global -> shared bulk copy; dst/src 16-B aligned, bytes % 16 == 0
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Staged byte window of elements [e0, e1) of an array: 16-B aligned outward.
+// A 16-B granule never straddles a page, so the outward rounding never faults.
+struct Window {
+  uintptr_t g0;
+  uint32_t bytes;
+  uint32_t skew;  // byte offset of element e0 inside the window
+};
+template <typename E>
+__device__ __forceinline__ Window window_of(const E *base, long long e0, long long e1) {
+  uintptr_t a0 = reinterpret_cast<uintptr_t>(base + e0);
+  uintptr_t a1 = reinterpret_cast<uintptr_t>(base + e1);
+  Window w;
+  w.g0 = a0 & ~uintptr_t(15);
+  w.bytes = static_cast<uint32_t>(((a1 + 15) & ~uintptr_t(15)) - w.g0);
+  w.skew = static_cast<uint32_t>(a0 - w.g0);
+  return w;
+}
+
+// host+device: bytes of a staging region for cap_e elements of size es
+__host__ __device__ constexpr uint32_t region_bytes(int cap_e, int es) {
+  return ((static_cast<uint32_t>(cap_e) * es + 32 + 15) / 16) * 16;
+}
+
+template <typename T>
+__device__ __forceinline__ T narrow_or_copy(double v);
+template <>
+__device__ __forceinline__ float narrow_or_copy<float>(double v) {
+  return __double2float_rn(v);
+}
+template <>
+__device__ __forceinline__ double narrow_or_copy<double>(double v) {
+  return v;
+}
+
+// IEEE ops without contraction (belt and braces on top of --fmad=false)
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float div_rn(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ double div_rn(double a, double b) { return __ddiv_rn(a, b); }
+
+}  // namespace mpb

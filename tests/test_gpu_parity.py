@@ -1,0 +1,270 @@
+"""GPU parity: libmpbjac.so against the reference's golden fixtures and the
+CPU oracle, through the drop-in API (which calls the C-ABI).
+
+Bit-exact expectations (thread-per-row, no FMA, IEEE division):
+  spmv, BjacPreconditioner.apply (fp64 and fp32, every partition regime,
+  every (k, t)), fmp_apply, inner_apply, narrowing;  whole PCG solves vs the
+  oracle's device-order replay (x, trace, branches, iteration count).
+Band expectations: PCG iteration counts vs the reference's own sequential
+dot order within max(2, envelope).
+"""
+import numpy as np
+import pytest
+
+from conftest import dense_to_csr, golden_cases, random_spd_csr
+
+pytestmark = pytest.mark.gpu
+
+KT = ((1, 1), (1, 2), (2, 2), (2, 3), (3, 2))
+POLICIES = ("uniform", "fixed-low", "adaptive-hl:10", "adaptive-lh:1e-5", "adaptive-hl:1e-3")
+
+
+def _parts(g, name):
+    return sorted({k.split("/")[1] for k in g if k.startswith(name + "/")
+                   and k.endswith("/offsets")} - {"pcg"})
+
+
+def _matrix(g, name):
+    from paper_2407_15973_b200 import SparseMatrix
+    rp = g[f"{name}/row_ptr"]
+    return SparseMatrix(rp.size - 1, rp.size - 1, rp, g[f"{name}/col_idx"], g[f"{name}/values"])
+
+
+def test_spmv_bitwise(golden, cuda):
+    from paper_2407_15973_b200 import Precision, convert_precision, spmv
+    for name in golden_cases(golden):
+        A = _matrix(golden, name)
+        x = np.cos(np.arange(A.n) * 0.37)
+        np.testing.assert_array_equal(spmv(A, x), golden[f"{name}/spmv64"])
+        A32 = convert_precision(A, Precision.F32)
+        np.testing.assert_array_equal(spmv(A32, x.astype(np.float32)), golden[f"{name}/spmv32"])
+
+
+def test_bjac_apply_bitwise_all_regimes(golden, cuda):
+    """Small blocks (fused smem kernel), nb=32 / nb=2 / nb=1 large blocks
+    (multi-launch path), 96-row 3-T blocks; fp64 and fp32; k,t up to 3."""
+    from paper_2407_15973_b200 import Precision
+    from paper_2407_15973_b200.bjac import BlockPartition, setup
+    n_checked = 0
+    for name in golden_cases(golden):
+        A = _matrix(golden, name)
+        r = golden[f"{name}/r"]
+        for pname in _parts(golden, name):
+            part = BlockPartition(golden[f"{name}/{pname}/offsets"])
+            for k, t in KT:
+                for prec in (Precision.F64, Precision.F32):
+                    P = setup(A, k=k, t=t, precision=prec, partition=part)
+                    z = P.apply(r.astype(prec.dtype))
+                    assert z.dtype == prec.dtype
+                    np.testing.assert_array_equal(
+                        z, golden[f"{name}/{pname}/apply_{prec}_k{k}t{t}"],
+                        err_msg=f"{name}/{pname} {prec} k={k} t={t}")
+                    n_checked += 1
+    assert n_checked > 100
+
+
+def test_fmp_apply_bitwise(golden, cuda):
+    from paper_2407_15973_b200.bjac import BlockPartition
+    from paper_2407_15973_b200.policies import PrecisionPolicy, build_mixed, fmp_apply
+    for name in golden_cases(golden):
+        A = _matrix(golden, name)
+        r = golden[f"{name}/r"]
+        for pname in _parts(golden, name):
+            part = BlockPartition(golden[f"{name}/{pname}/offsets"])
+            mp = build_mixed(A, PrecisionPolicy.parse("fixed-low"), k=2, t=2, partition=part)
+            z, br = fmp_apply(mp, r)
+            assert br == "low" and z.dtype == np.float64
+            np.testing.assert_array_equal(z, golden[f"{name}/{pname}/fmp_k2t2"])
+
+
+def test_inner_apply_matches_apply_rows(cuda):
+    from paper_2407_15973_b200.bjac import setup
+    rng = np.random.default_rng(21)
+    A = random_spd_csr(30, 0.3, rng)
+    P = setup(A, nb=4, k=1, t=3)
+    r = rng.standard_normal(30)
+    z = P.apply(r)
+    for b in range(P.partition.num_blocks):
+        s, e = P.partition.block_range(b)
+        np.testing.assert_array_equal(P.inner_apply(b, r[s:e]), z[s:e])
+
+
+def test_hand_derived_known_answers(cuda):
+    """pkg/tests/test_bjac.py:116-128 and :155-163."""
+    from paper_2407_15973_b200.bjac import setup
+    A = dense_to_csr([[2.0, -1.0], [-1.0, 2.0]])
+    np.testing.assert_array_equal(setup(A, nb=1, k=1, t=2).apply(np.ones(2)), [0.75, 0.75])
+    np.testing.assert_array_equal(setup(A, nb=1, k=2, t=2).apply(np.ones(2)), [0.9375, 0.9375])
+    d = np.array([2.0, 0.5, 8.0, 0.25])
+    D = dense_to_csr(np.diag(d))
+    r = np.array([1.3, -0.7, 2.9, 0.11])
+    for k, t in ((1, 3), (2, 2), (3, 1)):
+        np.testing.assert_array_equal(setup(D, nb=2, k=k, t=t).apply(r), r / d)
+
+
+def test_point_jacobi_is_exact_division(cuda):
+    """k = t = 1 returns r / diag bit for bit (test_acceptance.py:110-129)."""
+    from paper_2407_15973_b200 import Precision
+    from paper_2407_15973_b200.bjac import setup
+    for seed in range(6):
+        rng = np.random.default_rng(seed)
+        n = int(rng.integers(5, 40))
+        A = random_spd_csr(n, 0.3, rng)
+        for prec in (Precision.F64, Precision.F32):
+            P = setup(A, nb=min(4, n), k=1, t=1, precision=prec)
+            r = rng.standard_normal(n).astype(prec.dtype)
+            np.testing.assert_array_equal(P.apply(r), r / A.diagonal().astype(prec.dtype))
+
+
+def test_linearity_power_of_two(cuda):
+    from paper_2407_15973_b200.bjac import setup
+    from paper_2407_15973_b200.policies import PrecisionPolicy, build_mixed, fmp_apply
+    rng = np.random.default_rng(3)
+    A = random_spd_csr(25, 0.3, rng)
+    P = setup(A, nb=5, k=2, t=2)
+    r = rng.standard_normal(25)
+    np.testing.assert_array_equal(P.apply(4.0 * r), 4.0 * P.apply(r))
+    mp = build_mixed(A, PrecisionPolicy.parse("fixed-low"), nb=5)
+    np.testing.assert_array_equal(fmp_apply(mp, 8.0 * r)[0], 8.0 * fmp_apply(mp, r)[0])
+
+
+def test_setup_errors_match_reference(cuda):
+    from paper_2407_15973_b200 import NarrowingOverflowError, Precision, SparseMatrix
+    from paper_2407_15973_b200.bjac import BlockPartition, setup
+    with pytest.raises(ValueError, match="square"):
+        setup(SparseMatrix.from_coo(2, 3, [0, 1], [0, 1], [1.0, 1.0]), nb=1)
+    with pytest.raises(ValueError, match="row 1"):
+        setup(SparseMatrix.from_coo(2, 2, [0, 1], [0, 0], [1.0, 1.0]), nb=1)
+    with pytest.raises(ValueError, match="zero diagonal entry at row 1"):
+        setup(SparseMatrix(2, 2, [0, 1, 2], [0, 1], np.array([1.0, 0.0])), nb=1)
+    with pytest.raises(ValueError, match="underflows"):
+        setup(dense_to_csr([[1e-50, 0.0], [0.0, 1.0]]), nb=1, precision=Precision.F32)
+    with pytest.raises(ValueError, match="split"):
+        setup(dense_to_csr(np.eye(3)), nb=4)
+    with pytest.raises(ValueError, match="sweep"):
+        setup(dense_to_csr(np.eye(3)), nb=1, k=0)
+    with pytest.raises(ValueError, match="partition"):
+        setup(dense_to_csr(np.eye(3)), partition=BlockPartition([0, 2]))
+    with pytest.raises(NarrowingOverflowError):
+        setup(dense_to_csr([[1.0, 1e40], [1e40, 1.0]]), nb=1, precision=Precision.F32)
+
+
+def test_narrowing_and_norms(cuda, oracle):
+    from paper_2407_15973_b200 import NarrowingOverflowError, Precision, convert_precision, norm2, dot
+    with pytest.raises(NarrowingOverflowError, match="index 1"):
+        convert_precision(np.array([1.0, 1e39]), Precision.F32)
+    out = convert_precision(np.array([np.inf, -np.inf, np.nan]), Precision.F32)
+    assert np.isinf(out[0]) and np.isinf(out[1]) and np.isnan(out[2])
+    assert convert_precision(np.array([1.0 + 2.0 ** -24]), Precision.F32)[0] == np.float32(1.0)
+    assert norm2(np.array([3.0, 4.0])) == 5.0
+    x = np.full(4, 1e20, dtype=np.float32)
+    assert norm2(x) == pytest.approx(2e20, rel=1e-6)
+    rng = np.random.default_rng(5)
+    a, b = rng.standard_normal(100_000), rng.standard_normal(100_000)
+    tiles = np.append(np.arange(0, a.size, 512), a.size)
+    assert dot(a, b) == oracle.tree_dot(tiles, a, b)       # device order, bitwise
+    assert dot(a, b) == pytest.approx(float(np.dot(a, b)), rel=1e-12)
+
+
+def _solve_both(A, b, offs, pol, k, t, tol, oracle, stride=0, x0=None):
+    from paper_2407_15973_b200.bjac import BlockPartition
+    from paper_2407_15973_b200.policies import PrecisionPolicy, build_mixed
+    from paper_2407_15973_b200.solver import SolveConfig, pcg_solve
+    pp = PrecisionPolicy.parse(pol)
+    mp = build_mixed(A, pp, k=k, t=t, partition=BlockPartition(offs))
+    rep = pcg_solve(A, b, mp, SolveConfig(res_tol=tol, record_true_residual_every=stride), x0=x0)
+    orc = oracle.pcg_solve(A.row_ptr, A.col_idx, A.values, b, offs, kind=pp.kind.value,
+                           adp_tol=pp.adp_tol, k=k, t=t, res_tol=tol, stride=stride,
+                           order="device", x0=x0)
+    return rep, orc
+
+
+@pytest.mark.parametrize("pol", POLICIES)
+def test_pcg_bitwise_vs_oracle_and_band_vs_reference(golden, cuda, oracle, pol):
+    for name in golden_cases(golden):
+        A = _matrix(golden, name)
+        key = f"{name}/pcg/{pol}"
+        tol, k, t = golden[f"{key}/meta"]
+        rep, orc = _solve_both(A, golden[f"{name}/b"], golden[f"{name}/pcg/offsets"], pol,
+                               int(k), int(t), float(tol), oracle, stride=5)
+        # bit for bit against the device-order replay
+        assert rep.iterations == orc["iterations"], name
+        np.testing.assert_array_equal(rep.x, orc["x"], err_msg=name)
+        np.testing.assert_array_equal([r.implicit_relres for r in rep.trace], orc["relres"])
+        assert [r.branch for r in rep.trace] == orc["branch"]
+        assert rep.final_true_relres == orc["final_true_relres"]
+        tr = np.array([np.nan if r.true_relres is None else r.true_relres for r in rep.trace])
+        np.testing.assert_array_equal(tr, orc["true_relres"])
+        # within the band of the reference's own (sequential) run
+        ref_it = int(golden[f"{key}/iterations"])
+        assert abs(rep.iterations - ref_it) <= 2, (name, rep.iterations, ref_it)
+        assert rep.converged
+
+
+def test_pcg_x0_and_deterministic_rerun(cuda, oracle):
+    from paper_2407_15973_b200 import problems
+    cs = problems.make_config("c3", 16)
+    offs = np.append(np.arange(0, cs.A.n, 64), cs.A.n)
+    x0 = np.sin(np.arange(cs.A.n))
+    rep1, orc = _solve_both(cs.A, cs.b, offs, "adaptive-lh:1e-6", 2, 2, 1e-10, oracle, x0=x0)
+    rep2, _ = _solve_both(cs.A, cs.b, offs, "adaptive-lh:1e-6", 2, 2, 1e-10, oracle, x0=x0)
+    np.testing.assert_array_equal(rep1.x, orc["x"])
+    np.testing.assert_array_equal(rep1.x, rep2.x)
+    assert rep1.iterations == rep2.iterations == orc["iterations"]
+
+
+def test_pcg_error_paths(cuda):
+    from paper_2407_15973_b200.policies import PrecisionPolicy, build_mixed
+    from paper_2407_15973_b200.solver import (BreakdownError, IndefiniteOperatorError,
+                                              NonFiniteResidualError, SolveConfig, pcg_solve)
+    U = PrecisionPolicy.parse("uniform")
+    A = dense_to_csr(np.diag([1e308, 1e308]))
+    with pytest.raises(BreakdownError):
+        pcg_solve(A, np.array([1e-150, 1e-150]), build_mixed(A, U, nb=1, k=1, t=1))
+    A = dense_to_csr(np.diag([1.0, -1.0]))
+    with pytest.raises(IndefiniteOperatorError, match="preconditioner"):
+        pcg_solve(A, np.array([0.0, 1.0]), build_mixed(A, U, nb=1, k=1, t=1))
+    A = dense_to_csr([[1.0, 2.0], [2.0, 1.0]])
+    with pytest.raises(IndefiniteOperatorError, match="matrix"):
+        pcg_solve(A, np.array([1.0, -1.0]), build_mixed(A, U, nb=1, k=1, t=1))
+    A = dense_to_csr([[1e-300]])
+    with pytest.raises((NonFiniteResidualError, IndefiniteOperatorError)):
+        pcg_solve(A, np.array([1e300]), build_mixed(A, U, nb=1, k=1, t=1))
+    A = dense_to_csr(np.eye(3))
+    rep = pcg_solve(A, np.zeros(3), build_mixed(A, U, nb=1))
+    assert rep.converged and rep.iterations == 0 and rep.trace == []
+    A = dense_to_csr(np.eye(6))
+    rep = pcg_solve(A, np.arange(1.0, 7.0), build_mixed(A, U, nb=2))
+    assert rep.converged and rep.iterations == 1
+    np.testing.assert_array_equal(rep.x, np.arange(1.0, 7.0))
+    assert rep.final_true_relres == 0.0 and rep.trace[0].true_relres == 0.0
+    rng = np.random.default_rng(43)
+    A = random_spd_csr(40, 0.25, rng)
+    rep = pcg_solve(A, rng.standard_normal(40), build_mixed(A, U, nb=4), SolveConfig(max_iter=2))
+    assert not rep.converged and rep.iterations == 2 and rep.final_true_relres > 0
+
+
+def test_pcg_narrowing_overflow_raises(cuda):
+    from paper_2407_15973_b200 import NarrowingOverflowError
+    from paper_2407_15973_b200.policies import PrecisionPolicy, build_mixed
+    from paper_2407_15973_b200.solver import pcg_solve
+    A = dense_to_csr(np.eye(4))
+    mp = build_mixed(A, PrecisionPolicy.parse("fixed-low"), nb=2)
+    with pytest.raises(NarrowingOverflowError, match="first at index 2"):
+        pcg_solve(A, np.array([1.0, 2.0, 1e39, 1e39]), mp)
+
+
+def test_tensor_io_stays_on_device(cuda):
+    import torch
+    from paper_2407_15973_b200 import problems
+    from paper_2407_15973_b200.bjac import BlockPartition
+    from paper_2407_15973_b200.policies import PrecisionPolicy, build_mixed
+    from paper_2407_15973_b200.solver import pcg_solve
+    cs = problems.make_config("c1", 16)
+    mp = build_mixed(cs.A, PrecisionPolicy.parse("fixed-low"),
+                     partition=BlockPartition.fixed_size(cs.A.n, 64))
+    bt = torch.from_numpy(cs.b).cuda()
+    rep = pcg_solve(cs.A, bt, mp)
+    assert isinstance(rep.x, torch.Tensor) and rep.x.is_cuda
+    rep2 = pcg_solve(cs.A, cs.b, mp)
+    np.testing.assert_array_equal(rep.x.cpu().numpy(), rep2.x)
