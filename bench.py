@@ -1,0 +1,350 @@
+#!/usr/bin/env python
+"""Benchmark: PCG time-to-solution of the mixed-precision BJAC-PCG hot path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2]
+                    [--policy fixed-low] [--impl b200|reference]
+
+One step = one complete ``pcg_solve`` to rtol (default: BASELINE.json
+configs[1] = C2, 128^3 lognormal diffusion, fixed-low fMP-BJAC, 64-row
+blocks, k = t = 2, rtol 1e-10).  ``value`` is whole-job solves per second
+with b already resident in HBM (device-timed with CUDA events, max over
+ranks); ``e2e`` is the same through the public API with pinned host b and a
+host read of x every step.  The line also carries the per-kernel roofline
+(live CUDA-event timings of each kernel of an iteration, algorithmic bytes
+of DESIGN.md §4), the CPU baseline (the oracle restatement of the
+reference, 1 thread, bounded sample), clocks sampled during the timed
+region and the number of kernels launched.
+
+With --gpus N under torchrun, every rank solves its own C2 replica
+("replicas": the single-system z-slab sharding is a separate path, see
+DESIGN.md §6); ``--impl reference`` times the reference's CPU
+implementation (the oracle port, all host threads) on rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+#: iterations of the reference-order solve to rtol (oracle, sequential dot
+#: order, measured in the build container; the GPU run reports its own)
+REF_ITERS = {"c1": 63, "c2": 386}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--policy", default=None)
+    ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
+    ap.add_argument("--cpu-iters", type=int, default=40,
+                    help="iterations of the bounded CPU-baseline sample")
+    ap.add_argument("--ref-iters", type=int, default=60,
+                    help="iterations per --impl reference step")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-reps", type=int, default=20)
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        busy = [s for s in sm if mx and s > 0.5 * mx] or sm
+        return {"sm_mhz": float(np.median(busy)) if busy else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def kernel_bytes(Z, N, branch, ntiles):
+    """Algorithmic bytes per launch: every array streamed
+    once, gathered vector entries counted once, int32 indices."""
+    if branch == "low":
+        first, mid, last = 8 * Z + 16 * N, 8 * Z + 20 * N, 8 * Z + 20 * N
+        spmv = 12 * Z + 28 * N + 4 * N
+    else:
+        first, mid, last = 12 * Z + 20 * N, 12 * Z + 28 * N, 12 * Z + 28 * N
+        spmv = 12 * Z + 28 * N + 8 * N
+    return {"bjac_first": first, "bjac_middle": mid, "bjac_last": last,
+            "spmv_pq": spmv, "update": 48 * N, "scalar": 8 * ntiles}
+
+
+def cpu_sample(cs, part, policy, iters, threads, order="sequential"):
+    """Oracle solve capped at `iters` iterations; returns seconds."""
+    from oracle import oracle as O
+    O.build()
+    O.set_threads(threads)
+    kind, _, tol = policy.partition(":")
+    t0 = time.perf_counter()
+    out = O.pcg_solve(cs.A.row_ptr, cs.A.col_idx, cs.A.values, cs.b, part.offsets,
+                      kind=kind, adp_tol=float(tol) if tol else None, k=cs.k, t=cs.t,
+                      res_tol=cs.res_tol, max_iter=iters, order=order)
+    dt = time.perf_counter() - t0
+    return dt, out["iterations"]
+
+
+def metric_name(cfg):
+    return (f"PCG solves/s to rtol {cfg.res_tol:g} (time-to-solution), "
+            f"{cfg.name.upper()} {cfg.n}^3")
+
+
+def config_dict(cs, part, policy, extra=None):
+    d = {"workload": f"{cs.name.upper()}: {cs.note}, n={cs.n} (N={cs.A.n}, nnz={cs.A.nnz}), "
+                     f"{cs.block_rows}-row BJAC blocks, policy {policy}, k={cs.k} t={cs.t}, "
+                     f"rtol {cs.res_tol:g}, x0=0",
+         "n_rows": cs.A.n, "nnz": cs.A.nnz, "blocks": part.num_blocks,
+         "policy": policy, "k": cs.k, "t": cs.t, "res_tol": cs.res_tol,
+         "l2": "inputs larger than L2 (>= 650 MB streamed per iteration vs 126 MB L2); no flush"}
+    if extra:
+        d.update(extra)
+    return d
+
+
+def run_reference(args, world, rank):
+    from paper_2407_15973_b200 import problems
+    from paper_2407_15973_b200.bjac import BlockPartition
+    if rank != 0:
+        return
+    cs = problems.make_config(args.config)
+    policy = args.policy or cs.policies[0]
+    part = BlockPartition.fixed_size(cs.A.n, cs.block_rows)
+    threads = os.cpu_count() or 1
+    it_full = REF_ITERS.get(cs.name)
+    for _ in range(args.warmup):
+        cpu_sample(cs, part, policy, args.ref_iters, threads)
+    times = []
+    for _ in range(args.steps):
+        dt, its = cpu_sample(cs, part, policy, args.ref_iters, threads)
+        times.append(dt / its)
+    per_it = float(np.mean(times))
+    if it_full is None:
+        it_full = args.ref_iters
+    solve_s = per_it * it_full
+    value = 1.0 / solve_s
+    sample = (f"{cs.name.upper()} solve capped at {args.ref_iters} iterations per step "
+              f"(oracle restatement of the reference, reference dot order, {threads} OpenMP "
+              f"threads), extrapolated to the {it_full}-iteration solve to rtol")
+    line = {"impl": "reference", "metric": metric_name(cs), "value": value,
+            "unit": "solve/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * solve_s,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64 CG / f32 preconditioner", "data": "synthetic (seeded SplitMix64)",
+            "config": config_dict(cs, part, policy, {"parallelism": "1 CPU process"}),
+            "cpu_baseline": {"value": value, "unit": "solve/s", "cores": threads,
+                             "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": "solve/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_b200(args, world, rank, local):
+    import torch
+    from paper_2407_15973_b200 import _lib, problems
+    from paper_2407_15973_b200.bjac import BlockPartition
+    from paper_2407_15973_b200.policies import PrecisionPolicy, build_mixed
+    from paper_2407_15973_b200.solver import SolveConfig, pcg_solve, profile_iteration
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cs = problems.make_config(args.config)
+    policy = args.policy or cs.policies[0]
+    part = BlockPartition.fixed_size(cs.A.n, cs.block_rows)
+    pp = PrecisionPolicy.parse(policy)
+    mp = build_mixed(cs.A, pp, k=cs.k, t=cs.t, partition=part)
+    cfg = SolveConfig(res_tol=cs.res_tol)
+    b_dev = torch.from_numpy(cs.b).cuda()
+    h = _lib.Handle.get(local)
+
+    for _ in range(max(args.warmup, 1)):
+        rep = pcg_solve(cs.A, b_dev, mp, cfg)
+    # ---- device-resident timed region --------------------------------------
+    sampler = ClockSampler(local)
+    sampler.start()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches = 0
+    iters = []
+    ev0.record()
+    for _ in range(args.steps):
+        rep = pcg_solve(cs.A, b_dev, mp, cfg)
+        launches += rep.stats["kernel_launches"]
+        iters.append(rep.iterations)
+    ev1.record()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    clocks = sampler.stop()
+    ms = ev0.elapsed_time(ev1)
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    value = world * args.steps / (ms / 1e3)
+
+    # ---- end to end through the public API, host buffers -------------------
+    b_pin = torch.from_numpy(cs.b).pin_memory()
+    x_pin = torch.empty(cs.A.n, dtype=torch.float64).pin_memory()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    d2h = 0
+    for _ in range(args.steps):
+        r2 = pcg_solve(cs.A, b_pin, mp, cfg)
+        x_pin.copy_(r2.x, non_blocking=True)
+        d2h += 8 * cs.A.n + r2.iterations * (3 * 8 + 4)
+    e1.record()
+    torch.cuda.synchronize()
+    ems = e0.elapsed_time(e1)
+    if dist is not None:
+        t = torch.tensor([ems], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ems = float(t.item())
+    e2e = {"value": world * args.steps / (ems / 1e3), "unit": "solve/s",
+           "h2d_bytes_per_step": 8 * cs.A.n, "d2h_bytes_per_step": d2h // args.steps,
+           "ms_per_step": ems / args.steps}
+
+    # ---- per-kernel roofline (live CUDA events on the solve stream) --------
+    branch = rep.trace[-1].branch if rep.trace else "low"
+    prof = profile_iteration(cs.A, mp, config=cfg, branch=branch, reps=args.profile_reps)
+    ntiles = mp.any.plan.ntiles
+    kb = kernel_bytes(cs.A.nnz, cs.A.n, branch, ntiles)
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            peaks = json.load(fh)
+    except OSError:
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    kernels = {}
+    for name in ("bjac_first", "bjac_last", "spmv_pq", "update"):
+        t_ms = prof[name]
+        if t_ms <= 0:
+            continue
+        gbs = kb[name] / (t_ms * 1e-3) / 1e9
+        kernels[name] = {"ms": round(t_ms, 5), "bytes": kb[name], "gbs": round(gbs, 1),
+                         "frac": round(gbs / peak, 4)}
+    kernels["scalar"] = {"ms": round(prof["scalar"], 5), "launches_per_iter": 3}
+    per_iter_share = {k: v["ms"] * (3 if k == "scalar" else 1) for k, v in kernels.items()}
+    dom = max((k for k in kernels if k != "scalar"), key=lambda k: per_iter_share[k])
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as fh:
+            traffic = json.load(fh).get(cs.name, {}).get(dom)
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": kernels[dom]["gbs"],
+                "peak": peak, "unit": "GB/s", "frac": kernels[dom]["frac"],
+                "traffic": traffic, "peak_source": peak_src,
+                "bytes_per_launch": kb[dom]}
+    it_med = int(np.median(iters))
+    iter_bytes = (kb["bjac_first"] + max(cs.k - 2, 0) * kb["bjac_middle"]
+                  + (kb["bjac_last"] if cs.k > 1 else 0) + kb["spmv_pq"] + kb["update"])
+    solve_gbs = iter_bytes * it_med / (ms_per_step * 1e-3) / 1e9
+
+    # ---- CPU baseline (rank 0, N=1 only) -----------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        dt, its = cpu_sample(cs, part, policy, args.cpu_iters, 1)
+        it_full = REF_ITERS.get(cs.name, it_med)
+        cpu_solve = dt / its * it_full
+        cpu = {"value": 1.0 / cpu_solve, "unit": "solve/s", "cores": 1, "kind": "port",
+               "sample": f"{cs.name.upper()} solve capped at {its} iterations "
+                         f"({dt:.1f} s; oracle restatement of the reference, reference dot "
+                         f"order, 1 thread like the reference's numba kernels), "
+                         f"extrapolated to the {it_full}-iteration solve",
+               "host_cores": os.cpu_count()}
+    if rank == 0:
+        line = {
+            "metric": metric_name(cs), "value": value, "unit": "solve/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64 CG / f32 preconditioner" if pp.needs_low else "f64",
+            "data": "synthetic (seeded SplitMix64 fields per BASELINE.json configs)",
+            "config": config_dict(cs, part, policy, {
+                "parallelism": "1 GPU" if world == 1 else f"{world} replicas (one solve per GPU)",
+                "graph": "CUDA graph of 8 iterations replayed until the device sets done"}),
+            "iterations": it_med, "time_to_solution_ms": ms_per_step,
+            "converged": bool(rep.converged), "final_true_relres": rep.final_true_relres,
+            "solve_gbs": round(solve_gbs, 1),
+            "roofline": roofline, "kernels": kernels,
+            "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+    run_b200(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    main()

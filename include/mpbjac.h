@@ -51,6 +51,7 @@ extern "C" {
 #define MPB_ERR_INDEX32 (-5)    /* nnz or n does not fit int32 indexing    */
 #define MPB_ERR_POLICY (-6)     /* unknown policy kind / missing instance  */
 #define MPB_ERR_WORKSPACE (-7)  /* workspace too small                     */
+#define MPB_ERR_LAYOUT (-8)     /* SELL-32 layout / values missing         */
 
 /* policy kinds (policies.py:30-37) */
 #define MPB_UNIFORM 0
@@ -68,9 +69,17 @@ extern "C" {
 
 typedef struct mpb_handle mpb_handle;
 typedef struct mpb_plan mpb_plan;
+/* SELL-32 layout of a CSR structure (slice height 32 = one warp, rows in
+ * original order): entry j of row r at slice_ptr[r/32] + 32 j + r%32.  The
+ * hot kernels read the matrix in this layout (coalesced, thread per row,
+ * ascending column order); the library owns slice_ptr and the column array,
+ * the caller owns value arrays packed with mpb_sell_pack_*. */
+typedef struct mpb_sell mpb_sell;
 
 /* CSR matrix on the device.  int32 row_ptr/col_idx (n and nnz < 2^31),
- * columns strictly ascending within each row (sparse.py:59-104). */
+ * columns strictly ascending within each row (sparse.py:59-104).  The
+ * sell / sell_val* fields carry the same matrix in SELL-32 layout; they are
+ * required by the preconditioner, solve and true-residual entry points. */
 typedef struct mpb_csr {
   int64_t n;
   int64_t nnz;
@@ -78,6 +87,9 @@ typedef struct mpb_csr {
   const int32_t *col_idx; /* nnz */
   const double *val64;    /* nnz, A.values (also the fp64 instance's values) */
   const float *val32;     /* nnz, fp32 instance's values, NULL if unused     */
+  const mpb_sell *sell;   /* SELL-32 structure of row_ptr/col_idx            */
+  const double *sell_val64; /* val64 packed in SELL-32 (mpb_sell_nnz entries) */
+  const float *sell_val32;  /* val32 packed in SELL-32, NULL if unused        */
 } mpb_csr;
 
 typedef struct mpb_solve_options {
@@ -126,6 +138,21 @@ int mpb_plan_create(mpb_handle *h, int64_t n, int64_t nb,
 int mpb_plan_destroy(mpb_plan *p);
 int mpb_plan_info(const mpb_plan *p, int64_t *h_ntiles, int *h_large,
                   int64_t *h_max_tile_nnz);
+
+/* ---- SELL-32 layout (hot-path matrix format) ----------------------------- */
+/* Builds slice pointers (from the host row_ptr) and packs the column array on
+ * the device. */
+int mpb_sell_create(mpb_handle *h, int64_t n, const int64_t *h_row_ptr,
+                    const int32_t *row_ptr, const int32_t *col_idx,
+                    mpb_sell **out);
+int mpb_sell_destroy(mpb_sell *s);
+/* Padded entry count (length of every SELL value array). */
+int64_t mpb_sell_nnz(const mpb_sell *s);
+/* Pack CSR values into SELL-32 order (padding zero-filled). */
+int mpb_sell_pack_f64(mpb_handle *h, const mpb_sell *s, const int32_t *row_ptr,
+                      const double *csr_val, double *sell_val);
+int mpb_sell_pack_f32(mpb_handle *h, const mpb_sell *s, const int32_t *row_ptr,
+                      const float *csr_val, float *sell_val);
 
 /* ---- reference backend kernels (kernels_numba.py) ------------------------ */
 int mpb_csr_matvec_f64(mpb_handle *h, int64_t n, const int32_t *row_ptr,
@@ -203,6 +230,20 @@ int mpb_pcg_solve(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A,
                   double *tr_relres, double *tr_true, int32_t *tr_branch,
                   double *tr_time, void *workspace, int64_t workspace_bytes,
                   mpb_solve_result *res);
+/* Per-kernel timing of one PCG iteration (for the roofline report):
+ * launches each kernel of an iteration `reps` times on the solve stream,
+ * bracketing every launch with CUDA events, using the buffers of a prior
+ * mpb_pcg_solve with the same arguments (the solver state is reset to a
+ * mid-solve state before each launch).  branch: 0 fp64 / 1 fp32 instance.
+ * h_ms[8] receives the mean ms per launch of: 0 first BJAC pass,
+ * 1 middle passes (all of them, 0 when k < 3), 2 last BJAC pass,
+ * 3 fused p-update+SpMV, 4 x/r update, 5 one scalar step, 6 whole
+ * iteration as launched by the graph (sum of the above with 3 scalar steps),
+ * 7 unused. */
+int mpb_profile_iteration(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A,
+                          const mpb_solve_options *opt, const double *b, double *x,
+                          void *workspace, int64_t workspace_bytes, int branch,
+                          int reps, double *h_ms);
 /* ||b - A x|| / r0_norm in device order.  Synchronous. */
 int mpb_true_relres(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A,
                     const double *x, const double *b, double r0_norm,

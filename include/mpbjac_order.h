@@ -37,6 +37,6 @@
 #define MPB_TILE_THREADS   256
 #define MPB_TILE_MAX_ROWS  512
 #define MPB_TILE_PACK_NNZ  4096
-#define MPB_FIN_THREADS    1024
+#define MPB_FIN_THREADS    256
 
 #endif

@@ -34,7 +34,8 @@ EXPORTED = (
     "mpb_setup_diag_f32", "mpb_convert_values_f32", "mpb_bjac_apply_f64",
     "mpb_bjac_apply_f32", "mpb_fmp_apply", "mpb_bjac_inner_apply_f64",
     "mpb_bjac_inner_apply_f32", "mpb_solve_workspace_bytes", "mpb_pcg_solve",
-    "mpb_true_relres",
+    "mpb_true_relres", "mpb_profile_iteration", "mpb_sell_create",
+    "mpb_sell_destroy", "mpb_sell_nnz", "mpb_sell_pack_f64", "mpb_sell_pack_f32",
 )
 
 
@@ -45,7 +46,9 @@ class BackendUnavailableError(RuntimeError):
 class MpbCsr(C.Structure):
     _fields_ = [("n", C.c_int64), ("nnz", C.c_int64),
                 ("row_ptr", C.c_void_p), ("col_idx", C.c_void_p),
-                ("val64", C.c_void_p), ("val32", C.c_void_p)]
+                ("val64", C.c_void_p), ("val32", C.c_void_p),
+                ("sell", C.c_void_p), ("sell_val64", C.c_void_p),
+                ("sell_val32", C.c_void_p)]
 
 
 class MpbSolveOptions(C.Structure):
@@ -106,6 +109,13 @@ def _declare(L):
         "mpb_solve_workspace_bytes": ([_P, _I64], C.c_int64),
         "mpb_pcg_solve": ([_P, _P, C.POINTER(MpbCsr), C.POINTER(MpbSolveOptions), _P, _P, _P, _P, _P, _P,
                            _P, _I64, C.POINTER(MpbSolveResult)], C.c_int),
+        "mpb_profile_iteration": ([_P, _P, C.POINTER(MpbCsr), C.POINTER(MpbSolveOptions), _P, _P, _P, _I64,
+                                   C.c_int, C.c_int, C.POINTER(C.c_double)], C.c_int),
+        "mpb_sell_create": ([_P, _I64, _P, _P, _P, C.POINTER(_P)], C.c_int),
+        "mpb_sell_destroy": ([_P], C.c_int),
+        "mpb_sell_nnz": ([_P], C.c_int64),
+        "mpb_sell_pack_f64": ([_P, _P, _P, _P, _P], C.c_int),
+        "mpb_sell_pack_f32": ([_P, _P, _P, _P, _P], C.c_int),
         "mpb_true_relres": ([_P, _P, C.POINTER(MpbCsr), _P, _P, C.c_double, C.POINTER(C.c_double)], C.c_int),
     }
     for name, (args, res) in sig.items():

@@ -12,11 +12,11 @@
 
 namespace mpb {
 
-constexpr int kTileThreads = MPB_TILE_THREADS;
+constexpr int kTileThreads = MPB_TILE_THREADS;  // lanes of the tile sum order
 constexpr int kTileRows = MPB_TILE_MAX_ROWS;
-constexpr int kRowsPerThread = kTileRows / kTileThreads;
+constexpr int kCtaThreads = kTileRows;           // tile kernels: one thread per row
 constexpr int kFinThreads = MPB_FIN_THREADS;
-static_assert(kTileRows % kTileThreads == 0, "tile rows must be a multiple of threads");
+static_assert(kTileRows == 2 * kTileThreads, "lane j sums rows j and j + kTileThreads");
 
 // ---------------------------------------------------------------------------
 // solver state (device resident; one per solve)
@@ -44,6 +44,12 @@ struct SolverState {
   unsigned long long t0_ns;
   unsigned long long ovf_count;
   long long ovf_first;
+  // trace arrays (device, cap entries each)
+  double *tr_relres;
+  double *tr_true;
+  int *tr_branch;
+  double *tr_time;
+  unsigned int ticket[4];  // last-CTA counters of the fused scalar steps
   int kind;
   int branch;  // 0 high (fp64 instance), 1 low (fp32 instance)
   int first;   // p is None (solver.py:150-151)
@@ -86,12 +92,43 @@ __device__ __forceinline__ R block_tree(R v, R *ws) {
   return r;
 }
 
-// Global sum of tile partials, steps 1-3 with kFinThreads lanes.  Must be
-// called by all kFinThreads threads; result valid in thread 0.
+// Global sum of tile partials, steps 1-3 with kFinThreads lanes.  Called by
+// all threads of a CTA with at least kFinThreads threads (threads beyond
+// kFinThreads contribute nothing); result valid in thread 0.  Partials are
+// read through L2 (__ldcg): other SMs wrote them in the same kernel.  Loads
+// are issued in batches of 8 before the (ordered) adds.
 __device__ __forceinline__ double fin_sum(const double *part, long long count, double *ws) {
   double acc = 0.0;
-  for (long long i = threadIdx.x; i < count; i += kFinThreads) acc = __dadd_rn(acc, part[i]);
+  if (threadIdx.x < kFinThreads) {
+    for (long long i0 = threadIdx.x; i0 < count; i0 += 8LL * kFinThreads) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        const long long i = i0 + (long long)u * kFinThreads;
+        v[u] = i < count ? __ldcg(part + i) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; u++)
+        if (i0 + (long long)u * kFinThreads < count) acc = __dadd_rn(acc, v[u]);
+    }
+  }
   return block_tree<kFinThreads>(acc, ws);
+}
+
+// Thread 0 publishes `v` to part[slot] and takes a ticket; true in every
+// thread of the CTA that finished last among `nblocks` (all partials then
+// visible).  Must be called by all threads.
+__device__ __forceinline__ bool publish_last(double v, double *part, int slot, unsigned int *ticket,
+                                             unsigned int nblocks) {
+  __shared__ int am_last;
+  if (threadIdx.x == 0) {
+    part[slot] = v;
+    __threadfence();
+    am_last = ticket == nullptr ? 0 : (atomicAdd(ticket, 1u) == nblocks - 1u);
+  }
+  __syncthreads();
+  if (am_last) __threadfence();
+  return am_last != 0;
 }
 
 // ---------------------------------------------------------------------------

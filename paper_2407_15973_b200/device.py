@@ -63,10 +63,32 @@ def dtype_name(x) -> str:
     return str(np.asarray(x).dtype)
 
 
-class DeviceCSR:
-    """CSR matrix resident on one GPU (int32 indices)."""
+class DeviceSell:
+    """SELL-32 structure of a DeviceCSR (library-owned mpb_sell)."""
 
-    def __init__(self, n, m, row_ptr, col_idx, val64=None, val32=None):
+    def __init__(self, handle, n, host_row_ptr, row_ptr, col_idx):
+        import ctypes as C
+        self.h = handle
+        self.ptr = C.c_void_p()
+        hrp = np.ascontiguousarray(host_row_ptr, np.int64)
+        _lib.check(handle.lib.mpb_sell_create(
+            handle.ptr, int(n), hrp.ctypes.data_as(C.c_void_p),
+            _lib.ptr(row_ptr), _lib.ptr(col_idx), C.byref(self.ptr)), "mpb_sell_create")
+        self.nnz = int(handle.lib.mpb_sell_nnz(self.ptr))
+
+    def __del__(self):
+        try:
+            if self.ptr:
+                self.h.lib.mpb_sell_destroy(self.ptr)
+        except Exception:  # interpreter shutdown
+            pass
+
+
+class DeviceCSR:
+    """CSR matrix resident on one GPU (int32 indices), plus its SELL-32
+    layout (the hot kernels' format), built on first use."""
+
+    def __init__(self, n, m, row_ptr, col_idx, val64=None, val32=None, host_row_ptr=None):
         self.n = int(n)
         self.m = int(m)
         self.row_ptr = row_ptr
@@ -75,7 +97,9 @@ class DeviceCSR:
         self.val32 = val32
         self.nnz = int(col_idx.numel())
         self.device = row_ptr.device
-        self._struct = None
+        self.host_row_ptr = host_row_ptr
+        self.sell = None
+        self._sell_vals = {}
 
     @classmethod
     def from_host(cls, n, m, row_ptr, col_idx, values, device=None):
@@ -86,9 +110,37 @@ class DeviceCSR:
         rp = to_device(row_ptr.astype(np.int32, copy=False), device=device)
         ci = to_device(np.asarray(col_idx, np.int32), device=device)
         values = np.asarray(values)
+        hrp = np.asarray(row_ptr, np.int64)
         if values.dtype == np.float64:
-            return cls(n, m, rp, ci, val64=to_device(values, device=device))
-        return cls(n, m, rp, ci, val32=to_device(values, device=device))
+            return cls(n, m, rp, ci, val64=to_device(values, device=device), host_row_ptr=hrp)
+        return cls(n, m, rp, ci, val32=to_device(values, device=device), host_row_ptr=hrp)
+
+    def _ensure_sell(self, handle):
+        if self.sell is None:
+            hrp = self.host_row_ptr
+            if hrp is None:
+                hrp = self.row_ptr.cpu().numpy().astype(np.int64)
+            self.sell = DeviceSell(handle, self.n, hrp, self.row_ptr, self.col_idx)
+        return self.sell
+
+    def sell_values(self, values):
+        """SELL-32 packing of a CSR value tensor of this matrix (cached)."""
+        if values is None:
+            return None
+        key = (values.data_ptr(), str(values.dtype))
+        packed = self._sell_vals.get(key)
+        if packed is None:
+            t = torch()
+            h = _lib.Handle.get(self.device.index)
+            S = self._ensure_sell(h)
+            packed = t.empty(max(S.nnz, 1), dtype=values.dtype, device=self.device)
+            fn = h.lib.mpb_sell_pack_f64 if values.dtype == t.float64 else h.lib.mpb_sell_pack_f32
+            _lib.check(fn(h.ptr, S.ptr, _lib.ptr(self.row_ptr), _lib.ptr(values), _lib.ptr(packed)),
+                       "mpb_sell_pack")
+            self._sell_vals[key] = (values, packed)
+        else:
+            packed = packed[1]
+        return packed
 
     def c_struct(self, val64=None, val32=None) -> _lib.MpbCsr:
         s = _lib.MpbCsr()
@@ -100,6 +152,13 @@ class DeviceCSR:
         v32 = val32 if val32 is not None else self.val32
         s.val64 = v64.data_ptr() if v64 is not None else None
         s.val32 = v32.data_ptr() if v32 is not None else None
+        h = _lib.Handle.get(self.device.index)
+        S = self._ensure_sell(h)
+        s.sell = S.ptr
+        sv64 = self.sell_values(v64)
+        sv32 = self.sell_values(v32)
+        s.sell_val64 = sv64.data_ptr() if sv64 is not None else None
+        s.sell_val32 = sv32.data_ptr() if sv32 is not None else None
         return s
 
     def nbytes(self) -> int:
@@ -107,4 +166,8 @@ class DeviceCSR:
         for v in (self.val64, self.val32):
             if v is not None:
                 b += v.numel() * v.element_size()
+        if self.sell is not None:
+            b += self.sell.nnz * 4
+        for _, packed in self._sell_vals.values():
+            b += packed.numel() * packed.element_size()
         return b

@@ -160,6 +160,17 @@ def _workspace(mp, plan, n, device):
     return ws[1]
 
 
+def _solve_buffers(mp, n, cap, device):
+    torch = __import__("torch")
+    bufs = getattr(mp, "_solve_bufs", None)
+    if bufs is None or bufs[0] != (n, cap, str(device)):
+        f64 = dict(dtype=torch.float64, device=device)
+        bufs = ((n, cap, str(device)), torch.empty(n, **f64), torch.empty(n, **f64),
+                torch.empty((3, cap), **f64), torch.empty(cap, dtype=torch.int32, device=device))
+        mp._solve_bufs = bufs
+    return bufs[1:]
+
+
 def pcg_solve(A: SparseMatrix, b, mp: MixedPreconditioner,
               config: SolveConfig = SolveConfig(), x0=None, *,
               graph_iters: int = 0) -> SolveReport:
@@ -185,12 +196,12 @@ def pcg_solve(A: SparseMatrix, b, mp: MixedPreconditioner,
     P = mp.any
     h = _lib.Handle.get(D.device.index)
     cap = int(config.iteration_cap(A.n))
-    bd = to_device(b, device=D.device)
-    x = torch.empty(A.n, dtype=torch.float64, device=D.device)
+    # persistent per-preconditioner buffers keep the device pointers stable,
+    # so the captured CUDA graph is reused from one solve to the next
+    bd, x, tr, trb = _solve_buffers(mp, A.n, cap, D.device)
+    bd.copy_(b if is_tensor(b) else torch.from_numpy(np.ascontiguousarray(b)))
     if x0 is not None:
-        x.copy_(to_device(x0, device=D.device))
-    tr = torch.empty((3, cap), dtype=torch.float64, device=D.device)
-    trb = torch.empty(cap, dtype=torch.int32, device=D.device)
+        x.copy_(x0 if is_tensor(x0) else torch.from_numpy(np.ascontiguousarray(x0)))
     ws = _workspace(mp, P.plan, A.n, D.device)
     opt = _lib.MpbSolveOptions()
     opt.kind = KIND_CODE[mp.policy.kind]
@@ -213,8 +224,8 @@ def pcg_solve(A: SparseMatrix, b, mp: MixedPreconditioner,
     stats = {"device_seconds": float(res.device_seconds),
              "kernel_launches": int(res.kernel_launches),
              "r0_norm": float(res.r0_norm)}
+    xo = x.clone() if tensor_io else to_host(x)
     if res.r0_norm == 0.0:
-        xo = x if tensor_io else to_host(x)
         return SolveReport(True, 0, [], 0.0, 0.0, mp.policy, xo, stats)
     trh = to_host(tr[:, :it])
     brh = to_host(trb[:it])
@@ -222,7 +233,6 @@ def pcg_solve(A: SparseMatrix, b, mp: MixedPreconditioner,
                              None if math.isnan(trh[1, i]) else float(trh[1, i]),
                              "high" if brh[i] == 0 else "low", float(trh[2, i]))
              for i in range(it)]
-    xo = x if tensor_io else to_host(x)
     return SolveReport(bool(res.converged), it, trace,
                        float(res.final_true_relres), float(res.device_seconds),
                        mp.policy, xo, stats)
@@ -321,3 +331,31 @@ def report_summary(report: SolveReport, extra: dict | None = None) -> dict:
     if extra:
         d.update(extra)
     return d
+
+
+def profile_iteration(A: SparseMatrix, mp: MixedPreconditioner, *,
+                      config: SolveConfig = SolveConfig(), branch: str = "low",
+                      reps: int = 20) -> dict:
+    """Mean CUDA-event time (ms) per launch of each kernel of one PCG
+    iteration, on the buffers pcg_solve uses (mpb_profile_iteration).
+    Call after at least one pcg_solve with the same A / mp / config."""
+    D, s = _dev_struct(A, mp)
+    P = mp.any
+    h = _lib.Handle.get(D.device.index)
+    cap = int(config.iteration_cap(A.n))
+    bd, x, _, _ = _solve_buffers(mp, A.n, cap, D.device)
+    ws = _workspace(mp, P.plan, A.n, D.device)
+    opt = _lib.MpbSolveOptions()
+    opt.kind = KIND_CODE[mp.policy.kind]
+    opt.adp_tol = float(mp.policy.adp_tol) if mp.policy.adp_tol is not None else 0.0
+    opt.k, opt.t = P.k, P.t
+    opt.res_tol = float(config.res_tol)
+    opt.max_iter = cap
+    out = (C.c_double * 8)()
+    _lib.check(h.lib.mpb_profile_iteration(
+        h.ptr, P.plan.ptr, C.byref(s), C.byref(opt), _lib.ptr(bd), _lib.ptr(x),
+        _lib.ptr(ws), ws.numel(), 0 if branch == "high" else 1, int(reps), out),
+        "profile_iteration")
+    names = ("bjac_first", "bjac_middle", "bjac_last", "spmv_pq", "update",
+             "scalar", "iteration")
+    return {k: float(out[i]) for i, k in enumerate(names)}

@@ -268,3 +268,24 @@ def test_tensor_io_stays_on_device(cuda):
     assert isinstance(rep.x, torch.Tensor) and rep.x.is_cuda
     rep2 = pcg_solve(cs.A, cs.b, mp)
     np.testing.assert_array_equal(rep.x.cpu().numpy(), rep2.x)
+
+
+def test_unstaged_tiles_and_dense_rows_bitwise(cuda, oracle):
+    """Tiles whose CSR slice exceeds the shared-memory stage fall back to
+    direct global loads; results must not change."""
+    from paper_2407_15973_b200 import Precision
+    from paper_2407_15973_b200.bjac import BlockPartition, setup
+    rng = np.random.default_rng(77)
+    A = random_spd_csr(1200, 0.06, rng)          # ~140 nnz/row, tiles >> 8192 nnz
+    r = rng.standard_normal(A.n)
+    for offs in (np.arange(0, A.n + 1, 300), np.array([0, 5, 517, 1200]),
+                 np.append(np.arange(0, A.n, 64), A.n)):
+        part = BlockPartition(offs)
+        d64, d32, v32, inb = oracle.setup_arrays(A.row_ptr, A.col_idx, A.values, offs)
+        for k, t in ((1, 2), (2, 2), (3, 3)):
+            z = setup(A, k=k, t=t, partition=part).apply(r)
+            np.testing.assert_array_equal(
+                z, oracle.bjac_apply(A.row_ptr, A.col_idx, A.values, inb, d64, k, t, r))
+            z32 = setup(A, k=k, t=t, precision=Precision.F32, partition=part).apply(r.astype(np.float32))
+            np.testing.assert_array_equal(
+                z32, oracle.bjac_apply(A.row_ptr, A.col_idx, v32, inb, d32, k, t, r.astype(np.float32)))

@@ -1,5 +1,5 @@
 import time, sys, numpy as np, torch
-sys.path.insert(0, '.')
+sys.path.insert(0, __import__('os').path.dirname(__import__('os').path.dirname(__import__('os').path.abspath(__file__))))
 from paper_2407_15973_b200 import problems
 from paper_2407_15973_b200.bjac import BlockPartition
 from paper_2407_15973_b200.policies import PrecisionPolicy, build_mixed
