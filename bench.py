@@ -111,15 +111,17 @@ class ClockSampler:
 
 def kernel_bytes(Z, N, branch, ntiles):
     """Algorithmic bytes per launch: every array streamed
-    once, gathered vector entries counted once, int32 indices."""
+    once, gathered vector entries counted once, int32 SELL columns, 2-byte
+    per-row metadata; Z = stored nonzeros (SELL padding not counted)."""
     if branch == "low":
-        first, mid, last = 8 * Z + 16 * N, 8 * Z + 20 * N, 8 * Z + 20 * N
-        spmv = 12 * Z + 28 * N + 4 * N
+        first, mid, last = 8 * Z + 14 * N, 8 * Z + 18 * N, 8 * Z + 18 * N
+        pupd = 20 * N
     else:
-        first, mid, last = 12 * Z + 20 * N, 12 * Z + 28 * N, 12 * Z + 28 * N
-        spmv = 12 * Z + 28 * N + 8 * N
+        first, mid, last = 12 * Z + 18 * N, 12 * Z + 26 * N, 12 * Z + 26 * N
+        pupd = 24 * N
     return {"bjac_first": first, "bjac_middle": mid, "bjac_last": last,
-            "spmv_pq": spmv, "update": 48 * N, "scalar": 8 * ntiles}
+            "pupdate": pupd, "spmv_pq": 12 * Z + 16 * N, "update": 48 * N,
+            "scalar": 8 * ntiles}
 
 
 def cpu_sample(cs, part, policy, iters, threads, order="sequential"):
@@ -278,16 +280,15 @@ def run_b200(args, world, rank, local):
     peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
     kernels = {}
-    for name in ("bjac_first", "bjac_last", "spmv_pq", "update"):
+    for name in ("bjac_first", "bjac_last", "pupdate", "spmv_pq", "update"):
         t_ms = prof[name]
         if t_ms <= 0:
             continue
         gbs = kb[name] / (t_ms * 1e-3) / 1e9
         kernels[name] = {"ms": round(t_ms, 5), "bytes": kb[name], "gbs": round(gbs, 1),
                          "frac": round(gbs / peak, 4)}
-    kernels["scalar"] = {"ms": round(prof["scalar"], 5), "launches_per_iter": 3}
-    per_iter_share = {k: v["ms"] * (3 if k == "scalar" else 1) for k, v in kernels.items()}
-    dom = max((k for k in kernels if k != "scalar"), key=lambda k: per_iter_share[k])
+    per_iter_share = {k: v["ms"] for k, v in kernels.items()}
+    dom = max(kernels, key=lambda k: per_iter_share[k])
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
@@ -299,7 +300,8 @@ def run_b200(args, world, rank, local):
                 "bytes_per_launch": kb[dom]}
     it_med = int(np.median(iters))
     iter_bytes = (kb["bjac_first"] + max(cs.k - 2, 0) * kb["bjac_middle"]
-                  + (kb["bjac_last"] if cs.k > 1 else 0) + kb["spmv_pq"] + kb["update"])
+                  + (kb["bjac_last"] if cs.k > 1 else 0) + kb["pupdate"] + kb["spmv_pq"]
+                  + kb["update"])
     solve_gbs = iter_bytes * it_med / (ms_per_step * 1e-3) / 1e9
 
     # ---- CPU baseline (rank 0, N=1 only) -----------------------------------

@@ -128,7 +128,8 @@ int mpb_synchronize(mpb_handle *h);
 int64_t mpb_launch_count(const mpb_handle *h);
 
 /* ---- partition / tile plan (host-only math, include/mpbjac_order.h) ---- */
-/* h_tile_lo must hold nb + n/512 + 2 entries; returns ntiles. No GPU needed. */
+/* h_tile_lo must hold nb + n/MPB_TILE_MAX_ROWS + 2 entries; returns ntiles.
+ * No GPU needed. */
 int64_t mpb_plan_tiles_host(int64_t nb, const int64_t *h_offsets,
                             const int64_t *h_row_ptr, int64_t *h_tile_lo,
                             int *h_large);
@@ -136,6 +137,10 @@ int mpb_plan_create(mpb_handle *h, int64_t n, int64_t nb,
                     const int64_t *h_offsets, const int64_t *h_row_ptr,
                     mpb_plan **out);
 int mpb_plan_destroy(mpb_plan *p);
+/* Build the plan's per-row static structure (row length, diagonal slot,
+ * in-block slot range) against a SELL-32 layout of the matrix; required
+ * before the plan is used with that matrix by the preconditioner / solve. */
+int mpb_plan_bind_sell(mpb_handle *h, mpb_plan *p, const mpb_sell *sell);
 int mpb_plan_info(const mpb_plan *p, int64_t *h_ntiles, int *h_large,
                   int64_t *h_max_tile_nnz);
 
@@ -237,9 +242,9 @@ int mpb_pcg_solve(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A,
  * mid-solve state before each launch).  branch: 0 fp64 / 1 fp32 instance.
  * h_ms[8] receives the mean ms per launch of: 0 first BJAC pass,
  * 1 middle passes (all of them, 0 when k < 3), 2 last BJAC pass,
- * 3 fused p-update+SpMV, 4 x/r update, 5 one scalar step, 6 whole
- * iteration as launched by the graph (sum of the above with 3 scalar steps),
- * 7 unused. */
+ * 3 SpMV q = A p with the fused p.q step, 4 x/r update (fused relres
+ * step), 5 unused (scalar steps are fused), 6 whole iteration (sum),
+ * 7 p-update p = z + beta p. */
 int mpb_profile_iteration(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A,
                           const mpb_solve_options *opt, const double *b, double *x,
                           void *workspace, int64_t workspace_bytes, int branch,

@@ -24,7 +24,8 @@
  *
  * Tile sum of per-row values v[row] over rows [lo, hi):
  *   1. lane j in [0, MPB_TILE_THREADS): s_j = 0; s_j += v[lo + j + m*MPB_TILE_THREADS]
- *      for m = 0, 1, ... while the row is < hi (one rounding per add);
+ *      for m = 0, 1, ... while the row is < hi (one rounding per add; with
+ *      MPB_TILE_THREADS == MPB_TILE_MAX_ROWS every lane owns at most one row);
  *   2. each warp butterflies (xor 16, 8, 4, 2, 1) -> lane 0 holds W_w;
  *   3. warp 0 butterflies W_0..W_{nw-1} padded with +0.0 to 32 lanes.
  * Global sum of the tile partials P[0..T):
@@ -35,8 +36,8 @@
 #define MPBJAC_ORDER_H
 
 #define MPB_TILE_THREADS   256
-#define MPB_TILE_MAX_ROWS  512
-#define MPB_TILE_PACK_NNZ  4096
+#define MPB_TILE_MAX_ROWS  256
+#define MPB_TILE_PACK_NNZ  2048
 #define MPB_FIN_THREADS    256
 
 #endif

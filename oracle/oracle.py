@@ -62,9 +62,10 @@ class _Result(C.Structure):
 
 def build(force: bool = False) -> str:
     """Compile the oracle with its Makefile (gcc only; no GPU needed)."""
-    src = os.path.join(_HERE, "mpbjac_oracle.c")
+    srcs = [os.path.join(_HERE, "mpbjac_oracle.c"),
+            os.path.join(os.path.dirname(_HERE), "include", "mpbjac_order.h")]
     if force or not os.path.exists(_LIB_PATH) or \
-            os.path.getmtime(_LIB_PATH) < os.path.getmtime(src):
+            os.path.getmtime(_LIB_PATH) < max(os.path.getmtime(f) for f in srcs):
         subprocess.run(["make", "-s", "-C", _HERE, "libmpbjac_oracle.so"],
                        check=True)
     return _LIB_PATH
@@ -211,7 +212,7 @@ def plan_tiles(offsets, row_ptr):
     row_ptr = np.ascontiguousarray(row_ptr, np.int64)
     nb = offsets.size - 1
     n = int(offsets[-1])
-    out = np.empty(nb + n // 512 + 2, np.int64)
+    out = np.empty(nb + n // 256 + 2, np.int64)
     large = C.c_int(0)
     nt = lib().orc_plan_tiles(nb, offsets, row_ptr, out, C.byref(large))
     return out[:nt + 1].copy(), bool(large.value)

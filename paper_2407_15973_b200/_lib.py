@@ -36,6 +36,7 @@ EXPORTED = (
     "mpb_bjac_inner_apply_f32", "mpb_solve_workspace_bytes", "mpb_pcg_solve",
     "mpb_true_relres", "mpb_profile_iteration", "mpb_sell_create",
     "mpb_sell_destroy", "mpb_sell_nnz", "mpb_sell_pack_f64", "mpb_sell_pack_f32",
+    "mpb_plan_bind_sell",
 )
 
 
@@ -113,6 +114,7 @@ def _declare(L):
                                    C.c_int, C.c_int, C.POINTER(C.c_double)], C.c_int),
         "mpb_sell_create": ([_P, _I64, _P, _P, _P, C.POINTER(_P)], C.c_int),
         "mpb_sell_destroy": ([_P], C.c_int),
+        "mpb_plan_bind_sell": ([_P, _P, _P], C.c_int),
         "mpb_sell_nnz": ([_P], C.c_int64),
         "mpb_sell_pack_f64": ([_P, _P, _P, _P, _P], C.c_int),
         "mpb_sell_pack_f32": ([_P, _P, _P, _P, _P], C.c_int),

@@ -91,11 +91,21 @@ class DevicePlan:
             handle.ptr, partition.n, partition.num_blocks,
             offs.ctypes.data_as(C.c_void_p), rp.ctypes.data_as(C.c_void_p),
             C.byref(self.ptr)), "mpb_plan_create")
+        self.bound = None
         nt, large, mx = C.c_int64(), C.c_int(), C.c_int64()
         handle.lib.mpb_plan_info(self.ptr, C.byref(nt), C.byref(large), C.byref(mx))
         self.ntiles = int(nt.value)
         self.large = bool(large.value)
         self.max_tile_nnz = int(mx.value)
+
+    def bind(self, dcsr) -> "DevicePlan":
+        """Build the per-row static structure against the matrix's SELL-32
+        layout (mpb_plan_bind_sell)."""
+        S = dcsr._ensure_sell(self.h)
+        if self.bound is not S:
+            _lib.check(self.h.lib.mpb_plan_bind_sell(self.h.ptr, self.ptr, S.ptr), "mpb_plan_bind_sell")
+            self.bound = S
+        return self
 
     def __del__(self):
         try:
@@ -233,6 +243,18 @@ def _device_values(A: SparseMatrix, precision: Precision, h):
     return D, D.val64
 
 
+def _shared_plan(h, A: SparseMatrix, D, partition: BlockPartition) -> DevicePlan:
+    """One device plan per (matrix, partition): the fp64 and fp32 instances
+    of an adaptive policy share it."""
+    cache = A.__dict__.setdefault("_plans", {})
+    key = (partition.offsets.tobytes(), str(D.device))
+    plan = cache.get(key)
+    if plan is None:
+        plan = DevicePlan(h, partition, A.row_ptr).bind(D)
+        cache[key] = plan
+    return plan
+
+
 def setup(A: SparseMatrix, nb: int = 32, k: int = 2, t: int = 2,
           precision: Precision = Precision.F64,
           partition: BlockPartition | None = None) -> BjacPreconditioner:
@@ -280,7 +302,7 @@ def setup(A: SparseMatrix, nb: int = 32, k: int = 2, t: int = 2,
         if float(dsrc[zrow].item()) != 0.0:
             raise ValueError(f"diagonal of row {zrow} underflows to zero in {precision}")
         raise ValueError(f"zero diagonal entry at row {zrow}")
-    plan = DevicePlan(h, partition, A.row_ptr)
+    plan = _shared_plan(h, A, D, partition)
     return BjacPreconditioner(partition, int(k), int(t), precision, A, D,
                               dvals, ddiag, plan)
 

@@ -51,6 +51,11 @@ struct mpb_plan {
   int64_t n, nb, ntiles, max_tile_nnz;
   int large;
   int *d_tile_lo, *d_tile_bf, *d_tile_bl, *d_boff;
+  TileDesc *d_td;         // per-tile descriptors (rows, SELL slices/entries, blocks)
+  int max_tile_sell;      // max SELL entries of a tile
+  int max_sl, max_nbk;    // max slices / blocks per tile
+  uint16_t *d_meta;       // per-row static structure (mpb_plan_bind_sell)
+  const mpb_sell *bound;  // the SELL layout d_meta was built against
 };
 
 struct mpb_sell {
@@ -97,6 +102,76 @@ int ensure_scratch(mpb_handle *h, size_t bytes) {
 
 inline size_t al256(size_t b) { return (b + 255) & ~size_t(255); }
 
+// SELL-32 slice pointers from a host row_ptr (slice width = longest row of
+// the slice); shared by mpb_sell_create and the plan's tile descriptors so
+// both agree entry for entry.  Returns false if the layout exceeds int32.
+bool sell_slice_ptrs(int64_t n, const int64_t *h_rp, std::vector<int> &sp) {
+  const int64_t ns = (n + 31) / 32;
+  sp.assign(ns + 1, 0);
+  int64_t acc = 0;
+  for (int64_t s = 0; s < ns; s++) {
+    int64_t width = 0;
+    const int64_t r1 = std::min<int64_t>(n, 32 * s + 32);
+    for (int64_t r = 32 * s; r < r1; r++) width = std::max<int64_t>(width, h_rp[r + 1] - h_rp[r]);
+    sp[s] = static_cast<int>(acc);
+    acc += 32 * width;
+    if (acc >= (int64_t(1) << 31)) return false;
+  }
+  sp[ns] = static_cast<int>(acc);
+  return true;
+}
+
+constexpr int kStageCap = 4096;  // staged SELL entries per tile (2 stages per CTA)
+
+template <typename T>
+TileGeom geom_for(const mpb_plan *p) {
+  TileGeom g;
+  g.ntiles = static_cast<int>(p->ntiles);
+  g.cap_e = std::min(p->max_tile_sell, kStageCap);
+  g.max_sl = p->max_sl;
+  g.ns = 2;
+  return g;
+}
+
+int g_num_sms = 0;
+int num_sms() {
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+// Stage count for a persistent tile kernel: 3 stages (prefetch depth 2)
+// when that still leaves >= 2 co-resident CTAs per SM, else 2.
+template <typename K>
+int pick_stages(K kernel, uint32_t stage_bytes) {
+  auto per_sm = [&](int ns) {
+    const uint32_t dyn = ns * stage_bytes;
+    if (dyn > 220u * 1024u) return 0;
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn));
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, kWsThreads, dyn) != cudaSuccess) n = 0;
+    return n;
+  };
+  return per_sm(3) >= 2 ? 3 : 2;
+}
+
+// Persistent grid: as many CTAs as are co-resident at this shared-memory
+// size, never more than there are tiles.  Opts the kernel into the dynamic
+// shared memory it needs.
+template <typename K>
+int persistent_grid(K kernel, uint32_t dyn_smem, int64_t ntiles, int threads = kCtaThreads) {
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn_smem));
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, dyn_smem) != cudaSuccess ||
+      per_sm < 1)
+    per_sm = 1;
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ntiles, int64_t(per_sm) * num_sms())));
+}
+
 // Buffers one preconditioner application needs besides r and z.
 template <typename T>
 struct ApplyBufs {
@@ -104,13 +179,23 @@ struct ApplyBufs {
   T *res, *dg, *wA, *wB;  // large-block path (plan->large)
 };
 
+template <typename T, bool F, bool L, bool R64>
+int launch_tile_kernel(mpb_handle *h, cudaStream_t s, const mpb_plan *p, PassArgs<T> a) {
+  const StageLayout Ls = bjac_layout<T, F, R64>(a.g);
+  a.g.ns = pick_stages(k_bjac_tile<T, F, L, R64>, Ls.bytes);
+  const uint32_t dyn = a.g.ns * Ls.bytes;
+  const int grid = persistent_grid(k_bjac_tile<T, F, L, R64>, dyn, p->ntiles, kWsThreads);
+  k_bjac_tile<T, F, L, R64><<<grid, kWsThreads, dyn, s>>>(a);
+  MPB_LAUNCHED(h);
+  return MPB_OK;
+}
+
 template <typename T, bool F, bool L>
 int launch_pass(mpb_handle *h, cudaStream_t s, const mpb_plan *p, PassArgs<T> a, const ApplyBufs<T> &bufs) {
   const int nt = static_cast<int>(p->ntiles);
   if (!p->large) {
-    k_bjac_tile<T, F, L><<<nt, kCtaThreads, 0, s>>>(a);
-    MPB_LAUNCHED(h);
-    return MPB_OK;
+    if (a.r64 != nullptr) return launch_tile_kernel<T, F, L, true>(h, s, p, a);
+    return launch_tile_kernel<T, F, L, false>(h, s, p, a);
   }
   a.resbuf = bufs.res;
   a.dbuf = bufs.dg;
@@ -150,12 +235,11 @@ int launch_apply(mpb_handle *h, cudaStream_t s, const mpb_plan *p, const mpb_csr
   a.sp = A->sell->d_sp;
   a.scol = A->sell->d_col;
   a.sval = sell_vals<T>(A);
-  a.tile_lo = p->d_tile_lo;
-  a.tile_bf = p->d_tile_bf;
-  a.tile_bl = p->d_tile_bl;
+  a.meta = p->d_meta;
+  a.td = p->d_td;
   a.boff = p->d_boff;
+  a.g = geom_for<T>(p);
   a.t = t;
-  a.ntiles = static_cast<int>(p->ntiles);
   a.r64 = r64;
   a.rT = rT;
   a.ovf_count = ovf_count;
@@ -185,6 +269,10 @@ int check_csr(const mpb_csr *A) {
 }
 
 // hot entry points read the SELL-32 layout
+int check_bound(const mpb_plan *p, const mpb_csr *A) {
+  return (p != nullptr && A != nullptr && p->d_meta != nullptr && p->bound == A->sell) ? MPB_OK : MPB_ERR_LAYOUT;
+}
+
 int check_sell(const mpb_csr *A, bool need64, bool need32) {
   int rc = check_csr(A);
   if (rc) return rc;
@@ -377,6 +465,25 @@ int mpb_plan_create(mpb_handle *h, int64_t n, int64_t nb, const int64_t *h_offse
     blv[i] = static_cast<int>(e);
     max_nnz = std::max(max_nnz, h_row_ptr[hi] - h_row_ptr[lo]);
   }
+  // tile descriptors against the SELL-32 slice layout of this structure
+  std::vector<int> sp;
+  if (!sell_slice_ptrs(n, h_row_ptr, sp)) return MPB_ERR_INDEX32;
+  std::vector<TileDesc> td(nt);
+  int max_sell = 0, max_sl = 0, max_nbk = 0;
+  for (int64_t i = 0; i < nt; i++) {
+    TileDesc &d = td[i];
+    d.lo = tl[i];
+    d.hi = tl[i + 1];
+    d.s0 = d.lo >> 5;
+    d.s1 = (d.hi + 31) >> 5;
+    d.e0 = sp[d.s0];
+    d.e1 = sp[d.s1];
+    d.bf = bfv[i];
+    d.nbk = blv[i] - bfv[i] + 1;
+    max_sell = std::max(max_sell, d.e1 - d.e0);
+    max_sl = std::max(max_sl, d.s1 - d.s0);
+    max_nbk = std::max(max_nbk, d.nbk);
+  }
   MPB_CUDA(cudaSetDevice(h->device));
   mpb_plan *p = new mpb_plan();
   p->device = h->device;
@@ -385,6 +492,9 @@ int mpb_plan_create(mpb_handle *h, int64_t n, int64_t nb, const int64_t *h_offse
   p->ntiles = nt;
   p->large = large;
   p->max_tile_nnz = max_nnz;
+  p->max_tile_sell = max_sell;
+  p->max_sl = max_sl;
+  p->max_nbk = max_nbk;
   cudaError_t e = cudaMalloc(&p->d_tile_lo, sizeof(int) * (nt + 1));
   if (e == cudaSuccess) e = cudaMalloc(&p->d_tile_bf, sizeof(int) * nt);
   if (e == cudaSuccess) e = cudaMalloc(&p->d_tile_bl, sizeof(int) * nt);
@@ -393,6 +503,8 @@ int mpb_plan_create(mpb_handle *h, int64_t n, int64_t nb, const int64_t *h_offse
   if (e == cudaSuccess) e = cudaMemcpy(p->d_tile_bf, bfv.data(), sizeof(int) * nt, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(p->d_tile_bl, blv.data(), sizeof(int) * nt, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(p->d_boff, boff.data(), sizeof(int) * (nb + 1), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMalloc(&p->d_td, sizeof(TileDesc) * nt);
+  if (e == cudaSuccess) e = cudaMemcpy(p->d_td, td.data(), sizeof(TileDesc) * nt, cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
     mpb_plan_destroy(p);
     return status_of(e);
@@ -407,7 +519,22 @@ int mpb_plan_destroy(mpb_plan *p) {
   cudaFree(p->d_tile_bf);
   cudaFree(p->d_tile_bl);
   cudaFree(p->d_boff);
+  cudaFree(p->d_td);
+  cudaFree(p->d_meta);
   delete p;
+  return MPB_OK;
+}
+
+int mpb_plan_bind_sell(mpb_handle *h, mpb_plan *p, const mpb_sell *sell) {
+  if (!h || !p || !sell || sell->n != p->n) return MPB_ERR_ARG;
+  if (p->bound == sell && p->d_meta) return MPB_OK;
+  MPB_CUDA(cudaSetDevice(h->device));
+  if (!p->d_meta) MPB_CUDA(cudaMalloc(&p->d_meta, sizeof(uint16_t) * p->n));
+  k_build_meta<<<elt_blocks(p->n), kEltThreads, 0, h->user>>>(p->n, sell->d_sp, sell->d_col, p->d_boff,
+                                                            static_cast<int>(p->nb), p->d_meta);
+  MPB_LAUNCHED(h);
+  MPB_CUDA(cudaStreamSynchronize(h->user));
+  p->bound = sell;
   return MPB_OK;
 }
 
@@ -579,18 +706,9 @@ int mpb_sell_create(mpb_handle *h, int64_t n, const int64_t *h_row_ptr, const in
   *out = nullptr;
   if (n >= (int64_t(1) << 31) - 1) return MPB_ERR_INDEX32;
   const int64_t ns = (n + 31) / 32;
-  std::vector<int> sp(ns + 1);
-  int64_t acc = 0;
-  for (int64_t s = 0; s < ns; s++) {
-    int64_t width = 0;
-    const int64_t r1 = std::min<int64_t>(n, 32 * s + 32);
-    for (int64_t r = 32 * s; r < r1; r++) width = std::max<int64_t>(width, h_row_ptr[r + 1] - h_row_ptr[r]);
-    if (acc >= (int64_t(1) << 31)) return MPB_ERR_INDEX32;
-    sp[s] = static_cast<int>(acc);
-    acc += 32 * width;
-  }
-  if (acc >= (int64_t(1) << 31)) return MPB_ERR_INDEX32;
-  sp[ns] = static_cast<int>(acc);
+  std::vector<int> sp;
+  if (!sell_slice_ptrs(n, h_row_ptr, sp)) return MPB_ERR_INDEX32;
+  const int64_t acc = sp[ns];
   MPB_CUDA(cudaSetDevice(h->device));
   mpb_sell *S = new mpb_sell();
   S->n = n;
@@ -672,6 +790,7 @@ static int apply_bufs_scratch(mpb_handle *h, const mpb_plan *p, int64_t n, size_
 template <typename T>
 static int apply_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, int k, int t, const T *r, T *z) {
   int rc = check_sell(A, sizeof(T) == 8, sizeof(T) == 4);
+  if (rc == MPB_OK) rc = check_bound(plan, A);
   if (rc) return rc;
   if (!h || !plan || !r || !z) return MPB_ERR_ARG;
   if (plan->n != A->n) return MPB_ERR_PARTITION;
@@ -696,6 +815,7 @@ int mpb_bjac_apply_f32(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, in
 int mpb_fmp_apply(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, int k, int t, const double *r, double *z,
                   int64_t *h_overflow_count, int64_t *h_first_index) {
   int rc = check_sell(A, false, true);
+  if (rc == MPB_OK) rc = check_bound(plan, A);
   if (rc) return rc;
   if (!h || !plan || !r || !z) return MPB_ERR_ARG;
   if (plan->n != A->n) return MPB_ERR_PARTITION;
@@ -758,15 +878,24 @@ int64_t mpb_solve_workspace_bytes(const mpb_plan *plan, int64_t n) {
   return static_cast<int64_t>(carve(plan, n, nullptr).bytes);
 }
 
+static TileGeom spmv_geom(const mpb_plan *p) {
+  TileGeom g = geom_for<double>(p);
+  g.ns = pick_stages(k_spmv_pq, spmv_layout(g).bytes);
+  return g;
+}
+
+static uint32_t spmv_dyn_smem(const mpb_plan *p) {
+  const TileGeom g = spmv_geom(p);
+  return g.ns * spmv_layout(g).bytes;
+}
+
 static SpmvArgs spmv_args(const mpb_plan *p, const mpb_csr *A, const SolveWs &w) {
   SpmvArgs sa{};
   sa.sp = A->sell->d_sp;
   sa.scol = A->sell->d_col;
   sa.sval = A->sell_val64;
-  sa.tile_lo = p->d_tile_lo;
-  sa.ntiles = static_cast<int>(p->ntiles);
-  sa.z32 = w.z32;
-  sa.z64 = w.z64;
+  sa.td = p->d_td;
+  sa.g = spmv_geom(p);
   sa.p0 = w.p0;
   sa.p1 = w.p1;
   sa.q = w.q;
@@ -795,13 +924,20 @@ static int enqueue_iteration(mpb_handle *h, cudaStream_t s, const mpb_plan *p, c
                                  &w.st->ovf_first, w.st, 1, bb);
     if (rc) return rc;
   }
-  k_spmv_pq<<<nt, kCtaThreads, 0, s>>>(spmv_args(p, A, w));
+  k_pupdate<<<persistent_grid(k_pupdate, 0, p->ntiles), kCtaThreads, 0, s>>>(p->d_td, static_cast<int>(nt), w.z32,
+                                                                              w.z64, w.p0, w.p1, w.st);
   MPB_LAUNCHED(h);
-  k_update<<<nt, kCtaThreads, 0, s>>>(p->d_tile_lo, static_cast<int>(nt), x, w.p0, w.p1, w.q, w.r, w.part, w.st);
+  {
+    const uint32_t dyn = spmv_dyn_smem(p);
+    k_spmv_pq<<<persistent_grid(k_spmv_pq, dyn, p->ntiles, kWsThreads), kWsThreads, dyn, s>>>(spmv_args(p, A, w));
+  }
+  MPB_LAUNCHED(h);
+  k_update<<<persistent_grid(k_update, 0, p->ntiles), kCtaThreads, 0, s>>>(p->d_td, static_cast<int>(nt), x, w.p0,
+                                                                            w.p1, w.q, w.r, w.part, w.st);
   MPB_LAUNCHED(h);
   if (o->true_stride > 0) {
-    k_resid<true><<<nt, kCtaThreads, 0, s>>>(A->sell->d_sp, A->sell->d_col, A->sell_val64,
-                                              p->d_tile_lo, static_cast<int>(nt), b, x, nullptr, w.part, w.st, 1,
+    k_resid<true><<<persistent_grid(k_resid<true>, 0, p->ntiles), kCtaThreads, 0, s>>>(
+                                              A->sell->d_sp, A->sell->d_col, A->sell_val64, p->d_td, static_cast<int>(nt), b, x, nullptr, w.part, w.st, 1,
                                               kStepTrue);
     MPB_LAUNCHED(h);
   }
@@ -815,6 +951,7 @@ int mpb_pcg_solve(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, const m
   if (opt->kind < MPB_UNIFORM || opt->kind > MPB_ADAPTIVE_LH) return MPB_ERR_POLICY;
   if (!A || (opt->kind != MPB_UNIFORM && !A->sell_val32)) return MPB_ERR_POLICY;
   int rc = check_sell(A, true, opt->kind != MPB_UNIFORM);
+  if (rc == MPB_OK) rc = check_bound(plan, A);
   if (rc) return rc;
   if (!h || !plan || !b || !x || !tr_relres || !tr_true || !tr_branch || !tr_time || !res || !workspace)
     return MPB_ERR_ARG;
@@ -851,12 +988,12 @@ int mpb_pcg_solve(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, const m
   if (!opt->has_x0) MPB_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * A->n, s));
   // r0 = b - A x0 (or b) and ||r0|| (solver.py:118-130)
   if (opt->has_x0) {
-    k_resid<true><<<nt, kCtaThreads, 0, s>>>(A->sell->d_sp, A->sell->d_col, A->sell_val64,
-                                              plan->d_tile_lo, static_cast<int>(nt), b, x, w.r, w.part, w.st, 0,
+    k_resid<true><<<persistent_grid(k_resid<true>, 0, plan->ntiles), kCtaThreads, 0, s>>>(
+                                              A->sell->d_sp, A->sell->d_col, A->sell_val64, plan->d_td, static_cast<int>(nt), b, x, w.r, w.part, w.st, 0,
                                               kStepR0);
   } else {
-    k_resid<false><<<nt, kCtaThreads, 0, s>>>(A->sell->d_sp, A->sell->d_col, A->sell_val64,
-                                               plan->d_tile_lo, static_cast<int>(nt), b, nullptr, w.r, w.part, w.st,
+    k_resid<false><<<persistent_grid(k_resid<false>, 0, plan->ntiles), kCtaThreads, 0, s>>>(
+                                               A->sell->d_sp, A->sell->d_col, A->sell_val64, plan->d_td, static_cast<int>(nt), b, nullptr, w.r, w.part, w.st,
                                                0, kStepR0);
   }
   MPB_LAUNCHED(h);
@@ -930,8 +1067,8 @@ int mpb_pcg_solve(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, const m
   MPB_CUDA(cudaEventRecord(h->ev_t1, s));
   const SolverState st = *h->h_state;
   if (st.error == kOk) {  // final true residual (solver.py:179-182)
-    k_resid<true><<<nt, kCtaThreads, 0, s>>>(A->sell->d_sp, A->sell->d_col, A->sell_val64,
-                                              plan->d_tile_lo, static_cast<int>(nt), b, x, nullptr, w.part, w.st, 0,
+    k_resid<true><<<persistent_grid(k_resid<true>, 0, plan->ntiles), kCtaThreads, 0, s>>>(
+                                              A->sell->d_sp, A->sell->d_col, A->sell_val64, plan->d_td, static_cast<int>(nt), b, x, nullptr, w.part, w.st, 0,
                                               kStepFinal);
     MPB_LAUNCHED(h);
     MPB_CUDA(cudaMemcpyAsync(h->h_state, w.st, sizeof(SolverState), cudaMemcpyDeviceToHost, s));
@@ -963,6 +1100,7 @@ int mpb_profile_iteration(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A,
                           double *h_ms) {
   if (!opt) return MPB_ERR_ARG;
   int rc = check_sell(A, true, branch == 1);
+  if (rc == MPB_OK) rc = check_bound(plan, A);
   if (rc) return rc;
   if (!h || !plan || !b || !x || !workspace || !h_ms || reps < 1) return MPB_ERR_ARG;
   SolveWs w = carve(plan, A->n, static_cast<char *>(workspace));
@@ -993,7 +1131,7 @@ int mpb_profile_iteration(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A,
   auto reset = [&]() -> cudaError_t {
     return cudaMemcpyAsync(w.st, h->h_state, sizeof(SolverState), cudaMemcpyHostToDevice, s);
   };
-  for (int i = 0; i < 8; i++) h_ms[i] = 0.0;
+  for (int i = 0; i < 8; i++) h_ms[i] = 0.0;  // 7: p-update
   const unsigned nt = static_cast<unsigned>(plan->ntiles);
   auto timed = [&](int slot, auto &&launch) -> int {
     float total = 0.f;
@@ -1018,12 +1156,10 @@ int mpb_profile_iteration(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A,
     auto setup = [&](auto &a, auto zA, auto zB, auto zfinal, int want) {
       a.sp = A->sell->d_sp;
       a.scol = A->sell->d_col;
-      a.tile_lo = plan->d_tile_lo;
-      a.tile_bf = plan->d_tile_bf;
-      a.tile_bl = plan->d_tile_bl;
+      a.td = plan->d_td;
+      a.meta = plan->d_meta;
       a.boff = plan->d_boff;
       a.t = opt->t;
-      a.ntiles = static_cast<int>(plan->ntiles);
       a.r64 = w.r;
       a.st = w.st;
       a.want_branch = want;
@@ -1036,6 +1172,7 @@ int mpb_profile_iteration(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A,
       PassArgs<double> a{};
       setup(a, bb.zA, bb.zB, w.z64, 0);
       a.sval = A->sell_val64;
+      a.g = geom_for<double>(plan);
       if (first && last) return launch_pass<double, true, true>(h, s, plan, a, bb);
       if (first) return launch_pass<double, true, false>(h, s, plan, a, bb);
       if (last) return launch_pass<double, false, true>(h, s, plan, a, bb);
@@ -1045,6 +1182,7 @@ int mpb_profile_iteration(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A,
     PassArgs<float> a{};
     setup(a, bb.zA, bb.zB, w.z32, 1);
     a.sval = A->sell_val32;
+    a.g = geom_for<float>(plan);
     a.ovf_count = &w.st->ovf_count;
     a.ovf_first = &w.st->ovf_first;
     if (first && last) return launch_pass<float, true, true>(h, s, plan, a, bb);
@@ -1058,21 +1196,31 @@ int mpb_profile_iteration(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A,
     if (rc) return rc;
   }
   const SpmvArgs sa = spmv_args(plan, A, w);
+  const uint32_t sdyn = spmv_dyn_smem(plan);
+  const int sgrid = persistent_grid(k_spmv_pq, sdyn, plan->ntiles, kWsThreads);
+  const int ugrid = persistent_grid(k_update, 0, plan->ntiles);
+  const int pgrid = persistent_grid(k_pupdate, 0, plan->ntiles);
+  rc = timed(7, [&]() -> int {
+    k_pupdate<<<pgrid, kCtaThreads, 0, s>>>(plan->d_td, static_cast<int>(nt), w.z32, w.z64, w.p0, w.p1, w.st);
+    MPB_LAUNCHED(h);
+    return MPB_OK;
+  });
+  if (rc) return rc;
   rc = timed(3, [&]() -> int {
-    k_spmv_pq<<<nt, kCtaThreads, 0, s>>>(sa);
+    k_spmv_pq<<<sgrid, kWsThreads, sdyn, s>>>(sa);
     MPB_LAUNCHED(h);
     return MPB_OK;
   });
   if (rc) return rc;
   rc = timed(4, [&]() -> int {
-    k_update<<<nt, kCtaThreads, 0, s>>>(plan->d_tile_lo, static_cast<int>(nt), x, w.p0, w.p1, w.q, w.r, w.part,
+    k_update<<<ugrid, kCtaThreads, 0, s>>>(plan->d_td, static_cast<int>(nt), x, w.p0, w.p1, w.q, w.r, w.part,
                                          w.st);
     MPB_LAUNCHED(h);
     return MPB_OK;
   });
   if (rc) return rc;
   h_ms[5] = 0.0;  // scalar steps are fused into the kernels above
-  h_ms[6] = h_ms[0] + h_ms[1] * (opt->k > 2 ? opt->k - 2 : 0) + h_ms[2] + h_ms[3] + h_ms[4];
+  h_ms[6] = h_ms[0] + h_ms[1] * (opt->k > 2 ? opt->k - 2 : 0) + h_ms[2] + h_ms[3] + h_ms[4] + h_ms[7];
   MPB_CUDA(cudaEventRecord(h->ev_out, s));
   MPB_CUDA(cudaStreamWaitEvent(h->user, h->ev_out, 0));
   return MPB_OK;
@@ -1089,8 +1237,8 @@ int mpb_true_relres(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, const
   if (rc) return rc;
   double *part = static_cast<double *>(h->scratch);
   double *out = reinterpret_cast<double *>(static_cast<char *>(h->scratch) + al256(sizeof(double) * (nt + 1)));
-  k_resid<true><<<static_cast<unsigned>(nt), kCtaThreads, 0, h->user>>>(
-      A->sell->d_sp, A->sell->d_col, A->sell_val64, plan->d_tile_lo, static_cast<int>(nt), b, x, nullptr,
+  k_resid<true><<<persistent_grid(k_resid<true>, 0, nt), kCtaThreads, 0, h->user>>>(
+      A->sell->d_sp, A->sell->d_col, A->sell_val64, plan->d_td, static_cast<int>(nt), b, x, nullptr,
       part, nullptr, 0, kStepFinal);
   MPB_LAUNCHED(h);
   k_fin<double><<<1, kFinThreads, 0, h->user>>>(part, nt, out);

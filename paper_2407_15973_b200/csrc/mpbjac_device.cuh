@@ -16,7 +16,7 @@ constexpr int kTileThreads = MPB_TILE_THREADS;  // lanes of the tile sum order
 constexpr int kTileRows = MPB_TILE_MAX_ROWS;
 constexpr int kCtaThreads = kTileRows;           // tile kernels: one thread per row
 constexpr int kFinThreads = MPB_FIN_THREADS;
-static_assert(kTileRows == 2 * kTileThreads, "lane j sums rows j and j + kTileThreads");
+static_assert(kTileRows == kTileThreads, "one lane of the tile sum per row");
 
 // ---------------------------------------------------------------------------
 // solver state (device resident; one per solve)
@@ -92,6 +92,29 @@ __device__ __forceinline__ R block_tree(R v, R *ws) {
   return r;
 }
 
+// Named barrier among the first `n` threads (consumer warps of a
+// warp-specialised CTA; the producer warp does not take part).
+__device__ __forceinline__ void named_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// block_tree over the first NT threads using named barrier `bar`.
+template <int NT, typename R>
+__device__ __forceinline__ R block_tree_nb(R v, R *ws, int bar) {
+  static_assert(NT % 32 == 0 && NT <= 1024, "block size");
+  v = warp_bfly(v);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  named_sync(bar, NT);
+  if (lane == 0) ws[warp] = v;
+  named_sync(bar, NT);
+  R r = R(0);
+  if (warp == 0) {
+    r = lane < NT / 32 ? ws[lane] : R(0);
+    r = warp_bfly(r);
+  }
+  return r;
+}
+
 // Global sum of tile partials, steps 1-3 with kFinThreads lanes.  Called by
 // all threads of a CTA with at least kFinThreads threads (threads beyond
 // kFinThreads contribute nothing); result valid in thread 0.  Partials are
@@ -115,16 +138,14 @@ __device__ __forceinline__ double fin_sum(const double *part, long long count, d
   return block_tree<kFinThreads>(acc, ws);
 }
 
-// Thread 0 publishes `v` to part[slot] and takes a ticket; true in every
-// thread of the CTA that finished last among `nblocks` (all partials then
-// visible).  Must be called by all threads.
-__device__ __forceinline__ bool publish_last(double v, double *part, int slot, unsigned int *ticket,
-                                             unsigned int nblocks) {
+// Grid-wide "last CTA" detection: thread 0 fences (its tile partials become
+// visible) and takes a ticket; true in every thread of the CTA that finished
+// last among the kernel's gridDim.x CTAs.  Must be called by all threads.
+__device__ __forceinline__ bool grid_last(unsigned int *ticket) {
   __shared__ int am_last;
   if (threadIdx.x == 0) {
-    part[slot] = v;
     __threadfence();
-    am_last = ticket == nullptr ? 0 : (atomicAdd(ticket, 1u) == nblocks - 1u);
+    am_last = atomicAdd(ticket, 1u) == gridDim.x - 1u;
   }
   __syncthreads();
   if (am_last) __threadfence();

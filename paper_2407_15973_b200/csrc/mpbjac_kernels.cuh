@@ -1,37 +1,46 @@
 // mpbjac_kernels.cuh — the sm_100a kernels of the mixed-precision BJAC-PCG
 // hot path.
 //
-// Matrix layout on the hot path: SELL-32 (sliced ELLPACK, slice height 32 =
-// one warp, no row sorting).  Row r lives in slice r/32, lane r%32; its j-th
-// stored entry (CSR order, i.e. ascending column) is at
-// slice_ptr[r/32] + 32*j + r%32.  A warp therefore loads 32 rows' j-th entries
-// with one coalesced 128/256-byte access, while every thread still owns one
-// row and accumulates it sequentially in ascending column order without FMA —
-// which is what makes the kernels bit-identical to the reference's
-// row-sequential numba kernels (pkg/src/mpcg/kernels_numba.py:37-70).
-// Padding (slice width = longest row of the slice) carries column -1 and is
-// skipped, so the hot kernels need no row_ptr at all.  Each CTA owns one tile
-// (whole BJAC blocks, <= 512 rows) with one thread per row.
+// Matrix layout: SELL-32 (sliced ELLPACK, slice height 32 = one warp, rows
+// in original order).  Row r lives in slice r/32, lane r%32; its j-th stored
+// entry (CSR order = ascending column) is at sp[r/32] + 32*j + r%32; padding
+// slots carry column -1.  Every thread owns one row and accumulates it
+// sequentially in ascending column order without FMA, which makes the kernels
+// bit-identical to the reference's row-sequential numba kernels
+// (pkg/src/mpcg/kernels_numba.py:37-70).
+//
+// Work unit: a tile of whole BJAC blocks (<= 512 rows), one thread per row.
+// The hot kernels are persistent and warp-specialised: warp 16 of each CTA
+// is a TMA producer that streams every input of the next tiles (SELL columns
+// and values, slice pointers, per-row metadata, the residual and the tile's
+// own vector slices) into a ring of shared-memory stages (cp.async.bulk +
+// full/empty mbarriers); warps 0-15 only compute.  Per-row static structure
+// (row length, diagonal slot, in-block slot range) is precomputed once per
+// (matrix, partition) into 2 bytes per row, so the hot loops do no searching.
 //
 // Dot products follow the fixed tile-tree order of include/mpbjac_order.h.
 // The scalar steps of the recurrence (rho, alpha, beta, relres, the aMP
-// branch, error flags, trace) are executed by the last CTA of the kernel that
-// produces the corresponding partials (ticket in SolverState), so an
-// iteration is 4 kernels (k = 2: BJAC first pass, BJAC last pass, fused
-// p-update+SpMV, x/r update).
+// branch, error flags, trace) run in the last CTA of the kernel producing
+// their partials, so an iteration is 4 kernels (k = 2).
 #pragma once
+#include <type_traits>
+
 #include "mpbjac_device.cuh"
 
 namespace mpb {
 
-constexpr int kChunk = 8;  // row entries held in registers (stencils: all of them)
+constexpr int kSlots = 9;                      // register-resident row entries (stencils, 3-T rows)
+constexpr int kConsumers = kCtaThreads;        // compute threads (one per tile row)
+constexpr int kWsThreads = kCtaThreads + 32;   // + one TMA producer warp
+constexpr int kMaxStages = 4;
+constexpr int kBarConsumers = 1;               // named barrier id among consumers
+constexpr uint16_t kMetaGeneric = 0xFFFFu;
 
-// SELL-32 access: slice s = r / 32 spans sp[s] .. sp[s+1] (width * 32
-// entries); padding slots carry column -1 and value 0.
-struct SellRow {
-  int base;   // sp[s] + r % 32
-  int width;  // slots of the slice
-};
+// ---- per-row metadata: len | dpos << 4 | i0 << 8 | i1 << 12 ---------------
+__device__ __forceinline__ int meta_len(uint16_t m) { return m & 15; }
+__device__ __forceinline__ int meta_dpos(uint16_t m) { return (m >> 4) & 15; }
+__device__ __forceinline__ int meta_i0(uint16_t m) { return (m >> 8) & 15; }
+__device__ __forceinline__ int meta_i1(uint16_t m) { return m >> 12; }
 
 // ---------------------------------------------------------------------------
 // scalar steps of the recurrence (solver.py:128-177, policies.py:102-116)
@@ -127,27 +136,13 @@ __device__ __noinline__ void scalar_step(int step, double tot, SolverState *st) 
   }
 }
 
-// Tile sum in the fixed order with one thread per row (kCtaThreads = 512):
-// lane j < 256 adds its rows j and j + 256 in that order (rows past `count`
-// skipped), then the 256 lanes are reduced by block_tree.  Called by all
-// threads; result valid in thread 0.
-__device__ __forceinline__ double tile_sum(double v, int count, double *s_hi, double *ws) {
-  const int tid = threadIdx.x;
-  if (tid >= kTileThreads) s_hi[tid - kTileThreads] = v;
-  __syncthreads();
-  double acc = 0.0;
-  if (tid < kTileThreads) {
-    if (tid < count) acc = __dadd_rn(acc, v);
-    if (tid + kTileThreads < count) acc = __dadd_rn(acc, s_hi[tid]);
-  }
-  return block_tree<kTileThreads>(acc, ws);
-}
-
-// Publish the tile partial; the CTA that finishes last reduces all partials
-// in the fixed order and runs the scalar step (solve mode: st != null).
-__device__ __forceinline__ void publish_and_finish(double tile_total, double *part, int tile, unsigned ntiles,
-                                                   SolverState *st, int ticket, int step, double *ws) {
-  if (!publish_last(tile_total, part, tile, st ? &st->ticket[ticket] : nullptr, ntiles)) return;
+// After a kernel's CTAs have written all tile partials: the CTA that
+// finishes last reduces them in the fixed order and runs the scalar step.
+// Called by all threads of the CTA.
+__device__ __forceinline__ void finish_grid(SolverState *st, int ticket, int step, const double *part, int ntiles,
+                                            double *ws) {
+  if (st == nullptr) return;
+  if (!grid_last(&st->ticket[ticket])) return;
   const double tot = fin_sum(part, ntiles, ws);
   if (threadIdx.x == 0) {
     scalar_step(step, tot, st);
@@ -156,31 +151,172 @@ __device__ __forceinline__ void publish_and_finish(double tile_total, double *pa
 }
 
 // ---------------------------------------------------------------------------
+// tiles: descriptor, geometry, TMA stage layout
+// ---------------------------------------------------------------------------
+struct TileDesc {
+  int lo, hi;   // rows [lo, hi)
+  int s0, s1;   // SELL slices [s0, s1)
+  int e0, e1;   // SELL entries [e0, e1) = [sp[s0], sp[s1]) (multiples of 32)
+  int bf, nbk;  // blocks bf .. bf+nbk-1 overlap the tile
+};
+
+struct TileGeom {
+  int ntiles;
+  int cap_e;   // staged SELL entries per tile (max over tiles, capped)
+  int max_sl;  // max slices per tile
+  int ns;      // shared-memory stages (prefetch depth)
+};
+
+// Byte offsets of one shared-memory stage.
+struct StageLayout {
+  uint32_t col, val, sp, meta, v0, v1, v2, bytes;
+};
+__host__ __device__ inline uint32_t al16u(uint32_t b) { return (b + 15u) & ~15u; }
+// v*es: element sizes of up to three row-vector slices [lo, hi) (0: absent)
+__host__ __device__ inline StageLayout stage_layout(int cap_e, int es, int max_sl, bool meta, int v0es, int v1es,
+                                                    int v2es) {
+  StageLayout L;
+  uint32_t off = 0;
+  L.col = off;
+  off += al16u(static_cast<uint32_t>(cap_e) * 4u);
+  L.val = off;
+  off += al16u(static_cast<uint32_t>(cap_e) * es);
+  L.sp = off;
+  off += al16u(static_cast<uint32_t>(max_sl + 1) * 4u + 16u);
+  L.meta = off;
+  off += meta ? al16u(static_cast<uint32_t>(kTileRows) * 2u + 16u) : 0u;
+  L.v0 = off;
+  off += v0es ? al16u(static_cast<uint32_t>(kTileRows) * v0es + 16u) : 0u;
+  L.v1 = off;
+  off += v1es ? al16u(static_cast<uint32_t>(kTileRows) * v1es + 16u) : 0u;
+  L.v2 = off;
+  off += v2es ? al16u(static_cast<uint32_t>(kTileRows) * v2es + 16u) : 0u;
+  L.bytes = off;
+  return L;
+}
+
+// Ring of shared-memory stages filled by the producer warp.
+struct Ring {
+  uint64_t full[kMaxStages];   // TMA bytes landed
+  uint64_t empty[kMaxStages];  // consumers done with the stage
+  int ok[kMaxStages];          // tile fitted and was staged
+  TileDesc desc[kMaxStages];
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <typename E>
+__device__ __forceinline__ void tma_window(unsigned char *dst, const E *base, int lo, int hi, uint64_t *bar) {
+  const Window w = window_of(base, lo, hi);
+  bulk_g2s(dst, reinterpret_cast<const void *>(w.g0), w.bytes, bar);
+}
+template <typename E>
+__device__ __forceinline__ uint32_t window_bytes(const E *base, int lo, int hi) {
+  return base == nullptr ? 0u : window_of(base, lo, hi).bytes;
+}
+template <typename E>
+__device__ __forceinline__ const E *staged(const unsigned char *region, const E *base, int lo, int hi) {
+  return reinterpret_cast<const E *>(region + window_of(base, lo, hi).skew);
+}
+
+// Producer: stage tile `tile` into ring slot st (thread = producer lane 0).
+template <typename T, typename V0, typename V1, typename V2>
+__device__ __forceinline__ void produce(Ring &R, int st, const TileDesc *td, int tile, const TileGeom &g,
+                                        const StageLayout &L, unsigned char *stage, const int *sp, const int *scol,
+                                        const T *sval, const uint16_t *meta, const V0 *v0, const V1 *v1,
+                                        const V2 *v2) {
+  const TileDesc d = td[tile];
+  R.desc[st] = d;
+  const int nent = d.e1 - d.e0;
+  const bool fits = nent <= g.cap_e && (d.s1 - d.s0) <= g.max_sl;
+  R.ok[st] = fits ? 1 : 0;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (!fits) {
+    mbar_arrive(&R.full[st]);
+    return;
+  }
+  uint32_t bytes = static_cast<uint32_t>(nent) * (4u + sizeof(T)) + window_bytes(sp, d.s0, d.s1 + 1) +
+                   window_bytes(meta, d.lo, d.hi) + window_bytes(v0, d.lo, d.hi) + window_bytes(v1, d.lo, d.hi) +
+                   window_bytes(v2, d.lo, d.hi);
+  mbar_arrive_expect_tx(&R.full[st], bytes);
+  bulk_g2s(stage + L.col, scol + d.e0, static_cast<uint32_t>(nent) * 4u, &R.full[st]);
+  bulk_g2s(stage + L.val, sval + d.e0, static_cast<uint32_t>(nent) * sizeof(T), &R.full[st]);
+  tma_window(stage + L.sp, sp, d.s0, d.s1 + 1, &R.full[st]);
+  if (meta != nullptr) tma_window(stage + L.meta, meta, d.lo, d.hi, &R.full[st]);
+  if (v0 != nullptr) tma_window(stage + L.v0, v0, d.lo, d.hi, &R.full[st]);
+  if (v1 != nullptr) tma_window(stage + L.v1, v1, d.lo, d.hi, &R.full[st]);
+  if (v2 != nullptr) tma_window(stage + L.v2, v2, d.lo, d.hi, &R.full[st]);
+}
+
+// Producer loop (warp 16, lane 0): walks the CTA's tiles, waiting for a
+// stage to be released before refilling it.
+template <typename F>
+__device__ __forceinline__ void producer_loop(Ring &R, int ntiles, int ns, F &&fill) {
+  int st = 0, rnd = 0;  // stage, and how often it has been filled before
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    if (rnd > 0) mbar_wait(&R.empty[st], (rnd - 1) & 1);
+    fill(st, tile);
+    if (++st == ns) {
+      st = 0;
+      rnd++;
+    }
+  }
+}
+
+// consumer-side ring cursor: stage and mbarrier parity of the i-th tile
+struct RingCursor {
+  int st = 0, phase = 0;
+  __device__ __forceinline__ void advance(int ns) {
+    if (++st == ns) {
+      st = 0;
+      phase ^= 1;
+    }
+  }
+};
+
+__device__ __forceinline__ void ring_init(Ring &R, int ns) {
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < ns; st++) {
+      mbar_init(&R.full[st], 1);
+      mbar_init(&R.empty[st], kConsumers / 32);
+    }
+  }
+  __syncthreads();
+}
+
+// consumer warp releases its use of a stage (one arrive per warp)
+__device__ __forceinline__ void ring_release(Ring &R, int st) {
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive(&R.empty[st]);
+}
+
+// ---------------------------------------------------------------------------
 // fused block-Jacobi pass: z_out = z_in + D_b^{-1}(r - A z_in)
 // (bjac.py:127-149 one outer pass; kernels_numba.py:48-70 the t inner sweeps)
 // ---------------------------------------------------------------------------
 template <typename T>
 struct PassArgs {
-  const int *sp;       // SELL slice_ptr
-  const int *scol;     // SELL columns (-1 = padding)
-  const T *sval;       // SELL values in storage precision
-  const int *tile_lo;  // ntiles+1 row offsets
-  const int *tile_bf;  // first block overlapping each tile
-  const int *tile_bl;  // last block overlapping each tile
-  const int *boff;     // nb+1 block offsets
+  const int *sp;         // SELL slice_ptr
+  const int *scol;       // SELL columns (-1 = padding)
+  const T *sval;         // SELL values in storage precision
+  const uint16_t *meta;  // per-row static structure (plan-bound)
+  const TileDesc *td;    // tile descriptors
+  const int *boff;       // nb+1 block offsets (generic rows, large blocks)
+  TileGeom g;
   int t;
-  int ntiles;
-  const double *r64;   // fp64 residual, narrowed on load for T=float ...
-  const T *rT;         // ... or a residual already in T (when r64 == null)
-  const T *zin;        // previous pass output (null on the first pass)
-  T *zout;             // storage-precision output (may be null)
-  double *zout64;      // widened output (may be null)
-  double *part;        // r.z tile partials (last pass, needs r64)
+  const double *r64;     // fp64 residual, narrowed on load for T=float ...
+  const T *rT;           // ... or a residual already in T (when r64 == null)
+  const T *zin;          // previous pass output (null on the first pass)
+  T *zout;               // storage-precision output (may be null)
+  double *zout64;        // widened output (may be null)
+  double *part;          // r.z tile partials (last pass, needs r64)
   unsigned long long *ovf_count;  // narrowing overflow (first pass, T=float)
   long long *ovf_first;
-  T *resbuf;           // large-block path
+  T *resbuf;             // large-block path
   T *dbuf;
-  SolverState *st;     // solve mode: gate + fused scalar step
+  SolverState *st;       // solve mode: gate + fused scalar step
   int want_branch;
 };
 
@@ -190,140 +326,192 @@ __device__ __forceinline__ bool gated_off(const PassArgs<T> &a) {
 }
 
 template <typename T>
-__device__ __forceinline__ T load_residual(const PassArgs<T> &a, int row, bool check_ovf) {
-  if (a.r64 != nullptr) {
-    const double r = a.r64[row];
-    const T v = narrow_or_copy<T>(r);
-    if (sizeof(T) == 4 && check_ovf && a.ovf_count != nullptr && isinf(v) && isfinite(r)) {
-      atomicAdd(a.ovf_count, 1ull);
-      atomicMin(a.ovf_first, static_cast<long long>(row));
-    }
-    return v;
+__device__ __forceinline__ T narrow_checked(const PassArgs<T> &a, double r, int row, bool check_ovf) {
+  const T v = narrow_or_copy<T>(r);
+  if (sizeof(T) == 4 && check_ovf && a.ovf_count != nullptr && isinf(v) && isfinite(r)) {
+    atomicAdd(a.ovf_count, 1ull);
+    atomicMin(a.ovf_first, static_cast<long long>(row));
   }
-  return a.rT[row];
+  return v;
 }
 
-// block [blo, bhi) containing local row rl; s_boff holds nbk+1 local offsets
-__device__ __forceinline__ void find_block(const int *s_boff, int nbk, int rl, int &blo, int &bhi) {
+// block [blo, bhi) containing `row`; b holds nbk+1 absolute offsets
+__device__ __forceinline__ void find_block_abs(const int *b, int nbk, int row, int &blo, int &bhi) {
   int L = 0, H = nbk;
   while (H - L > 1) {
     const int M = (L + H) >> 1;
-    if (s_boff[M] <= rl) L = M; else H = M;
+    if (b[M] <= row) L = M; else H = M;
   }
-  blo = s_boff[L];
-  bhi = s_boff[L + 1];
+  blo = b[L];
+  bhi = b[L + 1];
 }
 
-// Shared tile prologue: slice pointers of the tile (s_sp) and block offsets
-// (s_boff) into shared memory.
-__device__ __forceinline__ void load_tile_tables(const int *sp, int lo, int hi, int *s_sp, const int *boff, int bf,
-                                                 int nbk, int *s_boff) {
-  const int s0 = lo >> 5, s1 = (hi + 31) >> 5;
-  for (int j = threadIdx.x; j <= s1 - s0; j += blockDim.x) s_sp[j] = sp[s0 + j];
-  if (s_boff != nullptr)
-    for (int j = threadIdx.x; j <= nbk; j += blockDim.x) s_boff[j] = boff[bf + j] - lo;
-}
-
-__device__ __forceinline__ SellRow sell_row(const int *s_sp, int lo, int row) {
-  const int s = (row >> 5) - (lo >> 5);
-  SellRow r;
-  r.base = s_sp[s] + (row & 31);
-  r.width = (s_sp[s + 1] - s_sp[s]) >> 5;
-  return r;
-}
-
-// fused pass, one tile (whole blocks) per CTA, one row per thread
-template <typename T, bool FIRST, bool LAST>
-__global__ void __launch_bounds__(kCtaThreads) k_bjac_tile(const PassArgs<T> a) {
-  if (gated_off(a)) return;
-  __shared__ T s_w[kTileRows];
-  __shared__ int s_boff[kTileRows + 2];
-  __shared__ int s_sp[kTileRows / 32 + 2];
-  __shared__ double s_hi[kTileThreads];
-  __shared__ double ws[32];
-  const int tid = threadIdx.x, tile = blockIdx.x;
-  const int lo = a.tile_lo[tile], hi = a.tile_lo[tile + 1];
-  const int bf = a.tile_bf[tile], nbk = a.tile_bl[tile] - bf + 1;
-  const int row = lo + tid;
-  const bool valid = row < hi;
-  const T rv = valid ? load_residual(a, row, FIRST) : T(0);
-  const T zown = (!FIRST && valid) ? __ldg(a.zin + row) : T(0);
-  load_tile_tables(a.sp, lo, hi, s_sp, a.boff, bf, nbk, s_boff);
-  __syncthreads();
-  // (1) row scan in ascending column order: az = A z_in, the diagonal and
-  //     the in-block slots (registers); rows wider than kChunk re-read
-  int c[kChunk];
-  T v[kChunk];
-  T res = T(0), d = T(1), w = T(0);
-  int blo = 0, bhi = 0;
-  SellRow sr{0, 0};
-  if (valid) {
-    sr = sell_row(s_sp, lo, row);
-    find_block(s_boff, nbk, tid, blo, bhi);
-    blo += lo;
-    bhi += lo;
-#pragma unroll
-    for (int u = 0; u < kChunk; u++) {
-      const bool ok = u < sr.width;
-      c[u] = ok ? __ldg(a.scol + sr.base + 32 * u) : -1;
-      v[u] = ok ? __ldg(a.sval + sr.base + 32 * u) : T(0);
-    }
-    T g[kChunk];
+// Generic row of a pass (rows whose structure does not fit the metadata):
+// scans its SELL entries with explicit block bounds.  Returns res; sets d.
+template <typename T, bool FIRST>
+__device__ __forceinline__ T generic_row_scan(const PassArgs<T> &a, const TileDesc &d, int row, int base, int width,
+                                              const int *col, const T *val, const T *zt, T rv, T &dd) {
+  const unsigned span = static_cast<unsigned>(d.hi - d.lo);
+  T az = T(0);
+  dd = T(0);
+  for (int j = 0; j < width; j++) {
+    const int cj = col[base + 32 * j];
+    if (cj < 0) continue;
+    const T vj = val[base + 32 * j];
     if (!FIRST) {
-#pragma unroll
-      for (int u = 0; u < kChunk; u++) g[u] = c[u] >= 0 ? __ldg(a.zin + c[u]) : T(0);
+      const unsigned o = static_cast<unsigned>(cj - d.lo);
+      az = add_rn(az, mul_rn(vj, o < span ? zt[o] : __ldg(a.zin + cj)));
     }
-    T az = T(0), dd = T(0);
+    if (cj == row) dd = vj;
+  }
+  return FIRST ? rv : sub_rn(rv, az);
+}
+
+template <typename T>
+__device__ __forceinline__ T generic_row_sweep(const PassArgs<T> &a, const TileDesc &d, int row, int base, int width,
+                                               const int *col, const T *val, const T *s_w) {
+  int blo, bhi;
+  find_block_abs(a.boff + d.bf, d.nbk, row, blo, bhi);
+  T acc = T(0);
+  for (int j = 0; j < width; j++) {
+    const int cj = col[base + 32 * j];
+    if (cj >= blo && cj < bhi) acc = add_rn(acc, mul_rn(val[base + 32 * j], s_w[cj - d.lo]));
+  }
+  return acc;
+}
+
+// One tile of a fused pass, consumer threads only.  Pointers are either the
+// shared stage or the global arrays offset to the tile (same indexing).
+template <typename T, bool FIRST, bool LAST>
+__device__ __forceinline__ void bjac_tile_body(const PassArgs<T> &a, int tile, const TileDesc &d, const int *col,
+                                               const T *val, const int *spp, const uint16_t *mt, const double *r64t,
+                                               const T *rTt, const T *zt, T *s_w, double *ws) {
+  const int tid = threadIdx.x;
+  const int lo = d.lo, hi = d.hi, row = lo + tid;
+  const bool valid = row < hi;
+  const unsigned span = static_cast<unsigned>(hi - lo);
+  T res = T(0), dd = T(1), w = T(0), zown = T(0);
+  uint16_t m = 0;
+  int base = 0, width = 0, i0 = 0, i1 = 0;
+  if (valid) {
+    const int si = (row >> 5) - d.s0;
+    const int sb = spp[si];
+    width = (spp[si + 1] - sb) >> 5;
+    base = sb - d.e0 + (row & 31);
+    m = mt[tid];
+    const T rv = r64t != nullptr ? narrow_checked(a, r64t[tid], row, FIRST) : rTt[tid];
+    if (!FIRST) zown = zt[tid];
+    if (m != kMetaGeneric) {
+      i0 = meta_i0(m);
+      i1 = meta_i1(m);
+      T az = T(0);
+      if (!FIRST) {  // az = A z_in, all slots, ascending column
+        const int len = meta_len(m);
+        int c[kSlots];
+        T v[kSlots], g[kSlots];
 #pragma unroll
-    for (int u = 0; u < kChunk; u++) {
-      if (c[u] >= 0) {
-        if (!FIRST) az = add_rn(az, mul_rn(v[u], g[u]));
-        if (c[u] == row) dd = v[u];
+        for (int u = 0; u < kSlots; u++) {
+          c[u] = u < len ? col[base + 32 * u] : lo;
+          v[u] = u < len ? val[base + 32 * u] : T(0);
+        }
+#pragma unroll
+        for (int u = 0; u < kSlots; u++) {
+          const unsigned o = static_cast<unsigned>(c[u] - lo);
+          g[u] = o < span ? zt[o] : __ldg(a.zin + c[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < kSlots; u++)
+          if (u < len) az = add_rn(az, mul_rn(v[u], g[u]));
       }
+      dd = val[base + 32 * meta_dpos(m)];
+      res = FIRST ? rv : sub_rn(rv, az);
+    } else {
+      res = generic_row_scan<T, FIRST>(a, d, row, base, width, col, val, zt, rv, dd);
     }
-    for (int j = kChunk; j < sr.width; j++) {  // long rows
-      const int cj = __ldg(a.scol + sr.base + 32 * j);
-      if (cj < 0) continue;
-      const T vj = __ldg(a.sval + sr.base + 32 * j);
-      if (!FIRST) az = add_rn(az, mul_rn(vj, __ldg(a.zin + cj)));
-      if (cj == row) dd = vj;
-    }
-    res = FIRST ? rv : sub_rn(rv, az);
-    d = dd;
     w = div_rn(res, dd);
     s_w[tid] = w;
   }
-  // (2) inner sweeps on the tile's blocks, w in shared memory
-  for (int s = 1; s < a.t; s++) {
-    __syncthreads();
+  for (int s = 1; s < a.t; s++) {  // inner sweeps, the tile's w in shared memory
+    named_sync(kBarConsumers, kConsumers);
     T acc = T(0);
     if (valid) {
-#pragma unroll
-      for (int u = 0; u < kChunk; u++)
-        if (c[u] >= blo && c[u] < bhi) acc = add_rn(acc, mul_rn(v[u], s_w[c[u] - lo]));
-      for (int j = kChunk; j < sr.width; j++) {
-        const int cj = __ldg(a.scol + sr.base + 32 * j);
-        if (cj >= blo && cj < bhi) acc = add_rn(acc, mul_rn(__ldg(a.sval + sr.base + 32 * j), s_w[cj - lo]));
+      if (m != kMetaGeneric) {
+        for (int j = i0; j < i1; j++) {
+          const int cj = col[base + 32 * j];
+          acc = add_rn(acc, mul_rn(val[base + 32 * j], s_w[cj - lo]));
+        }
+      } else {
+        acc = generic_row_sweep(a, d, row, base, width, col, val, s_w);
       }
     }
-    __syncthreads();
+    named_sync(kBarConsumers, kConsumers);
     if (valid) {
-      w = add_rn(w, div_rn(sub_rn(res, acc), d));
+      w = add_rn(w, div_rn(sub_rn(res, acc), dd));
       s_w[tid] = w;
     }
   }
-  // (3) z_out = z_in + w (or w); r.z partial and the fused rho step
   double prod = 0.0;
   if (valid) {
     const T zo = FIRST ? w : add_rn(zown, w);
     if (a.zout != nullptr) a.zout[row] = zo;
     if (a.zout64 != nullptr) a.zout64[row] = static_cast<double>(zo);
-    if (LAST && a.part != nullptr) prod = __dmul_rn(a.r64[row], static_cast<double>(zo));
+    if (LAST && a.part != nullptr) prod = __dmul_rn(r64t[tid], static_cast<double>(zo));
   }
   if (LAST && a.part != nullptr) {
-    const double tot = tile_sum(prod, hi - lo, s_hi, ws);
-    publish_and_finish(tot, a.part, tile, a.ntiles, a.st, 0, kStepRho, ws);
+    const double tot = block_tree_nb<kTileThreads>(prod, ws, kBarConsumers);
+    if (tid == 0) a.part[tile] = tot;
   }
+}
+
+template <typename T, bool FIRST, bool R64>
+__host__ __device__ inline StageLayout bjac_layout(const TileGeom &g) {
+  // v0: residual slice, v2: z_in slice (non-first passes)
+  return stage_layout(g.cap_e, sizeof(T), g.max_sl, true, R64 ? 8 : sizeof(T), 0, FIRST ? 0 : sizeof(T));
+}
+
+// Persistent, warp-specialised fused pass.
+template <typename T, bool FIRST, bool LAST, bool R64>
+__global__ void __launch_bounds__(kWsThreads) k_bjac_tile(const PassArgs<T> a) {
+  if (gated_off(a)) return;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ Ring R;
+  __shared__ T s_w[kTileRows];
+  __shared__ double ws[32];
+  const int ns = a.g.ns;
+  const StageLayout L = bjac_layout<T, FIRST, R64>(a.g);
+  ring_init(R, ns);
+  if (threadIdx.x >= kConsumers) {  // producer warp
+    using RT = typename std::conditional<R64, double, T>::type;
+    const RT *rsrc = R64 ? reinterpret_cast<const RT *>(a.r64) : reinterpret_cast<const RT *>(a.rT);
+    if (threadIdx.x == kConsumers)
+      producer_loop(R, a.g.ntiles, ns, [&](int st, int tile) {
+        produce<T, RT, uint8_t, T>(R, st, a.td, tile, a.g, L, smem + st * L.bytes, a.sp, a.scol, a.sval, a.meta,
+                                   rsrc, nullptr, FIRST ? nullptr : a.zin);
+      });
+  } else {
+    RingCursor cur;
+    for (int tile = blockIdx.x; tile < a.g.ntiles; tile += gridDim.x, cur.advance(ns)) {
+      const int st = cur.st;
+      mbar_wait(&R.full[st], cur.phase);
+      const TileDesc d = R.desc[st];
+      if (R.ok[st]) {
+        const unsigned char *sb = smem + st * L.bytes;
+        const double *r64t = R64 ? staged(sb + L.v0, a.r64, d.lo, d.hi) : nullptr;
+        const T *rTt = R64 ? nullptr : staged(sb + L.v0, a.rT, d.lo, d.hi);
+        const T *zt = FIRST ? nullptr : staged(sb + L.v2, a.zin, d.lo, d.hi);
+        bjac_tile_body<T, FIRST, LAST>(a, tile, d, reinterpret_cast<const int *>(sb + L.col),
+                                       reinterpret_cast<const T *>(sb + L.val),
+                                       staged(sb + L.sp, a.sp, d.s0, d.s1 + 1), staged(sb + L.meta, a.meta, d.lo, d.hi),
+                                       r64t, rTt, zt, s_w, ws);
+      } else {
+        bjac_tile_body<T, FIRST, LAST>(a, tile, d, a.scol + d.e0, a.sval + d.e0, a.sp + d.s0, a.meta + d.lo,
+                                       R64 ? a.r64 + d.lo : nullptr, R64 ? nullptr : a.rT + d.lo,
+                                       FIRST ? nullptr : a.zin + d.lo, s_w, ws);
+      }
+      ring_release(R, st);
+    }
+  }
+  if (LAST && a.part != nullptr) finish_grid(a.st, 0, kStepRho, a.part, a.g.ntiles, ws);
 }
 
 // ---- large blocks (> kTileRows rows): one launch per inner sweep ----------
@@ -331,19 +519,16 @@ __global__ void __launch_bounds__(kCtaThreads) k_bjac_tile(const PassArgs<T> a) 
 template <typename T, bool FIRST>
 __global__ void __launch_bounds__(kCtaThreads) k_big_resid(const PassArgs<T> a, T *w0) {
   if (gated_off(a)) return;
-  __shared__ int s_sp[kTileRows / 32 + 2];
-  const int lo = a.tile_lo[blockIdx.x], hi = a.tile_lo[blockIdx.x + 1];
-  load_tile_tables(a.sp, lo, hi, s_sp, nullptr, 0, 0, nullptr);
-  __syncthreads();
-  const int row = lo + threadIdx.x;
-  if (row >= hi) return;
-  const T rv = load_residual(a, row, FIRST);
-  const SellRow sr = sell_row(s_sp, lo, row);
+  const TileDesc d = a.td[blockIdx.x];
+  const int row = d.lo + threadIdx.x;
+  if (row >= d.hi) return;
+  const T rv = a.r64 != nullptr ? narrow_checked(a, a.r64[row], row, FIRST) : a.rT[row];
+  const int s = row >> 5, sb = a.sp[s], width = (a.sp[s + 1] - sb) >> 5, base = sb + (row & 31);
   T az = T(0), dd = T(0);
-  for (int j = 0; j < sr.width; j++) {
-    const int cj = __ldg(a.scol + sr.base + 32 * j);
+  for (int j = 0; j < width; j++) {
+    const int cj = __ldg(a.scol + base + 32 * j);
     if (cj < 0) continue;
-    const T vj = __ldg(a.sval + sr.base + 32 * j);
+    const T vj = __ldg(a.sval + base + 32 * j);
     if (!FIRST) az = add_rn(az, mul_rn(vj, __ldg(a.zin + cj)));
     if (cj == row) dd = vj;
   }
@@ -357,25 +542,16 @@ __global__ void __launch_bounds__(kCtaThreads) k_big_resid(const PassArgs<T> a, 
 template <typename T>
 __global__ void __launch_bounds__(kCtaThreads) k_big_sweep(const PassArgs<T> a, const T *wsrc, T *wdst) {
   if (gated_off(a)) return;
-  __shared__ int s_sp[kTileRows / 32 + 2];
-  const int tile = blockIdx.x;
-  const int lo = a.tile_lo[tile], hi = a.tile_lo[tile + 1];
-  const int bf = a.tile_bf[tile], bl = a.tile_bl[tile];
-  load_tile_tables(a.sp, lo, hi, s_sp, nullptr, 0, 0, nullptr);
-  __syncthreads();
-  const int row = lo + threadIdx.x;
-  if (row >= hi) return;
-  int L = bf, H = bl + 1;
-  while (H - L > 1) {
-    const int M = (L + H) >> 1;
-    if (a.boff[M] <= row) L = M; else H = M;
-  }
-  const int blo = a.boff[L], bhi = a.boff[L + 1];
-  const SellRow sr = sell_row(s_sp, lo, row);
+  const TileDesc d = a.td[blockIdx.x];
+  const int row = d.lo + threadIdx.x;
+  if (row >= d.hi) return;
+  int blo, bhi;
+  find_block_abs(a.boff + d.bf, d.nbk, row, blo, bhi);
+  const int s = row >> 5, sb = a.sp[s], width = (a.sp[s + 1] - sb) >> 5, base = sb + (row & 31);
   T acc = T(0);
-  for (int j = 0; j < sr.width; j++) {
-    const int cj = __ldg(a.scol + sr.base + 32 * j);
-    if (cj >= blo && cj < bhi) acc = add_rn(acc, mul_rn(__ldg(a.sval + sr.base + 32 * j), wsrc[cj]));
+  for (int j = 0; j < width; j++) {
+    const int cj = __ldg(a.scol + base + 32 * j);
+    if (cj >= blo && cj < bhi) acc = add_rn(acc, mul_rn(__ldg(a.sval + base + 32 * j), wsrc[cj]));
   }
   wdst[row] = add_rn(wsrc[row], div_rn(sub_rn(a.resbuf[row], acc), a.dbuf[row]));
 }
@@ -383,123 +559,198 @@ __global__ void __launch_bounds__(kCtaThreads) k_big_sweep(const PassArgs<T> a, 
 template <typename T, bool FIRST, bool LAST>
 __global__ void __launch_bounds__(kCtaThreads) k_big_finish(const PassArgs<T> a, const T *w) {
   if (gated_off(a)) return;
-  __shared__ double s_hi[kTileThreads];
   __shared__ double ws[32];
   const int tile = blockIdx.x;
-  const int lo = a.tile_lo[tile], hi = a.tile_lo[tile + 1];
-  const int row = lo + threadIdx.x;
+  const TileDesc d = a.td[tile];
+  const int row = d.lo + threadIdx.x;
   double prod = 0.0;
-  if (row < hi) {
+  if (row < d.hi) {
     const T zo = FIRST ? w[row] : add_rn(a.zin[row], w[row]);
     if (a.zout != nullptr) a.zout[row] = zo;
     if (a.zout64 != nullptr) a.zout64[row] = static_cast<double>(zo);
     if (LAST && a.part != nullptr) prod = __dmul_rn(a.r64[row], static_cast<double>(zo));
   }
   if (LAST && a.part != nullptr) {
-    const double tot = tile_sum(prod, hi - lo, s_hi, ws);
-    publish_and_finish(tot, a.part, tile, a.ntiles, a.st, 0, kStepRho, ws);
+    const double tot = block_tree<kTileThreads>(prod, ws);
+    if (threadIdx.x == 0) a.part[tile] = tot;
+    finish_grid(a.st, 0, kStepRho, a.part, a.g.ntiles, ws);
   }
 }
 
 // ---------------------------------------------------------------------------
-// fused p-update + fp64 SpMV + p.q partial (solver.py:150-159)
-//   p = z (first iteration) | z + beta * p_old ;  q = A p
-// Gathered p_j are recomputed from z_j and p_old_j: bitwise the value the
-// owning thread stores, so p never makes a separate HBM round trip.
+// p = z (first iteration) | z + beta * p_old   (solver.py:150-153)
+// Streaming, persistent; z is the fp32 (low) or fp64 (high) branch output.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kCtaThreads)
+    k_pupdate(const TileDesc *td, int ntiles, const float *z32, const double *z64, double *p0, double *p1,
+              const SolverState *st) {
+  if (st->done) return;
+  const bool low = st->branch == 1;
+  const bool first = st->first != 0;
+  const double beta = st->beta;
+  const bool odd = (st->it & 1) != 0;
+  const double *pold = odd ? p0 : p1;
+  double *pnew = odd ? p1 : p0;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const TileDesc d = td[tile];
+    const int row = d.lo + threadIdx.x;
+    if (row >= d.hi) continue;
+    const double zi = low ? static_cast<double>(z32[row]) : z64[row];
+    pnew[row] = first ? zi : __dadd_rn(zi, __dmul_rn(beta, pold[row]));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// q = A p and the p.q partial (solver.py:154-159), fp64 SELL-32.  The tile's
+// own p slice is staged with the matrix; out-of-tile p_j come from L2.
 // ---------------------------------------------------------------------------
 struct SpmvArgs {
   const int *sp;
   const int *scol;
   const double *sval;
-  const int *tile_lo;
-  int ntiles;
-  const float *z32;   // low-branch z (fp32; widening is exact)
-  const double *z64;  // high-branch z
-  double *p0, *p1;    // p ping-pong: new = p[it & 1]
+  const TileDesc *td;
+  TileGeom g;
+  double *p0, *p1;  // p ping-pong: current = p[it & 1]
   double *q;
   double *part;
   SolverState *st;
 };
 
-template <bool LOW>
-__device__ __forceinline__ double spmv_row(const SpmvArgs &a, const SellRow &sr, int row, bool first, double beta,
-                                           const double *pold, double *pnew) {
-  auto ZJ = [&](int j) -> double {
-    return LOW ? static_cast<double>(__ldg(a.z32 + j)) : __ldg(a.z64 + j);
-  };
-  const double zi = ZJ(row);
-  const double pi = first ? zi : __dadd_rn(zi, __dmul_rn(beta, __ldg(pold + row)));
-  double acc = 0.0;
-  for (int j0 = 0; j0 < sr.width; j0 += kChunk) {
-    int c[kChunk];
-    double v[kChunk], pj[kChunk];
-#pragma unroll
-    for (int u = 0; u < kChunk; u++) {
-      const bool ok = j0 + u < sr.width;
-      c[u] = ok ? __ldg(a.scol + sr.base + 32 * (j0 + u)) : -1;
-      v[u] = ok ? __ldg(a.sval + sr.base + 32 * (j0 + u)) : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < kChunk; u++) {
-      const double zg = c[u] >= 0 ? ZJ(c[u]) : 0.0;
-      const double pg = (c[u] >= 0 && !first) ? __ldg(pold + c[u]) : 0.0;
-      pj[u] = first ? zg : __dadd_rn(zg, __dmul_rn(beta, pg));
-    }
-#pragma unroll
-    for (int u = 0; u < kChunk; u++)
-      if (c[u] >= 0) acc = __dadd_rn(acc, __dmul_rn(v[u], pj[u]));
-  }
-  pnew[row] = pi;
-  a.q[row] = acc;
-  return __dmul_rn(pi, acc);
-}
-
-__global__ void __launch_bounds__(kCtaThreads) k_spmv_pq(const SpmvArgs a) {
-  if (a.st->done) return;
-  __shared__ int s_sp[kTileRows / 32 + 2];
-  __shared__ double s_hi[kTileThreads];
-  __shared__ double ws[32];
-  const bool low = a.st->branch == 1;
-  const bool first = a.st->first != 0;
-  const double beta = a.st->beta;
-  const bool odd = (a.st->it & 1) != 0;
-  const double *pold = odd ? a.p0 : a.p1;
-  double *pnew = odd ? a.p1 : a.p0;
-  const int tile = blockIdx.x;
-  const int lo = a.tile_lo[tile], hi = a.tile_lo[tile + 1];
-  load_tile_tables(a.sp, lo, hi, s_sp, nullptr, 0, 0, nullptr);
-  __syncthreads();
-  const int row = lo + threadIdx.x;
+__device__ __forceinline__ void spmv_tile_body(const SpmvArgs &a, int tile, const TileDesc &d, const int *col,
+                                               const double *val, const int *spp, const double *p,
+                                               const double *pt, double *ws) {
+  const int tid = threadIdx.x;
+  const int lo = d.lo, hi = d.hi, row = lo + tid;
+  const unsigned span = static_cast<unsigned>(hi - lo);
   double prod = 0.0;
   if (row < hi) {
-    const SellRow sr = sell_row(s_sp, lo, row);
-    prod = low ? spmv_row<true>(a, sr, row, first, beta, pold, pnew)
-               : spmv_row<false>(a, sr, row, first, beta, pold, pnew);
+    const int si = (row >> 5) - d.s0;
+    const int sb = spp[si];
+    const int width = (spp[si + 1] - sb) >> 5;
+    const int base = sb - d.e0 + (row & 31);
+    double acc = 0.0;
+    for (int j0 = 0; j0 < width; j0 += kSlots) {
+      int c[kSlots];
+      double vv[kSlots], pv[kSlots];
+#pragma unroll
+      for (int u = 0; u < kSlots; u++) {
+        const bool ok = j0 + u < width;
+        c[u] = ok ? col[base + 32 * (j0 + u)] : -1;
+        vv[u] = ok ? val[base + 32 * (j0 + u)] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < kSlots; u++) {
+        const unsigned o = static_cast<unsigned>(c[u] - lo);
+        pv[u] = c[u] < 0 ? 0.0 : (o < span ? pt[o] : __ldg(p + c[u]));
+      }
+#pragma unroll
+      for (int u = 0; u < kSlots; u++)
+        if (c[u] >= 0) acc = __dadd_rn(acc, __dmul_rn(vv[u], pv[u]));
+    }
+    a.q[row] = acc;
+    prod = __dmul_rn(pt[tid], acc);
   }
-  const double tot = tile_sum(prod, hi - lo, s_hi, ws);
-  publish_and_finish(tot, a.part, tile, a.ntiles, a.st, 1, kStepPq, ws);
+  const double tot = block_tree_nb<kTileThreads>(prod, ws, kBarConsumers);
+  if (tid == 0) a.part[tile] = tot;
+}
+
+__host__ __device__ inline StageLayout spmv_layout(const TileGeom &g) {
+  return stage_layout(g.cap_e, 8, g.max_sl, false, 8, 0, 0);
+}
+
+__global__ void __launch_bounds__(kWsThreads) k_spmv_pq(const SpmvArgs a) {
+  if (a.st->done) return;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ Ring R;
+  __shared__ double ws[32];
+  const int ns = a.g.ns;
+  const double *p = (a.st->it & 1) ? a.p1 : a.p0;
+  const StageLayout L = spmv_layout(a.g);
+  ring_init(R, ns);
+  if (threadIdx.x >= kConsumers) {
+    if (threadIdx.x == kConsumers)
+      producer_loop(R, a.g.ntiles, ns, [&](int st, int tile) {
+        produce<double, double, uint8_t, uint8_t>(R, st, a.td, tile, a.g, L, smem + st * L.bytes, a.sp, a.scol,
+                                                  a.sval, nullptr, p, nullptr, nullptr);
+      });
+  } else {
+    RingCursor cur;
+    for (int tile = blockIdx.x; tile < a.g.ntiles; tile += gridDim.x, cur.advance(ns)) {
+      const int st = cur.st;
+      mbar_wait(&R.full[st], cur.phase);
+      const TileDesc d = R.desc[st];
+      if (R.ok[st]) {
+        const unsigned char *sb = smem + st * L.bytes;
+        spmv_tile_body(a, tile, d, reinterpret_cast<const int *>(sb + L.col),
+                       reinterpret_cast<const double *>(sb + L.val), staged(sb + L.sp, a.sp, d.s0, d.s1 + 1), p,
+                       staged(sb + L.v0, p, d.lo, d.hi), ws);
+      } else {
+        spmv_tile_body(a, tile, d, a.scol + d.e0, a.sval + d.e0, a.sp + d.s0, p, p + d.lo, ws);
+      }
+      ring_release(R, st);
+    }
+  }
+  finish_grid(a.st, 1, kStepPq, a.part, a.g.ntiles, ws);
 }
 
 // x += alpha p ; r -= alpha q ; r.r partial   (solver.py:160-165)
+// Persistent and software-pipelined: the next tile's x, p, q, r are loaded
+// before the current tile's stores and tile sum.
 __global__ void __launch_bounds__(kCtaThreads)
-    k_update(const int *tile_lo, int ntiles, double *x, const double *p0, const double *p1, const double *q,
+    k_update(const TileDesc *td, int ntiles, double *x, const double *p0, const double *p1, const double *q,
              double *r, double *part, SolverState *st) {
   if (st->done) return;
-  __shared__ double s_hi[kTileThreads];
   __shared__ double ws[32];
   const double alpha = st->alpha;
   const double *p = (st->it & 1) ? p1 : p0;
-  const int lo = tile_lo[blockIdx.x], hi = tile_lo[blockIdx.x + 1];
-  const int row = lo + threadIdx.x;
-  double sq = 0.0;
-  if (row < hi) {
-    x[row] = __dadd_rn(x[row], __dmul_rn(alpha, p[row]));
-    const double rn = __dsub_rn(r[row], __dmul_rn(alpha, q[row]));
-    r[row] = rn;
-    sq = __dmul_rn(rn, rn);
+  int tile = blockIdx.x;
+  if (tile >= ntiles) {
+    finish_grid(st, 2, kStepRr, part, ntiles, ws);
+    return;
   }
-  const double tot = tile_sum(sq, hi - lo, s_hi, ws);
-  publish_and_finish(tot, part, blockIdx.x, ntiles, st, 2, kStepRr, ws);
+  TileDesc d = td[tile];
+  int row = d.lo + threadIdx.x;
+  double xv = 0.0, pv = 0.0, qv = 0.0, rv = 0.0;
+  if (row < d.hi) {
+    xv = x[row];
+    pv = p[row];
+    qv = q[row];
+    rv = r[row];
+  }
+  while (true) {
+    const int next = tile + gridDim.x;
+    TileDesc dn{};
+    double xn = 0.0, pn = 0.0, qn = 0.0, rn_ = 0.0;
+    int rown = -1;
+    if (next < ntiles) {
+      dn = td[next];
+      rown = dn.lo + threadIdx.x;
+      if (rown < dn.hi) {
+        xn = x[rown];
+        pn = p[rown];
+        qn = q[rown];
+        rn_ = r[rown];
+      }
+    }
+    double sq = 0.0;
+    if (row < d.hi) {
+      x[row] = __dadd_rn(xv, __dmul_rn(alpha, pv));
+      const double rnew = __dsub_rn(rv, __dmul_rn(alpha, qv));
+      r[row] = rnew;
+      sq = __dmul_rn(rnew, rnew);
+    }
+    const double tot = block_tree<kTileThreads>(sq, ws);
+    if (threadIdx.x == 0) part[tile] = tot;
+    if (next >= ntiles) break;
+    tile = next;
+    d = dn;
+    row = rown;
+    xv = xn;
+    pv = pn;
+    qv = qn;
+    rv = rn_;
+  }
+  finish_grid(st, 2, kStepRr, part, ntiles, ws);
 }
 
 // res = b - A x (or b), optionally stored; res.res partial; the last CTA runs
@@ -507,46 +758,43 @@ __global__ void __launch_bounds__(kCtaThreads)
 // gate: 0 always, 1 only when st->true_pending (strided true residual)
 template <bool HAS_X>
 __global__ void __launch_bounds__(kCtaThreads)
-    k_resid(const int *sp, const int *scol, const double *sval, const int *tile_lo, int ntiles, const double *b,
+    k_resid(const int *sp, const int *scol, const double *sval, const TileDesc *td, int ntiles, const double *b,
             const double *x, double *rout, double *part, SolverState *st, int gate, int step) {
   if (gate == 1 && (st == nullptr || !st->true_pending)) return;
-  __shared__ int s_sp[kTileRows / 32 + 2];
-  __shared__ double s_hi[kTileThreads];
   __shared__ double ws[32];
-  const int lo = tile_lo[blockIdx.x], hi = tile_lo[blockIdx.x + 1];
-  if (HAS_X) {
-    load_tile_tables(sp, lo, hi, s_sp, nullptr, 0, 0, nullptr);
-    __syncthreads();
-  }
-  const int row = lo + threadIdx.x;
-  double sq = 0.0;
-  if (row < hi) {
-    double res = b[row];
-    if (HAS_X) {
-      const SellRow sr = sell_row(s_sp, lo, row);
-      double ax = 0.0;
-      for (int j0 = 0; j0 < sr.width; j0 += kChunk) {
-        int c[kChunk];
-        double v[kChunk], g[kChunk];
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const TileDesc d = td[tile];
+    const int row = d.lo + threadIdx.x;
+    double sq = 0.0;
+    if (row < d.hi) {
+      double res = b[row];
+      if (HAS_X) {
+        const int s = row >> 5, sb = sp[s], width = (sp[s + 1] - sb) >> 5, base = sb + (row & 31);
+        double ax = 0.0;
+        for (int j0 = 0; j0 < width; j0 += kSlots) {
+          int c[kSlots];
+          double v[kSlots], g[kSlots];
 #pragma unroll
-        for (int u = 0; u < kChunk; u++) {
-          const bool ok = j0 + u < sr.width;
-          c[u] = ok ? __ldg(scol + sr.base + 32 * (j0 + u)) : -1;
-          v[u] = ok ? __ldg(sval + sr.base + 32 * (j0 + u)) : 0.0;
+          for (int u = 0; u < kSlots; u++) {
+            const bool ok = j0 + u < width;
+            c[u] = ok ? __ldg(scol + base + 32 * (j0 + u)) : -1;
+            v[u] = ok ? __ldg(sval + base + 32 * (j0 + u)) : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < kSlots; u++) g[u] = c[u] >= 0 ? __ldg(x + c[u]) : 0.0;
+#pragma unroll
+          for (int u = 0; u < kSlots; u++)
+            if (c[u] >= 0) ax = __dadd_rn(ax, __dmul_rn(v[u], g[u]));
         }
-#pragma unroll
-        for (int u = 0; u < kChunk; u++) g[u] = c[u] >= 0 ? __ldg(x + c[u]) : 0.0;
-#pragma unroll
-        for (int u = 0; u < kChunk; u++)
-          if (c[u] >= 0) ax = __dadd_rn(ax, __dmul_rn(v[u], g[u]));
+        res = __dsub_rn(res, ax);
       }
-      res = __dsub_rn(res, ax);
+      if (rout != nullptr) rout[row] = res;
+      sq = __dmul_rn(res, res);
     }
-    if (rout != nullptr) rout[row] = res;
-    sq = __dmul_rn(res, res);
+    const double tot = block_tree<kTileThreads>(sq, ws);
+    if (threadIdx.x == 0) part[tile] = tot;
   }
-  const double tot = tile_sum(sq, hi - lo, s_hi, ws);
-  publish_and_finish(tot, part, blockIdx.x, ntiles, st, 3, step, ws);
+  finish_grid(st, 3, step, part, ntiles, ws);
 }
 
 // one-thread scalar step (solve start: wall-clock origin of the trace)
@@ -569,6 +817,35 @@ __global__ void k_sell_pack(long long n, const int *rp, const int *sp, const E *
     const int base = sp[r >> 5] + static_cast<int>(r & 31);
     const int s = rp[r], len = rp[r + 1] - s;
     for (int j = 0; j < len; j++) sell[base + 32 * j] = csr[s + j];
+  }
+}
+
+// Per-row static structure against a block partition (plan-bound):
+// len | dpos << 4 | i0 << 8 | i1 << 12, or kMetaGeneric when a field does
+// not fit in 4 bits.  Needs the SELL columns of the matrix.
+__global__ void k_build_meta(long long n, const int *sp, const int *scol, const int *boff, int nb, uint16_t *meta) {
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x) {
+    const int row = static_cast<int>(r);
+    const int s = row >> 5, sb = sp[s], width = (sp[s + 1] - sb) >> 5, base = sb + (row & 31);
+    int L = 0, H = nb;
+    while (H - L > 1) {
+      const int M = (L + H) >> 1;
+      if (boff[M] <= row) L = M; else H = M;
+    }
+    const int blo = boff[L], bhi = boff[L + 1];
+    int len = 0, dpos = -1, i0 = -1, i1 = -1;
+    for (int j = 0; j < width; j++) {
+      const int c = scol[base + 32 * j];
+      if (c < 0) break;
+      len = j + 1;
+      if (c == row) dpos = j;
+      if (c >= blo && i0 < 0) i0 = j;
+      if (c >= bhi && i1 < 0) i1 = j;
+    }
+    if (i0 < 0) i0 = len;
+    if (i1 < 0) i1 = len;
+    const bool fits = len <= kSlots && dpos >= 0 && i1 <= 15;
+    meta[row] = fits ? static_cast<uint16_t>(len | (dpos << 4) | (i0 << 8) | (i1 << 12)) : kMetaGeneric;
   }
 }
 

@@ -357,5 +357,5 @@ def profile_iteration(A: SparseMatrix, mp: MixedPreconditioner, *,
         _lib.ptr(ws), ws.numel(), 0 if branch == "high" else 1, int(reps), out),
         "profile_iteration")
     names = ("bjac_first", "bjac_middle", "bjac_last", "spmv_pq", "update",
-             "scalar", "iteration")
+             "scalar", "iteration", "pupdate")
     return {k: float(out[i]) for i, k in enumerate(names)}

@@ -161,7 +161,7 @@ def test_narrowing_and_norms(cuda, oracle):
     assert norm2(x) == pytest.approx(2e20, rel=1e-6)
     rng = np.random.default_rng(5)
     a, b = rng.standard_normal(100_000), rng.standard_normal(100_000)
-    tiles = np.append(np.arange(0, a.size, 512), a.size)
+    tiles = np.append(np.arange(0, a.size, 256), a.size)
     assert dot(a, b) == oracle.tree_dot(tiles, a, b)       # device order, bitwise
     assert dot(a, b) == pytest.approx(float(np.dot(a, b)), rel=1e-12)
 
@@ -289,3 +289,16 @@ def test_unstaged_tiles_and_dense_rows_bitwise(cuda, oracle):
             z32 = setup(A, k=k, t=t, precision=Precision.F32, partition=part).apply(r.astype(np.float32))
             np.testing.assert_array_equal(
                 z32, oracle.bjac_apply(A.row_ptr, A.col_idx, v32, inb, d32, k, t, r.astype(np.float32)))
+
+
+@pytest.mark.parametrize("pol", ("fixed-low", "uniform", "adaptive-hl:1e-3"))
+def test_pcg_many_tiles_per_cta_bitwise(cuda, oracle, pol):
+    """n = 64 (512 tiles): every persistent CTA walks several tiles, so the
+    shared-memory stage ring wraps around; still bit-identical."""
+    from paper_2407_15973_b200 import problems
+    cs = problems.make_config("c2", 64)
+    offs = np.append(np.arange(0, cs.A.n, 64), cs.A.n)
+    rep, orc = _solve_both(cs.A, cs.b, offs, pol, 2, 2, 1e-10, oracle)
+    assert rep.iterations == orc["iterations"]
+    np.testing.assert_array_equal(rep.x, orc["x"])
+    np.testing.assert_array_equal([r.implicit_relres for r in rep.trace], orc["relres"])
