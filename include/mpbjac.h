@@ -90,6 +90,10 @@ typedef struct mpb_csr {
   const mpb_sell *sell;   /* SELL-32 structure of row_ptr/col_idx            */
   const double *sell_val64; /* val64 packed in SELL-32 (mpb_sell_nnz entries) */
   const float *sell_val32;  /* val32 packed in SELL-32, NULL if unused        */
+  /* in-block entries only, in the plan's in-block SELL-32 layout
+   * (mpb_plan_pack_inblock_*); read by the first BJAC pass */
+  const double *ib_val64;
+  const float *ib_val32;
 } mpb_csr;
 
 typedef struct mpb_solve_options {
@@ -141,6 +145,14 @@ int mpb_plan_destroy(mpb_plan *p);
  * in-block slot range) against a SELL-32 layout of the matrix; required
  * before the plan is used with that matrix by the preconditioner / solve. */
 int mpb_plan_bind_sell(mpb_handle *h, mpb_plan *p, const mpb_sell *sell);
+/* The bound plan's in-block SELL-32 layout (each row's entries inside its
+ * own block, ascending column): padded entry count, and value packing from
+ * SELL-32 values of the bound structure. */
+int64_t mpb_plan_inblock_nnz(const mpb_plan *p);
+int mpb_plan_pack_inblock_f64(mpb_handle *h, const mpb_plan *p,
+                              const double *sell_val, double *ib_val);
+int mpb_plan_pack_inblock_f32(mpb_handle *h, const mpb_plan *p,
+                              const float *sell_val, float *ib_val);
 int mpb_plan_info(const mpb_plan *p, int64_t *h_ntiles, int *h_large,
                   int64_t *h_max_tile_nnz);
 

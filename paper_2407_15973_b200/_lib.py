@@ -36,7 +36,8 @@ EXPORTED = (
     "mpb_bjac_inner_apply_f32", "mpb_solve_workspace_bytes", "mpb_pcg_solve",
     "mpb_true_relres", "mpb_profile_iteration", "mpb_sell_create",
     "mpb_sell_destroy", "mpb_sell_nnz", "mpb_sell_pack_f64", "mpb_sell_pack_f32",
-    "mpb_plan_bind_sell",
+    "mpb_plan_bind_sell", "mpb_plan_inblock_nnz", "mpb_plan_pack_inblock_f64",
+    "mpb_plan_pack_inblock_f32",
 )
 
 
@@ -49,7 +50,8 @@ class MpbCsr(C.Structure):
                 ("row_ptr", C.c_void_p), ("col_idx", C.c_void_p),
                 ("val64", C.c_void_p), ("val32", C.c_void_p),
                 ("sell", C.c_void_p), ("sell_val64", C.c_void_p),
-                ("sell_val32", C.c_void_p)]
+                ("sell_val32", C.c_void_p), ("ib_val64", C.c_void_p),
+                ("ib_val32", C.c_void_p)]
 
 
 class MpbSolveOptions(C.Structure):
@@ -115,6 +117,9 @@ def _declare(L):
         "mpb_sell_create": ([_P, _I64, _P, _P, _P, C.POINTER(_P)], C.c_int),
         "mpb_sell_destroy": ([_P], C.c_int),
         "mpb_plan_bind_sell": ([_P, _P, _P], C.c_int),
+        "mpb_plan_inblock_nnz": ([_P], C.c_int64),
+        "mpb_plan_pack_inblock_f64": ([_P, _P, _P, _P], C.c_int),
+        "mpb_plan_pack_inblock_f32": ([_P, _P, _P, _P], C.c_int),
         "mpb_sell_nnz": ([_P], C.c_int64),
         "mpb_sell_pack_f64": ([_P, _P, _P, _P, _P], C.c_int),
         "mpb_sell_pack_f32": ([_P, _P, _P, _P, _P], C.c_int),

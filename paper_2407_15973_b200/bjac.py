@@ -98,6 +98,27 @@ class DevicePlan:
         self.large = bool(large.value)
         self.max_tile_nnz = int(mx.value)
 
+    def inblock_values(self, sell_values):
+        """In-block SELL packing of SELL-32 values (cached per tensor)."""
+        if sell_values is None:
+            return None
+        torch = __import__("torch")
+        cache = self.__dict__.setdefault("_ib", {})
+        key = (sell_values.data_ptr(), str(sell_values.dtype))
+        hit = cache.get(key)
+        if hit is None:
+            nnz = int(self.h.lib.mpb_plan_inblock_nnz(self.ptr))
+            if nnz < 0:
+                _lib.check(nnz, "mpb_plan_inblock_nnz")
+            out = torch.empty(max(nnz, 1), dtype=sell_values.dtype, device=sell_values.device)
+            fn = (self.h.lib.mpb_plan_pack_inblock_f64 if sell_values.dtype == torch.float64
+                  else self.h.lib.mpb_plan_pack_inblock_f32)
+            _lib.check(fn(self.h.ptr, self.ptr, _lib.ptr(sell_values), _lib.ptr(out)),
+                       "mpb_plan_pack_inblock")
+            hit = (sell_values, out)
+            cache[key] = hit
+        return hit[1]
+
     def bind(self, dcsr) -> "DevicePlan":
         """Build the per-row static structure against the matrix's SELL-32
         layout (mpb_plan_bind_sell)."""
@@ -165,8 +186,8 @@ class BjacPreconditioner:
 
     def _csr_struct(self):
         if self.precision is Precision.F64:
-            return self.dcsr.c_struct(val64=self.dvalues, val32=None)
-        return self.dcsr.c_struct(val64=None, val32=self.dvalues)
+            return self.dcsr.c_struct(val64=self.dvalues, val32=None, plan=self.plan)
+        return self.dcsr.c_struct(val64=None, val32=self.dvalues, plan=self.plan)
 
     def _check_vector(self, r):
         if tuple(r.shape) != (self.n,):

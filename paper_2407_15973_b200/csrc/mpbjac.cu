@@ -56,6 +56,9 @@ struct mpb_plan {
   int max_sl, max_nbk;    // max slices / blocks per tile
   uint16_t *d_meta;       // per-row static structure (mpb_plan_bind_sell)
   const mpb_sell *bound;  // the SELL layout d_meta was built against
+  int *d_ib_sp, *d_ib_col;  // in-block SELL layout (first passes)
+  int64_t ib_nnz;
+  int max_tile_ib;
 };
 
 struct mpb_sell {
@@ -181,6 +184,12 @@ struct ApplyBufs {
 
 template <typename T, bool F, bool L, bool R64>
 int launch_tile_kernel(mpb_handle *h, cudaStream_t s, const mpb_plan *p, PassArgs<T> a) {
+  if (F && !L) {  // first pass streams the in-block layout
+    if (a.ib_val == nullptr) return MPB_ERR_LAYOUT;
+    a.ib_sp = p->d_ib_sp;
+    a.ib_col = p->d_ib_col;
+    a.g.cap_e = std::min(p->max_tile_ib, kStageCap);
+  }
   const StageLayout Ls = bjac_layout<T, F, R64>(a.g);
   a.g.ns = pick_stages(k_bjac_tile<T, F, L, R64>, Ls.bytes);
   const uint32_t dyn = a.g.ns * Ls.bytes;
@@ -222,6 +231,16 @@ template <>
 const float *sell_vals<float>(const mpb_csr *A) {
   return A->sell_val32;
 }
+template <typename T>
+const T *ib_vals(const mpb_csr *A);
+template <>
+const double *ib_vals<double>(const mpb_csr *A) {
+  return A->ib_val64;
+}
+template <>
+const float *ib_vals<float>(const mpb_csr *A) {
+  return A->ib_val32;
+}
 
 // k outer passes (bjac.py:127-149).  Residual from r64 (narrowed on load) or
 // rT; final output to zout (T) and/or zout64; r.z partials when part != null
@@ -235,6 +254,7 @@ int launch_apply(mpb_handle *h, cudaStream_t s, const mpb_plan *p, const mpb_csr
   a.sp = A->sell->d_sp;
   a.scol = A->sell->d_col;
   a.sval = sell_vals<T>(A);
+  a.ib_val = ib_vals<T>(A);
   a.meta = p->d_meta;
   a.td = p->d_td;
   a.boff = p->d_boff;
@@ -521,6 +541,8 @@ int mpb_plan_destroy(mpb_plan *p) {
   cudaFree(p->d_boff);
   cudaFree(p->d_td);
   cudaFree(p->d_meta);
+  cudaFree(p->d_ib_sp);
+  cudaFree(p->d_ib_col);
   delete p;
   return MPB_OK;
 }
@@ -533,9 +555,75 @@ int mpb_plan_bind_sell(mpb_handle *h, mpb_plan *p, const mpb_sell *sell) {
   k_build_meta<<<elt_blocks(p->n), kEltThreads, 0, h->user>>>(p->n, sell->d_sp, sell->d_col, p->d_boff,
                                                             static_cast<int>(p->nb), p->d_meta);
   MPB_LAUNCHED(h);
+  // in-block SELL layout: per-row in-block counts -> slice widths -> pack
+  const int64_t n = p->n, ns = (n + 31) / 32;
+  int *d_cnt = nullptr;
+  MPB_CUDA(cudaMalloc(&d_cnt, sizeof(int) * n));
+  k_ib_count<<<elt_blocks(n), kEltThreads, 0, h->user>>>(n, sell->d_sp, sell->d_col, p->d_boff,
+                                                       static_cast<int>(p->nb), d_cnt);
+  MPB_LAUNCHED(h);
+  std::vector<int> cnt(n);
+  MPB_CUDA(cudaMemcpyAsync(cnt.data(), d_cnt, sizeof(int) * n, cudaMemcpyDeviceToHost, h->user));
+  MPB_CUDA(cudaStreamSynchronize(h->user));
+  cudaFree(d_cnt);
+  std::vector<int> ib_sp(ns + 1);
+  int64_t acc = 0;
+  for (int64_t sl = 0; sl < ns; sl++) {
+    int wdt = 0;
+    for (int64_t r = 32 * sl; r < std::min<int64_t>(n, 32 * sl + 32); r++) wdt = std::max(wdt, cnt[r]);
+    ib_sp[sl] = static_cast<int>(acc);
+    acc += 32 * wdt;
+    if (acc >= (int64_t(1) << 31)) return MPB_ERR_INDEX32;
+  }
+  ib_sp[ns] = static_cast<int>(acc);
+  cudaFree(p->d_ib_sp);
+  cudaFree(p->d_ib_col);
+  p->d_ib_sp = nullptr;
+  p->d_ib_col = nullptr;
+  MPB_CUDA(cudaMalloc(&p->d_ib_sp, sizeof(int) * (ns + 1)));
+  MPB_CUDA(cudaMalloc(&p->d_ib_col, sizeof(int) * std::max<int64_t>(acc, 1)));
+  MPB_CUDA(cudaMemcpy(p->d_ib_sp, ib_sp.data(), sizeof(int) * (ns + 1), cudaMemcpyHostToDevice));
+  MPB_CUDA(cudaMemsetAsync(p->d_ib_col, 0xff, sizeof(int) * std::max<int64_t>(acc, 1), h->user));
+  k_ib_pack<int><<<elt_blocks(n), kEltThreads, 0, h->user>>>(n, sell->d_sp, sell->d_col, p->d_boff,
+                                                           static_cast<int>(p->nb), p->d_ib_sp, sell->d_col,
+                                                           p->d_ib_col);
+  MPB_LAUNCHED(h);
+  p->ib_nnz = acc;
+  // tile descriptors gain their in-block entry ranges
+  std::vector<TileDesc> td(p->ntiles);
+  MPB_CUDA(cudaMemcpy(td.data(), p->d_td, sizeof(TileDesc) * p->ntiles, cudaMemcpyDeviceToHost));
+  int mx = 0;
+  for (auto &d : td) {
+    d.ie0 = ib_sp[d.s0];
+    d.ie1 = ib_sp[d.s1];
+    mx = std::max(mx, d.ie1 - d.ie0);
+  }
+  p->max_tile_ib = mx;
+  MPB_CUDA(cudaMemcpy(p->d_td, td.data(), sizeof(TileDesc) * p->ntiles, cudaMemcpyHostToDevice));
   MPB_CUDA(cudaStreamSynchronize(h->user));
   p->bound = sell;
   return MPB_OK;
+}
+
+int64_t mpb_plan_inblock_nnz(const mpb_plan *p) { return (p && p->bound) ? p->ib_nnz : MPB_ERR_LAYOUT; }
+
+template <typename T>
+static int pack_ib_impl(mpb_handle *h, const mpb_plan *p, const T *sell_val, T *ib_val) {
+  if (!h || !p || !sell_val || !ib_val) return MPB_ERR_ARG;
+  if (!p->bound || !p->d_ib_sp) return MPB_ERR_LAYOUT;
+  MPB_CUDA(cudaMemsetAsync(ib_val, 0, sizeof(T) * std::max<int64_t>(p->ib_nnz, 1), h->user));
+  k_ib_pack<T><<<elt_blocks(p->n), kEltThreads, 0, h->user>>>(p->n, p->bound->d_sp, p->bound->d_col, p->d_boff,
+                                                             static_cast<int>(p->nb), p->d_ib_sp, sell_val, ib_val);
+  MPB_LAUNCHED(h);
+  return MPB_OK;
+}
+
+int mpb_plan_pack_inblock_f64(mpb_handle *h, const mpb_plan *p, const double *sell_val, double *ib_val) {
+  return pack_ib_impl<double>(h, p, sell_val, ib_val);
+}
+
+int mpb_plan_pack_inblock_f32(mpb_handle *h, const mpb_plan *p, const float *sell_val, float *ib_val) {
+  return pack_ib_impl<float>(h, p, sell_val, ib_val);
 }
 
 int mpb_plan_info(const mpb_plan *p, int64_t *h_ntiles, int *h_large, int64_t *h_max_tile_nnz) {
@@ -1172,6 +1260,7 @@ int mpb_profile_iteration(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A,
       PassArgs<double> a{};
       setup(a, bb.zA, bb.zB, w.z64, 0);
       a.sval = A->sell_val64;
+      a.ib_val = A->ib_val64;
       a.g = geom_for<double>(plan);
       if (first && last) return launch_pass<double, true, true>(h, s, plan, a, bb);
       if (first) return launch_pass<double, true, false>(h, s, plan, a, bb);
@@ -1182,6 +1271,7 @@ int mpb_profile_iteration(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A,
     PassArgs<float> a{};
     setup(a, bb.zA, bb.zB, w.z32, 1);
     a.sval = A->sell_val32;
+    a.ib_val = A->ib_val32;
     a.g = geom_for<float>(plan);
     a.ovf_count = &w.st->ovf_count;
     a.ovf_first = &w.st->ovf_first;

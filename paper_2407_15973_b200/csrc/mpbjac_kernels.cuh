@@ -150,6 +150,28 @@ __device__ __forceinline__ void finish_grid(SolverState *st, int ticket, int ste
   }
 }
 
+// U independent tile sums at once (same order as block_tree<kTileThreads>
+// for each): one pair of barriers for all U.  Result u valid in thread 0.
+template <int U>
+__device__ __forceinline__ void block_tree_multi(double (&v)[U], double (*ws)[32]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int u = 0; u < U; u++) v[u] = warp_bfly(v[u]);
+  __syncthreads();
+  if (lane == 0) {
+#pragma unroll
+    for (int u = 0; u < U; u++) ws[u][warp] = v[u];
+  }
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const double r = lane < kTileThreads / 32 ? ws[u][lane] : 0.0;
+      v[u] = warp_bfly(r);
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // tiles: descriptor, geometry, TMA stage layout
 // ---------------------------------------------------------------------------
@@ -158,6 +180,8 @@ struct TileDesc {
   int s0, s1;   // SELL slices [s0, s1)
   int e0, e1;   // SELL entries [e0, e1) = [sp[s0], sp[s1]) (multiples of 32)
   int bf, nbk;  // blocks bf .. bf+nbk-1 overlap the tile
+  int ie0, ie1; // in-block SELL entries [ib_sp[s0], ib_sp[s1])
+  int pad0, pad1;
 };
 
 struct TileGeom {
@@ -222,14 +246,15 @@ __device__ __forceinline__ const E *staged(const unsigned char *region, const E 
 }
 
 // Producer: stage tile `tile` into ring slot st (thread = producer lane 0).
-template <typename T, typename V0, typename V1, typename V2>
+template <typename T, typename V0, typename V1, typename V2, bool IB = false>
 __device__ __forceinline__ void produce(Ring &R, int st, const TileDesc *td, int tile, const TileGeom &g,
                                         const StageLayout &L, unsigned char *stage, const int *sp, const int *scol,
                                         const T *sval, const uint16_t *meta, const V0 *v0, const V1 *v1,
                                         const V2 *v2) {
   const TileDesc d = td[tile];
   R.desc[st] = d;
-  const int nent = d.e1 - d.e0;
+  const int e0 = IB ? d.ie0 : d.e0, e1 = IB ? d.ie1 : d.e1;
+  const int nent = e1 - e0;
   const bool fits = nent <= g.cap_e && (d.s1 - d.s0) <= g.max_sl;
   R.ok[st] = fits ? 1 : 0;
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -241,8 +266,8 @@ __device__ __forceinline__ void produce(Ring &R, int st, const TileDesc *td, int
                    window_bytes(meta, d.lo, d.hi) + window_bytes(v0, d.lo, d.hi) + window_bytes(v1, d.lo, d.hi) +
                    window_bytes(v2, d.lo, d.hi);
   mbar_arrive_expect_tx(&R.full[st], bytes);
-  bulk_g2s(stage + L.col, scol + d.e0, static_cast<uint32_t>(nent) * 4u, &R.full[st]);
-  bulk_g2s(stage + L.val, sval + d.e0, static_cast<uint32_t>(nent) * sizeof(T), &R.full[st]);
+  bulk_g2s(stage + L.col, scol + e0, static_cast<uint32_t>(nent) * 4u, &R.full[st]);
+  bulk_g2s(stage + L.val, sval + e0, static_cast<uint32_t>(nent) * sizeof(T), &R.full[st]);
   tma_window(stage + L.sp, sp, d.s0, d.s1 + 1, &R.full[st]);
   if (meta != nullptr) tma_window(stage + L.meta, meta, d.lo, d.hi, &R.full[st]);
   if (v0 != nullptr) tma_window(stage + L.v0, v0, d.lo, d.hi, &R.full[st]);
@@ -301,6 +326,9 @@ struct PassArgs {
   const int *sp;         // SELL slice_ptr
   const int *scol;       // SELL columns (-1 = padding)
   const T *sval;         // SELL values in storage precision
+  const int *ib_sp;      // in-block SELL (first pass): slice_ptr
+  const int *ib_col;     //   columns
+  const T *ib_val;       //   values
   const uint16_t *meta;  // per-row static structure (plan-bound)
   const TileDesc *td;    // tile descriptors
   const int *boff;       // nb+1 block offsets (generic rows, large blocks)
@@ -463,6 +491,58 @@ __device__ __forceinline__ void bjac_tile_body(const PassArgs<T> &a, int tile, c
   }
 }
 
+// First pass of a tile: z1 = D_b^{-1} r (bjac.py:134-136), reading only the
+// in-block entries (plan's in-block SELL): y = r / d, then t-1 sweeps
+// y += (r - A_b y) / d over the in-block entries in ascending column order.
+template <typename T>
+__device__ __forceinline__ void bjac_first_body(const PassArgs<T> &a, const TileDesc &d, const int *col,
+                                                const T *val, const int *spp, const uint16_t *mt,
+                                                const double *r64t, const T *rTt, T *s_w) {
+  const int tid = threadIdx.x;
+  const int lo = d.lo, hi = d.hi, row = lo + tid;
+  const bool valid = row < hi;
+  T res = T(0), dd = T(1), w = T(0);
+  int base = 0, nib = 0;
+  if (valid) {
+    const int si = (row >> 5) - d.s0;
+    const int sb = spp[si];
+    const int iwidth = (spp[si + 1] - sb) >> 5;
+    base = sb - d.ie0 + (row & 31);
+    const uint16_t m = mt[tid];
+    res = r64t != nullptr ? narrow_checked(a, r64t[tid], row, true) : rTt[tid];
+    if (m != kMetaGeneric) {
+      nib = meta_i1(m) - meta_i0(m);
+      dd = val[base + 32 * (meta_dpos(m) - meta_i0(m))];
+    } else {
+      for (int j = 0; j < iwidth; j++) {
+        const int c = col[base + 32 * j];
+        if (c < 0) break;
+        nib = j + 1;
+        if (c == row) dd = val[base + 32 * j];
+      }
+    }
+    w = div_rn(res, dd);
+    s_w[tid] = w;
+  }
+  for (int s = 1; s < a.t; s++) {
+    named_sync(kBarConsumers, kConsumers);
+    T acc = T(0);
+    for (int j = 0; j < nib; j++) {
+      const int c = col[base + 32 * j];
+      acc = add_rn(acc, mul_rn(val[base + 32 * j], s_w[c - lo]));
+    }
+    named_sync(kBarConsumers, kConsumers);
+    if (valid) {
+      w = add_rn(w, div_rn(sub_rn(res, acc), dd));
+      s_w[tid] = w;
+    }
+  }
+  if (valid) {
+    if (a.zout != nullptr) a.zout[row] = w;
+    if (a.zout64 != nullptr) a.zout64[row] = static_cast<double>(w);
+  }
+}
+
 template <typename T, bool FIRST, bool R64>
 __host__ __device__ inline StageLayout bjac_layout(const TileGeom &g) {
   // v0: residual slice, v2: z_in slice (non-first passes)
@@ -478,6 +558,7 @@ __global__ void __launch_bounds__(kWsThreads) k_bjac_tile(const PassArgs<T> a) {
   __shared__ T s_w[kTileRows];
   __shared__ double ws[32];
   const int ns = a.g.ns;
+  constexpr bool kIB = FIRST && !LAST;  // first pass alone: in-block entries only
   const StageLayout L = bjac_layout<T, FIRST, R64>(a.g);
   ring_init(R, ns);
   if (threadIdx.x >= kConsumers) {  // producer warp
@@ -485,8 +566,12 @@ __global__ void __launch_bounds__(kWsThreads) k_bjac_tile(const PassArgs<T> a) {
     const RT *rsrc = R64 ? reinterpret_cast<const RT *>(a.r64) : reinterpret_cast<const RT *>(a.rT);
     if (threadIdx.x == kConsumers)
       producer_loop(R, a.g.ntiles, ns, [&](int st, int tile) {
-        produce<T, RT, uint8_t, T>(R, st, a.td, tile, a.g, L, smem + st * L.bytes, a.sp, a.scol, a.sval, a.meta,
-                                   rsrc, nullptr, FIRST ? nullptr : a.zin);
+        if (kIB)
+          produce<T, RT, uint8_t, T, true>(R, st, a.td, tile, a.g, L, smem + st * L.bytes, a.ib_sp, a.ib_col,
+                                           a.ib_val, a.meta, rsrc, nullptr, nullptr);
+        else
+          produce<T, RT, uint8_t, T>(R, st, a.td, tile, a.g, L, smem + st * L.bytes, a.sp, a.scol, a.sval, a.meta,
+                                     rsrc, nullptr, FIRST ? nullptr : a.zin);
       });
   } else {
     RingCursor cur;
@@ -494,7 +579,18 @@ __global__ void __launch_bounds__(kWsThreads) k_bjac_tile(const PassArgs<T> a) {
       const int st = cur.st;
       mbar_wait(&R.full[st], cur.phase);
       const TileDesc d = R.desc[st];
-      if (R.ok[st]) {
+      if (kIB) {
+        if (R.ok[st]) {
+          const unsigned char *sb = smem + st * L.bytes;
+          bjac_first_body<T>(a, d, reinterpret_cast<const int *>(sb + L.col), reinterpret_cast<const T *>(sb + L.val),
+                             staged(sb + L.sp, a.ib_sp, d.s0, d.s1 + 1), staged(sb + L.meta, a.meta, d.lo, d.hi),
+                             R64 ? staged(sb + L.v0, a.r64, d.lo, d.hi) : nullptr,
+                             R64 ? nullptr : staged(sb + L.v0, a.rT, d.lo, d.hi), s_w);
+        } else {
+          bjac_first_body<T>(a, d, a.ib_col + d.ie0, a.ib_val + d.ie0, a.ib_sp + d.s0, a.meta + d.lo,
+                             R64 ? a.r64 + d.lo : nullptr, R64 ? nullptr : a.rT + d.lo, s_w);
+        }
+      } else if (R.ok[st]) {
         const unsigned char *sb = smem + st * L.bytes;
         const double *r64t = R64 ? staged(sb + L.v0, a.r64, d.lo, d.hi) : nullptr;
         const T *rTt = R64 ? nullptr : staged(sb + L.v0, a.rT, d.lo, d.hi);
@@ -581,6 +677,8 @@ __global__ void __launch_bounds__(kCtaThreads) k_big_finish(const PassArgs<T> a,
 // p = z (first iteration) | z + beta * p_old   (solver.py:150-153)
 // Streaming, persistent; z is the fp32 (low) or fp64 (high) branch output.
 // ---------------------------------------------------------------------------
+constexpr int kStreamTiles = 4;  // tiles per CTA iteration of the streaming kernels
+
 __global__ void __launch_bounds__(kCtaThreads)
     k_pupdate(const TileDesc *td, int ntiles, const float *z32, const double *z64, double *p0, double *p1,
               const SolverState *st) {
@@ -591,12 +689,27 @@ __global__ void __launch_bounds__(kCtaThreads)
   const bool odd = (st->it & 1) != 0;
   const double *pold = odd ? p0 : p1;
   double *pnew = odd ? p1 : p0;
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const TileDesc d = td[tile];
-    const int row = d.lo + threadIdx.x;
-    if (row >= d.hi) continue;
-    const double zi = low ? static_cast<double>(z32[row]) : z64[row];
-    pnew[row] = first ? zi : __dadd_rn(zi, __dmul_rn(beta, pold[row]));
+  constexpr int U = kStreamTiles;
+  for (int t0 = blockIdx.x; t0 < ntiles; t0 += U * gridDim.x) {
+    int row[U];
+    double zi[U], po[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int tile = t0 + u * gridDim.x;
+      row[u] = -1;
+      if (tile < ntiles) {
+        const TileDesc d = td[tile];
+        if (d.lo + (int)threadIdx.x < d.hi) row[u] = d.lo + threadIdx.x;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      zi[u] = row[u] < 0 ? 0.0 : (low ? static_cast<double>(z32[row[u]]) : z64[row[u]]);
+      po[u] = (row[u] < 0 || first) ? 0.0 : pold[row[u]];
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++)
+      if (row[u] >= 0) pnew[row[u]] = first ? zi[u] : __dadd_rn(zi[u], __dmul_rn(beta, po[u]));
   }
 }
 
@@ -694,63 +807,59 @@ __global__ void __launch_bounds__(kWsThreads) k_spmv_pq(const SpmvArgs a) {
 }
 
 // x += alpha p ; r -= alpha q ; r.r partial   (solver.py:160-165)
-// Persistent and software-pipelined: the next tile's x, p, q, r are loaded
-// before the current tile's stores and tile sum.
+// Persistent; each CTA iteration streams kStreamTiles tiles with every load
+// issued up front and one barrier pair for their tile sums.
 __global__ void __launch_bounds__(kCtaThreads)
     k_update(const TileDesc *td, int ntiles, double *x, const double *p0, const double *p1, const double *q,
              double *r, double *part, SolverState *st) {
   if (st->done) return;
-  __shared__ double ws[32];
+  __shared__ double ws[kStreamTiles][32];
+  __shared__ double wsf[32];
   const double alpha = st->alpha;
   const double *p = (st->it & 1) ? p1 : p0;
-  int tile = blockIdx.x;
-  if (tile >= ntiles) {
-    finish_grid(st, 2, kStepRr, part, ntiles, ws);
-    return;
-  }
-  TileDesc d = td[tile];
-  int row = d.lo + threadIdx.x;
-  double xv = 0.0, pv = 0.0, qv = 0.0, rv = 0.0;
-  if (row < d.hi) {
-    xv = x[row];
-    pv = p[row];
-    qv = q[row];
-    rv = r[row];
-  }
-  while (true) {
-    const int next = tile + gridDim.x;
-    TileDesc dn{};
-    double xn = 0.0, pn = 0.0, qn = 0.0, rn_ = 0.0;
-    int rown = -1;
-    if (next < ntiles) {
-      dn = td[next];
-      rown = dn.lo + threadIdx.x;
-      if (rown < dn.hi) {
-        xn = x[rown];
-        pn = p[rown];
-        qn = q[rown];
-        rn_ = r[rown];
+  constexpr int U = kStreamTiles;
+  for (int t0 = blockIdx.x; t0 < ntiles; t0 += U * gridDim.x) {
+    int row[U];
+    double xv[U], pv[U], qv[U], rv[U], sq[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int tile = t0 + u * gridDim.x;
+      row[u] = -1;
+      if (tile < ntiles) {
+        const TileDesc d = td[tile];
+        if (d.lo + (int)threadIdx.x < d.hi) row[u] = d.lo + threadIdx.x;
       }
     }
-    double sq = 0.0;
-    if (row < d.hi) {
-      x[row] = __dadd_rn(xv, __dmul_rn(alpha, pv));
-      const double rnew = __dsub_rn(rv, __dmul_rn(alpha, qv));
-      r[row] = rnew;
-      sq = __dmul_rn(rnew, rnew);
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const bool ok = row[u] >= 0;
+      xv[u] = ok ? x[row[u]] : 0.0;
+      pv[u] = ok ? p[row[u]] : 0.0;
+      qv[u] = ok ? q[row[u]] : 0.0;
+      rv[u] = ok ? r[row[u]] : 0.0;
     }
-    const double tot = block_tree<kTileThreads>(sq, ws);
-    if (threadIdx.x == 0) part[tile] = tot;
-    if (next >= ntiles) break;
-    tile = next;
-    d = dn;
-    row = rown;
-    xv = xn;
-    pv = pn;
-    qv = qn;
-    rv = rn_;
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      sq[u] = 0.0;
+      if (row[u] >= 0) {
+        x[row[u]] = __dadd_rn(xv[u], __dmul_rn(alpha, pv[u]));
+        const double rnew = __dsub_rn(rv[u], __dmul_rn(alpha, qv[u]));
+        r[row[u]] = rnew;
+        sq[u] = __dmul_rn(rnew, rnew);
+      }
+    }
+    // lane j of a tile owns row j only (<= kTileThreads rows), so the tile
+    // sum is the block tree of the per-row squares
+    block_tree_multi<U>(sq, ws);
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int tile = t0 + u * gridDim.x;
+        if (tile < ntiles) part[tile] = sq[u];
+      }
+    }
   }
-  finish_grid(st, 2, kStepRr, part, ntiles, ws);
+  finish_grid(st, 2, kStepRr, part, ntiles, wsf);
 }
 
 // res = b - A x (or b), optionally stored; res.res partial; the last CTA runs
@@ -846,6 +955,51 @@ __global__ void k_build_meta(long long n, const int *sp, const int *scol, const 
     if (i1 < 0) i1 = len;
     const bool fits = len <= kSlots && dpos >= 0 && i1 <= 15;
     meta[row] = fits ? static_cast<uint16_t>(len | (dpos << 4) | (i0 << 8) | (i1 << 12)) : kMetaGeneric;
+  }
+}
+
+// In-block entries of each row (columns inside the row's block): count, and
+// packing into the plan's in-block SELL-32 layout (same slices, widths =
+// longest in-block row of the slice), in ascending column order.
+__device__ __forceinline__ void row_block(const int *boff, int nb, int row, int &blo, int &bhi) {
+  int L = 0, H = nb;
+  while (H - L > 1) {
+    const int M = (L + H) >> 1;
+    if (boff[M] <= row) L = M; else H = M;
+  }
+  blo = boff[L];
+  bhi = boff[L + 1];
+}
+
+__global__ void k_ib_count(long long n, const int *sp, const int *scol, const int *boff, int nb, int *cnt) {
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x) {
+    const int row = static_cast<int>(r);
+    const int s = row >> 5, sb = sp[s], width = (sp[s + 1] - sb) >> 5, base = sb + (row & 31);
+    int blo, bhi;
+    row_block(boff, nb, row, blo, bhi);
+    int k = 0;
+    for (int j = 0; j < width; j++) {
+      const int c = scol[base + 32 * j];
+      k += (c >= blo && c < bhi) ? 1 : 0;
+    }
+    cnt[row] = k;
+  }
+}
+
+template <typename E>
+__global__ void k_ib_pack(long long n, const int *sp, const int *scol, const int *boff, int nb, const int *ib_sp,
+                          const E *src, E *dst) {
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x) {
+    const int row = static_cast<int>(r);
+    const int s = row >> 5, sb = sp[s], width = (sp[s + 1] - sb) >> 5, base = sb + (row & 31);
+    const int ibase = ib_sp[s] + (row & 31);
+    int blo, bhi;
+    row_block(boff, nb, row, blo, bhi);
+    int k = 0;
+    for (int j = 0; j < width; j++) {
+      const int c = scol[base + 32 * j];
+      if (c >= blo && c < bhi) dst[ibase + 32 * (k++)] = src[base + 32 * j];
+    }
   }
 }
 

@@ -142,7 +142,7 @@ class DeviceCSR:
             packed = packed[1]
         return packed
 
-    def c_struct(self, val64=None, val32=None) -> _lib.MpbCsr:
+    def c_struct(self, val64=None, val32=None, plan=None) -> _lib.MpbCsr:
         s = _lib.MpbCsr()
         s.n = self.n
         s.nnz = self.nnz
@@ -159,6 +159,11 @@ class DeviceCSR:
         sv32 = self.sell_values(v32)
         s.sell_val64 = sv64.data_ptr() if sv64 is not None else None
         s.sell_val32 = sv32.data_ptr() if sv32 is not None else None
+        if plan is not None:
+            iv64 = plan.inblock_values(sv64)
+            iv32 = plan.inblock_values(sv32)
+            s.ib_val64 = iv64.data_ptr() if iv64 is not None else None
+            s.ib_val32 = iv32.data_ptr() if iv32 is not None else None
         return s
 
     def nbytes(self) -> int:

@@ -120,7 +120,7 @@ def _dev_struct(A: SparseMatrix, mp: MixedPreconditioner):
             D.val64 = to_device(A.values, device=D.device)
         val64 = D.val64
     val32 = mp.p_low.dvalues if mp.p_low is not None else None
-    return D, D.c_struct(val64=val64, val32=val32)
+    return D, D.c_struct(val64=val64, val32=val32, plan=P.plan)
 
 
 def true_relres(A: SparseMatrix, x, b, r0_norm: float) -> float:
