@@ -32,6 +32,7 @@ sys.path.insert(0, ROOT)
 sys.path.insert(0, "/root/reference/pkg/src")
 
 import mpcg  # noqa: E402  (the reference)
+import mpcg.problems  # noqa: E402
 from mpcg import backend as ref_backend  # noqa: E402
 from mpcg.bjac import BlockPartition as RefPartition, setup as ref_setup  # noqa: E402
 from mpcg.policies import PrecisionPolicy as RefPolicy, build_mixed as ref_build, fmp_apply as ref_fmp  # noqa: E402
@@ -71,8 +72,13 @@ def cases():
                        ("nb1", RefPartition.equal_split(200, 1))])
     fams = {"const8": (8, P.Family.CONST, 1.0, 0), "ani6": (6, P.Family.ANI, 100.0, 0),
             "dis10": (10, P.Family.DIS, 1000.0, 0), "rand12": (12, P.Family.RAND, 1000.0, 3)}
+    from mpcg.problems import CoefficientField, Family as RefFamily, GridSpec, build_matrix
     for name, (n, fam, s, seed) in fams.items():
-        M = ref_matrix(P.family_matrix(n, fam, s, seed))
+        # the reference's own assembly; this repo's generator must match it bitwise
+        M = build_matrix(GridSpec(n), CoefficientField(RefFamily(fam.value), s, seed))
+        mine = P.family_matrix(n, fam, s, seed)
+        assert np.array_equal(M.values.view(np.uint64), mine.values.view(np.uint64))
+        assert np.array_equal(M.col_idx, mine.col_idx) and np.array_equal(M.row_ptr, mine.row_ptr)
         N = n ** 3
         parts = [("nb32", RefPartition.equal_split(N, 32)),
                  ("r64", RefPartition(np.append(np.arange(0, N, 64), N)))]
@@ -132,6 +138,9 @@ def main():
             fx[f"{key}/meta"] = np.array([tol, kk, tt])
             print(f"{name:12s} {pol:18s} it={rep.iterations:4d} "
                   f"final_true={rep.final_true_relres:.3e}")
+    # SplitMix64 / normal streams and the 3-T operator at a tiny size
+    fx["streams/splitmix64_s7"] = mpcg.problems.splitmix64_stream(7, 64)
+    fx["streams/splitmix64_s2pow40"] = mpcg.problems.splitmix64_stream(2 ** 40 + 3, 64)
     path = os.path.join(HERE, "golden.npz")
     np.savez_compressed(path, **fx)
     print("wrote", path, os.path.getsize(path), "bytes")
