@@ -52,6 +52,7 @@ extern "C" {
 #define MPB_ERR_POLICY (-6)     /* unknown policy kind / missing instance  */
 #define MPB_ERR_WORKSPACE (-7)  /* workspace too small                     */
 #define MPB_ERR_LAYOUT (-8)     /* SELL-32 layout / values missing         */
+#define MPB_ERR_COMM (-9)       /* NCCL missing or a collective failed     */
 
 /* policy kinds (policies.py:30-37) */
 #define MPB_UNIFORM 0
@@ -261,6 +262,39 @@ int mpb_profile_iteration(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A,
                           const mpb_solve_options *opt, const double *b, double *x,
                           void *workspace, int64_t workspace_bytes, int branch,
                           int reps, double *h_ms);
+/* ---- multi-GPU: z-slab row sharding over NCCL (one process per GPU) ---- */
+typedef struct mpb_comm mpb_comm;
+/* Ghost rows of one slab.  Own rows are 0..n-1 of the local matrix; columns
+ * outside the slab are renumbered to n..n+recv_lo-1 (rows just below the slab,
+ * owned by rank_lo) and n+recv_lo..n+recv_lo+recv_hi-1 (rows just above,
+ * owned by rank_hi), keeping every row's stored (ascending global column)
+ * order.  Each rank sends its first send_lo own rows to rank_lo and its last
+ * send_hi own rows to rank_hi (-1: no neighbour). */
+typedef struct mpb_halo {
+  int rank_lo, rank_hi;
+  int64_t recv_lo, recv_hi;
+  int64_t send_lo, send_hi;
+} mpb_halo;
+/* 128-byte NCCL unique id (rank 0 creates it, the ranks share it). */
+int mpb_comm_unique_id(void *h_id);
+int mpb_comm_create(mpb_handle *h, int rank, int nranks, const void *h_id,
+                    mpb_comm **out);
+int mpb_comm_destroy(mpb_comm *c);
+int64_t mpb_solve_workspace_bytes_dist(const mpb_plan *plan, int64_t n,
+                                       int64_t ghosts);
+/* mpb_pcg_solve on this rank's slab: b has n entries, x has n + ghosts
+ * (ghost part is scratch).  Halos of p and of the preconditioner's pass
+ * outputs are exchanged with ncclSend/ncclRecv, the three dot products are
+ * fp64 ncclAllReduce(sum) of the per-rank device-order sums; everything is
+ * captured in the iteration graph.  Every rank gets the same scalars, trace
+ * and stopping decision. */
+int mpb_pcg_solve_dist(mpb_handle *h, const mpb_comm *comm, const mpb_halo *halo,
+                       const mpb_plan *plan, const mpb_csr *A,
+                       const mpb_solve_options *opt, const double *b, double *x,
+                       double *tr_relres, double *tr_true, int32_t *tr_branch,
+                       double *tr_time, void *workspace, int64_t workspace_bytes,
+                       mpb_solve_result *res);
+
 /* ||b - A x|| / r0_norm in device order.  Synchronous. */
 int mpb_true_relres(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A,
                     const double *x, const double *b, double r0_norm,

@@ -37,7 +37,8 @@ EXPORTED = (
     "mpb_true_relres", "mpb_profile_iteration", "mpb_sell_create",
     "mpb_sell_destroy", "mpb_sell_nnz", "mpb_sell_pack_f64", "mpb_sell_pack_f32",
     "mpb_plan_bind_sell", "mpb_plan_inblock_nnz", "mpb_plan_pack_inblock_f64",
-    "mpb_plan_pack_inblock_f32",
+    "mpb_plan_pack_inblock_f32", "mpb_comm_unique_id", "mpb_comm_create",
+    "mpb_comm_destroy", "mpb_solve_workspace_bytes_dist", "mpb_pcg_solve_dist",
 )
 
 
@@ -52,6 +53,12 @@ class MpbCsr(C.Structure):
                 ("sell", C.c_void_p), ("sell_val64", C.c_void_p),
                 ("sell_val32", C.c_void_p), ("ib_val64", C.c_void_p),
                 ("ib_val32", C.c_void_p)]
+
+
+class MpbHalo(C.Structure):
+    _fields_ = [("rank_lo", C.c_int), ("rank_hi", C.c_int),
+                ("recv_lo", C.c_int64), ("recv_hi", C.c_int64),
+                ("send_lo", C.c_int64), ("send_hi", C.c_int64)]
 
 
 class MpbSolveOptions(C.Structure):
@@ -123,6 +130,12 @@ def _declare(L):
         "mpb_sell_nnz": ([_P], C.c_int64),
         "mpb_sell_pack_f64": ([_P, _P, _P, _P, _P], C.c_int),
         "mpb_sell_pack_f32": ([_P, _P, _P, _P, _P], C.c_int),
+        "mpb_comm_unique_id": ([_P], C.c_int),
+        "mpb_comm_create": ([_P, C.c_int, C.c_int, _P, C.POINTER(_P)], C.c_int),
+        "mpb_comm_destroy": ([_P], C.c_int),
+        "mpb_solve_workspace_bytes_dist": ([_P, _I64, _I64], C.c_int64),
+        "mpb_pcg_solve_dist": ([_P, _P, C.POINTER(MpbHalo), _P, C.POINTER(MpbCsr), C.POINTER(MpbSolveOptions), _P,
+                                _P, _P, _P, _P, _P, _P, _I64, C.POINTER(MpbSolveResult)], C.c_int),
         "mpb_true_relres": ([_P, _P, C.POINTER(MpbCsr), _P, _P, C.c_double, C.POINTER(C.c_double)], C.c_int),
     }
     for name, (args, res) in sig.items():

@@ -286,7 +286,6 @@ def setup(A: SparseMatrix, nb: int = 32, k: int = 2, t: int = 2,
     entry that is missing, zero, or underflows to zero is a ValueError naming
     the row.
     """
-    torch = __import__("torch")
     if A.n != A.m:
         raise ValueError(f"matrix is {A.n}x{A.m}, preconditioner needs square")
     if partition is None:
@@ -295,6 +294,14 @@ def setup(A: SparseMatrix, nb: int = 32, k: int = 2, t: int = 2,
         raise ValueError(f"partition covers {partition.n} rows, matrix has {A.n}")
     if k < 1 or t < 1:
         raise ValueError("sweep counts k and t must be at least 1")
+    return _setup_impl(A, k, t, precision, partition)
+
+
+def _setup_impl(A: SparseMatrix, k: int, t: int, precision: Precision,
+                partition: BlockPartition) -> BjacPreconditioner:
+    """setup() after argument checks; also used for multi-GPU slabs, whose
+    local matrix has ghost columns beyond its rows (distributed.py)."""
+    torch = __import__("torch")
     h = _lib.Handle.get()
     D = A.device()
     # stored-diagonal presence, checked on the source values first

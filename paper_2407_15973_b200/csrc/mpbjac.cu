@@ -14,6 +14,7 @@
 
 #include "../../include/mpbjac.h"
 #include "mpbjac_kernels.cuh"
+#include "mpbjac_nccl.h"
 
 using namespace mpb;
 
@@ -38,7 +39,7 @@ inline int status_of(cudaError_t e) { return e == cudaSuccess ? MPB_OK : static_
   } while (0)
 
 struct GraphKey {
-  const void *plan, *rp, *sell, *v64, *v32, *b, *x, *trr, *trt, *trb, *trw, *ws;
+  const void *plan, *rp, *sell, *v64, *v32, *b, *x, *trr, *trt, *trb, *trw, *ws, *comm;
   int kind, k, t, iters;
   long long stride, n;
   bool operator==(const GraphKey &o) const { return std::memcmp(this, &o, sizeof(GraphKey)) == 0; }
@@ -59,6 +60,11 @@ struct mpb_plan {
   int *d_ib_sp, *d_ib_col;  // in-block SELL layout (first passes)
   int64_t ib_nnz;
   int max_tile_ib;
+};
+
+struct mpb_comm {
+  mpb::ncclComm_t comm;
+  int rank, nranks;
 };
 
 struct mpb_sell {
@@ -245,11 +251,50 @@ const float *ib_vals<float>(const mpb_csr *A) {
 // k outer passes (bjac.py:127-149).  Residual from r64 (narrowed on load) or
 // rT; final output to zout (T) and/or zout64; r.z partials when part != null
 // (and, in solve mode, the fused rho step in the last CTA).
+// multi-GPU context of a solve (null on one GPU)
+struct DistCtx {
+  const mpb_comm *comm;
+  mpb_halo halo;
+};
+
+// Fill the ghost rows [n, n+ng) of `buf` from the neighbouring slabs and
+// send ours (NCCL grouped point-to-point, on the solve stream).
+int halo_exchange(const DistCtx *dc, void *buf, int es, int64_t n, cudaStream_t s) {
+  if (dc == nullptr) return MPB_OK;
+  NcclApi &N = nccl();
+  const mpb_halo &hl = dc->halo;
+  const int dt = es == 8 ? kNcclFloat64 : kNcclFloat32;
+  char *b = static_cast<char *>(buf);
+  if (N.GroupStart() != 0) return MPB_ERR_COMM;
+  int e = 0;
+  if (hl.rank_lo >= 0) {
+    if (hl.send_lo > 0) e |= N.Send(b, hl.send_lo, dt, hl.rank_lo, dc->comm->comm, s);
+    if (hl.recv_lo > 0) e |= N.Recv(b + n * es, hl.recv_lo, dt, hl.rank_lo, dc->comm->comm, s);
+  }
+  if (hl.rank_hi >= 0) {
+    if (hl.send_hi > 0) e |= N.Send(b + (n - hl.send_hi) * es, hl.send_hi, dt, hl.rank_hi, dc->comm->comm, s);
+    if (hl.recv_hi > 0) e |= N.Recv(b + (n + hl.recv_lo) * es, hl.recv_hi, dt, hl.rank_hi, dc->comm->comm, s);
+  }
+  e |= N.GroupEnd();
+  return e ? MPB_ERR_COMM : MPB_OK;
+}
+
+// Multi-GPU scalar step: all-reduce this rank's sum, then run the step.
+int dist_step(mpb_handle *h, const DistCtx *dc, SolverState *st, int step, int gate, cudaStream_t s) {
+  if (dc == nullptr) return MPB_OK;
+  NcclApi &N = nccl();
+  if (N.AllReduce(st->red_local, st->red_global, 2, kNcclFloat64, kNcclSum, dc->comm->comm, s) != 0)
+    return MPB_ERR_COMM;
+  k_apply_step<<<1, 32, 0, s>>>(step, st, gate);
+  MPB_LAUNCHED(h);
+  return MPB_OK;
+}
+
 template <typename T>
 int launch_apply(mpb_handle *h, cudaStream_t s, const mpb_plan *p, const mpb_csr *A, int k, int t,
                  const double *r64, const T *rT, T *zout, double *zout64, double *part,
                  unsigned long long *ovf_count, long long *ovf_first, SolverState *st, int want_branch,
-                 const ApplyBufs<T> &bufs) {
+                 const ApplyBufs<T> &bufs, const DistCtx *dc = nullptr) {
   PassArgs<T> a{};
   a.sp = A->sell->d_sp;
   a.scol = A->sell->d_col;
@@ -278,6 +323,10 @@ int launch_apply(mpb_handle *h, cudaStream_t s, const mpb_plan *p, const mpb_csr
     else if (last) rc = launch_pass<T, false, true>(h, s, p, a, bufs);
     else rc = launch_pass<T, false, false>(h, s, p, a, bufs);
     if (rc) return rc;
+    if (!last) {  // the next pass gathers this pass's output across slabs
+      rc = halo_exchange(dc, a.zout, sizeof(T), A->n, s);
+      if (rc) return rc;
+    }
   }
   return MPB_OK;
 }
@@ -332,7 +381,7 @@ int64_t plan_tiles(int64_t nb, const int64_t *offs, const int64_t *rp, int64_t *
 
 // Solve-time workspace layout
 struct SolveWs {
-  double *r, *q, *p0, *p1, *z64, *zA64, *zB64;
+  double *r, *q, *p, *z64, *zA64, *zB64;
   float *z32, *zA32, *zB32;
   double *res64, *dg64, *wA64, *wB64;
   float *res32, *dg32, *wA32, *wB32;
@@ -341,7 +390,9 @@ struct SolveWs {
   size_t bytes;
 };
 
-SolveWs carve(const mpb_plan *p, int64_t n, char *base) {
+// ng: ghost rows of a multi-GPU slab (0 on one GPU); vectors that kernels
+// gather from (p, pass outputs) carry them after the n own rows
+SolveWs carve(const mpb_plan *p, int64_t n, char *base, int64_t ng = 0) {
   SolveWs w{};
   size_t off = 0;
   auto take = [&](size_t bytes) -> char * {
@@ -350,16 +401,16 @@ SolveWs carve(const mpb_plan *p, int64_t n, char *base) {
     return q;
   };
   const size_t d = sizeof(double) * (n + 2), f = sizeof(float) * (n + 4);
+  const size_t dg = sizeof(double) * (n + ng + 2), fg = sizeof(float) * (n + ng + 4);
   w.r = (double *)take(d);
   w.q = (double *)take(d);
-  w.p0 = (double *)take(d);
-  w.p1 = (double *)take(d);
+  w.p = (double *)take(dg);
   w.z64 = (double *)take(d);
-  w.zA64 = (double *)take(d);
-  w.zB64 = (double *)take(d);
+  w.zA64 = (double *)take(dg);
+  w.zB64 = (double *)take(dg);
   w.z32 = (float *)take(f);
-  w.zA32 = (float *)take(f);
-  w.zB32 = (float *)take(f);
+  w.zA32 = (float *)take(fg);
+  w.zB32 = (float *)take(fg);
   if (p->large) {
     w.res64 = (double *)take(d);
     w.dg64 = (double *)take(d);
@@ -395,6 +446,7 @@ const char *mpb_status_string(int status) {
     case MPB_ERR_POLICY: return "policy needs a preconditioner instance that was not set up";
     case MPB_ERR_WORKSPACE: return "workspace too small";
     case MPB_ERR_LAYOUT: return "matrix has no SELL-32 layout (mpb_sell_create / mpb_sell_pack_*)";
+    case MPB_ERR_COMM: return "NCCL unavailable or a collective failed";
     default: break;
   }
   if (status > 0) return cudaGetErrorString(static_cast<cudaError_t>(status));
@@ -984,57 +1036,133 @@ static SpmvArgs spmv_args(const mpb_plan *p, const mpb_csr *A, const SolveWs &w)
   sa.sval = A->sell_val64;
   sa.td = p->d_td;
   sa.g = spmv_geom(p);
-  sa.p0 = w.p0;
-  sa.p1 = w.p1;
+  sa.p = w.p;
   sa.q = w.q;
   sa.part = w.part;
   sa.st = w.st;
   return sa;
 }
 
-// One PCG iteration (solver.py:140-177): preconditioner of the branch(es) the
-// policy can take (each gated on st->branch), fused rho step in its last
-// CTA; fused p-update+SpMV with the pq step; x/r update with the relres /
-// branch / convergence step; optional strided true residual.
+// One PCG iteration (solver.py:140-177): preconditioner of the branch(es)
+// the policy can take (each gated on st->branch) with the fused rho step;
+// p-update; SpMV with the pq step; x/r update with the relres / branch /
+// convergence step; optional strided true residual.  Multi-GPU: halo
+// exchanges before every gathering kernel, all-reduced scalar steps.
 static int enqueue_iteration(mpb_handle *h, cudaStream_t s, const mpb_plan *p, const mpb_csr *A,
-                             const mpb_solve_options *o, const SolveWs &w, const double *b, double *x) {
+                             const mpb_solve_options *o, const SolveWs &w, const double *b, double *x,
+                             const DistCtx *dc) {
   const bool high = o->kind != MPB_FIXED_LOW, low = o->kind != MPB_UNIFORM;
   const unsigned nt = static_cast<unsigned>(p->ntiles);
+  int rc;
   if (high) {
     ApplyBufs<double> bb{w.zA64, w.zB64, w.res64, w.dg64, w.wA64, w.wB64};
-    int rc = launch_apply<double>(h, s, p, A, o->k, o->t, w.r, nullptr, w.z64, nullptr, w.part, nullptr, nullptr,
-                                  w.st, 0, bb);
+    rc = launch_apply<double>(h, s, p, A, o->k, o->t, w.r, nullptr, w.z64, nullptr, w.part, nullptr, nullptr, w.st,
+                              0, bb, dc);
     if (rc) return rc;
   }
   if (low) {
     ApplyBufs<float> bb{w.zA32, w.zB32, w.res32, w.dg32, w.wA32, w.wB32};
-    int rc = launch_apply<float>(h, s, p, A, o->k, o->t, w.r, nullptr, w.z32, nullptr, w.part, &w.st->ovf_count,
-                                 &w.st->ovf_first, w.st, 1, bb);
+    rc = launch_apply<float>(h, s, p, A, o->k, o->t, w.r, nullptr, w.z32, nullptr, w.part, &w.st->ovf_count,
+                             &w.st->ovf_first, w.st, 1, bb, dc);
     if (rc) return rc;
   }
+  if ((rc = dist_step(h, dc, w.st, kStepRho, 2, s))) return rc;
   k_pupdate<<<persistent_grid(k_pupdate, 0, p->ntiles), kCtaThreads, 0, s>>>(p->d_td, static_cast<int>(nt), w.z32,
-                                                                              w.z64, w.p0, w.p1, w.st);
+                                                                              w.z64, w.p, w.st);
   MPB_LAUNCHED(h);
+  if ((rc = halo_exchange(dc, w.p, 8, A->n, s))) return rc;
   {
     const uint32_t dyn = spmv_dyn_smem(p);
     k_spmv_pq<<<persistent_grid(k_spmv_pq, dyn, p->ntiles, kWsThreads), kWsThreads, dyn, s>>>(spmv_args(p, A, w));
   }
   MPB_LAUNCHED(h);
-  k_update<<<persistent_grid(k_update, 0, p->ntiles), kCtaThreads, 0, s>>>(p->d_td, static_cast<int>(nt), x, w.p0,
-                                                                            w.p1, w.q, w.r, w.part, w.st);
+  if ((rc = dist_step(h, dc, w.st, kStepPq, 2, s))) return rc;
+  k_update<<<persistent_grid(k_update, 0, p->ntiles), kCtaThreads, 0, s>>>(p->d_td, static_cast<int>(nt), x, w.p,
+                                                                            w.q, w.r, w.part, w.st);
   MPB_LAUNCHED(h);
+  if ((rc = dist_step(h, dc, w.st, kStepRr, 2, s))) return rc;
   if (o->true_stride > 0) {
+    if ((rc = halo_exchange(dc, x, 8, A->n, s))) return rc;
     k_resid<true><<<persistent_grid(k_resid<true>, 0, p->ntiles), kCtaThreads, 0, s>>>(
-                                              A->sell->d_sp, A->sell->d_col, A->sell_val64, p->d_td, static_cast<int>(nt), b, x, nullptr, w.part, w.st, 1,
-                                              kStepTrue);
+        A->sell->d_sp, A->sell->d_col, A->sell_val64, p->d_td, static_cast<int>(nt), b, x, nullptr, w.part, w.st, 1,
+        kStepTrue);
     MPB_LAUNCHED(h);
+    if ((rc = dist_step(h, dc, w.st, kStepTrue, 1, s))) return rc;
   }
   return MPB_OK;
 }
 
+static int solve_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, const mpb_solve_options *opt,
+                      const double *b, double *x, double *tr_relres, double *tr_true, int32_t *tr_branch,
+                      double *tr_time, void *workspace, int64_t workspace_bytes, mpb_solve_result *res,
+                      const DistCtx *dc);
+
 int mpb_pcg_solve(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, const mpb_solve_options *opt,
                   const double *b, double *x, double *tr_relres, double *tr_true, int32_t *tr_branch,
                   double *tr_time, void *workspace, int64_t workspace_bytes, mpb_solve_result *res) {
+  return solve_impl(h, plan, A, opt, b, x, tr_relres, tr_true, tr_branch, tr_time, workspace, workspace_bytes, res,
+                    nullptr);
+}
+
+int mpb_pcg_solve_dist(mpb_handle *h, const mpb_comm *comm, const mpb_halo *halo, const mpb_plan *plan,
+                       const mpb_csr *A, const mpb_solve_options *opt, const double *b, double *x,
+                       double *tr_relres, double *tr_true, int32_t *tr_branch, double *tr_time, void *workspace,
+                       int64_t workspace_bytes, mpb_solve_result *res) {
+  if (!comm || !halo) return MPB_ERR_ARG;
+  if (halo->recv_lo < 0 || halo->recv_hi < 0 || halo->send_lo < 0 || halo->send_hi < 0) return MPB_ERR_ARG;
+  if (halo->send_lo > A->n || halo->send_hi > A->n) return MPB_ERR_SHAPE;
+  DistCtx dc{comm, *halo};
+  return solve_impl(h, plan, A, opt, b, x, tr_relres, tr_true, tr_branch, tr_time, workspace, workspace_bytes, res,
+                    &dc);
+}
+
+int64_t mpb_solve_workspace_bytes_dist(const mpb_plan *plan, int64_t n, int64_t ghosts) {
+  if (!plan || n != plan->n || ghosts < 0) return MPB_ERR_ARG;
+  return static_cast<int64_t>(carve(plan, n, nullptr, ghosts).bytes);
+}
+
+// ---- communicator ----------------------------------------------------------
+int mpb_comm_unique_id(void *h_id) {
+  if (!h_id) return MPB_ERR_ARG;
+  NcclApi &N = nccl();
+  if (!N.ok) return MPB_ERR_COMM;
+  ncclUniqueId id;
+  if (N.GetUniqueId(&id) != 0) return MPB_ERR_COMM;
+  std::memcpy(h_id, &id, sizeof(id));
+  return MPB_OK;
+}
+
+int mpb_comm_create(mpb_handle *h, int rank, int nranks, const void *h_id, mpb_comm **out) {
+  if (!h || !h_id || !out || nranks < 1 || rank < 0 || rank >= nranks) return MPB_ERR_ARG;
+  *out = nullptr;
+  NcclApi &N = nccl();
+  if (!N.ok) return MPB_ERR_COMM;
+  MPB_CUDA(cudaSetDevice(h->device));
+  ncclUniqueId id;
+  std::memcpy(&id, h_id, sizeof(id));
+  mpb_comm *c = new mpb_comm();
+  c->rank = rank;
+  c->nranks = nranks;
+  if (N.CommInitRank(&c->comm, nranks, id, rank) != 0) {
+    delete c;
+    return MPB_ERR_COMM;
+  }
+  *out = c;
+  return MPB_OK;
+}
+
+int mpb_comm_destroy(mpb_comm *c) {
+  if (!c) return MPB_OK;
+  NcclApi &N = nccl();
+  if (N.ok && c->comm) N.CommDestroy(c->comm);
+  delete c;
+  return MPB_OK;
+}
+
+static int solve_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, const mpb_solve_options *opt,
+                      const double *b, double *x, double *tr_relres, double *tr_true, int32_t *tr_branch,
+                      double *tr_time, void *workspace, int64_t workspace_bytes, mpb_solve_result *res,
+                      const DistCtx *dc) {
   if (!opt) return MPB_ERR_ARG;
   if (opt->kind < MPB_UNIFORM || opt->kind > MPB_ADAPTIVE_LH) return MPB_ERR_POLICY;
   if (!A || (opt->kind != MPB_UNIFORM && !A->sell_val32)) return MPB_ERR_POLICY;
@@ -1046,7 +1174,8 @@ int mpb_pcg_solve(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, const m
   if (plan->n != A->n) return MPB_ERR_PARTITION;
   if (opt->k < 1 || opt->t < 1) return MPB_ERR_SWEEPS;
   if (opt->max_iter < 1) return MPB_ERR_ARG;
-  SolveWs w = carve(plan, A->n, static_cast<char *>(workspace));
+  const int64_t ng = dc ? dc->halo.recv_lo + dc->halo.recv_hi : 0;
+  SolveWs w = carve(plan, A->n, static_cast<char *>(workspace), ng);
   if (workspace_bytes < static_cast<int64_t>(w.bytes)) return MPB_ERR_WORKSPACE;
   std::memset(res, 0, sizeof(*res));
   res->overflow_index = -1;
@@ -1069,6 +1198,7 @@ int mpb_pcg_solve(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, const m
   init.tr_true = tr_true;
   init.tr_branch = tr_branch;
   init.tr_time = tr_time;
+  init.dist = dc ? 1 : 0;
   *h->h_state = init;
   MPB_CUDA(cudaMemcpyAsync(w.st, h->h_state, sizeof(SolverState), cudaMemcpyHostToDevice, s));
   k_fill<<<elt_blocks(opt->max_iter), kEltThreads, 0, s>>>(tr_true, opt->max_iter, NAN);
@@ -1076,6 +1206,7 @@ int mpb_pcg_solve(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, const m
   if (!opt->has_x0) MPB_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * A->n, s));
   // r0 = b - A x0 (or b) and ||r0|| (solver.py:118-130)
   if (opt->has_x0) {
+    if ((rc = halo_exchange(dc, x, 8, A->n, s))) return rc;
     k_resid<true><<<persistent_grid(k_resid<true>, 0, plan->ntiles), kCtaThreads, 0, s>>>(
                                               A->sell->d_sp, A->sell->d_col, A->sell_val64, plan->d_td, static_cast<int>(nt), b, x, w.r, w.part, w.st, 0,
                                               kStepR0);
@@ -1085,6 +1216,7 @@ int mpb_pcg_solve(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, const m
                                                0, kStepR0);
   }
   MPB_LAUNCHED(h);
+  if ((rc = dist_step(h, dc, w.st, kStepR0, 0, s))) return rc;
   MPB_CUDA(cudaMemcpyAsync(h->h_state, w.st, sizeof(SolverState), cudaMemcpyDeviceToHost, s));
   MPB_CUDA(cudaStreamSynchronize(s));
   res->r0_norm = h->h_state->r0;
@@ -1118,6 +1250,7 @@ int mpb_pcg_solve(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, const m
   key.iters = G;
   key.stride = opt->true_stride;
   key.n = A->n;
+  key.comm = dc ? dc->comm : nullptr;
   if (!(h->have_graph && h->gkey == key)) {
     if (h->have_graph) {
       cudaGraphExecDestroy(h->gexec);
@@ -1126,7 +1259,7 @@ int mpb_pcg_solve(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, const m
     const int64_t l0 = h->launches;
     MPB_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     int crc = MPB_OK;
-    for (int i = 0; i < G && crc == MPB_OK; i++) crc = enqueue_iteration(h, s, plan, A, opt, w, b, x);
+    for (int i = 0; i < G && crc == MPB_OK; i++) crc = enqueue_iteration(h, s, plan, A, opt, w, b, x, dc);
     cudaGraph_t graph = nullptr;
     cudaError_t ce = cudaStreamEndCapture(s, &graph);
     if (crc != MPB_OK) {
@@ -1155,10 +1288,12 @@ int mpb_pcg_solve(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, const m
   MPB_CUDA(cudaEventRecord(h->ev_t1, s));
   const SolverState st = *h->h_state;
   if (st.error == kOk) {  // final true residual (solver.py:179-182)
+    if ((rc = halo_exchange(dc, x, 8, A->n, s))) return rc;
     k_resid<true><<<persistent_grid(k_resid<true>, 0, plan->ntiles), kCtaThreads, 0, s>>>(
                                               A->sell->d_sp, A->sell->d_col, A->sell_val64, plan->d_td, static_cast<int>(nt), b, x, nullptr, w.part, w.st, 0,
                                               kStepFinal);
     MPB_LAUNCHED(h);
+    if ((rc = dist_step(h, dc, w.st, kStepFinal, 0, s))) return rc;
     MPB_CUDA(cudaMemcpyAsync(h->h_state, w.st, sizeof(SolverState), cudaMemcpyDeviceToHost, s));
   }
   MPB_CUDA(cudaStreamSynchronize(s));
@@ -1291,7 +1426,7 @@ int mpb_profile_iteration(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A,
   const int ugrid = persistent_grid(k_update, 0, plan->ntiles);
   const int pgrid = persistent_grid(k_pupdate, 0, plan->ntiles);
   rc = timed(7, [&]() -> int {
-    k_pupdate<<<pgrid, kCtaThreads, 0, s>>>(plan->d_td, static_cast<int>(nt), w.z32, w.z64, w.p0, w.p1, w.st);
+    k_pupdate<<<pgrid, kCtaThreads, 0, s>>>(plan->d_td, static_cast<int>(nt), w.z32, w.z64, w.p, w.st);
     MPB_LAUNCHED(h);
     return MPB_OK;
   });
@@ -1303,7 +1438,7 @@ int mpb_profile_iteration(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A,
   });
   if (rc) return rc;
   rc = timed(4, [&]() -> int {
-    k_update<<<ugrid, kCtaThreads, 0, s>>>(plan->d_td, static_cast<int>(nt), x, w.p0, w.p1, w.q, w.r, w.part,
+    k_update<<<ugrid, kCtaThreads, 0, s>>>(plan->d_td, static_cast<int>(nt), x, w.p, w.q, w.r, w.part,
                                          w.st);
     MPB_LAUNCHED(h);
     return MPB_OK;

@@ -50,6 +50,9 @@ struct SolverState {
   int *tr_branch;
   double *tr_time;
   unsigned int ticket[4];  // last-CTA counters of the fused scalar steps
+  double red_local[2];     // multi-GPU: this rank's sum (and overflow count)
+  double red_global[2];    //            after the all-reduce
+  int dist;                // multi-GPU: scalar steps wait for the all-reduce
   int kind;
   int branch;  // 0 high (fp64 instance), 1 low (fp32 instance)
   int first;   // p is None (solver.py:150-151)

@@ -145,9 +145,24 @@ __device__ __forceinline__ void finish_grid(SolverState *st, int ticket, int ste
   if (!grid_last(&st->ticket[ticket])) return;
   const double tot = fin_sum(part, ntiles, ws);
   if (threadIdx.x == 0) {
-    scalar_step(step, tot, st);
+    if (st->dist) {  // multi-GPU: all-reduce first, k_apply_step runs the step
+      st->red_local[0] = tot;
+      st->red_local[1] = static_cast<double>(st->ovf_count);
+    } else {
+      scalar_step(step, tot, st);
+    }
     st->ticket[ticket] = 0u;
   }
+}
+
+// multi-GPU: the scalar step on the all-reduced sum (every rank computes the
+// same state from the same global values)
+__global__ void k_apply_step(int step, SolverState *st, int gate) {
+  if (threadIdx.x != 0) return;
+  if (gate == 1 && !st->true_pending) return;
+  if (gate == 2 && st->done) return;
+  if (step == kStepRho) st->ovf_count = static_cast<unsigned long long>(st->red_global[1]);
+  scalar_step(step, st->red_global[0], st);
 }
 
 // U independent tile sums at once (same order as block_tree<kTileThreads>
@@ -680,15 +695,11 @@ __global__ void __launch_bounds__(kCtaThreads) k_big_finish(const PassArgs<T> a,
 constexpr int kStreamTiles = 4;  // tiles per CTA iteration of the streaming kernels
 
 __global__ void __launch_bounds__(kCtaThreads)
-    k_pupdate(const TileDesc *td, int ntiles, const float *z32, const double *z64, double *p0, double *p1,
-              const SolverState *st) {
+    k_pupdate(const TileDesc *td, int ntiles, const float *z32, const double *z64, double *p, const SolverState *st) {
   if (st->done) return;
   const bool low = st->branch == 1;
   const bool first = st->first != 0;
   const double beta = st->beta;
-  const bool odd = (st->it & 1) != 0;
-  const double *pold = odd ? p0 : p1;
-  double *pnew = odd ? p1 : p0;
   constexpr int U = kStreamTiles;
   for (int t0 = blockIdx.x; t0 < ntiles; t0 += U * gridDim.x) {
     int row[U];
@@ -705,11 +716,11 @@ __global__ void __launch_bounds__(kCtaThreads)
 #pragma unroll
     for (int u = 0; u < U; u++) {
       zi[u] = row[u] < 0 ? 0.0 : (low ? static_cast<double>(z32[row[u]]) : z64[row[u]]);
-      po[u] = (row[u] < 0 || first) ? 0.0 : pold[row[u]];
+      po[u] = (row[u] < 0 || first) ? 0.0 : p[row[u]];
     }
 #pragma unroll
     for (int u = 0; u < U; u++)
-      if (row[u] >= 0) pnew[row[u]] = first ? zi[u] : __dadd_rn(zi[u], __dmul_rn(beta, po[u]));
+      if (row[u] >= 0) p[row[u]] = first ? zi[u] : __dadd_rn(zi[u], __dmul_rn(beta, po[u]));
   }
 }
 
@@ -723,7 +734,7 @@ struct SpmvArgs {
   const double *sval;
   const TileDesc *td;
   TileGeom g;
-  double *p0, *p1;  // p ping-pong: current = p[it & 1]
+  const double *p;  // search direction (updated in place by k_pupdate)
   double *q;
   double *part;
   SolverState *st;
@@ -777,7 +788,7 @@ __global__ void __launch_bounds__(kWsThreads) k_spmv_pq(const SpmvArgs a) {
   __shared__ Ring R;
   __shared__ double ws[32];
   const int ns = a.g.ns;
-  const double *p = (a.st->it & 1) ? a.p1 : a.p0;
+  const double *p = a.p;
   const StageLayout L = spmv_layout(a.g);
   ring_init(R, ns);
   if (threadIdx.x >= kConsumers) {
@@ -810,13 +821,12 @@ __global__ void __launch_bounds__(kWsThreads) k_spmv_pq(const SpmvArgs a) {
 // Persistent; each CTA iteration streams kStreamTiles tiles with every load
 // issued up front and one barrier pair for their tile sums.
 __global__ void __launch_bounds__(kCtaThreads)
-    k_update(const TileDesc *td, int ntiles, double *x, const double *p0, const double *p1, const double *q,
-             double *r, double *part, SolverState *st) {
+    k_update(const TileDesc *td, int ntiles, double *x, const double *p, const double *q, double *r, double *part,
+             SolverState *st) {
   if (st->done) return;
   __shared__ double ws[kStreamTiles][32];
   __shared__ double wsf[32];
   const double alpha = st->alpha;
-  const double *p = (st->it & 1) ? p1 : p0;
   constexpr int U = kStreamTiles;
   for (int t0 = blockIdx.x; t0 < ntiles; t0 += U * gridDim.x) {
     int row[U];
@@ -942,18 +952,23 @@ __global__ void k_build_meta(long long n, const int *sp, const int *scol, const 
       if (boff[M] <= row) L = M; else H = M;
     }
     const int blo = boff[L], bhi = boff[L + 1];
-    int len = 0, dpos = -1, i0 = -1, i1 = -1;
+    // in-block entries form one contiguous slot range (columns ascend in
+    // global order; multi-GPU ghost renumbering keeps the stored order and
+    // maps only out-of-slab columns, which are never in-block)
+    int len = 0, dpos = -1, i0 = -1, i1 = -1, nin = 0;
     for (int j = 0; j < width; j++) {
       const int c = scol[base + 32 * j];
       if (c < 0) break;
       len = j + 1;
       if (c == row) dpos = j;
-      if (c >= blo && i0 < 0) i0 = j;
-      if (c >= bhi && i1 < 0) i1 = j;
+      if (c >= blo && c < bhi) {
+        if (i0 < 0) i0 = j;
+        i1 = j + 1;
+        nin++;
+      }
     }
-    if (i0 < 0) i0 = len;
-    if (i1 < 0) i1 = len;
-    const bool fits = len <= kSlots && dpos >= 0 && i1 <= 15;
+    if (i0 < 0) i0 = i1 = 0;
+    const bool fits = len <= kSlots && dpos >= 0 && i1 <= 15 && nin == i1 - i0;
     meta[row] = fits ? static_cast<uint16_t>(len | (dpos << 4) | (i0 << 8) | (i1 << 12)) : kMetaGeneric;
   }
 }

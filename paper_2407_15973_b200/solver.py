@@ -147,25 +147,26 @@ def true_relres(A: SparseMatrix, x, b, r0_norm: float) -> float:
     return float(out.value)
 
 
-def _workspace(mp, plan, n, device):
+def _workspace(mp, plan, n, device, ghosts=0):
     torch = __import__("torch")
     ws = getattr(mp, "_workspace", None)
-    if ws is None or ws[0] is not plan:
-        nbytes = int(_lib.load().mpb_solve_workspace_bytes(plan.ptr, n))
+    if ws is None or ws[0] is not plan or ws[2] != ghosts:
+        nbytes = int(_lib.load().mpb_solve_workspace_bytes_dist(plan.ptr, n, ghosts))
         if nbytes < 0:
             _lib.check(nbytes, "workspace")
         buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
-        ws = (plan, buf)
+        ws = (plan, buf, ghosts)
         mp._workspace = ws
     return ws[1]
 
 
-def _solve_buffers(mp, n, cap, device):
+def _solve_buffers(mp, n, cap, device, ghosts=0):
     torch = __import__("torch")
     bufs = getattr(mp, "_solve_bufs", None)
-    if bufs is None or bufs[0] != (n, cap, str(device)):
+    key = (n, cap, str(device), ghosts)
+    if bufs is None or bufs[0] != key:
         f64 = dict(dtype=torch.float64, device=device)
-        bufs = ((n, cap, str(device)), torch.empty(n, **f64), torch.empty(n, **f64),
+        bufs = (key, torch.empty(n, **f64), torch.empty(n + ghosts, **f64),
                 torch.empty((3, cap), **f64), torch.empty(cap, dtype=torch.int32, device=device))
         mp._solve_bufs = bufs
     return bufs[1:]
@@ -182,9 +183,16 @@ def pcg_solve(A: SparseMatrix, b, mp: MixedPreconditioner,
     of iterations returns converged=False.  b (and x0) may be numpy arrays or
     CUDA tensors; x comes back in the same kind.
     """
-    torch = __import__("torch")
     if A.n != A.m:
         raise ValueError(f"matrix is {A.n}x{A.m}, solver needs square")
+    return _run_solve(A, b, mp, config, x0, graph_iters=graph_iters)
+
+
+def _run_solve(A: SparseMatrix, b, mp: MixedPreconditioner, config: SolveConfig, x0=None,
+               dist=None, n_global=None, graph_iters: int = 0) -> SolveReport:
+    """pcg_solve after the square check.  dist = (comm, halo, ghosts): this
+    rank's slab of a multi-GPU solve (distributed.SlabSolver)."""
+    torch = __import__("torch")
     if tuple(b.shape) != (A.n,) or dtype_name(b) != "float64":
         raise ValueError(f"rhs must be float64 of shape ({A.n},)")
     if mp.n != A.n:
@@ -195,14 +203,16 @@ def pcg_solve(A: SparseMatrix, b, mp: MixedPreconditioner,
     D, s = _dev_struct(A, mp)
     P = mp.any
     h = _lib.Handle.get(D.device.index)
-    cap = int(config.iteration_cap(A.n))
+    cap = int(config.iteration_cap(A.n if n_global is None else n_global))
+    ghosts = 0 if dist is None else int(dist[2])
     # persistent per-preconditioner buffers keep the device pointers stable,
     # so the captured CUDA graph is reused from one solve to the next
-    bd, x, tr, trb = _solve_buffers(mp, A.n, cap, D.device)
+    bd, x_ext, tr, trb = _solve_buffers(mp, A.n, cap, D.device, ghosts)
+    x = x_ext[:A.n]
     bd.copy_(b if is_tensor(b) else torch.from_numpy(np.ascontiguousarray(b)))
     if x0 is not None:
         x.copy_(x0 if is_tensor(x0) else torch.from_numpy(np.ascontiguousarray(x0)))
-    ws = _workspace(mp, P.plan, A.n, D.device)
+    ws = _workspace(mp, P.plan, A.n, D.device, ghosts)
     opt = _lib.MpbSolveOptions()
     opt.kind = KIND_CODE[mp.policy.kind]
     opt.adp_tol = float(mp.policy.adp_tol) if mp.policy.adp_tol is not None else 0.0
@@ -213,10 +223,17 @@ def pcg_solve(A: SparseMatrix, b, mp: MixedPreconditioner,
     opt.has_x0 = 0 if x0 is None else 1
     opt.graph_iters = int(graph_iters)
     res = _lib.MpbSolveResult()
-    _lib.check(h.lib.mpb_pcg_solve(
-        h.ptr, P.plan.ptr, C.byref(s), C.byref(opt), _lib.ptr(bd), _lib.ptr(x),
-        _lib.ptr(tr[0]), _lib.ptr(tr[1]), _lib.ptr(trb), _lib.ptr(tr[2]),
-        _lib.ptr(ws), ws.numel(), C.byref(res)), "pcg_solve")
+    if dist is None:
+        _lib.check(h.lib.mpb_pcg_solve(
+            h.ptr, P.plan.ptr, C.byref(s), C.byref(opt), _lib.ptr(bd), _lib.ptr(x_ext),
+            _lib.ptr(tr[0]), _lib.ptr(tr[1]), _lib.ptr(trb), _lib.ptr(tr[2]),
+            _lib.ptr(ws), ws.numel(), C.byref(res)), "pcg_solve")
+    else:
+        comm, halo, _ = dist
+        _lib.check(h.lib.mpb_pcg_solve_dist(
+            h.ptr, comm, C.byref(halo), P.plan.ptr, C.byref(s), C.byref(opt), _lib.ptr(bd),
+            _lib.ptr(x_ext), _lib.ptr(tr[0]), _lib.ptr(tr[1]), _lib.ptr(trb), _lib.ptr(tr[2]),
+            _lib.ptr(ws), ws.numel(), C.byref(res)), "pcg_solve_dist")
     it = int(res.iterations)
     err = int(res.error)
     if err:

@@ -302,3 +302,23 @@ def test_pcg_many_tiles_per_cta_bitwise(cuda, oracle, pol):
     assert rep.iterations == orc["iterations"]
     np.testing.assert_array_equal(rep.x, orc["x"])
     np.testing.assert_array_equal([r.implicit_relres for r in rep.trace], orc["relres"])
+
+
+@pytest.mark.parametrize("pol", ("fixed-low", "adaptive-hl:1e-3"))
+def test_slab_solver_single_rank_matches_single_gpu(cuda, oracle, pol):
+    """The multi-GPU path (NCCL communicator, all-reduced scalar steps
+    applied by k_apply_step) on one rank is bit-identical to pcg_solve."""
+    from paper_2407_15973_b200 import problems
+    from paper_2407_15973_b200.bjac import BlockPartition
+    from paper_2407_15973_b200.distributed import SlabSolver
+    from paper_2407_15973_b200.policies import PrecisionPolicy
+    from paper_2407_15973_b200.solver import SolveConfig
+    cs = problems.make_config("c2", 16)
+    offs = np.append(np.arange(0, cs.A.n, 64), cs.A.n)
+    rep, orc = _solve_both(cs.A, cs.b, offs, pol, 2, 2, 1e-10, oracle, stride=4)
+    ss = SlabSolver(cs.A, BlockPartition(offs), PrecisionPolicy.parse(pol), k=2, t=2, rank=0, nranks=1)
+    drep = ss.solve(cs.b, SolveConfig(res_tol=1e-10, record_true_residual_every=4))
+    assert drep.iterations == rep.iterations == orc["iterations"]
+    np.testing.assert_array_equal(drep.x, orc["x"])
+    np.testing.assert_array_equal([r.implicit_relres for r in drep.trace], orc["relres"])
+    assert drep.final_true_relres == orc["final_true_relres"]
