@@ -15,9 +15,10 @@ of DESIGN.md §4), the CPU baseline (the oracle restatement of the
 reference, 1 thread, bounded sample), clocks sampled during the timed
 region and the number of kernels launched.
 
-With --gpus N under torchrun, every rank solves its own C2 replica
-("replicas": the single-system z-slab sharding is a separate path, see
-DESIGN.md §6); ``--impl reference`` times the reference's CPU
+With --gpus N under torchrun the one system is cut into z-slabs, one per
+rank (strong scaling: ``value`` stays global solves per second), with NCCL
+halos and all-reduces inside the iteration graph (DESIGN.md §6);
+``--impl reference`` times the reference's CPU
 implementation (the oracle port, all host threads) on rank 0 only.
 """
 from __future__ import annotations
@@ -53,6 +54,8 @@ def parse():
     ap.add_argument("--ref-iters", type=int, default=60,
                     help="iterations per --impl reference step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the multi-GPU slab path even at N=1 (always on for N>1)")
     ap.add_argument("--profile-reps", type=int, default=20)
     return ap.parse_args()
 
@@ -190,7 +193,7 @@ def run_reference(args, world, rank):
     line = {"impl": "reference", "metric": metric_name(cs), "value": value,
             "unit": "solve/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * solve_s,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64 CG / f32 preconditioner", "data": "synthetic (seeded SplitMix64)",
             "config": config_dict(cs, part, policy, {"parallelism": "1 CPU process"}),
             "cpu_baseline": {"value": value, "unit": "solve/s", "cores": threads,
@@ -198,6 +201,15 @@ def run_reference(args, world, rank):
             "e2e": {"value": value, "unit": "solve/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def _inblock_nnz_local(row_ptr, col_idx, offsets, m):
+    """Zb of a slab (ghost columns >= m are never in a block)."""
+    blk = np.searchsorted(offsets, np.arange(m), side="right") - 1
+    rows = np.repeat(np.arange(m), np.diff(row_ptr))
+    c = np.asarray(col_idx, np.int64)
+    own = c < m
+    return int(np.count_nonzero(blk[rows[own]] == blk[c[own]]))
 
 
 def run_b200(args, world, rank, local):
@@ -216,13 +228,38 @@ def run_b200(args, world, rank, local):
     policy = args.policy or cs.policies[0]
     part = BlockPartition.fixed_size(cs.A.n, cs.block_rows)
     pp = PrecisionPolicy.parse(policy)
-    mp = build_mixed(cs.A, pp, k=cs.k, t=cs.t, partition=part)
     cfg = SolveConfig(res_tol=cs.res_tol)
-    b_dev = torch.from_numpy(cs.b).cuda()
-    h = _lib.Handle.get(local)
+    sharded = world > 1 or args.sharded
+    if sharded:
+        # strong scaling: one global solve, z-slabs over the ranks
+        from paper_2407_15973_b200.distributed import SlabSolver
+        ss = SlabSolver(cs.A, part, pp, k=cs.k, t=cs.t, rank=rank, nranks=world, device=local)
+        lo, hi = ss.slab.lo, ss.slab.hi
+
+        def solve(b):
+            return ss.solve(b, cfg)
+
+        def profile(branch):
+            return ss.profile_iteration(cfg, branch=branch, reps=args.profile_reps)
+        A_loc, plan = ss.A_loc, ss.mp.any.plan
+        zb = _inblock_nnz_local(ss.slab.row_ptr, ss.slab.col_idx, ss.slab.offsets, hi - lo)
+    else:
+        mp = build_mixed(cs.A, pp, k=cs.k, t=cs.t, partition=part)
+        lo, hi = 0, cs.A.n
+
+        def solve(b):
+            return pcg_solve(cs.A, b, mp, cfg)
+
+        def profile(branch):
+            return profile_iteration(cs.A, mp, config=cfg, branch=branch, reps=args.profile_reps)
+        A_loc, plan = cs.A, mp.any.plan
+        zb = inblock_nnz(cs.A, part)
+    m = hi - lo
+    b_loc = np.ascontiguousarray(cs.b[lo:hi])
+    b_dev = torch.from_numpy(b_loc).cuda()
 
     for _ in range(max(args.warmup, 1)):
-        rep = pcg_solve(cs.A, b_dev, mp, cfg)
+        rep = solve(b_dev)
     # ---- device-resident timed region --------------------------------------
     sampler = ClockSampler(local)
     sampler.start()
@@ -234,7 +271,7 @@ def run_b200(args, world, rank, local):
     iters = []
     ev0.record()
     for _ in range(args.steps):
-        rep = pcg_solve(cs.A, b_dev, mp, cfg)
+        rep = solve(b_dev)
         launches += rep.stats["kernel_launches"]
         iters.append(rep.iterations)
     ev1.record()
@@ -248,11 +285,11 @@ def run_b200(args, world, rank, local):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_per_step = ms / args.steps
-    value = world * args.steps / (ms / 1e3)
+    value = args.steps / (ms / 1e3)        # global solves per second
 
     # ---- end to end through the public API, host buffers -------------------
-    b_pin = torch.from_numpy(cs.b).pin_memory()
-    x_pin = torch.empty(cs.A.n, dtype=torch.float64).pin_memory()
+    b_pin = torch.from_numpy(b_loc).pin_memory()
+    x_pin = torch.empty(m, dtype=torch.float64).pin_memory()
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
@@ -260,9 +297,9 @@ def run_b200(args, world, rank, local):
     e0.record()
     d2h = 0
     for _ in range(args.steps):
-        r2 = pcg_solve(cs.A, b_pin, mp, cfg)
+        r2 = solve(b_pin)
         x_pin.copy_(r2.x, non_blocking=True)
-        d2h += 8 * cs.A.n + r2.iterations * (3 * 8 + 4)
+        d2h += 8 * m + r2.iterations * (3 * 8 + 4)
     e1.record()
     torch.cuda.synchronize()
     ems = e0.elapsed_time(e1)
@@ -270,15 +307,17 @@ def run_b200(args, world, rank, local):
         t = torch.tensor([ems], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ems = float(t.item())
-    e2e = {"value": world * args.steps / (ems / 1e3), "unit": "solve/s",
-           "h2d_bytes_per_step": 8 * cs.A.n, "d2h_bytes_per_step": d2h // args.steps,
-           "ms_per_step": ems / args.steps}
+    e2e = {"value": args.steps / (ems / 1e3), "unit": "solve/s",
+           "h2d_bytes_per_step": 8 * m, "d2h_bytes_per_step": d2h // args.steps,
+           "ms_per_step": ems / args.steps,
+           "note": "per rank: its slab of b in, its slab of x and the trace out" if sharded else
+                   "b in, x and the trace out"}
 
     # ---- per-kernel roofline (live CUDA events on the solve stream) --------
     branch = rep.trace[-1].branch if rep.trace else "low"
-    prof = profile_iteration(cs.A, mp, config=cfg, branch=branch, reps=args.profile_reps)
-    ntiles = mp.any.plan.ntiles
-    kb = kernel_bytes(cs.A.nnz, cs.A.n, branch, ntiles, inblock_nnz(cs.A, part))
+    prof = profile(branch)
+    ntiles = plan.ntiles
+    kb = kernel_bytes(A_loc.nnz, m, branch, ntiles, zb)
     peaks = {}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -299,7 +338,7 @@ def run_b200(args, world, rank, local):
     dom = max(kernels, key=lambda k: per_iter_share[k])
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath):
+    if os.path.exists(tpath) and world == 1:
         with open(tpath) as fh:
             traffic = json.load(fh).get(cs.name, {}).get(dom)
     roofline = {"bound": "hbm", "kernel": dom, "achieved": kernels[dom]["gbs"],
@@ -310,7 +349,7 @@ def run_b200(args, world, rank, local):
     iter_bytes = (kb["bjac_first"] + max(cs.k - 2, 0) * kb["bjac_middle"]
                   + (kb["bjac_last"] if cs.k > 1 else 0) + kb["pupdate"] + kb["spmv_pq"]
                   + kb["update"])
-    solve_gbs = iter_bytes * it_med / (ms_per_step * 1e-3) / 1e9
+    solve_gbs = world * iter_bytes * it_med / (ms_per_step * 1e-3) / 1e9
 
     # ---- CPU baseline (rank 0, N=1 only) -----------------------------------
     cpu = None
@@ -328,11 +367,12 @@ def run_b200(args, world, rank, local):
         line = {
             "metric": metric_name(cs), "value": value, "unit": "solve/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64 CG / f32 preconditioner" if pp.needs_low else "f64",
             "data": "synthetic (seeded SplitMix64 fields per BASELINE.json configs)",
             "config": config_dict(cs, part, policy, {
-                "parallelism": "1 GPU" if world == 1 else f"{world} replicas (one solve per GPU)",
+                "parallelism": (f"z-slabs over {world} GPU(s), NCCL halos + fp64 all-reduce"
+                                if sharded else "1 GPU"),
                 "graph": "CUDA graph of 8 iterations replayed until the device sets done"}),
             "iterations": it_med, "time_to_solution_ms": ms_per_step,
             "converged": bool(rep.converged), "final_true_relres": rep.final_true_relres,

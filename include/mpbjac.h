@@ -294,6 +294,14 @@ int mpb_pcg_solve_dist(mpb_handle *h, const mpb_comm *comm, const mpb_halo *halo
                        double *tr_relres, double *tr_true, int32_t *tr_branch,
                        double *tr_time, void *workspace, int64_t workspace_bytes,
                        mpb_solve_result *res);
+/* mpb_profile_iteration on one slab (x and the workspace sized with
+ * `ghosts` as for mpb_pcg_solve_dist): the local kernels only, no halo or
+ * all-reduce (those are timed by the whole-solve measurement). */
+int mpb_profile_iteration_dist(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A,
+                               const mpb_solve_options *opt, int64_t ghosts,
+                               const double *b, double *x, void *workspace,
+                               int64_t workspace_bytes, int branch, int reps,
+                               double *h_ms);
 
 /* ||b - A x|| / r0_norm in device order.  Synchronous. */
 int mpb_true_relres(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A,

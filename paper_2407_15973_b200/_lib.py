@@ -39,6 +39,7 @@ EXPORTED = (
     "mpb_plan_bind_sell", "mpb_plan_inblock_nnz", "mpb_plan_pack_inblock_f64",
     "mpb_plan_pack_inblock_f32", "mpb_comm_unique_id", "mpb_comm_create",
     "mpb_comm_destroy", "mpb_solve_workspace_bytes_dist", "mpb_pcg_solve_dist",
+    "mpb_profile_iteration_dist",
 )
 
 
@@ -121,6 +122,8 @@ def _declare(L):
                            _P, _I64, C.POINTER(MpbSolveResult)], C.c_int),
         "mpb_profile_iteration": ([_P, _P, C.POINTER(MpbCsr), C.POINTER(MpbSolveOptions), _P, _P, _P, _I64,
                                    C.c_int, C.c_int, C.POINTER(C.c_double)], C.c_int),
+        "mpb_profile_iteration_dist": ([_P, _P, C.POINTER(MpbCsr), C.POINTER(MpbSolveOptions), _I64, _P, _P,
+                                        _P, _I64, C.c_int, C.c_int, C.POINTER(C.c_double)], C.c_int),
         "mpb_sell_create": ([_P, _I64, _P, _P, _P, C.POINTER(_P)], C.c_int),
         "mpb_sell_destroy": ([_P], C.c_int),
         "mpb_plan_bind_sell": ([_P, _P, _P], C.c_int),

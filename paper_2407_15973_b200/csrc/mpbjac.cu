@@ -1321,12 +1321,18 @@ static int solve_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, con
 int mpb_profile_iteration(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, const mpb_solve_options *opt,
                           const double *b, double *x, void *workspace, int64_t workspace_bytes, int branch, int reps,
                           double *h_ms) {
-  if (!opt) return MPB_ERR_ARG;
+  return mpb_profile_iteration_dist(h, plan, A, opt, 0, b, x, workspace, workspace_bytes, branch, reps, h_ms);
+}
+
+int mpb_profile_iteration_dist(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, const mpb_solve_options *opt,
+                               int64_t ghosts, const double *b, double *x, void *workspace,
+                               int64_t workspace_bytes, int branch, int reps, double *h_ms) {
+  if (!opt || ghosts < 0) return MPB_ERR_ARG;
   int rc = check_sell(A, true, branch == 1);
   if (rc == MPB_OK) rc = check_bound(plan, A);
   if (rc) return rc;
   if (!h || !plan || !b || !x || !workspace || !h_ms || reps < 1) return MPB_ERR_ARG;
-  SolveWs w = carve(plan, A->n, static_cast<char *>(workspace));
+  SolveWs w = carve(plan, A->n, static_cast<char *>(workspace), ghosts);
   if (workspace_bytes < static_cast<int64_t>(w.bytes)) return MPB_ERR_WORKSPACE;
   cudaStream_t s = h->solve;
   MPB_CUDA(cudaEventRecord(h->ev_in, h->user));

@@ -172,6 +172,13 @@ class SlabSolver:
                           dist=(self.comm, self.slab.halo(), self.slab.ghosts),
                           n_global=self.bounds[-1][1])
 
+    def profile_iteration(self, config=None, branch: str = "low", reps: int = 20) -> dict:
+        """Per-kernel times of one iteration on this slab (no communication)."""
+        from .solver import SolveConfig, profile_iteration
+        config = config or SolveConfig()
+        return profile_iteration(self.A_loc, self.mp, config=config, branch=branch, reps=reps,
+                                 ghosts=self.slab.ghosts, n_global=self.bounds[-1][1])
+
     def __del__(self):
         try:
             if self.comm:

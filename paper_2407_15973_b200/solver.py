@@ -352,16 +352,17 @@ def report_summary(report: SolveReport, extra: dict | None = None) -> dict:
 
 def profile_iteration(A: SparseMatrix, mp: MixedPreconditioner, *,
                       config: SolveConfig = SolveConfig(), branch: str = "low",
-                      reps: int = 20) -> dict:
+                      reps: int = 20, ghosts: int = 0, n_global=None) -> dict:
     """Mean CUDA-event time (ms) per launch of each kernel of one PCG
     iteration, on the buffers pcg_solve uses (mpb_profile_iteration).
-    Call after at least one pcg_solve with the same A / mp / config."""
+    Call after at least one pcg_solve with the same A / mp / config.
+    ghosts > 0: a slab of a multi-GPU solve (local kernels only)."""
     D, s = _dev_struct(A, mp)
     P = mp.any
     h = _lib.Handle.get(D.device.index)
-    cap = int(config.iteration_cap(A.n))
-    bd, x, _, _ = _solve_buffers(mp, A.n, cap, D.device)
-    ws = _workspace(mp, P.plan, A.n, D.device)
+    cap = int(config.iteration_cap(A.n if n_global is None else n_global))
+    bd, x, _, _ = _solve_buffers(mp, A.n, cap, D.device, ghosts)
+    ws = _workspace(mp, P.plan, A.n, D.device, ghosts)
     opt = _lib.MpbSolveOptions()
     opt.kind = KIND_CODE[mp.policy.kind]
     opt.adp_tol = float(mp.policy.adp_tol) if mp.policy.adp_tol is not None else 0.0
@@ -369,8 +370,8 @@ def profile_iteration(A: SparseMatrix, mp: MixedPreconditioner, *,
     opt.res_tol = float(config.res_tol)
     opt.max_iter = cap
     out = (C.c_double * 8)()
-    _lib.check(h.lib.mpb_profile_iteration(
-        h.ptr, P.plan.ptr, C.byref(s), C.byref(opt), _lib.ptr(bd), _lib.ptr(x),
+    _lib.check(h.lib.mpb_profile_iteration_dist(
+        h.ptr, P.plan.ptr, C.byref(s), C.byref(opt), int(ghosts), _lib.ptr(bd), _lib.ptr(x),
         _lib.ptr(ws), ws.numel(), 0 if branch == "high" else 1, int(reps), out),
         "profile_iteration")
     names = ("bjac_first", "bjac_middle", "bjac_last", "spmv_pq", "update",
