@@ -113,19 +113,28 @@ class ClockSampler:
 
 
 def kernel_bytes(Z, N, branch, ntiles, Zb):
-    """Algorithmic bytes per launch: every array streamed
-    once, gathered vector entries counted once, int32 SELL columns, 2-byte
-    per-row metadata; Z = stored nonzeros (SELL padding not counted)."""
-    # first pass: in-block entries only (Zb of them), r, z1 out, 2-byte meta
+    """Algorithmic bytes per launch, SURVEY.md §8(d) model (CSR, int32
+    row_ptr and col_idx, every array streamed once, gathered vector entries
+    counted once): what ``roofline.achieved`` is computed from."""
     if branch == "low":
-        first, mid, last = 8 * Zb + 14 * N, 8 * Z + 18 * N, 8 * Z + 18 * N
-        pupd = 20 * N
+        first, mid, last, pupd = 8 * Z + 16 * N, 8 * Z + 20 * N, 8 * Z + 24 * N, 24 * N
     else:
-        first, mid, last = 12 * Zb + 18 * N, 12 * Z + 26 * N, 12 * Z + 26 * N
-        pupd = 24 * N
+        first, mid, last, pupd = 12 * Z + 20 * N, 12 * Z + 28 * N, 12 * Z + 28 * N, 24 * N
     return {"bjac_first": first, "bjac_middle": mid, "bjac_last": last,
-            "pupdate": pupd, "spmv_pq": 12 * Z + 16 * N, "update": 48 * N,
+            "pupdate": pupd, "spmv_pq": 12 * Z + 20 * N, "update": 48 * N,
             "scalar": 8 * ntiles}
+
+
+def format_bytes(Z, N, branch, Zb):
+    """Bytes our layout has to move per launch: SELL values
+    only (row-pattern rows carry no column index), 2-byte row metadata, the
+    first pass reads in-block entries only (Zb), z_in / p gathered once."""
+    if branch == "low":
+        first, mid, last, pupd = 4 * Zb + 14 * N, 4 * Z + 18 * N, 4 * Z + 18 * N, 20 * N
+    else:
+        first, mid, last, pupd = 8 * Zb + 18 * N, 8 * Z + 26 * N, 8 * Z + 26 * N, 24 * N
+    return {"bjac_first": first, "bjac_middle": mid, "bjac_last": last,
+            "pupdate": pupd, "spmv_pq": 8 * Z + 18 * N, "update": 48 * N}
 
 
 def inblock_nnz(A, part):
@@ -318,6 +327,7 @@ def run_b200(args, world, rank, local):
     prof = profile(branch)
     ntiles = plan.ntiles
     kb = kernel_bytes(A_loc.nnz, m, branch, ntiles, zb)
+    fb = format_bytes(A_loc.nnz, m, branch, zb)
     peaks = {}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -332,8 +342,10 @@ def run_b200(args, world, rank, local):
         if t_ms <= 0:
             continue
         gbs = kb[name] / (t_ms * 1e-3) / 1e9
+        fgbs = fb[name] / (t_ms * 1e-3) / 1e9
         kernels[name] = {"ms": round(t_ms, 5), "bytes": kb[name], "gbs": round(gbs, 1),
-                         "frac": round(gbs / peak, 4)}
+                         "frac": round(gbs / peak, 4), "format_bytes": fb[name],
+                         "format_gbs": round(fgbs, 1)}
     per_iter_share = {k: v["ms"] for k, v in kernels.items()}
     dom = max(kernels, key=lambda k: per_iter_share[k])
     traffic = None
@@ -344,7 +356,9 @@ def run_b200(args, world, rank, local):
     roofline = {"bound": "hbm", "kernel": dom, "achieved": kernels[dom]["gbs"],
                 "peak": peak, "unit": "GB/s", "frac": kernels[dom]["frac"],
                 "traffic": traffic, "peak_source": peak_src,
-                "bytes_per_launch": kb[dom]}
+                "bytes_per_launch": kb[dom], "bytes_model": "SURVEY.md 8(d) CSR model",
+                "format_bytes_per_launch": fb[dom],
+                "format_frac": round(kernels[dom]["format_gbs"] / peak, 4)}
     it_med = int(np.median(iters))
     iter_bytes = (kb["bjac_first"] + max(cs.k - 2, 0) * kb["bjac_middle"]
                   + (kb["bjac_last"] if cs.k > 1 else 0) + kb["pupdate"] + kb["spmv_pq"]
@@ -373,7 +387,8 @@ def run_b200(args, world, rank, local):
             "config": config_dict(cs, part, policy, {
                 "parallelism": (f"z-slabs over {world} GPU(s), NCCL halos + fp64 all-reduce"
                                 if sharded else "1 GPU"),
-                "graph": "CUDA graph of 8 iterations replayed until the device sets done"}),
+                "graph": "CUDA graph of 8 iterations replayed until the device sets done",
+                "row_patterns": plan.layout_info()}),
             "iterations": it_med, "time_to_solution_ms": ms_per_step,
             "converged": bool(rep.converged), "final_true_relres": rep.final_true_relres,
             "solve_gbs": round(solve_gbs, 1),

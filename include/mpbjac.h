@@ -156,6 +156,10 @@ int mpb_plan_pack_inblock_f32(mpb_handle *h, const mpb_plan *p,
                               const float *sell_val, float *ib_val);
 int mpb_plan_info(const mpb_plan *p, int64_t *h_ntiles, int *h_large,
                   int64_t *h_max_tile_nnz);
+/* Row patterns of the bound SELL structure (after mpb_plan_bind_sell): rows
+ * whose column offsets match one of *h_npat (<= 128) patterns carry no column
+ * index on the hot path; *h_ngeneric rows read their SELL columns. */
+int mpb_plan_layout_info(const mpb_plan *p, int *h_npat, int64_t *h_ngeneric);
 
 /* ---- SELL-32 layout (hot-path matrix format) ----------------------------- */
 /* Builds slice pointers (from the host row_ptr) and packs the column array on

@@ -128,6 +128,13 @@ class DevicePlan:
             self.bound = S
         return self
 
+    def layout_info(self) -> dict:
+        """Row patterns of the bound structure: {"patterns", "generic_rows"}."""
+        npat, ngen = C.c_int(), C.c_int64()
+        _lib.check(self.h.lib.mpb_plan_layout_info(self.ptr, C.byref(npat), C.byref(ngen)),
+                   "mpb_plan_layout_info")
+        return {"patterns": int(npat.value), "generic_rows": int(ngen.value)}
+
     def __del__(self):
         try:
             if self.ptr:

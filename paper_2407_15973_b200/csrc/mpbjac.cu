@@ -60,6 +60,9 @@ struct mpb_plan {
   int *d_ib_sp, *d_ib_col;  // in-block SELL layout (first passes)
   int64_t ib_nnz;
   int max_tile_ib;
+  const int *d_pat;         // the bound SELL's row-pattern table (not owned)
+  int npat;
+  int64_t ngeneric;         // rows without a usable pattern (kMetaGeneric)
 };
 
 struct mpb_comm {
@@ -71,6 +74,9 @@ struct mpb_sell {
   int64_t n, nslices, nnz;  // nnz: padded entry count
   int *d_sp;                // nslices+1
   int *d_col;               // nnz
+  uint8_t *d_pid;           // per-row pattern id or kPidGeneric
+  int *d_pat;               // npat table entries of kPatStride ints
+  int npat;
 };
 
 struct mpb_handle {
@@ -139,6 +145,8 @@ TileGeom geom_for(const mpb_plan *p) {
   g.cap_e = std::min(p->max_tile_sell, kStageCap);
   g.max_sl = p->max_sl;
   g.ns = 2;
+  g.cols = p->ngeneric > 0 ? 1 : 0;
+  g.npat = p->npat;
   return g;
 }
 
@@ -301,6 +309,7 @@ int launch_apply(mpb_handle *h, cudaStream_t s, const mpb_plan *p, const mpb_csr
   a.sval = sell_vals<T>(A);
   a.ib_val = ib_vals<T>(A);
   a.meta = p->d_meta;
+  a.pat = p->d_pat;
   a.td = p->d_td;
   a.boff = p->d_boff;
   a.g = geom_for<T>(p);
@@ -604,9 +613,15 @@ int mpb_plan_bind_sell(mpb_handle *h, mpb_plan *p, const mpb_sell *sell) {
   if (p->bound == sell && p->d_meta) return MPB_OK;
   MPB_CUDA(cudaSetDevice(h->device));
   if (!p->d_meta) MPB_CUDA(cudaMalloc(&p->d_meta, sizeof(uint16_t) * p->n));
-  k_build_meta<<<elt_blocks(p->n), kEltThreads, 0, h->user>>>(p->n, sell->d_sp, sell->d_col, p->d_boff,
+  k_build_meta<<<elt_blocks(p->n), kEltThreads, 0, h->user>>>(p->n, sell->d_pid, sell->d_pat, p->d_boff,
                                                             static_cast<int>(p->nb), p->d_meta);
   MPB_LAUNCHED(h);
+  p->d_pat = sell->d_pat;
+  p->npat = sell->npat;
+  if (!p->large) {
+    k_tile_generic<<<static_cast<unsigned>(p->ntiles), kTileRows, 0, h->user>>>(p->d_td, p->d_meta);
+    MPB_LAUNCHED(h);
+  }
   // in-block SELL layout: per-row in-block counts -> slice widths -> pack
   const int64_t n = p->n, ns = (n + 31) / 32;
   int *d_cnt = nullptr;
@@ -643,12 +658,15 @@ int mpb_plan_bind_sell(mpb_handle *h, mpb_plan *p, const mpb_sell *sell) {
   p->ib_nnz = acc;
   // tile descriptors gain their in-block entry ranges
   std::vector<TileDesc> td(p->ntiles);
+  MPB_CUDA(cudaStreamSynchronize(h->user));
   MPB_CUDA(cudaMemcpy(td.data(), p->d_td, sizeof(TileDesc) * p->ntiles, cudaMemcpyDeviceToHost));
   int mx = 0;
+  p->ngeneric = 0;
   for (auto &d : td) {
     d.ie0 = ib_sp[d.s0];
     d.ie1 = ib_sp[d.s1];
     mx = std::max(mx, d.ie1 - d.ie0);
+    p->ngeneric += d.ngen;
   }
   p->max_tile_ib = mx;
   MPB_CUDA(cudaMemcpy(p->d_td, td.data(), sizeof(TileDesc) * p->ntiles, cudaMemcpyHostToDevice));
@@ -683,6 +701,13 @@ int mpb_plan_info(const mpb_plan *p, int64_t *h_ntiles, int *h_large, int64_t *h
   if (h_ntiles) *h_ntiles = p->ntiles;
   if (h_large) *h_large = p->large;
   if (h_max_tile_nnz) *h_max_tile_nnz = p->max_tile_nnz;
+  return MPB_OK;
+}
+
+int mpb_plan_layout_info(const mpb_plan *p, int *h_npat, int64_t *h_ngeneric) {
+  if (!p || !p->bound) return MPB_ERR_ARG;
+  if (h_npat) *h_npat = p->npat;
+  if (h_ngeneric) *h_ngeneric = p->ngeneric;
   return MPB_OK;
 }
 
@@ -840,6 +865,60 @@ int mpb_setup_diag_f32(mpb_handle *h, int64_t n, const int32_t *row_ptr, const i
 
 
 // ---- SELL-32 layout ------------------------------------------------------------
+// Row-pattern dictionary of a SELL structure (see mpbjac_kernels.cuh): count
+// the rows of every distinct (length, column offsets) pattern on the device,
+// keep the kPatMax most frequent, then tag every row with its verified
+// pattern id (or kPidGeneric).
+static cudaError_t build_patterns(mpb_handle *h, mpb_sell *S) {
+  const int64_t n = S->n;
+  PatSlot *d_tab = nullptr;
+  int *d_aux = nullptr;
+  cudaError_t e = cudaMalloc(&d_tab, sizeof(PatSlot) * kPatHash);
+  if (e == cudaSuccess) e = cudaMalloc(&d_aux, sizeof(int) * (kPatHash + kPatMax));
+  if (e == cudaSuccess) e = cudaMalloc(&S->d_pat, sizeof(int) * kPatMax * kPatStride);
+  if (e == cudaSuccess) e = cudaMalloc(&S->d_pid, std::max<int64_t>(n, 1));
+  if (e == cudaSuccess) e = cudaMemsetAsync(d_tab, 0, sizeof(PatSlot) * kPatHash, h->user);
+  if (e == cudaSuccess) e = cudaMemsetAsync(S->d_pat, 0, sizeof(int) * kPatMax * kPatStride, h->user);
+  if (e == cudaSuccess) {
+    k_pat_insert<<<static_cast<unsigned>((n + 255) / 256), 256, 0, h->user>>>(n, S->d_sp, S->d_col, d_tab);
+    h->launches++;
+    e = cudaGetLastError();
+  }
+  std::vector<PatSlot> tab(kPatHash);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(tab.data(), d_tab, sizeof(PatSlot) * kPatHash, cudaMemcpyDeviceToHost,
+                                            h->user);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->user);
+  if (e == cudaSuccess) {
+    std::vector<int> order;
+    for (int i = 0; i < kPatHash; i++)
+      if (tab[i].key != 0ull && tab[i].count > 0) order.push_back(i);
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return tab[a].count > tab[b].count; });
+    if (order.size() > static_cast<size_t>(kPatMax)) order.resize(kPatMax);
+    S->npat = static_cast<int>(order.size());
+    std::vector<int> aux(kPatHash + kPatMax, -1);  // slot -> pid, then the representative rows
+    for (int i = 0; i < S->npat; i++) {
+      aux[order[i]] = i;
+      aux[kPatHash + i] = tab[order[i]].rep;
+    }
+    e = cudaMemcpyAsync(d_aux, aux.data(), sizeof(int) * aux.size(), cudaMemcpyHostToDevice, h->user);
+    if (e == cudaSuccess && S->npat > 0) {
+      k_pat_fetch<<<1, kPatMax, 0, h->user>>>(d_aux + kPatHash, S->npat, S->d_sp, S->d_col, S->d_pat);
+      h->launches++;
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) {
+      k_pat_assign<<<elt_blocks(n), kEltThreads, 0, h->user>>>(n, S->d_sp, S->d_col, d_tab, d_aux, S->d_pat,
+                                                              S->d_pid);
+      h->launches++;
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->user);
+  }
+  cudaFree(d_tab);
+  cudaFree(d_aux);
+  return e;
+}
+
 int mpb_sell_create(mpb_handle *h, int64_t n, const int64_t *h_row_ptr, const int32_t *row_ptr,
                     const int32_t *col_idx, mpb_sell **out) {
   if (!h || !out || !h_row_ptr || !row_ptr || !col_idx || n < 1) return MPB_ERR_ARG;
@@ -865,6 +944,7 @@ int mpb_sell_create(mpb_handle *h, int64_t n, const int64_t *h_row_ptr, const in
     e = cudaGetLastError();
   }
   if (e == cudaSuccess) e = cudaStreamSynchronize(h->user);
+  if (e == cudaSuccess) e = build_patterns(h, S);
   if (e != cudaSuccess) {
     mpb_sell_destroy(S);
     return status_of(e);
@@ -877,6 +957,8 @@ int mpb_sell_destroy(mpb_sell *s) {
   if (!s) return MPB_OK;
   cudaFree(s->d_sp);
   cudaFree(s->d_col);
+  cudaFree(s->d_pid);
+  cudaFree(s->d_pat);
   delete s;
   return MPB_OK;
 }
@@ -1034,6 +1116,8 @@ static SpmvArgs spmv_args(const mpb_plan *p, const mpb_csr *A, const SolveWs &w)
   sa.sp = A->sell->d_sp;
   sa.scol = A->sell->d_col;
   sa.sval = A->sell_val64;
+  sa.meta = p->d_meta;
+  sa.pat = p->d_pat;
   sa.td = p->d_td;
   sa.g = spmv_geom(p);
   sa.p = w.p;
@@ -1387,6 +1471,7 @@ int mpb_profile_iteration_dist(mpb_handle *h, const mpb_plan *plan, const mpb_cs
       a.scol = A->sell->d_col;
       a.td = plan->d_td;
       a.meta = plan->d_meta;
+      a.pat = plan->d_pat;
       a.boff = plan->d_boff;
       a.t = opt->t;
       a.r64 = w.r;

@@ -9,14 +9,22 @@
 // bit-identical to the reference's row-sequential numba kernels
 // (pkg/src/mpcg/kernels_numba.py:37-70).
 //
-// Work unit: a tile of whole BJAC blocks (<= 512 rows), one thread per row.
-// The hot kernels are persistent and warp-specialised: warp 16 of each CTA
-// is a TMA producer that streams every input of the next tiles (SELL columns
-// and values, slice pointers, per-row metadata, the residual and the tile's
-// own vector slices) into a ring of shared-memory stages (cp.async.bulk +
-// full/empty mbarriers); warps 0-15 only compute.  Per-row static structure
-// (row length, diagonal slot, in-block slot range) is precomputed once per
-// (matrix, partition) into 2 bytes per row, so the hot loops do no searching.
+// Work unit: a tile of whole BJAC blocks (<= 256 rows), one thread per row.
+// The hot kernels are persistent and warp-specialised: warp 8 of each CTA
+// is a TMA producer that streams the inputs of the next tiles (SELL values,
+// slice pointers, per-row metadata, the residual) into a ring of
+// shared-memory stages (cp.async.bulk + full/empty mbarriers); warps 0-7 only
+// compute.
+//
+// Column indices are not streamed.  Every row whose stored columns, taken as
+// offsets from the row (c_j - row, in stored order), match one of <= 128
+// "row patterns" of the matrix (a 7-point stencil has 27, a 3-T system 81)
+// keeps only a pattern id in its 2-byte metadata, next to the slot range of
+// its in-block entries: columns are rebuilt as row + offset from the pattern
+// table held in shared memory.  Rows without a pattern ("generic" rows: long
+// or irregular rows) read their SELL columns, staged only for tiles that
+// contain such rows.  This removes 4 of the 8 bytes per fp32 entry (4 of 12
+// per fp64 entry) of every pass.  Vector gathers (z_in, p) go through L1.
 //
 // Dot products follow the fixed tile-tree order of include/mpbjac_order.h.
 // The scalar steps of the recurrence (rho, alpha, beta, relres, the aMP
@@ -36,11 +44,29 @@ constexpr int kMaxStages = 4;
 constexpr int kBarConsumers = 1;               // named barrier id among consumers
 constexpr uint16_t kMetaGeneric = 0xFFFFu;
 
-// ---- per-row metadata: len | dpos << 4 | i0 << 8 | i1 << 12 ---------------
-__device__ __forceinline__ int meta_len(uint16_t m) { return m & 15; }
-__device__ __forceinline__ int meta_dpos(uint16_t m) { return (m >> 4) & 15; }
+// ---- row patterns ------------------------------------------------------------
+constexpr int kPatMax = 128;     // pattern ids 0..127
+constexpr int kPatStride = 10;   // ints per table entry: len | dpos << 8, then kSlots offsets
+constexpr int kPatHash = 4096;   // slots of the setup-time pattern hash table (power of 2)
+constexpr uint8_t kPidGeneric = 255;
+struct PatSlot {
+  unsigned long long key;  // 0 = empty
+  int count, rep;          // rows with the pattern, one of them
+};
+
+// ---- per-row metadata: pid | i0 << 8 | i1 << 12, or kMetaGeneric -------------
+// (pid < kPatMax, so a pattern row never reads as kMetaGeneric)
+__device__ __forceinline__ int meta_pid(uint16_t m) { return m & 0xFF; }
 __device__ __forceinline__ int meta_i0(uint16_t m) { return (m >> 8) & 15; }
 __device__ __forceinline__ int meta_i1(uint16_t m) { return m >> 12; }
+__device__ __forceinline__ int pat_len(int hdr) { return hdr & 0xFF; }
+__device__ __forceinline__ int pat_dpos(int hdr) { return hdr >> 8; }
+
+// the pattern table into shared memory (all threads of the CTA, before the
+// __syncthreads of ring_init)
+__device__ __forceinline__ void load_patterns(int *s_pat, const int *pat, int npat) {
+  for (int i = threadIdx.x; i < npat * kPatStride; i += blockDim.x) s_pat[i] = __ldg(pat + i);
+}
 
 // ---------------------------------------------------------------------------
 // scalar steps of the recurrence (solver.py:128-177, policies.py:102-116)
@@ -196,7 +222,8 @@ struct TileDesc {
   int e0, e1;   // SELL entries [e0, e1) = [sp[s0], sp[s1]) (multiples of 32)
   int bf, nbk;  // blocks bf .. bf+nbk-1 overlap the tile
   int ie0, ie1; // in-block SELL entries [ib_sp[s0], ib_sp[s1])
-  int pad0, pad1;
+  int ngen;     // generic rows (kMetaGeneric) in the tile
+  int pad1;
 };
 
 struct TileGeom {
@@ -204,6 +231,8 @@ struct TileGeom {
   int cap_e;   // staged SELL entries per tile (max over tiles, capped)
   int max_sl;  // max slices per tile
   int ns;      // shared-memory stages (prefetch depth)
+  int cols;    // stages carry a column region (the plan has generic rows)
+  int npat;    // row patterns in the table
 };
 
 // Byte offsets of one shared-memory stage.
@@ -212,12 +241,12 @@ struct StageLayout {
 };
 __host__ __device__ inline uint32_t al16u(uint32_t b) { return (b + 15u) & ~15u; }
 // v*es: element sizes of up to three row-vector slices [lo, hi) (0: absent)
-__host__ __device__ inline StageLayout stage_layout(int cap_e, int es, int max_sl, bool meta, int v0es, int v1es,
-                                                    int v2es) {
+__host__ __device__ inline StageLayout stage_layout(int cap_e, int es, int max_sl, bool cols, bool meta, int v0es,
+                                                    int v1es, int v2es) {
   StageLayout L;
   uint32_t off = 0;
   L.col = off;
-  off += al16u(static_cast<uint32_t>(cap_e) * 4u);
+  off += cols ? al16u(static_cast<uint32_t>(cap_e) * 4u) : 0u;
   L.val = off;
   off += al16u(static_cast<uint32_t>(cap_e) * es);
   L.sp = off;
@@ -277,11 +306,12 @@ __device__ __forceinline__ void produce(Ring &R, int st, const TileDesc *td, int
     mbar_arrive(&R.full[st]);
     return;
   }
-  uint32_t bytes = static_cast<uint32_t>(nent) * (4u + sizeof(T)) + window_bytes(sp, d.s0, d.s1 + 1) +
+  const bool cols = g.cols && d.ngen > 0;  // pattern rows rebuild their columns
+  uint32_t bytes = static_cast<uint32_t>(nent) * ((cols ? 4u : 0u) + sizeof(T)) + window_bytes(sp, d.s0, d.s1 + 1) +
                    window_bytes(meta, d.lo, d.hi) + window_bytes(v0, d.lo, d.hi) + window_bytes(v1, d.lo, d.hi) +
                    window_bytes(v2, d.lo, d.hi);
   mbar_arrive_expect_tx(&R.full[st], bytes);
-  bulk_g2s(stage + L.col, scol + e0, static_cast<uint32_t>(nent) * 4u, &R.full[st]);
+  if (cols) bulk_g2s(stage + L.col, scol + e0, static_cast<uint32_t>(nent) * 4u, &R.full[st]);
   bulk_g2s(stage + L.val, sval + e0, static_cast<uint32_t>(nent) * sizeof(T), &R.full[st]);
   tma_window(stage + L.sp, sp, d.s0, d.s1 + 1, &R.full[st]);
   if (meta != nullptr) tma_window(stage + L.meta, meta, d.lo, d.hi, &R.full[st]);
@@ -339,12 +369,13 @@ __device__ __forceinline__ void ring_release(Ring &R, int st) {
 template <typename T>
 struct PassArgs {
   const int *sp;         // SELL slice_ptr
-  const int *scol;       // SELL columns (-1 = padding)
+  const int *scol;       // SELL columns (-1 = padding; generic rows only)
   const T *sval;         // SELL values in storage precision
   const int *ib_sp;      // in-block SELL (first pass): slice_ptr
-  const int *ib_col;     //   columns
+  const int *ib_col;     //   columns (generic rows only)
   const T *ib_val;       //   values
   const uint16_t *meta;  // per-row static structure (plan-bound)
+  const int *pat;        // row-pattern table (g.npat entries of kPatStride ints)
   const TileDesc *td;    // tile descriptors
   const int *boff;       // nb+1 block offsets (generic rows, large blocks)
   TileGeom g;
@@ -389,22 +420,18 @@ __device__ __forceinline__ void find_block_abs(const int *b, int nbk, int row, i
   bhi = b[L + 1];
 }
 
-// Generic row of a pass (rows whose structure does not fit the metadata):
-// scans its SELL entries with explicit block bounds.  Returns res; sets d.
+// Generic row of a pass (no row pattern): scans its SELL entries with
+// explicit block bounds.  Returns res; sets d.
 template <typename T, bool FIRST>
-__device__ __forceinline__ T generic_row_scan(const PassArgs<T> &a, const TileDesc &d, int row, int base, int width,
-                                              const int *col, const T *val, const T *zt, T rv, T &dd) {
-  const unsigned span = static_cast<unsigned>(d.hi - d.lo);
+__device__ __forceinline__ T generic_row_scan(const PassArgs<T> &a, int row, int base, int width, const int *col,
+                                              const T *val, T rv, T &dd) {
   T az = T(0);
   dd = T(0);
   for (int j = 0; j < width; j++) {
     const int cj = col[base + 32 * j];
     if (cj < 0) continue;
     const T vj = val[base + 32 * j];
-    if (!FIRST) {
-      const unsigned o = static_cast<unsigned>(cj - d.lo);
-      az = add_rn(az, mul_rn(vj, o < span ? zt[o] : __ldg(a.zin + cj)));
-    }
+    if (!FIRST) az = add_rn(az, mul_rn(vj, __ldg(a.zin + cj)));
     if (cj == row) dd = vj;
   }
   return FIRST ? rv : sub_rn(rv, az);
@@ -423,19 +450,21 @@ __device__ __forceinline__ T generic_row_sweep(const PassArgs<T> &a, const TileD
   return acc;
 }
 
-// One tile of a fused pass, consumer threads only.  Pointers are either the
-// shared stage or the global arrays offset to the tile (same indexing).
+// One tile of a fused (non-first-only) pass, consumer threads only.  col /
+// val / spp / mt are the shared stage or the global arrays offset to the
+// tile (same indexing); r64t / rTt the tile's residual slice.
 template <typename T, bool FIRST, bool LAST>
 __device__ __forceinline__ void bjac_tile_body(const PassArgs<T> &a, int tile, const TileDesc &d, const int *col,
                                                const T *val, const int *spp, const uint16_t *mt, const double *r64t,
-                                               const T *rTt, const T *zt, T *s_w, double *ws) {
+                                               const T *rTt, const int *s_pat, T *s_w, double *ws) {
   const int tid = threadIdx.x;
   const int lo = d.lo, hi = d.hi, row = lo + tid;
   const bool valid = row < hi;
-  const unsigned span = static_cast<unsigned>(hi - lo);
   T res = T(0), dd = T(1), w = T(0), zown = T(0);
-  uint16_t m = 0;
-  int base = 0, width = 0, i0 = 0, i1 = 0;
+  uint16_t m = kMetaGeneric;
+  int base = 0, width = 0;
+  const int *P = s_pat;
+  int i0 = 0, i1 = 0;  // in-block slots [i0, i1)
   if (valid) {
     const int si = (row >> 5) - d.s0;
     const int sb = spp[si];
@@ -443,33 +472,29 @@ __device__ __forceinline__ void bjac_tile_body(const PassArgs<T> &a, int tile, c
     base = sb - d.e0 + (row & 31);
     m = mt[tid];
     const T rv = r64t != nullptr ? narrow_checked(a, r64t[tid], row, FIRST) : rTt[tid];
-    if (!FIRST) zown = zt[tid];
+    if (!FIRST) zown = __ldg(a.zin + row);
     if (m != kMetaGeneric) {
+      P = s_pat + meta_pid(m) * kPatStride;
+      const int hdr = P[0], len = pat_len(hdr);
       i0 = meta_i0(m);
       i1 = meta_i1(m);
       T az = T(0);
-      if (!FIRST) {  // az = A z_in, all slots, ascending column
-        const int len = meta_len(m);
-        int c[kSlots];
+      if (!FIRST) {  // az = A z_in, all slots, stored (ascending column) order
         T v[kSlots], g[kSlots];
 #pragma unroll
         for (int u = 0; u < kSlots; u++) {
-          c[u] = u < len ? col[base + 32 * u] : lo;
-          v[u] = u < len ? val[base + 32 * u] : T(0);
-        }
-#pragma unroll
-        for (int u = 0; u < kSlots; u++) {
-          const unsigned o = static_cast<unsigned>(c[u] - lo);
-          g[u] = o < span ? zt[o] : __ldg(a.zin + c[u]);
+          const bool ok = u < len;
+          v[u] = ok ? val[base + 32 * u] : T(0);
+          g[u] = __ldg(a.zin + (ok ? row + P[1 + u] : row));
         }
 #pragma unroll
         for (int u = 0; u < kSlots; u++)
           if (u < len) az = add_rn(az, mul_rn(v[u], g[u]));
       }
-      dd = val[base + 32 * meta_dpos(m)];
+      dd = val[base + 32 * pat_dpos(hdr)];
       res = FIRST ? rv : sub_rn(rv, az);
     } else {
-      res = generic_row_scan<T, FIRST>(a, d, row, base, width, col, val, zt, rv, dd);
+      res = generic_row_scan<T, FIRST>(a, row, base, width, col, val, rv, dd);
     }
     w = div_rn(res, dd);
     s_w[tid] = w;
@@ -479,10 +504,7 @@ __device__ __forceinline__ void bjac_tile_body(const PassArgs<T> &a, int tile, c
     T acc = T(0);
     if (valid) {
       if (m != kMetaGeneric) {
-        for (int j = i0; j < i1; j++) {
-          const int cj = col[base + 32 * j];
-          acc = add_rn(acc, mul_rn(val[base + 32 * j], s_w[cj - lo]));
-        }
+        for (int j = i0; j < i1; j++) acc = add_rn(acc, mul_rn(val[base + 32 * j], s_w[tid + P[1 + j]]));
       } else {
         acc = generic_row_sweep(a, d, row, base, width, col, val, s_w);
       }
@@ -512,28 +534,32 @@ __device__ __forceinline__ void bjac_tile_body(const PassArgs<T> &a, int tile, c
 template <typename T>
 __device__ __forceinline__ void bjac_first_body(const PassArgs<T> &a, const TileDesc &d, const int *col,
                                                 const T *val, const int *spp, const uint16_t *mt,
-                                                const double *r64t, const T *rTt, T *s_w) {
+                                                const double *r64t, const T *rTt, const int *s_pat, T *s_w) {
   const int tid = threadIdx.x;
   const int lo = d.lo, hi = d.hi, row = lo + tid;
   const bool valid = row < hi;
   T res = T(0), dd = T(1), w = T(0);
+  uint16_t m = kMetaGeneric;
   int base = 0, nib = 0;
+  const int *P = s_pat;  // pattern row: offsets of its in-block slots
   if (valid) {
     const int si = (row >> 5) - d.s0;
     const int sb = spp[si];
     const int iwidth = (spp[si + 1] - sb) >> 5;
     base = sb - d.ie0 + (row & 31);
-    const uint16_t m = mt[tid];
+    m = mt[tid];
     res = r64t != nullptr ? narrow_checked(a, r64t[tid], row, true) : rTt[tid];
     if (m != kMetaGeneric) {
-      nib = meta_i1(m) - meta_i0(m);
-      dd = val[base + 32 * (meta_dpos(m) - meta_i0(m))];
+      const int i0 = meta_i0(m);
+      nib = meta_i1(m) - i0;
+      dd = val[base + 32 * (pat_dpos(s_pat[meta_pid(m) * kPatStride]) - i0)];
+      P = s_pat + meta_pid(m) * kPatStride + 1 + i0;
     } else {
       for (int j = 0; j < iwidth; j++) {
-        const int c = col[base + 32 * j];
-        if (c < 0) break;
+        const int cc = col[base + 32 * j];
+        if (cc < 0) break;
         nib = j + 1;
-        if (c == row) dd = val[base + 32 * j];
+        if (cc == row) dd = val[base + 32 * j];
       }
     }
     w = div_rn(res, dd);
@@ -542,9 +568,10 @@ __device__ __forceinline__ void bjac_first_body(const PassArgs<T> &a, const Tile
   for (int s = 1; s < a.t; s++) {
     named_sync(kBarConsumers, kConsumers);
     T acc = T(0);
-    for (int j = 0; j < nib; j++) {
-      const int c = col[base + 32 * j];
-      acc = add_rn(acc, mul_rn(val[base + 32 * j], s_w[c - lo]));
+    if (m != kMetaGeneric) {
+      for (int j = 0; j < nib; j++) acc = add_rn(acc, mul_rn(val[base + 32 * j], s_w[tid + P[j]]));
+    } else {
+      for (int j = 0; j < nib; j++) acc = add_rn(acc, mul_rn(val[base + 32 * j], s_w[col[base + 32 * j] - lo]));
     }
     named_sync(kBarConsumers, kConsumers);
     if (valid) {
@@ -560,8 +587,8 @@ __device__ __forceinline__ void bjac_first_body(const PassArgs<T> &a, const Tile
 
 template <typename T, bool FIRST, bool R64>
 __host__ __device__ inline StageLayout bjac_layout(const TileGeom &g) {
-  // v0: residual slice, v2: z_in slice (non-first passes)
-  return stage_layout(g.cap_e, sizeof(T), g.max_sl, true, R64 ? 8 : sizeof(T), 0, FIRST ? 0 : sizeof(T));
+  // v0: the residual slice
+  return stage_layout(g.cap_e, sizeof(T), g.max_sl, g.cols != 0, true, R64 ? 8 : sizeof(T), 0, 0);
 }
 
 // Persistent, warp-specialised fused pass.
@@ -572,9 +599,11 @@ __global__ void __launch_bounds__(kWsThreads) k_bjac_tile(const PassArgs<T> a) {
   __shared__ Ring R;
   __shared__ T s_w[kTileRows];
   __shared__ double ws[32];
+  __shared__ int s_pat[kPatMax * kPatStride];
   const int ns = a.g.ns;
   constexpr bool kIB = FIRST && !LAST;  // first pass alone: in-block entries only
   const StageLayout L = bjac_layout<T, FIRST, R64>(a.g);
+  load_patterns(s_pat, a.pat, a.g.npat);
   ring_init(R, ns);
   if (threadIdx.x >= kConsumers) {  // producer warp
     using RT = typename std::conditional<R64, double, T>::type;
@@ -582,11 +611,11 @@ __global__ void __launch_bounds__(kWsThreads) k_bjac_tile(const PassArgs<T> a) {
     if (threadIdx.x == kConsumers)
       producer_loop(R, a.g.ntiles, ns, [&](int st, int tile) {
         if (kIB)
-          produce<T, RT, uint8_t, T, true>(R, st, a.td, tile, a.g, L, smem + st * L.bytes, a.ib_sp, a.ib_col,
-                                           a.ib_val, a.meta, rsrc, nullptr, nullptr);
+          produce<T, RT, uint8_t, uint8_t, true>(R, st, a.td, tile, a.g, L, smem + st * L.bytes, a.ib_sp, a.ib_col,
+                                                 a.ib_val, a.meta, rsrc, nullptr, nullptr);
         else
-          produce<T, RT, uint8_t, T>(R, st, a.td, tile, a.g, L, smem + st * L.bytes, a.sp, a.scol, a.sval, a.meta,
-                                     rsrc, nullptr, FIRST ? nullptr : a.zin);
+          produce<T, RT, uint8_t, uint8_t>(R, st, a.td, tile, a.g, L, smem + st * L.bytes, a.sp, a.scol, a.sval,
+                                           a.meta, rsrc, nullptr, nullptr);
       });
   } else {
     RingCursor cur;
@@ -594,30 +623,33 @@ __global__ void __launch_bounds__(kWsThreads) k_bjac_tile(const PassArgs<T> a) {
       const int st = cur.st;
       mbar_wait(&R.full[st], cur.phase);
       const TileDesc d = R.desc[st];
+      const unsigned char *sb = smem + st * L.bytes;
+      const bool ok = R.ok[st] != 0;
+      const bool scols = ok && a.g.cols && d.ngen > 0;
       if (kIB) {
-        if (R.ok[st]) {
-          const unsigned char *sb = smem + st * L.bytes;
-          bjac_first_body<T>(a, d, reinterpret_cast<const int *>(sb + L.col), reinterpret_cast<const T *>(sb + L.val),
+        const int *col = scols ? reinterpret_cast<const int *>(sb + L.col) : a.ib_col + d.ie0;
+        if (ok) {
+          bjac_first_body<T>(a, d, col, reinterpret_cast<const T *>(sb + L.val),
                              staged(sb + L.sp, a.ib_sp, d.s0, d.s1 + 1), staged(sb + L.meta, a.meta, d.lo, d.hi),
                              R64 ? staged(sb + L.v0, a.r64, d.lo, d.hi) : nullptr,
-                             R64 ? nullptr : staged(sb + L.v0, a.rT, d.lo, d.hi), s_w);
+                             R64 ? nullptr : staged(sb + L.v0, a.rT, d.lo, d.hi), s_pat, s_w);
         } else {
-          bjac_first_body<T>(a, d, a.ib_col + d.ie0, a.ib_val + d.ie0, a.ib_sp + d.s0, a.meta + d.lo,
-                             R64 ? a.r64 + d.lo : nullptr, R64 ? nullptr : a.rT + d.lo, s_w);
+          bjac_first_body<T>(a, d, col, a.ib_val + d.ie0, a.ib_sp + d.s0, a.meta + d.lo,
+                             R64 ? a.r64 + d.lo : nullptr, R64 ? nullptr : a.rT + d.lo, s_pat, s_w);
         }
-      } else if (R.ok[st]) {
-        const unsigned char *sb = smem + st * L.bytes;
-        const double *r64t = R64 ? staged(sb + L.v0, a.r64, d.lo, d.hi) : nullptr;
-        const T *rTt = R64 ? nullptr : staged(sb + L.v0, a.rT, d.lo, d.hi);
-        const T *zt = FIRST ? nullptr : staged(sb + L.v2, a.zin, d.lo, d.hi);
-        bjac_tile_body<T, FIRST, LAST>(a, tile, d, reinterpret_cast<const int *>(sb + L.col),
-                                       reinterpret_cast<const T *>(sb + L.val),
-                                       staged(sb + L.sp, a.sp, d.s0, d.s1 + 1), staged(sb + L.meta, a.meta, d.lo, d.hi),
-                                       r64t, rTt, zt, s_w, ws);
       } else {
-        bjac_tile_body<T, FIRST, LAST>(a, tile, d, a.scol + d.e0, a.sval + d.e0, a.sp + d.s0, a.meta + d.lo,
-                                       R64 ? a.r64 + d.lo : nullptr, R64 ? nullptr : a.rT + d.lo,
-                                       FIRST ? nullptr : a.zin + d.lo, s_w, ws);
+        const int *col = scols ? reinterpret_cast<const int *>(sb + L.col) : a.scol + d.e0;
+        if (ok) {
+          bjac_tile_body<T, FIRST, LAST>(a, tile, d, col, reinterpret_cast<const T *>(sb + L.val),
+                                         staged(sb + L.sp, a.sp, d.s0, d.s1 + 1),
+                                         staged(sb + L.meta, a.meta, d.lo, d.hi),
+                                         R64 ? staged(sb + L.v0, a.r64, d.lo, d.hi) : nullptr,
+                                         R64 ? nullptr : staged(sb + L.v0, a.rT, d.lo, d.hi), s_pat, s_w, ws);
+        } else {
+          bjac_tile_body<T, FIRST, LAST>(a, tile, d, col, a.sval + d.e0, a.sp + d.s0, a.meta + d.lo,
+                                         R64 ? a.r64 + d.lo : nullptr, R64 ? nullptr : a.rT + d.lo, s_pat, s_w,
+                                         ws);
+        }
       }
       ring_release(R, st);
     }
@@ -725,13 +757,15 @@ __global__ void __launch_bounds__(kCtaThreads)
 }
 
 // ---------------------------------------------------------------------------
-// q = A p and the p.q partial (solver.py:154-159), fp64 SELL-32.  The tile's
-// own p slice is staged with the matrix; out-of-tile p_j come from L2.
+// q = A p and the p.q partial (solver.py:154-159), fp64 SELL-32.  Values,
+// slice pointers and row metadata are staged; p_j is gathered through L1.
 // ---------------------------------------------------------------------------
 struct SpmvArgs {
   const int *sp;
   const int *scol;
   const double *sval;
+  const uint16_t *meta;
+  const int *pat;
   const TileDesc *td;
   TileGeom g;
   const double *p;  // search direction (updated in place by k_pupdate)
@@ -741,45 +775,47 @@ struct SpmvArgs {
 };
 
 __device__ __forceinline__ void spmv_tile_body(const SpmvArgs &a, int tile, const TileDesc &d, const int *col,
-                                               const double *val, const int *spp, const double *p,
-                                               const double *pt, double *ws) {
+                                               const double *val, const int *spp, const uint16_t *mt,
+                                               const int *s_pat, double *ws) {
   const int tid = threadIdx.x;
   const int lo = d.lo, hi = d.hi, row = lo + tid;
-  const unsigned span = static_cast<unsigned>(hi - lo);
+  const double *p = a.p;
   double prod = 0.0;
   if (row < hi) {
     const int si = (row >> 5) - d.s0;
     const int sb = spp[si];
-    const int width = (spp[si + 1] - sb) >> 5;
     const int base = sb - d.e0 + (row & 31);
+    const uint16_t m = mt[tid];
     double acc = 0.0;
-    for (int j0 = 0; j0 < width; j0 += kSlots) {
-      int c[kSlots];
+    if (m != kMetaGeneric) {
+      const int *P = s_pat + meta_pid(m) * kPatStride;
+      const int len = pat_len(P[0]);
       double vv[kSlots], pv[kSlots];
 #pragma unroll
       for (int u = 0; u < kSlots; u++) {
-        const bool ok = j0 + u < width;
-        c[u] = ok ? col[base + 32 * (j0 + u)] : -1;
-        vv[u] = ok ? val[base + 32 * (j0 + u)] : 0.0;
-      }
-#pragma unroll
-      for (int u = 0; u < kSlots; u++) {
-        const unsigned o = static_cast<unsigned>(c[u] - lo);
-        pv[u] = c[u] < 0 ? 0.0 : (o < span ? pt[o] : __ldg(p + c[u]));
+        const bool ok = u < len;
+        vv[u] = ok ? val[base + 32 * u] : 0.0;
+        pv[u] = __ldg(p + (ok ? row + P[1 + u] : row));
       }
 #pragma unroll
       for (int u = 0; u < kSlots; u++)
-        if (c[u] >= 0) acc = __dadd_rn(acc, __dmul_rn(vv[u], pv[u]));
+        if (u < len) acc = __dadd_rn(acc, __dmul_rn(vv[u], pv[u]));
+    } else {
+      const int width = (spp[si + 1] - sb) >> 5;
+      for (int j = 0; j < width; j++) {
+        const int c = col[base + 32 * j];
+        if (c >= 0) acc = __dadd_rn(acc, __dmul_rn(val[base + 32 * j], __ldg(p + c)));
+      }
     }
     a.q[row] = acc;
-    prod = __dmul_rn(pt[tid], acc);
+    prod = __dmul_rn(__ldg(p + row), acc);
   }
   const double tot = block_tree_nb<kTileThreads>(prod, ws, kBarConsumers);
   if (tid == 0) a.part[tile] = tot;
 }
 
 __host__ __device__ inline StageLayout spmv_layout(const TileGeom &g) {
-  return stage_layout(g.cap_e, 8, g.max_sl, false, 8, 0, 0);
+  return stage_layout(g.cap_e, 8, g.max_sl, g.cols != 0, true, 0, 0, 0);
 }
 
 __global__ void __launch_bounds__(kWsThreads) k_spmv_pq(const SpmvArgs a) {
@@ -787,15 +823,16 @@ __global__ void __launch_bounds__(kWsThreads) k_spmv_pq(const SpmvArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ Ring R;
   __shared__ double ws[32];
+  __shared__ int s_pat[kPatMax * kPatStride];
   const int ns = a.g.ns;
-  const double *p = a.p;
   const StageLayout L = spmv_layout(a.g);
+  load_patterns(s_pat, a.pat, a.g.npat);
   ring_init(R, ns);
   if (threadIdx.x >= kConsumers) {
     if (threadIdx.x == kConsumers)
       producer_loop(R, a.g.ntiles, ns, [&](int st, int tile) {
-        produce<double, double, uint8_t, uint8_t>(R, st, a.td, tile, a.g, L, smem + st * L.bytes, a.sp, a.scol,
-                                                  a.sval, nullptr, p, nullptr, nullptr);
+        produce<double, uint8_t, uint8_t, uint8_t>(R, st, a.td, tile, a.g, L, smem + st * L.bytes, a.sp, a.scol,
+                                                   a.sval, a.meta, nullptr, nullptr, nullptr);
       });
   } else {
     RingCursor cur;
@@ -803,13 +840,13 @@ __global__ void __launch_bounds__(kWsThreads) k_spmv_pq(const SpmvArgs a) {
       const int st = cur.st;
       mbar_wait(&R.full[st], cur.phase);
       const TileDesc d = R.desc[st];
+      const unsigned char *sb = smem + st * L.bytes;
       if (R.ok[st]) {
-        const unsigned char *sb = smem + st * L.bytes;
-        spmv_tile_body(a, tile, d, reinterpret_cast<const int *>(sb + L.col),
-                       reinterpret_cast<const double *>(sb + L.val), staged(sb + L.sp, a.sp, d.s0, d.s1 + 1), p,
-                       staged(sb + L.v0, p, d.lo, d.hi), ws);
+        const int *col = (a.g.cols && d.ngen > 0) ? reinterpret_cast<const int *>(sb + L.col) : a.scol + d.e0;
+        spmv_tile_body(a, tile, d, col, reinterpret_cast<const double *>(sb + L.val),
+                       staged(sb + L.sp, a.sp, d.s0, d.s1 + 1), staged(sb + L.meta, a.meta, d.lo, d.hi), s_pat, ws);
       } else {
-        spmv_tile_body(a, tile, d, a.scol + d.e0, a.sval + d.e0, a.sp + d.s0, p, p + d.lo, ws);
+        spmv_tile_body(a, tile, d, a.scol + d.e0, a.sval + d.e0, a.sp + d.s0, a.meta + d.lo, s_pat, ws);
       }
       ring_release(R, st);
     }
@@ -939,38 +976,141 @@ __global__ void k_sell_pack(long long n, const int *rp, const int *sp, const E *
   }
 }
 
-// Per-row static structure against a block partition (plan-bound):
-// len | dpos << 4 | i0 << 8 | i1 << 12, or kMetaGeneric when a field does
-// not fit in 4 bits.  Needs the SELL columns of the matrix.
-__global__ void k_build_meta(long long n, const int *sp, const int *scol, const int *boff, int nb, uint16_t *meta) {
-  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x) {
-    const int row = static_cast<int>(r);
-    const int s = row >> 5, sb = sp[s], width = (sp[s + 1] - sb) >> 5, base = sb + (row & 31);
-    int L = 0, H = nb;
-    while (H - L > 1) {
-      const int M = (L + H) >> 1;
-      if (boff[M] <= row) L = M; else H = M;
-    }
-    const int blo = boff[L], bhi = boff[L + 1];
-    // in-block entries form one contiguous slot range (columns ascend in
-    // global order; multi-GPU ghost renumbering keeps the stored order and
-    // maps only out-of-slab columns, which are never in-block)
-    int len = 0, dpos = -1, i0 = -1, i1 = -1, nin = 0;
-    for (int j = 0; j < width; j++) {
-      const int c = scol[base + 32 * j];
-      if (c < 0) break;
-      len = j + 1;
-      if (c == row) dpos = j;
-      if (c >= blo && c < bhi) {
-        if (i0 < 0) i0 = j;
-        i1 = j + 1;
-        nin++;
+// ---- row patterns (setup, per SELL structure) --------------------------------
+// The row's stored columns as offsets from the row, in stored order, and a
+// 64-bit key of (length, offsets); key 0 = no pattern (longer than kSlots).
+__device__ __forceinline__ unsigned long long row_pattern(const int *sp, const int *scol, int row, int (&off)[kSlots],
+                                                          int &len) {
+  const int s = row >> 5, sb = sp[s], width = (sp[s + 1] - sb) >> 5, base = sb + (row & 31);
+  len = 0;
+  for (int j = 0; j < width; j++) {
+    const int c = scol[base + 32 * j];
+    if (c < 0) break;
+    if (j < kSlots) off[j] = c - row;
+    len = j + 1;
+  }
+  if (len > kSlots) return 0ull;
+  unsigned long long h = 0x9E3779B97F4A7C15ull ^ static_cast<unsigned long long>(len);
+  for (int j = 0; j < len; j++) {
+    h ^= static_cast<unsigned int>(off[j]);
+    h *= 0x100000001B3ull;
+    h ^= h >> 29;
+  }
+  return h | 1ull;
+}
+
+// count the rows of every pattern into an open-addressing table (one atomic
+// per distinct pattern per warp)
+__global__ void k_pat_insert(long long n, const int *sp, const int *scol, PatSlot *tab) {
+  const long long r = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  int off[kSlots], len = 0;
+  const unsigned long long key = r < n ? row_pattern(sp, scol, static_cast<int>(r), off, len) : 0ull;
+  const unsigned peers = __match_any_sync(0xffffffffu, key);
+  if (key == 0ull || (threadIdx.x & 31) != __ffs(peers) - 1) return;
+  unsigned s = static_cast<unsigned>(key) & (kPatHash - 1);
+  for (int probe = 0; probe < kPatHash; probe++, s = (s + 1) & (kPatHash - 1)) {
+    unsigned long long k = *reinterpret_cast<volatile unsigned long long *>(&tab[s].key);
+    if (k == 0ull) {
+      k = atomicCAS(&tab[s].key, 0ull, key);
+      if (k == 0ull) {
+        tab[s].rep = static_cast<int>(r);
+        k = key;
       }
     }
-    if (i0 < 0) i0 = i1 = 0;
-    const bool fits = len <= kSlots && dpos >= 0 && i1 <= 15 && nin == i1 - i0;
-    meta[row] = fits ? static_cast<uint16_t>(len | (dpos << 4) | (i0 << 8) | (i1 << 12)) : kMetaGeneric;
+    if (k == key) {
+      atomicAdd(&tab[s].count, __popc(peers));
+      return;
+    }
   }
+}
+
+// table entries of the chosen patterns from one representative row each
+__global__ void k_pat_fetch(const int *reps, int npat, const int *sp, const int *scol, int *pat) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= npat) return;
+  const int row = reps[i];
+  int off[kSlots], len = 0;
+  row_pattern(sp, scol, row, off, len);
+  int dpos = 255;
+  for (int j = 0; j < len; j++)
+    if (off[j] == 0) dpos = j;
+  pat[i * kPatStride] = len | (dpos << 8);
+  for (int j = 0; j < kSlots; j++) pat[i * kPatStride + 1 + j] = j < len ? off[j] : 0;
+}
+
+// each row's pattern id (verified entry by entry) or kPidGeneric
+__global__ void k_pat_assign(long long n, const int *sp, const int *scol, const PatSlot *tab, const int *slot_pid,
+                             const int *pat, uint8_t *pid) {
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x) {
+    int off[kSlots], len = 0;
+    const unsigned long long key = row_pattern(sp, scol, static_cast<int>(r), off, len);
+    uint8_t out = kPidGeneric;
+    if (key != 0ull) {
+      unsigned s = static_cast<unsigned>(key) & (kPatHash - 1);
+      int cand = -1;
+      for (int probe = 0; probe < kPatHash; probe++, s = (s + 1) & (kPatHash - 1)) {
+        const unsigned long long k = tab[s].key;
+        if (k == key) {
+          cand = slot_pid[s];
+          break;
+        }
+        if (k == 0ull) break;
+      }
+      if (cand >= 0) {
+        const int *P = pat + cand * kPatStride;
+        bool same = pat_len(P[0]) == len;
+        for (int j = 0; j < len; j++) same = same && P[1 + j] == off[j];
+        if (same) out = static_cast<uint8_t>(cand);
+      }
+    }
+    pid[r] = out;
+  }
+}
+
+// Per-row static structure against a block partition (plan-bound): pattern
+// id and in-block slot range, or kMetaGeneric (no pattern, no stored
+// diagonal, or in-block entries not one contiguous slot range).
+__global__ void k_build_meta(long long n, const uint8_t *pid, const int *pat, const int *boff, int nb,
+                             uint16_t *meta) {
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x) {
+    const int row = static_cast<int>(r);
+    uint16_t m = kMetaGeneric;
+    const int id = pid[row];
+    if (id != kPidGeneric) {
+      const int *P = pat + id * kPatStride;
+      const int len = pat_len(P[0]), dpos = pat_dpos(P[0]);
+      int L = 0, H = nb;
+      while (H - L > 1) {
+        const int M = (L + H) >> 1;
+        if (boff[M] <= row) L = M; else H = M;
+      }
+      const int blo = boff[L], bhi = boff[L + 1];
+      // in-block entries form one contiguous slot range (columns ascend in
+      // global order; multi-GPU ghost renumbering keeps the stored order and
+      // maps only out-of-slab columns, which are never in-block)
+      int i0 = -1, i1 = -1, nin = 0;
+      for (int j = 0; j < len; j++) {
+        const int c = row + P[1 + j];
+        if (c >= blo && c < bhi) {
+          if (i0 < 0) i0 = j;
+          i1 = j + 1;
+          nin++;
+        }
+      }
+      if (i0 < 0) i0 = i1 = 0;
+      if (dpos < len && nin == i1 - i0 && i1 <= 15)
+        m = static_cast<uint16_t>(id | (i0 << 8) | (i1 << 12));
+    }
+    meta[row] = m;
+  }
+}
+
+// generic rows per tile (TileDesc::ngen)
+__global__ void k_tile_generic(TileDesc *td, const uint16_t *meta) {
+  const TileDesc d = td[blockIdx.x];
+  const int row = d.lo + threadIdx.x;
+  const int gen = __syncthreads_count(row < d.hi && meta[row] == kMetaGeneric);
+  if (threadIdx.x == 0) td[blockIdx.x].ngen = gen;
 }
 
 // In-block entries of each row (columns inside the row's block): count, and

@@ -322,3 +322,37 @@ def test_slab_solver_single_rank_matches_single_gpu(cuda, oracle, pol):
     np.testing.assert_array_equal(drep.x, orc["x"])
     np.testing.assert_array_equal([r.implicit_relres for r in drep.trace], orc["relres"])
     assert drep.final_true_relres == orc["final_true_relres"]
+
+
+def test_row_patterns_and_generic_rows_bitwise(cuda, oracle):
+    """Rows with a row pattern rebuild their columns from the pattern table;
+    rows without one (too many distinct patterns, long rows) read SELL
+    columns, mixed within the same tiles.  Both must be bit-identical."""
+    from paper_2407_15973_b200 import Precision, problems
+    from paper_2407_15973_b200.bjac import BlockPartition, setup
+    cs = problems.make_config("c2", 16)
+    P = setup(cs.A, k=2, t=2, partition=BlockPartition.fixed_size(cs.A.n, 64))
+    info = P.plan.layout_info()
+    assert info == {"patterns": 27, "generic_rows": 0}       # 7-point stencil, all boundary cases
+    rng = np.random.default_rng(91)
+    A = random_spd_csr(3000, 0.0012, rng)                    # thousands of distinct patterns
+    r = rng.standard_normal(A.n)
+    for offs in (np.append(np.arange(0, A.n, 64), A.n), np.array([0, 7, 300, 301, 1500, 3000])):
+        part = BlockPartition(offs)
+        d64, d32, v32, inb = oracle.setup_arrays(A.row_ptr, A.col_idx, A.values, offs)
+        for k, t in ((1, 1), (2, 2), (3, 3)):
+            P64 = setup(A, k=k, t=t, partition=part)
+            info = P64.plan.layout_info()
+            assert info["patterns"] == 128
+            assert P64.plan.large or 0 < info["generic_rows"] < A.n   # large blocks: no tiles
+            np.testing.assert_array_equal(
+                P64.apply(r), oracle.bjac_apply(A.row_ptr, A.col_idx, A.values, inb, d64, k, t, r))
+            z32 = setup(A, k=k, t=t, precision=Precision.F32, partition=part).apply(r.astype(np.float32))
+            np.testing.assert_array_equal(
+                z32, oracle.bjac_apply(A.row_ptr, A.col_idx, v32, inb, d32, k, t, r.astype(np.float32)))
+    b = rng.standard_normal(A.n)
+    offs = np.append(np.arange(0, A.n, 64), A.n)
+    for pol in ("fixed-low", "uniform"):
+        rep, orc = _solve_both(A, b, offs, pol, 2, 2, 1e-10, oracle)
+        assert rep.iterations == orc["iterations"]
+        np.testing.assert_array_equal(rep.x, orc["x"])
