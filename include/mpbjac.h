@@ -260,8 +260,9 @@ int mpb_pcg_solve(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A,
  * h_ms[8] receives the mean ms per launch of: 0 first BJAC pass,
  * 1 middle passes (all of them, 0 when k < 3), 2 last BJAC pass,
  * 3 SpMV q = A p with the fused p.q step, 4 x/r update (fused relres
- * step), 5 unused (scalar steps are fused), 6 whole iteration (sum),
- * 7 p-update p = z + beta p. */
+ * step), 5 x/r update fused with the next iteration's first pass (what the
+ * solve runs when k >= 2 on one GPU; 0 otherwise), 6 whole iteration (sum of
+ * the kernels the solve runs), 7 p-update p = z + beta p. */
 int mpb_profile_iteration(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A,
                           const mpb_solve_options *opt, const double *b, double *x,
                           void *workspace, int64_t workspace_bytes, int branch,

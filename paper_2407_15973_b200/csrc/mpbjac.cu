@@ -7,8 +7,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <utility>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -40,7 +42,7 @@ inline int status_of(cudaError_t e) { return e == cudaSuccess ? MPB_OK : static_
 
 struct GraphKey {
   const void *plan, *rp, *sell, *v64, *v32, *b, *x, *trr, *trt, *trb, *trw, *ws, *comm;
-  int kind, k, t, iters;
+  int kind, k, t, iters, loop;
   long long stride, n;
   bool operator==(const GraphKey &o) const { return std::memcmp(this, &o, sizeof(GraphKey)) == 0; }
 };
@@ -62,6 +64,7 @@ struct mpb_plan {
   int max_tile_ib;
   const int *d_pat;         // the bound SELL's row-pattern table (not owned)
   int npat;
+  int ks;                   // compile-time slot count of the hot kernels (7 or 9)
   int64_t ngeneric;         // rows without a usable pattern (kMetaGeneric)
 };
 
@@ -77,6 +80,7 @@ struct mpb_sell {
   uint8_t *d_pid;           // per-row pattern id or kPidGeneric
   int *d_pat;               // npat table entries of kPatStride ints
   int npat;
+  int max_len;              // longest row pattern (slots)
 };
 
 struct mpb_handle {
@@ -87,8 +91,10 @@ struct mpb_handle {
   void *scratch;
   size_t scratch_bytes;
   SolverState *h_state;  // pinned
+  unsigned int *d_ctr;   // tile-claim counters of the persistent kernels (reset by each launch)
   int64_t launches;
   cudaGraphExec_t gexec;
+  cudaGraphConditionalHandle cond;  // while node of gexec (device-side solve loop)
   GraphKey gkey;
   int64_t graph_kernels;
   bool have_graph;
@@ -161,8 +167,9 @@ int num_sms() {
   return g_num_sms;
 }
 
-// Stage count for a persistent tile kernel: 3 stages (prefetch depth 2)
-// when that still leaves >= 2 co-resident CTAs per SM, else 2.
+// Stage count for a persistent tile kernel: the deepest ring (<= kMaxStages)
+// that keeps the co-resident CTA count registers and threads allow
+// (MPB_STAGES=n forces n; MPB_VERBOSE=1 reports the choice).
 template <typename K>
 int pick_stages(K kernel, uint32_t stage_bytes) {
   auto per_sm = [&](int ns) {
@@ -173,7 +180,14 @@ int pick_stages(K kernel, uint32_t stage_bytes) {
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, kWsThreads, dyn) != cudaSuccess) n = 0;
     return n;
   };
-  return per_sm(3) >= 2 ? 3 : 2;
+  static const int forced = std::getenv("MPB_STAGES") ? std::atoi(std::getenv("MPB_STAGES")) : 0;
+  const int base = per_sm(2);
+  int ns = 2;
+  const int cap = forced >= 2 ? std::min(forced, kMaxStages) : 3;
+  while (ns < cap && per_sm(ns + 1) >= (forced ? 1 : base)) ns++;
+  static const bool verbose = std::getenv("MPB_VERBOSE") != nullptr;
+  if (verbose) std::fprintf(stderr, "[mpb] stage %u B: %d stages, %d CTAs/SM\n", stage_bytes, ns, per_sm(ns));
+  return ns;
 }
 
 // Persistent grid: as many CTAs as are co-resident at this shared-memory
@@ -189,6 +203,33 @@ int persistent_grid(K kernel, uint32_t dyn_smem, int64_t ntiles, int threads = k
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ntiles, int64_t(per_sm) * num_sms())));
 }
 
+// Kernel launch, optionally with programmatic stream serialization (PDL):
+// the kernel may then start while its predecessor drains, and waits in
+// pdl_wait() for the predecessor's results.  Used for the hot kernels of
+// the captured single-GPU iteration (MPB_NO_PDL=1 turns it off).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(bool pdl, void (*kernel)(KArgs...), unsigned grid, unsigned block, size_t smem,
+                     cudaStream_t s, Args &&...args) {
+  static const bool off = std::getenv("MPB_NO_PDL") != nullptr;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = (pdl && !off) ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
+// MPB_DIRECT=1: one CTA per tile, no TMA ring (experiment)
+inline bool direct_kernels() {
+  static const bool on = std::getenv("MPB_DIRECT") != nullptr;
+  return on;
+}
+
 // Buffers one preconditioner application needs besides r and z.
 template <typename T>
 struct ApplyBufs {
@@ -196,7 +237,7 @@ struct ApplyBufs {
   T *res, *dg, *wA, *wB;  // large-block path (plan->large)
 };
 
-template <typename T, bool F, bool L, bool R64>
+template <typename T, bool F, bool L, bool R64, int KS>
 int launch_tile_kernel(mpb_handle *h, cudaStream_t s, const mpb_plan *p, PassArgs<T> a) {
   if (F && !L) {  // first pass streams the in-block layout
     if (a.ib_val == nullptr) return MPB_ERR_LAYOUT;
@@ -204,11 +245,17 @@ int launch_tile_kernel(mpb_handle *h, cudaStream_t s, const mpb_plan *p, PassArg
     a.ib_col = p->d_ib_col;
     a.g.cap_e = std::min(p->max_tile_ib, kStageCap);
   }
+  if (direct_kernels()) {
+    MPB_CUDA(launch_k(a.pdl != 0, k_bjac_direct<T, F, L, R64, KS>, static_cast<unsigned>(p->ntiles), kTileRows, 0,
+                      s, a));
+    MPB_LAUNCHED(h);
+    return MPB_OK;
+  }
   const StageLayout Ls = bjac_layout<T, F, R64>(a.g);
-  a.g.ns = pick_stages(k_bjac_tile<T, F, L, R64>, Ls.bytes);
+  a.g.ns = pick_stages(k_bjac_tile<T, F, L, R64, KS>, Ls.bytes);
   const uint32_t dyn = a.g.ns * Ls.bytes;
-  const int grid = persistent_grid(k_bjac_tile<T, F, L, R64>, dyn, p->ntiles, kWsThreads);
-  k_bjac_tile<T, F, L, R64><<<grid, kWsThreads, dyn, s>>>(a);
+  const int grid = persistent_grid(k_bjac_tile<T, F, L, R64, KS>, dyn, p->ntiles, kWsThreads);
+  MPB_CUDA(launch_k(a.pdl != 0, k_bjac_tile<T, F, L, R64, KS>, grid, kWsThreads, dyn, s, a));
   MPB_LAUNCHED(h);
   return MPB_OK;
 }
@@ -217,8 +264,12 @@ template <typename T, bool F, bool L>
 int launch_pass(mpb_handle *h, cudaStream_t s, const mpb_plan *p, PassArgs<T> a, const ApplyBufs<T> &bufs) {
   const int nt = static_cast<int>(p->ntiles);
   if (!p->large) {
-    if (a.r64 != nullptr) return launch_tile_kernel<T, F, L, true>(h, s, p, a);
-    return launch_tile_kernel<T, F, L, false>(h, s, p, a);
+    if (p->ks == 7) {
+      if (a.r64 != nullptr) return launch_tile_kernel<T, F, L, true, 7>(h, s, p, a);
+      return launch_tile_kernel<T, F, L, false, 7>(h, s, p, a);
+    }
+    if (a.r64 != nullptr) return launch_tile_kernel<T, F, L, true, kSlots>(h, s, p, a);
+    return launch_tile_kernel<T, F, L, false, kSlots>(h, s, p, a);
   }
   a.resbuf = bufs.res;
   a.dbuf = bufs.dg;
@@ -302,7 +353,8 @@ template <typename T>
 int launch_apply(mpb_handle *h, cudaStream_t s, const mpb_plan *p, const mpb_csr *A, int k, int t,
                  const double *r64, const T *rT, T *zout, double *zout64, double *part,
                  unsigned long long *ovf_count, long long *ovf_first, SolverState *st, int want_branch,
-                 const ApplyBufs<T> &bufs, const DistCtx *dc = nullptr) {
+                 const ApplyBufs<T> &bufs, const DistCtx *dc = nullptr, int from_pass = 0, int to_pass = 1 << 30,
+                 int z1_gate = 0) {
   PassArgs<T> a{};
   a.sp = A->sell->d_sp;
   a.scol = A->sell->d_col;
@@ -311,6 +363,7 @@ int launch_apply(mpb_handle *h, cudaStream_t s, const mpb_plan *p, const mpb_csr
   a.meta = p->d_meta;
   a.pat = p->d_pat;
   a.td = p->d_td;
+  a.ctr = h->d_ctr + 0;
   a.boff = p->d_boff;
   a.g = geom_for<T>(p);
   a.t = t;
@@ -320,7 +373,9 @@ int launch_apply(mpb_handle *h, cudaStream_t s, const mpb_plan *p, const mpb_csr
   a.ovf_first = ovf_first;
   a.st = st;
   a.want_branch = want_branch;
-  for (int pass = 0; pass < k; pass++) {
+  a.pdl = (st != nullptr && dc == nullptr) ? 1 : 0;  // captured single-GPU iteration
+  a.gate = z1_gate;
+  for (int pass = from_pass; pass < std::min(k, to_pass); pass++) {
     const bool first = pass == 0, last = pass == k - 1;
     a.zin = first ? nullptr : ((pass - 1) & 1 ? bufs.zB : bufs.zA);
     a.zout = last ? zout : (pass & 1 ? bufs.zB : bufs.zA);
@@ -337,6 +392,49 @@ int launch_apply(mpb_handle *h, cudaStream_t s, const mpb_plan *p, const mpb_csr
       if (rc) return rc;
     }
   }
+  return MPB_OK;
+}
+
+// The fused x/r update + next first pass (k_update_first) of one branch.
+template <typename T>
+int launch_update_first(mpb_handle *h, cudaStream_t s, const mpb_plan *p, const mpb_csr *A, int t, T *z1,
+                        double *x, const double *pv, const double *q, double *r, double *part,
+                        unsigned long long *ovf_count, long long *ovf_first, SolverState *st, int want_branch) {
+  PassArgs<T> a{};
+  a.sp = A->sell->d_sp;
+  a.scol = A->sell->d_col;
+  a.sval = sell_vals<T>(A);
+  a.ib_val = ib_vals<T>(A);
+  a.ib_sp = p->d_ib_sp;
+  a.ib_col = p->d_ib_col;
+  if (a.ib_val == nullptr) return MPB_ERR_LAYOUT;
+  a.meta = p->d_meta;
+  a.pat = p->d_pat;
+  a.td = p->d_td;
+  a.ctr = h->d_ctr + 1;
+  a.boff = p->d_boff;
+  a.g = geom_for<T>(p);
+  a.g.cap_e = std::min(p->max_tile_ib, kStageCap);
+  a.t = t;
+  a.zout = z1;
+  a.part = part;
+  a.ovf_count = ovf_count;
+  a.ovf_first = ovf_first;
+  a.st = st;
+  a.want_branch = want_branch;
+  a.gate = 2;
+  if (direct_kernels()) {
+    MPB_CUDA(launch_k(true, k_update_first_direct<T>, static_cast<unsigned>(p->ntiles), kTileRows, 0, s, a, x, pv,
+                      q, r));
+    MPB_LAUNCHED(h);
+    return MPB_OK;
+  }
+  const StageLayout L = update_first_layout<T>(a.g);
+  a.g.ns = pick_stages(k_update_first<T>, L.bytes);
+  const uint32_t dyn = a.g.ns * L.bytes;
+  const int grid = persistent_grid(k_update_first<T>, dyn, p->ntiles, kWsThreads);
+  MPB_CUDA(launch_k(true, k_update_first<T>, grid, kWsThreads, dyn, s, a, x, pv, q, r));
+  MPB_LAUNCHED(h);
   return MPB_OK;
 }
 
@@ -475,6 +573,8 @@ int mpb_create(int device, void *stream, mpb_handle **out) {
   if (e == cudaSuccess) e = cudaEventCreate(&h->ev_t0);
   if (e == cudaSuccess) e = cudaEventCreate(&h->ev_t1);
   if (e == cudaSuccess) e = cudaMallocHost(&h->h_state, sizeof(SolverState));
+  if (e == cudaSuccess) e = cudaMalloc(&h->d_ctr, 16 * sizeof(unsigned int));
+  if (e == cudaSuccess) e = cudaMemset(h->d_ctr, 0, 16 * sizeof(unsigned int));
   if (e != cudaSuccess) {
     delete h;
     return status_of(e);
@@ -490,6 +590,7 @@ int mpb_destroy(mpb_handle *h) {
   if (h->have_graph) cudaGraphExecDestroy(h->gexec);
   if (h->scratch) cudaFree(h->scratch);
   cudaFreeHost(h->h_state);
+  cudaFree(h->d_ctr);
   cudaEventDestroy(h->ev_in);
   cudaEventDestroy(h->ev_out);
   cudaEventDestroy(h->ev_t0);
@@ -618,6 +719,7 @@ int mpb_plan_bind_sell(mpb_handle *h, mpb_plan *p, const mpb_sell *sell) {
   MPB_LAUNCHED(h);
   p->d_pat = sell->d_pat;
   p->npat = sell->npat;
+  p->ks = sell->max_len <= 7 ? 7 : kSlots;
   if (!p->large) {
     k_tile_generic<<<static_cast<unsigned>(p->ntiles), kTileRows, 0, h->user>>>(p->d_td, p->d_meta);
     MPB_LAUNCHED(h);
@@ -906,6 +1008,14 @@ static cudaError_t build_patterns(mpb_handle *h, mpb_sell *S) {
       h->launches++;
       e = cudaGetLastError();
     }
+    S->max_len = 0;
+    if (e == cudaSuccess && S->npat > 0) {
+      std::vector<int> pat(static_cast<size_t>(S->npat) * kPatStride);
+      e = cudaMemcpyAsync(pat.data(), S->d_pat, sizeof(int) * pat.size(), cudaMemcpyDeviceToHost, h->user);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(h->user);
+      for (int i = 0; i < S->npat && e == cudaSuccess; i++)
+        S->max_len = std::max(S->max_len, pat[static_cast<size_t>(i) * kPatStride] & 0xFF);
+    }
     if (e == cudaSuccess) {
       k_pat_assign<<<elt_blocks(n), kEltThreads, 0, h->user>>>(n, S->d_sp, S->d_col, d_tab, d_aux, S->d_pat,
                                                               S->d_pid);
@@ -1100,9 +1210,11 @@ int64_t mpb_solve_workspace_bytes(const mpb_plan *plan, int64_t n) {
   return static_cast<int64_t>(carve(plan, n, nullptr).bytes);
 }
 
+static void (*spmv_kernel(const mpb_plan *p))(SpmvArgs) { return p->ks == 7 ? k_spmv_pq<7> : k_spmv_pq<kSlots>; }
+
 static TileGeom spmv_geom(const mpb_plan *p) {
   TileGeom g = geom_for<double>(p);
-  g.ns = pick_stages(k_spmv_pq, spmv_layout(g).bytes);
+  g.ns = pick_stages(spmv_kernel(p), spmv_layout(g).bytes);
   return g;
 }
 
@@ -1111,7 +1223,7 @@ static uint32_t spmv_dyn_smem(const mpb_plan *p) {
   return g.ns * spmv_layout(g).bytes;
 }
 
-static SpmvArgs spmv_args(const mpb_plan *p, const mpb_csr *A, const SolveWs &w) {
+static SpmvArgs spmv_args(const mpb_handle *h, const mpb_plan *p, const mpb_csr *A, const SolveWs &w) {
   SpmvArgs sa{};
   sa.sp = A->sell->d_sp;
   sa.scol = A->sell->d_col;
@@ -1119,6 +1231,7 @@ static SpmvArgs spmv_args(const mpb_plan *p, const mpb_csr *A, const SolveWs &w)
   sa.meta = p->d_meta;
   sa.pat = p->d_pat;
   sa.td = p->d_td;
+  sa.ctr = h->d_ctr + 2;
   sa.g = spmv_geom(p);
   sa.p = w.p;
   sa.q = w.q;
@@ -1132,38 +1245,88 @@ static SpmvArgs spmv_args(const mpb_plan *p, const mpb_csr *A, const SolveWs &w)
 // p-update; SpMV with the pq step; x/r update with the relres / branch /
 // convergence step; optional strided true residual.  Multi-GPU: halo
 // exchanges before every gathering kernel, all-reduced scalar steps.
-static int enqueue_iteration(mpb_handle *h, cudaStream_t s, const mpb_plan *p, const mpb_csr *A,
-                             const mpb_solve_options *o, const SolveWs &w, const double *b, double *x,
-                             const DistCtx *dc) {
+// Fused mode (single GPU, k >= 2, tile plan): the x/r update of iteration i
+// and the first BJAC pass of iteration i+1 are one kernel (k_update_first).
+static bool fused_mode(const mpb_plan *p, const mpb_solve_options *o, const DistCtx *dc) {
+  static const bool off = std::getenv("MPB_NO_FUSE") != nullptr;
+  return !off && o->k >= 2 && !p->large && dc == nullptr;
+}
+
+// Standalone first passes of the policy's branches (gated on st->branch and,
+// z1_gate, on the fused update not having produced z1 already).
+static int enqueue_first_passes(mpb_handle *h, cudaStream_t s, const mpb_plan *p, const mpb_csr *A,
+                                const mpb_solve_options *o, const SolveWs &w) {
   const bool high = o->kind != MPB_FIXED_LOW, low = o->kind != MPB_UNIFORM;
-  const unsigned nt = static_cast<unsigned>(p->ntiles);
   int rc;
   if (high) {
     ApplyBufs<double> bb{w.zA64, w.zB64, w.res64, w.dg64, w.wA64, w.wB64};
     rc = launch_apply<double>(h, s, p, A, o->k, o->t, w.r, nullptr, w.z64, nullptr, w.part, nullptr, nullptr, w.st,
-                              0, bb, dc);
+                              0, bb, nullptr, 0, 1, 1);
     if (rc) return rc;
   }
   if (low) {
     ApplyBufs<float> bb{w.zA32, w.zB32, w.res32, w.dg32, w.wA32, w.wB32};
     rc = launch_apply<float>(h, s, p, A, o->k, o->t, w.r, nullptr, w.z32, nullptr, w.part, &w.st->ovf_count,
-                             &w.st->ovf_first, w.st, 1, bb, dc);
+                             &w.st->ovf_first, w.st, 1, bb, nullptr, 0, 1, 1);
+    if (rc) return rc;
+  }
+  return MPB_OK;
+}
+
+static int enqueue_iteration(mpb_handle *h, cudaStream_t s, const mpb_plan *p, const mpb_csr *A,
+                             const mpb_solve_options *o, const SolveWs &w, const double *b, double *x,
+                             const DistCtx *dc) {
+  const bool high = o->kind != MPB_FIXED_LOW, low = o->kind != MPB_UNIFORM;
+  const unsigned nt = static_cast<unsigned>(p->ntiles);
+  const bool fused = fused_mode(p, o, dc);
+  int rc;
+  // adaptive policies: the branch may have changed, invalidating the fused z1
+  if (fused && high && low && (rc = enqueue_first_passes(h, s, p, A, o, w))) return rc;
+  const int from = fused ? 1 : 0;
+  if (high) {
+    ApplyBufs<double> bb{w.zA64, w.zB64, w.res64, w.dg64, w.wA64, w.wB64};
+    rc = launch_apply<double>(h, s, p, A, o->k, o->t, w.r, nullptr, w.z64, nullptr, w.part, nullptr, nullptr, w.st,
+                              0, bb, dc, from);
+    if (rc) return rc;
+  }
+  if (low) {
+    ApplyBufs<float> bb{w.zA32, w.zB32, w.res32, w.dg32, w.wA32, w.wB32};
+    rc = launch_apply<float>(h, s, p, A, o->k, o->t, w.r, nullptr, w.z32, nullptr, w.part, &w.st->ovf_count,
+                             &w.st->ovf_first, w.st, 1, bb, dc, from);
     if (rc) return rc;
   }
   if ((rc = dist_step(h, dc, w.st, kStepRho, 2, s))) return rc;
-  k_pupdate<<<persistent_grid(k_pupdate, 0, p->ntiles), kCtaThreads, 0, s>>>(p->d_td, static_cast<int>(nt), w.z32,
-                                                                              w.z64, w.p, w.st);
+  const bool pdl = dc == nullptr;
+  MPB_CUDA(launch_k(pdl, k_pupdate, persistent_grid(k_pupdate, 0, p->ntiles), kCtaThreads, 0, s,
+                    static_cast<const TileDesc *>(p->d_td), static_cast<int>(nt), static_cast<const float *>(w.z32),
+                    static_cast<const double *>(w.z64), w.p, static_cast<const SolverState *>(w.st)));
   MPB_LAUNCHED(h);
   if ((rc = halo_exchange(dc, w.p, 8, A->n, s))) return rc;
   {
-    const uint32_t dyn = spmv_dyn_smem(p);
-    k_spmv_pq<<<persistent_grid(k_spmv_pq, dyn, p->ntiles, kWsThreads), kWsThreads, dyn, s>>>(spmv_args(p, A, w));
+    if (direct_kernels()) {
+      MPB_CUDA(launch_k(pdl, p->ks == 7 ? k_spmv_direct<7> : k_spmv_direct<kSlots>,
+                        static_cast<unsigned>(p->ntiles), kTileRows, 0, s, spmv_args(h, p, A, w)));
+    } else {
+      const uint32_t dyn = spmv_dyn_smem(p);
+      MPB_CUDA(launch_k(pdl, spmv_kernel(p), persistent_grid(spmv_kernel(p), dyn, p->ntiles, kWsThreads),
+                        kWsThreads, dyn, s, spmv_args(h, p, A, w)));
+    }
   }
   MPB_LAUNCHED(h);
   if ((rc = dist_step(h, dc, w.st, kStepPq, 2, s))) return rc;
-  k_update<<<persistent_grid(k_update, 0, p->ntiles), kCtaThreads, 0, s>>>(p->d_td, static_cast<int>(nt), x, w.p,
-                                                                            w.q, w.r, w.part, w.st);
-  MPB_LAUNCHED(h);
+  if (fused) {
+    if (high && (rc = launch_update_first<double>(h, s, p, A, o->t, w.zA64, x, w.p, w.q, w.r, w.part, nullptr,
+                                                  nullptr, w.st, 0)))
+      return rc;
+    if (low && (rc = launch_update_first<float>(h, s, p, A, o->t, w.zA32, x, w.p, w.q, w.r, w.part,
+                                                &w.st->ovf_count, &w.st->ovf_first, w.st, 1)))
+      return rc;
+  } else {
+    MPB_CUDA(launch_k(pdl, k_update, persistent_grid(k_update, 0, p->ntiles), kCtaThreads, 0, s,
+                      static_cast<const TileDesc *>(p->d_td), static_cast<int>(nt), x,
+                      static_cast<const double *>(w.p), static_cast<const double *>(w.q), w.r, w.part, w.st));
+    MPB_LAUNCHED(h);
+  }
   if ((rc = dist_step(h, dc, w.st, kStepRr, 2, s))) return rc;
   if (o->true_stride > 0) {
     if ((rc = halo_exchange(dc, x, 8, A->n, s))) return rc;
@@ -1335,22 +1498,51 @@ static int solve_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, con
   key.stride = opt->true_stride;
   key.n = A->n;
   key.comm = dc ? dc->comm : nullptr;
+  // one GPU: the loop over graph bodies runs on the device (a while node
+  // whose condition the x/r update's scalar step clears when the solve is
+  // done); multi-GPU: host-polled replays
+  const bool loop = dc == nullptr && std::getenv("MPB_NO_WHILE") == nullptr;
+  key.loop = loop ? 1 : 0;
   if (!(h->have_graph && h->gkey == key)) {
     if (h->have_graph) {
       cudaGraphExecDestroy(h->gexec);
       h->have_graph = false;
     }
     const int64_t l0 = h->launches;
-    MPB_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    cudaGraph_t graph = nullptr, body = nullptr;
+    if (loop) {
+      MPB_CUDA(cudaGraphCreate(&graph, 0));
+      cudaError_t ce = cudaGraphConditionalHandleCreate(&h->cond, graph, 1, cudaGraphCondAssignDefault);
+      cudaGraphNodeParams np{};
+      np.type = cudaGraphNodeTypeConditional;
+      np.conditional.handle = h->cond;
+      np.conditional.type = cudaGraphCondTypeWhile;
+      np.conditional.size = 1;
+      cudaGraphNode_t node;
+      if (ce == cudaSuccess) ce = cudaGraphAddNode(&node, graph, nullptr, 0, &np);
+      if (ce == cudaSuccess) body = np.conditional.phGraph_out[0];
+      if (ce == cudaSuccess)
+        ce = cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+      if (ce != cudaSuccess) {
+        cudaGraphDestroy(graph);
+        return status_of(ce);
+      }
+    } else {
+      MPB_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    }
     int crc = MPB_OK;
     for (int i = 0; i < G && crc == MPB_OK; i++) crc = enqueue_iteration(h, s, plan, A, opt, w, b, x, dc);
-    cudaGraph_t graph = nullptr;
-    cudaError_t ce = cudaStreamEndCapture(s, &graph);
+    cudaGraph_t captured = nullptr;
+    cudaError_t ce = cudaStreamEndCapture(s, &captured);
+    if (!loop) graph = captured;
     if (crc != MPB_OK) {
       if (graph) cudaGraphDestroy(graph);
       return crc;
     }
-    MPB_CUDA(ce);
+    if (ce != cudaSuccess) {
+      if (graph) cudaGraphDestroy(graph);
+      return status_of(ce);
+    }
     ce = cudaGraphInstantiate(&h->gexec, graph, 0);
     cudaGraphDestroy(graph);
     MPB_CUDA(ce);
@@ -1362,11 +1554,20 @@ static int solve_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, con
   k_scalar_start<<<1, 32, 0, s>>>(w.st);
   MPB_LAUNCHED(h);
   MPB_CUDA(cudaEventRecord(h->ev_t0, s));
+  // fused mode: the first iteration's first pass runs ahead of the graph
+  if (fused_mode(plan, opt, dc) && (rc = enqueue_first_passes(h, s, plan, A, opt, w))) return rc;
+  h->h_state->cond = loop ? static_cast<unsigned long long>(h->cond) : 0ull;
+  MPB_CUDA(cudaMemcpyAsync(&w.st->cond, &h->h_state->cond, sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
   for (;;) {
     MPB_CUDA(cudaGraphLaunch(h->gexec, s));
-    h->launches += h->graph_kernels;
     MPB_CUDA(cudaMemcpyAsync(h->h_state, w.st, sizeof(SolverState), cudaMemcpyDeviceToHost, s));
     MPB_CUDA(cudaStreamSynchronize(s));
+    const long long ran = h->h_state->error ? h->h_state->err_it : h->h_state->last_it;
+    if (loop) {  // bodies the while node ran
+      h->launches += h->graph_kernels * std::max<long long>(1, (ran + G - 1) / G);
+      break;
+    }
+    h->launches += h->graph_kernels;
     if (h->h_state->done) break;
   }
   MPB_CUDA(cudaEventRecord(h->ev_t1, s));
@@ -1432,6 +1633,7 @@ int mpb_profile_iteration_dist(mpb_handle *h, const mpb_plan *plan, const mpb_cs
   mid.first = 0;
   mid.branch = branch;
   mid.alpha = 1e-30;
+  mid.upd_branch = branch;
   mid.beta = 0.5;
   mid.rho = mid.rho_prev = 1.0;
   mid.r0 = 1.0;
@@ -1470,6 +1672,7 @@ int mpb_profile_iteration_dist(mpb_handle *h, const mpb_plan *plan, const mpb_cs
       a.sp = A->sell->d_sp;
       a.scol = A->sell->d_col;
       a.td = plan->d_td;
+      a.ctr = h->d_ctr + 0;
       a.meta = plan->d_meta;
       a.pat = plan->d_pat;
       a.boff = plan->d_boff;
@@ -1511,9 +1714,9 @@ int mpb_profile_iteration_dist(mpb_handle *h, const mpb_plan *plan, const mpb_cs
     rc = timed(slot, [&]() { return run_pass(pass); });
     if (rc) return rc;
   }
-  const SpmvArgs sa = spmv_args(plan, A, w);
+  const SpmvArgs sa = spmv_args(h, plan, A, w);
   const uint32_t sdyn = spmv_dyn_smem(plan);
-  const int sgrid = persistent_grid(k_spmv_pq, sdyn, plan->ntiles, kWsThreads);
+  const int sgrid = persistent_grid(spmv_kernel(plan), sdyn, plan->ntiles, kWsThreads);
   const int ugrid = persistent_grid(k_update, 0, plan->ntiles);
   const int pgrid = persistent_grid(k_pupdate, 0, plan->ntiles);
   rc = timed(7, [&]() -> int {
@@ -1523,7 +1726,7 @@ int mpb_profile_iteration_dist(mpb_handle *h, const mpb_plan *plan, const mpb_cs
   });
   if (rc) return rc;
   rc = timed(3, [&]() -> int {
-    k_spmv_pq<<<sgrid, kWsThreads, sdyn, s>>>(sa);
+    spmv_kernel(plan)<<<sgrid, kWsThreads, sdyn, s>>>(sa);
     MPB_LAUNCHED(h);
     return MPB_OK;
   });
@@ -1535,8 +1738,21 @@ int mpb_profile_iteration_dist(mpb_handle *h, const mpb_plan *plan, const mpb_cs
     return MPB_OK;
   });
   if (rc) return rc;
-  h_ms[5] = 0.0;  // scalar steps are fused into the kernels above
-  h_ms[6] = h_ms[0] + h_ms[1] * (opt->k > 2 ? opt->k - 2 : 0) + h_ms[2] + h_ms[3] + h_ms[4] + h_ms[7];
+  // the fused x/r update + next first pass, when the solve uses it
+  h_ms[5] = 0.0;
+  const bool fused = opt->k >= 2 && !plan->large && std::getenv("MPB_NO_FUSE") == nullptr;
+  if (fused) {
+    rc = timed(5, [&]() -> int {
+      if (branch == 0)
+        return launch_update_first<double>(h, s, plan, A, opt->t, w.zA64, x, w.p, w.q, w.r, w.part, nullptr, nullptr,
+                                           w.st, 0);
+      return launch_update_first<float>(h, s, plan, A, opt->t, w.zA32, x, w.p, w.q, w.r, w.part, &w.st->ovf_count,
+                                        &w.st->ovf_first, w.st, 1);
+    });
+    if (rc) return rc;
+  }
+  const double passes = h_ms[1] * (opt->k > 2 ? opt->k - 2 : 0) + h_ms[2];
+  h_ms[6] = fused ? passes + h_ms[3] + h_ms[5] + h_ms[7] : h_ms[0] + passes + h_ms[3] + h_ms[4] + h_ms[7];
   MPB_CUDA(cudaEventRecord(h->ev_out, s));
   MPB_CUDA(cudaStreamWaitEvent(h->user, h->ev_out, 0));
   return MPB_OK;

@@ -60,7 +60,10 @@ struct SolverState {
   int converged;
   int error;
   int true_pending;
+  int z1_ok;       // the fused update already ran the next first pass for `branch`
+  int upd_branch;  // branch of the iteration whose x/r update is pending (set at kStepPq)
   int pad;
+  unsigned long long cond;  // while-node handle of the solve graph (0: host-polled loop)
 };
 
 // ---------------------------------------------------------------------------
@@ -193,6 +196,12 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+
+// Programmatic dependent launch: a kernel launched with programmatic stream
+// serialization may start while its predecessor drains; everything before
+// pdl_wait() must touch only data the predecessor does not write.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
   unsigned long long t;

@@ -71,7 +71,11 @@ __device__ __forceinline__ void load_patterns(int *s_pat, const int *pat, int np
 // ---------------------------------------------------------------------------
 // scalar steps of the recurrence (solver.py:128-177, policies.py:102-116)
 // ---------------------------------------------------------------------------
-enum ScalarStep { kStepR0 = 0, kStepRho = 1, kStepPq = 2, kStepRr = 3, kStepTrue = 4, kStepFinal = 5, kStepStart = 6 };
+// kStepRrZ: kStepRr after the fused update, which also ran the next
+// iteration's first BJAC pass for the current branch (valid iff it stays)
+enum ScalarStep {
+  kStepR0 = 0, kStepRho = 1, kStepPq = 2, kStepRr = 3, kStepTrue = 4, kStepFinal = 5, kStepStart = 6, kStepRrZ = 7
+};
 
 __device__ __forceinline__ int choose_branch(int kind, double tol, double relres) {
   if (kind == 0) return 0;
@@ -80,11 +84,17 @@ __device__ __forceinline__ int choose_branch(int kind, double tol, double relres
   return relres >= tol ? 1 : 0;
 }
 
+// the solve graph's device-side loop continues while the solve is not done
+__device__ __forceinline__ void set_loop(const SolverState *st) {
+  if (st->cond != 0ull) cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(st->cond), st->done ? 0u : 1u);
+}
+
 __device__ __forceinline__ void fail(SolverState *st, int code, double val) {
   st->error = code;
   st->err_it = st->it;
   st->err_val = val;
   st->done = 1;
+  set_loop(st);
 }
 
 // Executed by one thread once the global sum `tot` of a step is known.
@@ -117,9 +127,12 @@ __device__ __noinline__ void scalar_step(int step, double tot, SolverState *st) 
       st->pq = tot;
       if (tot <= 0.0) { fail(st, kIndefMatrix, tot); break; }
       st->alpha = st->rho / tot;
+      st->upd_branch = st->branch;
       break;
     }
-    case kStepRr: {
+    case kStepRr:
+    case kStepRrZ: {
+      const int old_branch = st->branch;
       const double rnorm = sqrt(tot);
       st->rnorm = rnorm;
       st->rho_prev = st->rho;
@@ -142,6 +155,12 @@ __device__ __noinline__ void scalar_step(int step, double tot, SolverState *st) 
         st->it = it + 1;
         st->branch = choose_branch(st->kind, st->adp_tol, relres);
       }
+      st->z1_ok = (step == kStepRrZ && st->branch == old_branch) ? 1 : 0;
+      if (step == kStepRrZ && st->branch != old_branch) {  // speculative narrowing no longer applies
+        st->ovf_count = 0ull;
+        st->ovf_first = 0x7fffffffffffffffLL;
+      }
+      set_loop(st);
       break;
     }
     case kStepTrue: {
@@ -237,12 +256,12 @@ struct TileGeom {
 
 // Byte offsets of one shared-memory stage.
 struct StageLayout {
-  uint32_t col, val, sp, meta, v0, v1, v2, bytes;
+  uint32_t col, val, sp, meta, v0, v1, v2, v3, bytes;
 };
 __host__ __device__ inline uint32_t al16u(uint32_t b) { return (b + 15u) & ~15u; }
 // v*es: element sizes of up to three row-vector slices [lo, hi) (0: absent)
 __host__ __device__ inline StageLayout stage_layout(int cap_e, int es, int max_sl, bool cols, bool meta, int v0es,
-                                                    int v1es, int v2es) {
+                                                    int v1es, int v2es, int v3es = 0) {
   StageLayout L;
   uint32_t off = 0;
   L.col = off;
@@ -259,6 +278,8 @@ __host__ __device__ inline StageLayout stage_layout(int cap_e, int es, int max_s
   off += v1es ? al16u(static_cast<uint32_t>(kTileRows) * v1es + 16u) : 0u;
   L.v2 = off;
   off += v2es ? al16u(static_cast<uint32_t>(kTileRows) * v2es + 16u) : 0u;
+  L.v3 = off;
+  off += v3es ? al16u(static_cast<uint32_t>(kTileRows) * v3es + 16u) : 0u;
   L.bytes = off;
   return L;
 }
@@ -268,6 +289,7 @@ struct Ring {
   uint64_t full[kMaxStages];   // TMA bytes landed
   uint64_t empty[kMaxStages];  // consumers done with the stage
   int ok[kMaxStages];          // tile fitted and was staged
+  int tile[kMaxStages];        // tile in the stage, -1: no more tiles
   TileDesc desc[kMaxStages];
 };
 
@@ -290,11 +312,11 @@ __device__ __forceinline__ const E *staged(const unsigned char *region, const E 
 }
 
 // Producer: stage tile `tile` into ring slot st (thread = producer lane 0).
-template <typename T, typename V0, typename V1, typename V2, bool IB = false>
+template <typename T, typename V0, typename V1, typename V2, bool IB = false, typename V3 = uint8_t>
 __device__ __forceinline__ void produce(Ring &R, int st, const TileDesc *td, int tile, const TileGeom &g,
                                         const StageLayout &L, unsigned char *stage, const int *sp, const int *scol,
                                         const T *sval, const uint16_t *meta, const V0 *v0, const V1 *v1,
-                                        const V2 *v2) {
+                                        const V2 *v2, const V3 *v3 = nullptr) {
   const TileDesc d = td[tile];
   R.desc[st] = d;
   const int e0 = IB ? d.ie0 : d.e0, e1 = IB ? d.ie1 : d.e1;
@@ -309,7 +331,7 @@ __device__ __forceinline__ void produce(Ring &R, int st, const TileDesc *td, int
   const bool cols = g.cols && d.ngen > 0;  // pattern rows rebuild their columns
   uint32_t bytes = static_cast<uint32_t>(nent) * ((cols ? 4u : 0u) + sizeof(T)) + window_bytes(sp, d.s0, d.s1 + 1) +
                    window_bytes(meta, d.lo, d.hi) + window_bytes(v0, d.lo, d.hi) + window_bytes(v1, d.lo, d.hi) +
-                   window_bytes(v2, d.lo, d.hi);
+                   window_bytes(v2, d.lo, d.hi) + window_bytes(v3, d.lo, d.hi);
   mbar_arrive_expect_tx(&R.full[st], bytes);
   if (cols) bulk_g2s(stage + L.col, scol + e0, static_cast<uint32_t>(nent) * 4u, &R.full[st]);
   bulk_g2s(stage + L.val, sval + e0, static_cast<uint32_t>(nent) * sizeof(T), &R.full[st]);
@@ -318,15 +340,35 @@ __device__ __forceinline__ void produce(Ring &R, int st, const TileDesc *td, int
   if (v0 != nullptr) tma_window(stage + L.v0, v0, d.lo, d.hi, &R.full[st]);
   if (v1 != nullptr) tma_window(stage + L.v1, v1, d.lo, d.hi, &R.full[st]);
   if (v2 != nullptr) tma_window(stage + L.v2, v2, d.lo, d.hi, &R.full[st]);
+  if (v3 != nullptr) tma_window(stage + L.v3, v3, d.lo, d.hi, &R.full[st]);
 }
 
-// Producer loop (warp 16, lane 0): walks the CTA's tiles, waiting for a
-// stage to be released before refilling it.
+// Producer loop (producer warp, lane 0): claims tiles from the launch's
+// counter (dynamic scheduling: CTAs that start late or run slow take fewer
+// tiles), waiting for a stage to be released before refilling it, and ends
+// the consumers' walk with tile -1.  The globally last claim (ntiles +
+// gridDim claims in all) resets the counter for the next launch.  ctr ==
+// null: static walk blockIdx.x, +gridDim.x, ...
 template <typename F>
-__device__ __forceinline__ void producer_loop(Ring &R, int ntiles, int ns, F &&fill) {
+__device__ __forceinline__ void producer_loop(Ring &R, int ntiles, int ns, unsigned int *ctr, F &&fill) {
   int st = 0, rnd = 0;  // stage, and how often it has been filled before
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  int next = blockIdx.x;
+  for (;;) {
     if (rnd > 0) mbar_wait(&R.empty[st], (rnd - 1) & 1);
+    int tile;
+    if (ctr != nullptr) {
+      const unsigned int v = atomicAdd(ctr, 1u);
+      if (v == static_cast<unsigned int>(ntiles) + gridDim.x - 1u) atomicExch(ctr, 0u);
+      tile = v < static_cast<unsigned int>(ntiles) ? static_cast<int>(v) : -1;
+    } else {
+      tile = next < ntiles ? next : -1;
+      next += gridDim.x;
+    }
+    R.tile[st] = tile;
+    if (tile < 0) {
+      mbar_arrive(&R.full[st]);
+      return;
+    }
     fill(st, tile);
     if (++st == ns) {
       st = 0;
@@ -377,6 +419,7 @@ struct PassArgs {
   const uint16_t *meta;  // per-row static structure (plan-bound)
   const int *pat;        // row-pattern table (g.npat entries of kPatStride ints)
   const TileDesc *td;    // tile descriptors
+  unsigned int *ctr;     // tile-claim counter of the launch (null: static walk)
   const int *boff;       // nb+1 block offsets (generic rows, large blocks)
   TileGeom g;
   int t;
@@ -392,11 +435,16 @@ struct PassArgs {
   T *dbuf;
   SolverState *st;       // solve mode: gate + fused scalar step
   int want_branch;
+  int gate;              // 0: st->branch; 1: also skip when the fused update ran this first pass;
+                         // 2: st->upd_branch (fused update: the step inside may change st->branch)
+  int pdl;               // host side: launch with programmatic serialization
 };
 
 template <typename T>
 __device__ __forceinline__ bool gated_off(const PassArgs<T> &a) {
-  return a.st != nullptr && (a.st->done || a.st->branch != a.want_branch);
+  if (a.st == nullptr) return false;
+  const int b = a.gate == 2 ? a.st->upd_branch : a.st->branch;
+  return a.st->done || b != a.want_branch || (a.gate == 1 && a.st->z1_ok);
 }
 
 template <typename T>
@@ -453,7 +501,9 @@ __device__ __forceinline__ T generic_row_sweep(const PassArgs<T> &a, const TileD
 // One tile of a fused (non-first-only) pass, consumer threads only.  col /
 // val / spp / mt are the shared stage or the global arrays offset to the
 // tile (same indexing); r64t / rTt the tile's residual slice.
-template <typename T, bool FIRST, bool LAST>
+// KS: slots of the longest row pattern (compile time, 7 for 7-point stencils);
+// table entries past a pattern's length are 0, so gathers need no predicate.
+template <typename T, bool FIRST, bool LAST, int KS>
 __device__ __forceinline__ void bjac_tile_body(const PassArgs<T> &a, int tile, const TileDesc &d, const int *col,
                                                const T *val, const int *spp, const uint16_t *mt, const double *r64t,
                                                const T *rTt, const int *s_pat, T *s_w, double *ws) {
@@ -472,7 +522,8 @@ __device__ __forceinline__ void bjac_tile_body(const PassArgs<T> &a, int tile, c
     base = sb - d.e0 + (row & 31);
     m = mt[tid];
     const T rv = r64t != nullptr ? narrow_checked(a, r64t[tid], row, FIRST) : rTt[tid];
-    if (!FIRST) zown = __ldg(a.zin + row);
+    const T *zr = FIRST ? nullptr : a.zin + row;
+    if (!FIRST) zown = __ldg(zr);
     if (m != kMetaGeneric) {
       P = s_pat + meta_pid(m) * kPatStride;
       const int hdr = P[0], len = pat_len(hdr);
@@ -480,15 +531,14 @@ __device__ __forceinline__ void bjac_tile_body(const PassArgs<T> &a, int tile, c
       i1 = meta_i1(m);
       T az = T(0);
       if (!FIRST) {  // az = A z_in, all slots, stored (ascending column) order
-        T v[kSlots], g[kSlots];
+        T v[KS], g[KS];
 #pragma unroll
-        for (int u = 0; u < kSlots; u++) {
-          const bool ok = u < len;
-          v[u] = ok ? val[base + 32 * u] : T(0);
-          g[u] = __ldg(a.zin + (ok ? row + P[1 + u] : row));
+        for (int u = 0; u < KS; u++) {
+          v[u] = u < len ? val[base + 32 * u] : T(0);
+          g[u] = __ldg(zr + P[1 + u]);
         }
 #pragma unroll
-        for (int u = 0; u < kSlots; u++)
+        for (int u = 0; u < KS; u++)
           if (u < len) az = add_rn(az, mul_rn(v[u], g[u]));
       }
       dd = val[base + 32 * pat_dpos(hdr)];
@@ -504,6 +554,7 @@ __device__ __forceinline__ void bjac_tile_body(const PassArgs<T> &a, int tile, c
     T acc = T(0);
     if (valid) {
       if (m != kMetaGeneric) {
+#pragma unroll 1
         for (int j = i0; j < i1; j++) acc = add_rn(acc, mul_rn(val[base + 32 * j], s_w[tid + P[1 + j]]));
       } else {
         acc = generic_row_sweep(a, d, row, base, width, col, val, s_w);
@@ -531,14 +582,15 @@ __device__ __forceinline__ void bjac_tile_body(const PassArgs<T> &a, int tile, c
 // First pass of a tile: z1 = D_b^{-1} r (bjac.py:134-136), reading only the
 // in-block entries (plan's in-block SELL): y = r / d, then t-1 sweeps
 // y += (r - A_b y) / d over the in-block entries in ascending column order.
+// res: the row's residual in T (valid rows).
 template <typename T>
 __device__ __forceinline__ void bjac_first_body(const PassArgs<T> &a, const TileDesc &d, const int *col,
-                                                const T *val, const int *spp, const uint16_t *mt,
-                                                const double *r64t, const T *rTt, const int *s_pat, T *s_w) {
+                                                const T *val, const int *spp, const uint16_t *mt, T res,
+                                                const int *s_pat, T *s_w) {
   const int tid = threadIdx.x;
   const int lo = d.lo, hi = d.hi, row = lo + tid;
   const bool valid = row < hi;
-  T res = T(0), dd = T(1), w = T(0);
+  T dd = T(1), w = T(0);
   uint16_t m = kMetaGeneric;
   int base = 0, nib = 0;
   const int *P = s_pat;  // pattern row: offsets of its in-block slots
@@ -548,7 +600,6 @@ __device__ __forceinline__ void bjac_first_body(const PassArgs<T> &a, const Tile
     const int iwidth = (spp[si + 1] - sb) >> 5;
     base = sb - d.ie0 + (row & 31);
     m = mt[tid];
-    res = r64t != nullptr ? narrow_checked(a, r64t[tid], row, true) : rTt[tid];
     if (m != kMetaGeneric) {
       const int i0 = meta_i0(m);
       nib = meta_i1(m) - i0;
@@ -569,6 +620,7 @@ __device__ __forceinline__ void bjac_first_body(const PassArgs<T> &a, const Tile
     named_sync(kBarConsumers, kConsumers);
     T acc = T(0);
     if (m != kMetaGeneric) {
+#pragma unroll 1
       for (int j = 0; j < nib; j++) acc = add_rn(acc, mul_rn(val[base + 32 * j], s_w[tid + P[j]]));
     } else {
       for (int j = 0; j < nib; j++) acc = add_rn(acc, mul_rn(val[base + 32 * j], s_w[col[base + 32 * j] - lo]));
@@ -592,9 +644,8 @@ __host__ __device__ inline StageLayout bjac_layout(const TileGeom &g) {
 }
 
 // Persistent, warp-specialised fused pass.
-template <typename T, bool FIRST, bool LAST, bool R64>
+template <typename T, bool FIRST, bool LAST, bool R64, int KS>
 __global__ void __launch_bounds__(kWsThreads) k_bjac_tile(const PassArgs<T> a) {
-  if (gated_off(a)) return;
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ Ring R;
   __shared__ T s_w[kTileRows];
@@ -605,11 +656,13 @@ __global__ void __launch_bounds__(kWsThreads) k_bjac_tile(const PassArgs<T> a) {
   const StageLayout L = bjac_layout<T, FIRST, R64>(a.g);
   load_patterns(s_pat, a.pat, a.g.npat);
   ring_init(R, ns);
+  pdl_wait();
+  if (gated_off(a)) return;
   if (threadIdx.x >= kConsumers) {  // producer warp
     using RT = typename std::conditional<R64, double, T>::type;
     const RT *rsrc = R64 ? reinterpret_cast<const RT *>(a.r64) : reinterpret_cast<const RT *>(a.rT);
     if (threadIdx.x == kConsumers)
-      producer_loop(R, a.g.ntiles, ns, [&](int st, int tile) {
+      producer_loop(R, a.g.ntiles, ns, a.ctr, [&](int st, int tile) {
         if (kIB)
           produce<T, RT, uint8_t, uint8_t, true>(R, st, a.td, tile, a.g, L, smem + st * L.bytes, a.ib_sp, a.ib_col,
                                                  a.ib_val, a.meta, rsrc, nullptr, nullptr);
@@ -618,35 +671,40 @@ __global__ void __launch_bounds__(kWsThreads) k_bjac_tile(const PassArgs<T> a) {
                                            a.meta, rsrc, nullptr, nullptr);
       });
   } else {
-    RingCursor cur;
-    for (int tile = blockIdx.x; tile < a.g.ntiles; tile += gridDim.x, cur.advance(ns)) {
+    for (RingCursor cur;; cur.advance(ns)) {
       const int st = cur.st;
       mbar_wait(&R.full[st], cur.phase);
+      const int tile = R.tile[st];
+      if (tile < 0) break;
       const TileDesc d = R.desc[st];
       const unsigned char *sb = smem + st * L.bytes;
       const bool ok = R.ok[st] != 0;
       const bool scols = ok && a.g.cols && d.ngen > 0;
       if (kIB) {
         const int *col = scols ? reinterpret_cast<const int *>(sb + L.col) : a.ib_col + d.ie0;
+        const int row = d.lo + static_cast<int>(threadIdx.x);
+        T rv = T(0);
+        if (row < d.hi) {
+          if (R64) rv = narrow_checked(a, ok ? staged(sb + L.v0, a.r64, d.lo, d.hi)[threadIdx.x] : a.r64[row], row, true);
+          else rv = ok ? staged(sb + L.v0, a.rT, d.lo, d.hi)[threadIdx.x] : a.rT[row];
+        }
         if (ok) {
           bjac_first_body<T>(a, d, col, reinterpret_cast<const T *>(sb + L.val),
-                             staged(sb + L.sp, a.ib_sp, d.s0, d.s1 + 1), staged(sb + L.meta, a.meta, d.lo, d.hi),
-                             R64 ? staged(sb + L.v0, a.r64, d.lo, d.hi) : nullptr,
-                             R64 ? nullptr : staged(sb + L.v0, a.rT, d.lo, d.hi), s_pat, s_w);
+                             staged(sb + L.sp, a.ib_sp, d.s0, d.s1 + 1), staged(sb + L.meta, a.meta, d.lo, d.hi), rv,
+                             s_pat, s_w);
         } else {
-          bjac_first_body<T>(a, d, col, a.ib_val + d.ie0, a.ib_sp + d.s0, a.meta + d.lo,
-                             R64 ? a.r64 + d.lo : nullptr, R64 ? nullptr : a.rT + d.lo, s_pat, s_w);
+          bjac_first_body<T>(a, d, col, a.ib_val + d.ie0, a.ib_sp + d.s0, a.meta + d.lo, rv, s_pat, s_w);
         }
       } else {
         const int *col = scols ? reinterpret_cast<const int *>(sb + L.col) : a.scol + d.e0;
         if (ok) {
-          bjac_tile_body<T, FIRST, LAST>(a, tile, d, col, reinterpret_cast<const T *>(sb + L.val),
+          bjac_tile_body<T, FIRST, LAST, KS>(a, tile, d, col, reinterpret_cast<const T *>(sb + L.val),
                                          staged(sb + L.sp, a.sp, d.s0, d.s1 + 1),
                                          staged(sb + L.meta, a.meta, d.lo, d.hi),
                                          R64 ? staged(sb + L.v0, a.r64, d.lo, d.hi) : nullptr,
                                          R64 ? nullptr : staged(sb + L.v0, a.rT, d.lo, d.hi), s_pat, s_w, ws);
         } else {
-          bjac_tile_body<T, FIRST, LAST>(a, tile, d, col, a.sval + d.e0, a.sp + d.s0, a.meta + d.lo,
+          bjac_tile_body<T, FIRST, LAST, KS>(a, tile, d, col, a.sval + d.e0, a.sp + d.s0, a.meta + d.lo,
                                          R64 ? a.r64 + d.lo : nullptr, R64 ? nullptr : a.rT + d.lo, s_pat, s_w,
                                          ws);
         }
@@ -654,6 +712,30 @@ __global__ void __launch_bounds__(kWsThreads) k_bjac_tile(const PassArgs<T> a) {
       ring_release(R, st);
     }
   }
+  pdl_trigger();  // dependents may launch into the SMs this grid drains
+  if (LAST && a.part != nullptr) finish_grid(a.st, 0, kStepRho, a.part, a.g.ntiles, ws);
+}
+
+// One CTA per tile, no TMA ring: the same tile bodies on global pointers;
+// the hardware CTA scheduler keeps many tiles per SM in flight.
+template <typename T, bool FIRST, bool LAST, bool R64, int KS>
+__global__ void __launch_bounds__(kTileRows) k_bjac_direct(const PassArgs<T> a) {
+  __shared__ T s_w[kTileRows];
+  __shared__ double ws[32];
+  pdl_wait();
+  if (gated_off(a)) return;
+  const int tile = blockIdx.x;
+  const TileDesc d = a.td[tile];
+  if (FIRST && !LAST) {
+    const int row = d.lo + static_cast<int>(threadIdx.x);
+    T rv = T(0);
+    if (row < d.hi) rv = R64 ? narrow_checked(a, a.r64[row], row, true) : a.rT[row];
+    bjac_first_body<T>(a, d, a.ib_col + d.ie0, a.ib_val + d.ie0, a.ib_sp + d.s0, a.meta + d.lo, rv, a.pat, s_w);
+  } else {
+    bjac_tile_body<T, FIRST, LAST, KS>(a, tile, d, a.scol + d.e0, a.sval + d.e0, a.sp + d.s0, a.meta + d.lo,
+                                       R64 ? a.r64 + d.lo : nullptr, R64 ? nullptr : a.rT + d.lo, a.pat, s_w, ws);
+  }
+  pdl_trigger();  // dependents may launch into the SMs this grid drains
   if (LAST && a.part != nullptr) finish_grid(a.st, 0, kStepRho, a.part, a.g.ntiles, ws);
 }
 
@@ -728,6 +810,7 @@ constexpr int kStreamTiles = 4;  // tiles per CTA iteration of the streaming ker
 
 __global__ void __launch_bounds__(kCtaThreads)
     k_pupdate(const TileDesc *td, int ntiles, const float *z32, const double *z64, double *p, const SolverState *st) {
+  pdl_wait();
   if (st->done) return;
   const bool low = st->branch == 1;
   const bool first = st->first != 0;
@@ -767,6 +850,7 @@ struct SpmvArgs {
   const uint16_t *meta;
   const int *pat;
   const TileDesc *td;
+  unsigned int *ctr;
   TileGeom g;
   const double *p;  // search direction (updated in place by k_pupdate)
   double *q;
@@ -774,6 +858,7 @@ struct SpmvArgs {
   SolverState *st;
 };
 
+template <int KS>
 __device__ __forceinline__ void spmv_tile_body(const SpmvArgs &a, int tile, const TileDesc &d, const int *col,
                                                const double *val, const int *spp, const uint16_t *mt,
                                                const int *s_pat, double *ws) {
@@ -790,15 +875,15 @@ __device__ __forceinline__ void spmv_tile_body(const SpmvArgs &a, int tile, cons
     if (m != kMetaGeneric) {
       const int *P = s_pat + meta_pid(m) * kPatStride;
       const int len = pat_len(P[0]);
-      double vv[kSlots], pv[kSlots];
+      const double *pr = p + row;
+      double vv[KS], pv[KS];
 #pragma unroll
-      for (int u = 0; u < kSlots; u++) {
-        const bool ok = u < len;
-        vv[u] = ok ? val[base + 32 * u] : 0.0;
-        pv[u] = __ldg(p + (ok ? row + P[1 + u] : row));
+      for (int u = 0; u < KS; u++) {
+        vv[u] = u < len ? val[base + 32 * u] : 0.0;
+        pv[u] = __ldg(pr + P[1 + u]);
       }
 #pragma unroll
-      for (int u = 0; u < kSlots; u++)
+      for (int u = 0; u < KS; u++)
         if (u < len) acc = __dadd_rn(acc, __dmul_rn(vv[u], pv[u]));
     } else {
       const int width = (spp[si + 1] - sb) >> 5;
@@ -818,8 +903,8 @@ __host__ __device__ inline StageLayout spmv_layout(const TileGeom &g) {
   return stage_layout(g.cap_e, 8, g.max_sl, g.cols != 0, true, 0, 0, 0);
 }
 
+template <int KS>
 __global__ void __launch_bounds__(kWsThreads) k_spmv_pq(const SpmvArgs a) {
-  if (a.st->done) return;
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ Ring R;
   __shared__ double ws[32];
@@ -828,29 +913,45 @@ __global__ void __launch_bounds__(kWsThreads) k_spmv_pq(const SpmvArgs a) {
   const StageLayout L = spmv_layout(a.g);
   load_patterns(s_pat, a.pat, a.g.npat);
   ring_init(R, ns);
+  pdl_wait();
+  if (a.st->done) return;
   if (threadIdx.x >= kConsumers) {
     if (threadIdx.x == kConsumers)
-      producer_loop(R, a.g.ntiles, ns, [&](int st, int tile) {
+      producer_loop(R, a.g.ntiles, ns, a.ctr, [&](int st, int tile) {
         produce<double, uint8_t, uint8_t, uint8_t>(R, st, a.td, tile, a.g, L, smem + st * L.bytes, a.sp, a.scol,
                                                    a.sval, a.meta, nullptr, nullptr, nullptr);
       });
   } else {
-    RingCursor cur;
-    for (int tile = blockIdx.x; tile < a.g.ntiles; tile += gridDim.x, cur.advance(ns)) {
+    for (RingCursor cur;; cur.advance(ns)) {
       const int st = cur.st;
       mbar_wait(&R.full[st], cur.phase);
+      const int tile = R.tile[st];
+      if (tile < 0) break;
       const TileDesc d = R.desc[st];
       const unsigned char *sb = smem + st * L.bytes;
       if (R.ok[st]) {
         const int *col = (a.g.cols && d.ngen > 0) ? reinterpret_cast<const int *>(sb + L.col) : a.scol + d.e0;
-        spmv_tile_body(a, tile, d, col, reinterpret_cast<const double *>(sb + L.val),
+        spmv_tile_body<KS>(a, tile, d, col, reinterpret_cast<const double *>(sb + L.val),
                        staged(sb + L.sp, a.sp, d.s0, d.s1 + 1), staged(sb + L.meta, a.meta, d.lo, d.hi), s_pat, ws);
       } else {
-        spmv_tile_body(a, tile, d, a.scol + d.e0, a.sval + d.e0, a.sp + d.s0, a.meta + d.lo, s_pat, ws);
+        spmv_tile_body<KS>(a, tile, d, a.scol + d.e0, a.sval + d.e0, a.sp + d.s0, a.meta + d.lo, s_pat, ws);
       }
       ring_release(R, st);
     }
   }
+  pdl_trigger();
+  finish_grid(a.st, 1, kStepPq, a.part, a.g.ntiles, ws);
+}
+
+template <int KS>
+__global__ void __launch_bounds__(kTileRows) k_spmv_direct(const SpmvArgs a) {
+  __shared__ double ws[32];
+  pdl_wait();
+  if (a.st->done) return;
+  const int tile = blockIdx.x;
+  const TileDesc d = a.td[tile];
+  spmv_tile_body<KS>(a, tile, d, a.scol + d.e0, a.sval + d.e0, a.sp + d.s0, a.meta + d.lo, a.pat, ws);
+  pdl_trigger();
   finish_grid(a.st, 1, kStepPq, a.part, a.g.ntiles, ws);
 }
 
@@ -860,6 +961,7 @@ __global__ void __launch_bounds__(kWsThreads) k_spmv_pq(const SpmvArgs a) {
 __global__ void __launch_bounds__(kCtaThreads)
     k_update(const TileDesc *td, int ntiles, double *x, const double *p, const double *q, double *r, double *part,
              SolverState *st) {
+  pdl_wait();
   if (st->done) return;
   __shared__ double ws[kStreamTiles][32];
   __shared__ double wsf[32];
@@ -906,7 +1008,110 @@ __global__ void __launch_bounds__(kCtaThreads)
       }
     }
   }
+  pdl_trigger();
   finish_grid(st, 2, kStepRr, part, ntiles, wsf);
+}
+
+// Fused x/r update + the next iteration's first BJAC pass (solver.py:160-165
+// then bjac.py:134-136 for the branch in force): each tile updates its own
+// x and r rows, adds its r.r partial, narrows the new r (fp32 branch, with
+// the overflow count) and runs the in-block sweeps into z1.  The last CTA
+// runs kStepRrZ; if the step changes the branch, z1 is discarded and the
+// standalone first pass of the new branch runs instead (z1_gate).
+template <typename T>
+__host__ __device__ inline StageLayout update_first_layout(const TileGeom &g) {
+  // v0 r, v1 x, v2 p, v3 q (fp64 slices)
+  return stage_layout(g.cap_e, sizeof(T), g.max_sl, g.cols != 0, true, 8, 8, 8, 8);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kWsThreads) k_update_first(const PassArgs<T> a, double *x, const double *p,
+                                                               const double *q, double *r) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ Ring R;
+  __shared__ T s_w[kTileRows];
+  __shared__ double ws[32];
+  __shared__ int s_pat[kPatMax * kPatStride];
+  const int ns = a.g.ns;
+  const StageLayout L = update_first_layout<T>(a.g);
+  load_patterns(s_pat, a.pat, a.g.npat);
+  ring_init(R, ns);
+  pdl_wait();
+  if (gated_off(a)) return;
+  if (threadIdx.x >= kConsumers) {
+    if (threadIdx.x == kConsumers)
+      producer_loop(R, a.g.ntiles, ns, a.ctr, [&](int st, int tile) {
+        produce<T, double, double, double, true, double>(R, st, a.td, tile, a.g, L, smem + st * L.bytes, a.ib_sp,
+                                                         a.ib_col, a.ib_val, a.meta, r, x, p, q);
+      });
+  } else {
+    const double alpha = a.st->alpha;
+    for (RingCursor cur;; cur.advance(ns)) {
+      const int st = cur.st;
+      mbar_wait(&R.full[st], cur.phase);
+      const int tile = R.tile[st];
+      if (tile < 0) break;
+      const TileDesc d = R.desc[st];
+      const unsigned char *sb = smem + st * L.bytes;
+      const bool ok = R.ok[st] != 0;
+      const int row = d.lo + static_cast<int>(threadIdx.x);
+      double sq = 0.0;
+      T rv = T(0);
+      if (row < d.hi) {
+        const int i = threadIdx.x;
+        const double xv = ok ? staged(sb + L.v1, x, d.lo, d.hi)[i] : x[row];
+        const double pv = ok ? staged(sb + L.v2, p, d.lo, d.hi)[i] : p[row];
+        const double qv = ok ? staged(sb + L.v3, q, d.lo, d.hi)[i] : q[row];
+        const double ro = ok ? staged(sb + L.v0, r, d.lo, d.hi)[i] : r[row];
+        x[row] = __dadd_rn(xv, __dmul_rn(alpha, pv));
+        const double rn = __dsub_rn(ro, __dmul_rn(alpha, qv));
+        r[row] = rn;
+        sq = __dmul_rn(rn, rn);
+        rv = narrow_checked(a, rn, row, true);
+      }
+      const double tot = block_tree_nb<kTileThreads>(sq, ws, kBarConsumers);
+      if (threadIdx.x == 0) a.part[tile] = tot;
+      const bool scols = ok && a.g.cols && d.ngen > 0;
+      const int *col = scols ? reinterpret_cast<const int *>(sb + L.col) : a.ib_col + d.ie0;
+      if (ok)
+        bjac_first_body<T>(a, d, col, reinterpret_cast<const T *>(sb + L.val),
+                           staged(sb + L.sp, a.ib_sp, d.s0, d.s1 + 1), staged(sb + L.meta, a.meta, d.lo, d.hi), rv,
+                           s_pat, s_w);
+      else
+        bjac_first_body<T>(a, d, col, a.ib_val + d.ie0, a.ib_sp + d.s0, a.meta + d.lo, rv, s_pat, s_w);
+      ring_release(R, st);
+    }
+  }
+  pdl_trigger();
+  finish_grid(a.st, 2, kStepRrZ, a.part, a.g.ntiles, ws);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kTileRows) k_update_first_direct(const PassArgs<T> a, double *x, const double *p,
+                                                                     const double *q, double *r) {
+  __shared__ T s_w[kTileRows];
+  __shared__ double ws[32];
+  pdl_wait();
+  if (gated_off(a)) return;
+  const double alpha = a.st->alpha;
+  const int tile = blockIdx.x;
+  const TileDesc d = a.td[tile];
+  const int row = d.lo + static_cast<int>(threadIdx.x);
+  double sq = 0.0;
+  T rv = T(0);
+  if (row < d.hi) {
+    const double xv = x[row], pv = p[row], qv = q[row], ro = r[row];
+    x[row] = __dadd_rn(xv, __dmul_rn(alpha, pv));
+    const double rn = __dsub_rn(ro, __dmul_rn(alpha, qv));
+    r[row] = rn;
+    sq = __dmul_rn(rn, rn);
+    rv = narrow_checked(a, rn, row, true);
+  }
+  const double tot = block_tree_nb<kTileThreads>(sq, ws, kBarConsumers);
+  if (threadIdx.x == 0) a.part[tile] = tot;
+  bjac_first_body<T>(a, d, a.ib_col + d.ie0, a.ib_val + d.ie0, a.ib_sp + d.s0, a.meta + d.lo, rv, a.pat, s_w);
+  pdl_trigger();
+  finish_grid(a.st, 2, kStepRrZ, a.part, a.g.ntiles, ws);
 }
 
 // res = b - A x (or b), optionally stored; res.res partial; the last CTA runs

@@ -375,5 +375,5 @@ def profile_iteration(A: SparseMatrix, mp: MixedPreconditioner, *,
         _lib.ptr(ws), ws.numel(), 0 if branch == "high" else 1, int(reps), out),
         "profile_iteration")
     names = ("bjac_first", "bjac_middle", "bjac_last", "spmv_pq", "update",
-             "scalar", "iteration", "pupdate")
+             "update_first", "iteration", "pupdate")
     return {k: float(out[i]) for i, k in enumerate(names)}
