@@ -488,7 +488,7 @@ int64_t plan_tiles(int64_t nb, const int64_t *offs, const int64_t *rp, int64_t *
 
 // Solve-time workspace layout
 struct SolveWs {
-  double *r, *q, *p, *z64, *zA64, *zB64;
+  double *r, *q, *p, *p2, *z64, *zA64, *zB64;  // p2: second search-direction buffer (fused mode)
   float *z32, *zA32, *zB32;
   double *res64, *dg64, *wA64, *wB64;
   float *res32, *dg32, *wA32, *wB32;
@@ -512,6 +512,7 @@ SolveWs carve(const mpb_plan *p, int64_t n, char *base, int64_t ng = 0) {
   w.r = (double *)take(d);
   w.q = (double *)take(d);
   w.p = (double *)take(dg);
+  w.p2 = (double *)take(dg);
   w.z64 = (double *)take(d);
   w.zA64 = (double *)take(dg);
   w.zB64 = (double *)take(dg);
@@ -1223,7 +1224,9 @@ static uint32_t spmv_dyn_smem(const mpb_plan *p) {
   return g.ns * spmv_layout(g).bytes;
 }
 
-static SpmvArgs spmv_args(const mpb_handle *h, const mpb_plan *p, const mpb_csr *A, const SolveWs &w) {
+// pnew != null: p rebuilt from z and pold inside the SpMV (fused mode)
+static SpmvArgs spmv_args(const mpb_handle *h, const mpb_plan *p, const mpb_csr *A, const SolveWs &w,
+                          const double *pold = nullptr, double *pnew = nullptr) {
   SpmvArgs sa{};
   sa.sp = A->sell->d_sp;
   sa.scol = A->sell->d_col;
@@ -1234,6 +1237,10 @@ static SpmvArgs spmv_args(const mpb_handle *h, const mpb_plan *p, const mpb_csr 
   sa.ctr = h->d_ctr + 2;
   sa.g = spmv_geom(p);
   sa.p = w.p;
+  sa.z32 = w.z32;
+  sa.z64 = w.z64;
+  sa.pold = pold;
+  sa.pnew = pnew;
   sa.q = w.q;
   sa.part = w.part;
   sa.st = w.st;
@@ -1273,9 +1280,11 @@ static int enqueue_first_passes(mpb_handle *h, cudaStream_t s, const mpb_plan *p
   return MPB_OK;
 }
 
+// it: iteration index inside the captured body (fused mode alternates the
+// two p buffers; the body holds an even number of iterations)
 static int enqueue_iteration(mpb_handle *h, cudaStream_t s, const mpb_plan *p, const mpb_csr *A,
                              const mpb_solve_options *o, const SolveWs &w, const double *b, double *x,
-                             const DistCtx *dc) {
+                             const DistCtx *dc, int it) {
   const bool high = o->kind != MPB_FIXED_LOW, low = o->kind != MPB_UNIFORM;
   const unsigned nt = static_cast<unsigned>(p->ntiles);
   const bool fused = fused_mode(p, o, dc);
@@ -1297,28 +1306,37 @@ static int enqueue_iteration(mpb_handle *h, cudaStream_t s, const mpb_plan *p, c
   }
   if ((rc = dist_step(h, dc, w.st, kStepRho, 2, s))) return rc;
   const bool pdl = dc == nullptr;
-  MPB_CUDA(launch_k(pdl, k_pupdate, persistent_grid(k_pupdate, 0, p->ntiles), kCtaThreads, 0, s,
-                    static_cast<const TileDesc *>(p->d_td), static_cast<int>(nt), static_cast<const float *>(w.z32),
-                    static_cast<const double *>(w.z64), w.p, static_cast<const SolverState *>(w.st)));
-  MPB_LAUNCHED(h);
-  if ((rc = halo_exchange(dc, w.p, 8, A->n, s))) return rc;
-  {
-    if (direct_kernels()) {
-      MPB_CUDA(launch_k(pdl, p->ks == 7 ? k_spmv_direct<7> : k_spmv_direct<kSlots>,
-                        static_cast<unsigned>(p->ntiles), kTileRows, 0, s, spmv_args(h, p, A, w)));
-    } else {
-      const uint32_t dyn = spmv_dyn_smem(p);
-      MPB_CUDA(launch_k(pdl, spmv_kernel(p), persistent_grid(spmv_kernel(p), dyn, p->ntiles, kWsThreads),
-                        kWsThreads, dyn, s, spmv_args(h, p, A, w)));
-    }
+  // fused mode: p = z + beta p_old is rebuilt inside the SpMV (no p-update
+  // kernel); p ping-pongs between two buffers
+  double *pcur = w.p;
+  SpmvArgs sa;
+  if (fused) {
+    const double *pold = (it & 1) ? w.p2 : w.p;
+    pcur = (it & 1) ? w.p : w.p2;
+    sa = spmv_args(h, p, A, w, pold, pcur);
+  } else {
+    MPB_CUDA(launch_k(pdl, k_pupdate, persistent_grid(k_pupdate, 0, p->ntiles), kCtaThreads, 0, s,
+                      static_cast<const TileDesc *>(p->d_td), static_cast<int>(nt), static_cast<const float *>(w.z32),
+                      static_cast<const double *>(w.z64), w.p, static_cast<const SolverState *>(w.st)));
+    MPB_LAUNCHED(h);
+    if ((rc = halo_exchange(dc, w.p, 8, A->n, s))) return rc;
+    sa = spmv_args(h, p, A, w);
+  }
+  if (direct_kernels()) {
+    MPB_CUDA(launch_k(pdl, p->ks == 7 ? k_spmv_direct<7> : k_spmv_direct<kSlots>, static_cast<unsigned>(p->ntiles),
+                      kTileRows, 0, s, sa));
+  } else {
+    const uint32_t dyn = spmv_dyn_smem(p);
+    MPB_CUDA(launch_k(pdl, spmv_kernel(p), persistent_grid(spmv_kernel(p), dyn, p->ntiles, kWsThreads), kWsThreads,
+                      dyn, s, sa));
   }
   MPB_LAUNCHED(h);
   if ((rc = dist_step(h, dc, w.st, kStepPq, 2, s))) return rc;
   if (fused) {
-    if (high && (rc = launch_update_first<double>(h, s, p, A, o->t, w.zA64, x, w.p, w.q, w.r, w.part, nullptr,
+    if (high && (rc = launch_update_first<double>(h, s, p, A, o->t, w.zA64, x, pcur, w.q, w.r, w.part, nullptr,
                                                   nullptr, w.st, 0)))
       return rc;
-    if (low && (rc = launch_update_first<float>(h, s, p, A, o->t, w.zA32, x, w.p, w.q, w.r, w.part,
+    if (low && (rc = launch_update_first<float>(h, s, p, A, o->t, w.zA32, x, pcur, w.q, w.r, w.part,
                                                 &w.st->ovf_count, &w.st->ovf_first, w.st, 1)))
       return rc;
   } else {
@@ -1476,7 +1494,8 @@ static int solve_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, con
   }
 
   // capture G iterations once (cached across solves with the same buffers)
-  const int G = opt->graph_iters > 0 ? opt->graph_iters : kDefaultGraphIters;
+  int G = opt->graph_iters > 0 ? opt->graph_iters : kDefaultGraphIters;
+  if (fused_mode(plan, opt, dc) && (G & 1)) G++;  // the two p buffers alternate per iteration
   GraphKey key;
   std::memset(&key, 0, sizeof(key));
   key.plan = plan;
@@ -1531,7 +1550,7 @@ static int solve_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, con
       MPB_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     }
     int crc = MPB_OK;
-    for (int i = 0; i < G && crc == MPB_OK; i++) crc = enqueue_iteration(h, s, plan, A, opt, w, b, x, dc);
+    for (int i = 0; i < G && crc == MPB_OK; i++) crc = enqueue_iteration(h, s, plan, A, opt, w, b, x, dc, i);
     cudaGraph_t captured = nullptr;
     cudaError_t ce = cudaStreamEndCapture(s, &captured);
     if (!loop) graph = captured;
@@ -1714,17 +1733,23 @@ int mpb_profile_iteration_dist(mpb_handle *h, const mpb_plan *plan, const mpb_cs
     rc = timed(slot, [&]() { return run_pass(pass); });
     if (rc) return rc;
   }
-  const SpmvArgs sa = spmv_args(h, plan, A, w);
+  // fused mode (what the solve runs when k >= 2 on a tile plan): the SpMV
+  // rebuilds p from z (no p-update kernel), the x/r update carries the next
+  // first pass
+  const bool fused = opt->k >= 2 && !plan->large && std::getenv("MPB_NO_FUSE") == nullptr;
+  const SpmvArgs sa = fused ? spmv_args(h, plan, A, w, w.p, w.p2) : spmv_args(h, plan, A, w);
   const uint32_t sdyn = spmv_dyn_smem(plan);
   const int sgrid = persistent_grid(spmv_kernel(plan), sdyn, plan->ntiles, kWsThreads);
   const int ugrid = persistent_grid(k_update, 0, plan->ntiles);
   const int pgrid = persistent_grid(k_pupdate, 0, plan->ntiles);
-  rc = timed(7, [&]() -> int {
-    k_pupdate<<<pgrid, kCtaThreads, 0, s>>>(plan->d_td, static_cast<int>(nt), w.z32, w.z64, w.p, w.st);
-    MPB_LAUNCHED(h);
-    return MPB_OK;
-  });
-  if (rc) return rc;
+  if (!fused) {
+    rc = timed(7, [&]() -> int {
+      k_pupdate<<<pgrid, kCtaThreads, 0, s>>>(plan->d_td, static_cast<int>(nt), w.z32, w.z64, w.p, w.st);
+      MPB_LAUNCHED(h);
+      return MPB_OK;
+    });
+    if (rc) return rc;
+  }
   rc = timed(3, [&]() -> int {
     spmv_kernel(plan)<<<sgrid, kWsThreads, sdyn, s>>>(sa);
     MPB_LAUNCHED(h);
@@ -1740,13 +1765,12 @@ int mpb_profile_iteration_dist(mpb_handle *h, const mpb_plan *plan, const mpb_cs
   if (rc) return rc;
   // the fused x/r update + next first pass, when the solve uses it
   h_ms[5] = 0.0;
-  const bool fused = opt->k >= 2 && !plan->large && std::getenv("MPB_NO_FUSE") == nullptr;
   if (fused) {
     rc = timed(5, [&]() -> int {
       if (branch == 0)
-        return launch_update_first<double>(h, s, plan, A, opt->t, w.zA64, x, w.p, w.q, w.r, w.part, nullptr, nullptr,
-                                           w.st, 0);
-      return launch_update_first<float>(h, s, plan, A, opt->t, w.zA32, x, w.p, w.q, w.r, w.part, &w.st->ovf_count,
+        return launch_update_first<double>(h, s, plan, A, opt->t, w.zA64, x, w.p2, w.q, w.r, w.part, nullptr,
+                                           nullptr, w.st, 0);
+      return launch_update_first<float>(h, s, plan, A, opt->t, w.zA32, x, w.p2, w.q, w.r, w.part, &w.st->ovf_count,
                                         &w.st->ovf_first, w.st, 1);
     });
     if (rc) return rc;

@@ -354,7 +354,7 @@ __device__ __forceinline__ void producer_loop(Ring &R, int ntiles, int ns, unsig
   int st = 0, rnd = 0;  // stage, and how often it has been filled before
   int next = blockIdx.x;
   for (;;) {
-    if (rnd > 0) mbar_wait(&R.empty[st], (rnd - 1) & 1);
+    if (rnd > 0) mbar_wait_sleep(&R.empty[st], (rnd - 1) & 1);
     int tile;
     if (ctr != nullptr) {
       const unsigned int v = atomicAdd(ctr, 1u);
@@ -852,19 +852,37 @@ struct SpmvArgs {
   const TileDesc *td;
   unsigned int *ctr;
   TileGeom g;
-  const double *p;  // search direction (updated in place by k_pupdate)
+  const double *p;  // search direction (k_pupdate output), or ...
+  // ... (pnew != null) p = z (first) | z + beta pold computed where it is
+  // gathered (solver.py:150-153 fused into the SpMV); own rows stored to pnew
+  const float *z32;
+  const double *z64;
+  const double *pold;
+  double *pnew;
   double *q;
   double *part;
   SolverState *st;
 };
 
-template <int KS>
+// p_j as the SpMV reads it: stored (ZT = void) or rebuilt from z (ZT = the
+// preconditioner branch's type) and the previous p -- every thread that
+// needs p_j computes the same two roundings, so all copies agree bit for bit
+template <typename ZT>
+__device__ __forceinline__ double p_at(const SpmvArgs &a, int c, bool first, double beta) {
+  if constexpr (std::is_same<ZT, void>::value) {
+    return __ldg(a.p + c);
+  } else {
+    const double zv = std::is_same<ZT, float>::value ? static_cast<double>(__ldg(a.z32 + c)) : __ldg(a.z64 + c);
+    return first ? zv : __dadd_rn(zv, __dmul_rn(beta, __ldg(a.pold + c)));
+  }
+}
+
+template <int KS, typename ZT>
 __device__ __forceinline__ void spmv_tile_body(const SpmvArgs &a, int tile, const TileDesc &d, const int *col,
                                                const double *val, const int *spp, const uint16_t *mt,
-                                               const int *s_pat, double *ws) {
+                                               const int *s_pat, double *ws, bool first, double beta) {
   const int tid = threadIdx.x;
   const int lo = d.lo, hi = d.hi, row = lo + tid;
-  const double *p = a.p;
   double prod = 0.0;
   if (row < hi) {
     const int si = (row >> 5) - d.s0;
@@ -875,12 +893,11 @@ __device__ __forceinline__ void spmv_tile_body(const SpmvArgs &a, int tile, cons
     if (m != kMetaGeneric) {
       const int *P = s_pat + meta_pid(m) * kPatStride;
       const int len = pat_len(P[0]);
-      const double *pr = p + row;
       double vv[KS], pv[KS];
 #pragma unroll
       for (int u = 0; u < KS; u++) {
         vv[u] = u < len ? val[base + 32 * u] : 0.0;
-        pv[u] = __ldg(pr + P[1 + u]);
+        pv[u] = p_at<ZT>(a, row + P[1 + u], first, beta);
       }
 #pragma unroll
       for (int u = 0; u < KS; u++)
@@ -889,11 +906,13 @@ __device__ __forceinline__ void spmv_tile_body(const SpmvArgs &a, int tile, cons
       const int width = (spp[si + 1] - sb) >> 5;
       for (int j = 0; j < width; j++) {
         const int c = col[base + 32 * j];
-        if (c >= 0) acc = __dadd_rn(acc, __dmul_rn(val[base + 32 * j], __ldg(p + c)));
+        if (c >= 0) acc = __dadd_rn(acc, __dmul_rn(val[base + 32 * j], p_at<ZT>(a, c, first, beta)));
       }
     }
     a.q[row] = acc;
-    prod = __dmul_rn(__ldg(p + row), acc);
+    const double pown = p_at<ZT>(a, row, first, beta);
+    if (!std::is_same<ZT, void>::value) a.pnew[row] = pown;
+    prod = __dmul_rn(pown, acc);
   }
   const double tot = block_tree_nb<kTileThreads>(prod, ws, kBarConsumers);
   if (tid == 0) a.part[tile] = tot;
@@ -901,6 +920,16 @@ __device__ __forceinline__ void spmv_tile_body(const SpmvArgs &a, int tile, cons
 
 __host__ __device__ inline StageLayout spmv_layout(const TileGeom &g) {
   return stage_layout(g.cap_e, 8, g.max_sl, g.cols != 0, true, 0, 0, 0);
+}
+
+// one tile of the SpMV with p stored or rebuilt (branch of the iteration)
+template <int KS>
+__device__ __forceinline__ void spmv_tile(const SpmvArgs &a, int tile, const TileDesc &d, const int *col,
+                                          const double *val, const int *spp, const uint16_t *mt, const int *s_pat,
+                                          double *ws, int mode, bool first, double beta) {
+  if (mode == 0) spmv_tile_body<KS, void>(a, tile, d, col, val, spp, mt, s_pat, ws, first, beta);
+  else if (mode == 1) spmv_tile_body<KS, float>(a, tile, d, col, val, spp, mt, s_pat, ws, first, beta);
+  else spmv_tile_body<KS, double>(a, tile, d, col, val, spp, mt, s_pat, ws, first, beta);
 }
 
 template <int KS>
@@ -915,6 +944,9 @@ __global__ void __launch_bounds__(kWsThreads) k_spmv_pq(const SpmvArgs a) {
   ring_init(R, ns);
   pdl_wait();
   if (a.st->done) return;
+  const int mode = a.pnew == nullptr ? 0 : (a.st->branch == 1 ? 1 : 2);
+  const bool first = a.st->first != 0;
+  const double beta = a.st->beta;
   if (threadIdx.x >= kConsumers) {
     if (threadIdx.x == kConsumers)
       producer_loop(R, a.g.ntiles, ns, a.ctr, [&](int st, int tile) {
@@ -931,10 +963,12 @@ __global__ void __launch_bounds__(kWsThreads) k_spmv_pq(const SpmvArgs a) {
       const unsigned char *sb = smem + st * L.bytes;
       if (R.ok[st]) {
         const int *col = (a.g.cols && d.ngen > 0) ? reinterpret_cast<const int *>(sb + L.col) : a.scol + d.e0;
-        spmv_tile_body<KS>(a, tile, d, col, reinterpret_cast<const double *>(sb + L.val),
-                       staged(sb + L.sp, a.sp, d.s0, d.s1 + 1), staged(sb + L.meta, a.meta, d.lo, d.hi), s_pat, ws);
+        spmv_tile<KS>(a, tile, d, col, reinterpret_cast<const double *>(sb + L.val),
+                      staged(sb + L.sp, a.sp, d.s0, d.s1 + 1), staged(sb + L.meta, a.meta, d.lo, d.hi), s_pat, ws,
+                      mode, first, beta);
       } else {
-        spmv_tile_body<KS>(a, tile, d, a.scol + d.e0, a.sval + d.e0, a.sp + d.s0, a.meta + d.lo, s_pat, ws);
+        spmv_tile<KS>(a, tile, d, a.scol + d.e0, a.sval + d.e0, a.sp + d.s0, a.meta + d.lo, s_pat, ws, mode, first,
+                      beta);
       }
       ring_release(R, st);
     }
@@ -950,7 +984,8 @@ __global__ void __launch_bounds__(kTileRows) k_spmv_direct(const SpmvArgs a) {
   if (a.st->done) return;
   const int tile = blockIdx.x;
   const TileDesc d = a.td[tile];
-  spmv_tile_body<KS>(a, tile, d, a.scol + d.e0, a.sval + d.e0, a.sp + d.s0, a.meta + d.lo, a.pat, ws);
+  spmv_tile<KS>(a, tile, d, a.scol + d.e0, a.sval + d.e0, a.sp + d.s0, a.meta + d.lo, a.pat, ws,
+                a.pnew == nullptr ? 0 : (a.st->branch == 1 ? 1 : 2), a.st->first != 0, a.st->beta);
   pdl_trigger();
   finish_grid(a.st, 1, kStepPq, a.part, a.g.ntiles, ws);
 }
