@@ -224,12 +224,6 @@ cudaError_t launch_k(bool pdl, void (*kernel)(KArgs...), unsigned grid, unsigned
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
-// MPB_DIRECT=1: one CTA per tile, no TMA ring (experiment)
-inline bool direct_kernels() {
-  static const bool on = std::getenv("MPB_DIRECT") != nullptr;
-  return on;
-}
-
 // Buffers one preconditioner application needs besides r and z.
 template <typename T>
 struct ApplyBufs {
@@ -244,12 +238,6 @@ int launch_tile_kernel(mpb_handle *h, cudaStream_t s, const mpb_plan *p, PassArg
     a.ib_sp = p->d_ib_sp;
     a.ib_col = p->d_ib_col;
     a.g.cap_e = std::min(p->max_tile_ib, kStageCap);
-  }
-  if (direct_kernels()) {
-    MPB_CUDA(launch_k(a.pdl != 0, k_bjac_direct<T, F, L, R64, KS>, static_cast<unsigned>(p->ntiles), kTileRows, 0,
-                      s, a));
-    MPB_LAUNCHED(h);
-    return MPB_OK;
   }
   const StageLayout Ls = bjac_layout<T, F, R64>(a.g);
   a.g.ns = pick_stages(k_bjac_tile<T, F, L, R64, KS>, Ls.bytes);
@@ -423,12 +411,6 @@ int launch_update_first(mpb_handle *h, cudaStream_t s, const mpb_plan *p, const 
   a.st = st;
   a.want_branch = want_branch;
   a.gate = 2;
-  if (direct_kernels()) {
-    MPB_CUDA(launch_k(true, k_update_first_direct<T>, static_cast<unsigned>(p->ntiles), kTileRows, 0, s, a, x, pv,
-                      q, r));
-    MPB_LAUNCHED(h);
-    return MPB_OK;
-  }
   const StageLayout L = update_first_layout<T>(a.g);
   a.g.ns = pick_stages(k_update_first<T>, L.bytes);
   const uint32_t dyn = a.g.ns * L.bytes;
@@ -1322,10 +1304,7 @@ static int enqueue_iteration(mpb_handle *h, cudaStream_t s, const mpb_plan *p, c
     if ((rc = halo_exchange(dc, w.p, 8, A->n, s))) return rc;
     sa = spmv_args(h, p, A, w);
   }
-  if (direct_kernels()) {
-    MPB_CUDA(launch_k(pdl, p->ks == 7 ? k_spmv_direct<7> : k_spmv_direct<kSlots>, static_cast<unsigned>(p->ntiles),
-                      kTileRows, 0, s, sa));
-  } else {
+  {
     const uint32_t dyn = spmv_dyn_smem(p);
     MPB_CUDA(launch_k(pdl, spmv_kernel(p), persistent_grid(spmv_kernel(p), dyn, p->ntiles, kWsThreads), kWsThreads,
                       dyn, s, sa));

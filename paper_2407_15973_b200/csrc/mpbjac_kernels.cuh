@@ -38,8 +38,10 @@
 namespace mpb {
 
 constexpr int kSlots = 9;                      // register-resident row entries (stencils, 3-T rows)
-constexpr int kConsumers = kCtaThreads;        // compute threads (one per tile row)
-constexpr int kWsThreads = kCtaThreads + 32;   // + one TMA producer warp
+constexpr int kRowsPerThread = 1;              // tile rows per consumer thread (2 measured slower: fewer warps per SM)
+constexpr int kConsumers = kCtaThreads / kRowsPerThread;  // compute threads of the warp-specialised kernels
+constexpr int kWsThreads = kConsumers + 32;    // + one TMA producer warp
+static_assert(kWsThreads >= kFinThreads, "the last CTA's fin_sum uses kFinThreads threads");
 constexpr int kMaxStages = 4;
 constexpr int kBarConsumers = 1;               // named barrier id among consumers
 constexpr uint16_t kMetaGeneric = 0xFFFFu;
@@ -501,139 +503,228 @@ __device__ __forceinline__ T generic_row_sweep(const PassArgs<T> &a, const TileD
 // One tile of a fused (non-first-only) pass, consumer threads only.  col /
 // val / spp / mt are the shared stage or the global arrays offset to the
 // tile (same indexing); r64t / rTt the tile's residual slice.
+// ---- pass bodies: one consumer thread owns rows tid and tid + kConsumers ----
+// (kRowsPerThread rows per thread halve the per-tile instruction overhead
+// and give each thread two independent dependency chains; the tile sums keep
+// the 256-lane order of include/mpbjac_order.h: value k of thread t is lane
+// t + k * kConsumers.)
+
+// Tile sum of kRowsPerThread values per consumer thread in the fixed order:
+// virtual lane t + k kConsumers, virtual warps butterfly, warp 0 butterflies
+// the kTileThreads/32 warp sums padded with +0.  Result valid in thread 0.
+template <typename R>
+__device__ __forceinline__ R tile_tree_rows(const R (&v)[kRowsPerThread], R *ws, int bar) {
+  constexpr int kWarps = kConsumers / 32;
+  static_assert(kConsumers * kRowsPerThread == kTileThreads, "tile lanes");
+  R s[kRowsPerThread];
+#pragma unroll
+  for (int k = 0; k < kRowsPerThread; k++) s[k] = warp_bfly(v[k]);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  named_sync(bar, kConsumers);
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < kRowsPerThread; k++) ws[warp + k * kWarps] = s[k];
+  }
+  named_sync(bar, kConsumers);
+  R r = R(0);
+  if (warp == 0) {
+    r = lane < kTileThreads / 32 ? ws[lane] : R(0);
+    r = warp_bfly(r);
+  }
+  return r;
+}
+
 // KS: slots of the longest row pattern (compile time, 7 for 7-point stencils);
 // table entries past a pattern's length are 0, so gathers need no predicate.
+template <typename T>
+struct PassRow {
+  T res, dd, w, zown;
+  const int *P;  // pattern row
+  int base, width, i0, i1;  // SELL slot of the row; in-block slots [i0, i1)
+  uint16_t m;
+  bool valid;
+};
+
+// A pass up to its first inner sweep for one row: res = r - A z_in (all
+// slots, stored order), d, w = res / d (written to the tile's s_w).
+template <typename T, bool FIRST, int KS>
+__device__ __forceinline__ void pass_row_init(PassRow<T> &q, const PassArgs<T> &a, const TileDesc &d, int tid,
+                                              const int *col, const T *val, const int *spp, const uint16_t *mt,
+                                              const double *r64t, const T *rTt, const int *s_pat, T *s_w) {
+  const int row = d.lo + tid;
+  q.res = T(0);
+  q.dd = T(1);
+  q.w = T(0);
+  q.zown = T(0);
+  q.P = s_pat;
+  q.base = q.width = q.i0 = q.i1 = 0;
+  q.m = kMetaGeneric;
+  q.valid = row < d.hi;
+  if (!q.valid) return;
+  const int si = (row >> 5) - d.s0;
+  const int sb = spp[si];
+  q.width = (spp[si + 1] - sb) >> 5;
+  q.base = sb - d.e0 + (row & 31);
+  q.m = mt[tid];
+  const T rv = r64t != nullptr ? narrow_checked(a, r64t[tid], row, FIRST) : rTt[tid];
+  const T *zr = FIRST ? nullptr : a.zin + row;
+  if (!FIRST) q.zown = __ldg(zr);
+  if (q.m != kMetaGeneric) {
+    q.P = s_pat + meta_pid(q.m) * kPatStride;
+    const int hdr = q.P[0], len = pat_len(hdr);
+    q.i0 = meta_i0(q.m);
+    q.i1 = meta_i1(q.m);
+    T az = T(0);
+    if (!FIRST) {
+      T v[KS], g[KS];
+#pragma unroll
+      for (int u = 0; u < KS; u++) {
+        v[u] = u < len ? val[q.base + 32 * u] : T(0);
+        g[u] = __ldg(zr + q.P[1 + u]);
+      }
+#pragma unroll
+      for (int u = 0; u < KS; u++)
+        if (u < len) az = add_rn(az, mul_rn(v[u], g[u]));
+    }
+    q.dd = val[q.base + 32 * pat_dpos(hdr)];
+    q.res = FIRST ? rv : sub_rn(rv, az);
+  } else {
+    q.res = generic_row_scan<T, FIRST>(a, row, q.base, q.width, col, val, rv, q.dd);
+  }
+  q.w = div_rn(q.res, q.dd);
+  s_w[tid] = q.w;
+}
+
+// A_b w over the row's in-block entries (one inner sweep's sum)
+template <typename T>
+__device__ __forceinline__ T pass_row_sweep(const PassRow<T> &q, const PassArgs<T> &a, const TileDesc &d, int tid,
+                                            const int *col, const T *val, const T *s_w) {
+  T acc = T(0);
+  if (!q.valid) return acc;
+  if (q.m != kMetaGeneric) {
+#pragma unroll 1
+    for (int j = q.i0; j < q.i1; j++) acc = add_rn(acc, mul_rn(val[q.base + 32 * j], s_w[tid + q.P[1 + j]]));
+  } else {
+    acc = generic_row_sweep(a, d, d.lo + tid, q.base, q.width, col, val, s_w);
+  }
+  return acc;
+}
+
+// One tile of a fused (non-first-only) pass, consumer threads only.  col /
+// val / spp / mt are the shared stage or the global arrays offset to the
+// tile (same indexing); r64t / rTt the tile's residual slice.
 template <typename T, bool FIRST, bool LAST, int KS>
 __device__ __forceinline__ void bjac_tile_body(const PassArgs<T> &a, int tile, const TileDesc &d, const int *col,
                                                const T *val, const int *spp, const uint16_t *mt, const double *r64t,
                                                const T *rTt, const int *s_pat, T *s_w, double *ws) {
-  const int tid = threadIdx.x;
-  const int lo = d.lo, hi = d.hi, row = lo + tid;
-  const bool valid = row < hi;
-  T res = T(0), dd = T(1), w = T(0), zown = T(0);
-  uint16_t m = kMetaGeneric;
-  int base = 0, width = 0;
-  const int *P = s_pat;
-  int i0 = 0, i1 = 0;  // in-block slots [i0, i1)
-  if (valid) {
-    const int si = (row >> 5) - d.s0;
-    const int sb = spp[si];
-    width = (spp[si + 1] - sb) >> 5;
-    base = sb - d.e0 + (row & 31);
-    m = mt[tid];
-    const T rv = r64t != nullptr ? narrow_checked(a, r64t[tid], row, FIRST) : rTt[tid];
-    const T *zr = FIRST ? nullptr : a.zin + row;
-    if (!FIRST) zown = __ldg(zr);
-    if (m != kMetaGeneric) {
-      P = s_pat + meta_pid(m) * kPatStride;
-      const int hdr = P[0], len = pat_len(hdr);
-      i0 = meta_i0(m);
-      i1 = meta_i1(m);
-      T az = T(0);
-      if (!FIRST) {  // az = A z_in, all slots, stored (ascending column) order
-        T v[KS], g[KS];
+  PassRow<T> q[kRowsPerThread];
 #pragma unroll
-        for (int u = 0; u < KS; u++) {
-          v[u] = u < len ? val[base + 32 * u] : T(0);
-          g[u] = __ldg(zr + P[1 + u]);
-        }
-#pragma unroll
-        for (int u = 0; u < KS; u++)
-          if (u < len) az = add_rn(az, mul_rn(v[u], g[u]));
-      }
-      dd = val[base + 32 * pat_dpos(hdr)];
-      res = FIRST ? rv : sub_rn(rv, az);
-    } else {
-      res = generic_row_scan<T, FIRST>(a, row, base, width, col, val, rv, dd);
-    }
-    w = div_rn(res, dd);
-    s_w[tid] = w;
-  }
+  for (int k = 0; k < kRowsPerThread; k++)
+    pass_row_init<T, FIRST, KS>(q[k], a, d, threadIdx.x + k * kConsumers, col, val, spp, mt, r64t, rTt, s_pat, s_w);
   for (int s = 1; s < a.t; s++) {  // inner sweeps, the tile's w in shared memory
     named_sync(kBarConsumers, kConsumers);
-    T acc = T(0);
-    if (valid) {
-      if (m != kMetaGeneric) {
-#pragma unroll 1
-        for (int j = i0; j < i1; j++) acc = add_rn(acc, mul_rn(val[base + 32 * j], s_w[tid + P[1 + j]]));
-      } else {
-        acc = generic_row_sweep(a, d, row, base, width, col, val, s_w);
-      }
-    }
+    T acc[kRowsPerThread];
+#pragma unroll
+    for (int k = 0; k < kRowsPerThread; k++)
+      acc[k] = pass_row_sweep(q[k], a, d, threadIdx.x + k * kConsumers, col, val, s_w);
     named_sync(kBarConsumers, kConsumers);
-    if (valid) {
-      w = add_rn(w, div_rn(sub_rn(res, acc), dd));
-      s_w[tid] = w;
+#pragma unroll
+    for (int k = 0; k < kRowsPerThread; k++) {
+      if (!q[k].valid) continue;
+      q[k].w = add_rn(q[k].w, div_rn(sub_rn(q[k].res, acc[k]), q[k].dd));
+      s_w[threadIdx.x + k * kConsumers] = q[k].w;
     }
   }
-  double prod = 0.0;
-  if (valid) {
-    const T zo = FIRST ? w : add_rn(zown, w);
+  double prod[kRowsPerThread];
+#pragma unroll
+  for (int k = 0; k < kRowsPerThread; k++) {
+    prod[k] = 0.0;
+    if (!q[k].valid) continue;
+    const int tid = threadIdx.x + k * kConsumers, row = d.lo + tid;
+    const T zo = FIRST ? q[k].w : add_rn(q[k].zown, q[k].w);
     if (a.zout != nullptr) a.zout[row] = zo;
     if (a.zout64 != nullptr) a.zout64[row] = static_cast<double>(zo);
-    if (LAST && a.part != nullptr) prod = __dmul_rn(r64t[tid], static_cast<double>(zo));
+    if (LAST && a.part != nullptr) prod[k] = __dmul_rn(r64t[tid], static_cast<double>(zo));
   }
   if (LAST && a.part != nullptr) {
-    const double tot = block_tree_nb<kTileThreads>(prod, ws, kBarConsumers);
-    if (tid == 0) a.part[tile] = tot;
+    const double tot = tile_tree_rows(prod, ws, kBarConsumers);
+    if (threadIdx.x == 0) a.part[tile] = tot;
   }
 }
 
 // First pass of a tile: z1 = D_b^{-1} r (bjac.py:134-136), reading only the
 // in-block entries (plan's in-block SELL): y = r / d, then t-1 sweeps
 // y += (r - A_b y) / d over the in-block entries in ascending column order.
-// res: the row's residual in T (valid rows).
+// res[k]: row tid + k kConsumers's residual in T (valid rows).
 template <typename T>
 __device__ __forceinline__ void bjac_first_body(const PassArgs<T> &a, const TileDesc &d, const int *col,
-                                                const T *val, const int *spp, const uint16_t *mt, T res,
-                                                const int *s_pat, T *s_w) {
-  const int tid = threadIdx.x;
-  const int lo = d.lo, hi = d.hi, row = lo + tid;
-  const bool valid = row < hi;
-  T dd = T(1), w = T(0);
-  uint16_t m = kMetaGeneric;
-  int base = 0, nib = 0;
-  const int *P = s_pat;  // pattern row: offsets of its in-block slots
-  if (valid) {
+                                                const T *val, const int *spp, const uint16_t *mt,
+                                                const T (&res)[kRowsPerThread], const int *s_pat, T *s_w) {
+  T dd[kRowsPerThread], w[kRowsPerThread];
+  const int *P[kRowsPerThread];
+  int base[kRowsPerThread], nib[kRowsPerThread];
+  bool pat[kRowsPerThread], valid[kRowsPerThread];
+#pragma unroll
+  for (int k = 0; k < kRowsPerThread; k++) {
+    const int tid = threadIdx.x + k * kConsumers, row = d.lo + tid;
+    dd[k] = T(1);
+    w[k] = T(0);
+    P[k] = s_pat;
+    base[k] = nib[k] = 0;
+    pat[k] = true;
+    valid[k] = row < d.hi;
+    if (!valid[k]) continue;
     const int si = (row >> 5) - d.s0;
     const int sb = spp[si];
-    const int iwidth = (spp[si + 1] - sb) >> 5;
-    base = sb - d.ie0 + (row & 31);
-    m = mt[tid];
-    if (m != kMetaGeneric) {
+    base[k] = sb - d.ie0 + (row & 31);
+    const uint16_t m = mt[tid];
+    pat[k] = m != kMetaGeneric;
+    if (pat[k]) {
       const int i0 = meta_i0(m);
-      nib = meta_i1(m) - i0;
-      dd = val[base + 32 * (pat_dpos(s_pat[meta_pid(m) * kPatStride]) - i0)];
-      P = s_pat + meta_pid(m) * kPatStride + 1 + i0;
+      nib[k] = meta_i1(m) - i0;
+      dd[k] = val[base[k] + 32 * (pat_dpos(s_pat[meta_pid(m) * kPatStride]) - i0)];
+      P[k] = s_pat + meta_pid(m) * kPatStride + 1 + i0;
     } else {
+      const int iwidth = (spp[si + 1] - sb) >> 5;
       for (int j = 0; j < iwidth; j++) {
-        const int cc = col[base + 32 * j];
+        const int cc = col[base[k] + 32 * j];
         if (cc < 0) break;
-        nib = j + 1;
-        if (cc == row) dd = val[base + 32 * j];
+        nib[k] = j + 1;
+        if (cc == row) dd[k] = val[base[k] + 32 * j];
       }
     }
-    w = div_rn(res, dd);
-    s_w[tid] = w;
+    w[k] = div_rn(res[k], dd[k]);
+    s_w[tid] = w[k];
   }
   for (int s = 1; s < a.t; s++) {
     named_sync(kBarConsumers, kConsumers);
-    T acc = T(0);
-    if (m != kMetaGeneric) {
+    T acc[kRowsPerThread];
+#pragma unroll
+    for (int k = 0; k < kRowsPerThread; k++) {
+      const int tid = threadIdx.x + k * kConsumers;
+      acc[k] = T(0);
+      if (pat[k]) {
 #pragma unroll 1
-      for (int j = 0; j < nib; j++) acc = add_rn(acc, mul_rn(val[base + 32 * j], s_w[tid + P[j]]));
-    } else {
-      for (int j = 0; j < nib; j++) acc = add_rn(acc, mul_rn(val[base + 32 * j], s_w[col[base + 32 * j] - lo]));
+        for (int j = 0; j < nib[k]; j++) acc[k] = add_rn(acc[k], mul_rn(val[base[k] + 32 * j], s_w[tid + P[k][j]]));
+      } else {
+        for (int j = 0; j < nib[k]; j++)
+          acc[k] = add_rn(acc[k], mul_rn(val[base[k] + 32 * j], s_w[col[base[k] + 32 * j] - d.lo]));
+      }
     }
     named_sync(kBarConsumers, kConsumers);
-    if (valid) {
-      w = add_rn(w, div_rn(sub_rn(res, acc), dd));
-      s_w[tid] = w;
+#pragma unroll
+    for (int k = 0; k < kRowsPerThread; k++) {
+      if (!valid[k]) continue;
+      w[k] = add_rn(w[k], div_rn(sub_rn(res[k], acc[k]), dd[k]));
+      s_w[threadIdx.x + k * kConsumers] = w[k];
     }
   }
-  if (valid) {
-    if (a.zout != nullptr) a.zout[row] = w;
-    if (a.zout64 != nullptr) a.zout64[row] = static_cast<double>(w);
+#pragma unroll
+  for (int k = 0; k < kRowsPerThread; k++) {
+    if (!valid[k]) continue;
+    const int row = d.lo + threadIdx.x + k * kConsumers;
+    if (a.zout != nullptr) a.zout[row] = w[k];
+    if (a.zout64 != nullptr) a.zout64[row] = static_cast<double>(w[k]);
   }
 }
 
@@ -682,11 +773,14 @@ __global__ void __launch_bounds__(kWsThreads) k_bjac_tile(const PassArgs<T> a) {
       const bool scols = ok && a.g.cols && d.ngen > 0;
       if (kIB) {
         const int *col = scols ? reinterpret_cast<const int *>(sb + L.col) : a.ib_col + d.ie0;
-        const int row = d.lo + static_cast<int>(threadIdx.x);
-        T rv = T(0);
-        if (row < d.hi) {
-          if (R64) rv = narrow_checked(a, ok ? staged(sb + L.v0, a.r64, d.lo, d.hi)[threadIdx.x] : a.r64[row], row, true);
-          else rv = ok ? staged(sb + L.v0, a.rT, d.lo, d.hi)[threadIdx.x] : a.rT[row];
+        T rv[kRowsPerThread];
+#pragma unroll
+        for (int k = 0; k < kRowsPerThread; k++) {
+          const int tid = threadIdx.x + k * kConsumers, row = d.lo + tid;
+          rv[k] = T(0);
+          if (row >= d.hi) continue;
+          if (R64) rv[k] = narrow_checked(a, ok ? staged(sb + L.v0, a.r64, d.lo, d.hi)[tid] : a.r64[row], row, true);
+          else rv[k] = ok ? staged(sb + L.v0, a.rT, d.lo, d.hi)[tid] : a.rT[row];
         }
         if (ok) {
           bjac_first_body<T>(a, d, col, reinterpret_cast<const T *>(sb + L.val),
@@ -699,41 +793,18 @@ __global__ void __launch_bounds__(kWsThreads) k_bjac_tile(const PassArgs<T> a) {
         const int *col = scols ? reinterpret_cast<const int *>(sb + L.col) : a.scol + d.e0;
         if (ok) {
           bjac_tile_body<T, FIRST, LAST, KS>(a, tile, d, col, reinterpret_cast<const T *>(sb + L.val),
-                                         staged(sb + L.sp, a.sp, d.s0, d.s1 + 1),
-                                         staged(sb + L.meta, a.meta, d.lo, d.hi),
-                                         R64 ? staged(sb + L.v0, a.r64, d.lo, d.hi) : nullptr,
-                                         R64 ? nullptr : staged(sb + L.v0, a.rT, d.lo, d.hi), s_pat, s_w, ws);
+                                             staged(sb + L.sp, a.sp, d.s0, d.s1 + 1),
+                                             staged(sb + L.meta, a.meta, d.lo, d.hi),
+                                             R64 ? staged(sb + L.v0, a.r64, d.lo, d.hi) : nullptr,
+                                             R64 ? nullptr : staged(sb + L.v0, a.rT, d.lo, d.hi), s_pat, s_w, ws);
         } else {
           bjac_tile_body<T, FIRST, LAST, KS>(a, tile, d, col, a.sval + d.e0, a.sp + d.s0, a.meta + d.lo,
-                                         R64 ? a.r64 + d.lo : nullptr, R64 ? nullptr : a.rT + d.lo, s_pat, s_w,
-                                         ws);
+                                             R64 ? a.r64 + d.lo : nullptr, R64 ? nullptr : a.rT + d.lo, s_pat, s_w,
+                                             ws);
         }
       }
       ring_release(R, st);
     }
-  }
-  pdl_trigger();  // dependents may launch into the SMs this grid drains
-  if (LAST && a.part != nullptr) finish_grid(a.st, 0, kStepRho, a.part, a.g.ntiles, ws);
-}
-
-// One CTA per tile, no TMA ring: the same tile bodies on global pointers;
-// the hardware CTA scheduler keeps many tiles per SM in flight.
-template <typename T, bool FIRST, bool LAST, bool R64, int KS>
-__global__ void __launch_bounds__(kTileRows) k_bjac_direct(const PassArgs<T> a) {
-  __shared__ T s_w[kTileRows];
-  __shared__ double ws[32];
-  pdl_wait();
-  if (gated_off(a)) return;
-  const int tile = blockIdx.x;
-  const TileDesc d = a.td[tile];
-  if (FIRST && !LAST) {
-    const int row = d.lo + static_cast<int>(threadIdx.x);
-    T rv = T(0);
-    if (row < d.hi) rv = R64 ? narrow_checked(a, a.r64[row], row, true) : a.rT[row];
-    bjac_first_body<T>(a, d, a.ib_col + d.ie0, a.ib_val + d.ie0, a.ib_sp + d.s0, a.meta + d.lo, rv, a.pat, s_w);
-  } else {
-    bjac_tile_body<T, FIRST, LAST, KS>(a, tile, d, a.scol + d.e0, a.sval + d.e0, a.sp + d.s0, a.meta + d.lo,
-                                       R64 ? a.r64 + d.lo : nullptr, R64 ? nullptr : a.rT + d.lo, a.pat, s_w, ws);
   }
   pdl_trigger();  // dependents may launch into the SMs this grid drains
   if (LAST && a.part != nullptr) finish_grid(a.st, 0, kStepRho, a.part, a.g.ntiles, ws);
@@ -881,10 +952,12 @@ template <int KS, typename ZT>
 __device__ __forceinline__ void spmv_tile_body(const SpmvArgs &a, int tile, const TileDesc &d, const int *col,
                                                const double *val, const int *spp, const uint16_t *mt,
                                                const int *s_pat, double *ws, bool first, double beta) {
-  const int tid = threadIdx.x;
-  const int lo = d.lo, hi = d.hi, row = lo + tid;
-  double prod = 0.0;
-  if (row < hi) {
+  double prod[kRowsPerThread];
+#pragma unroll
+  for (int k = 0; k < kRowsPerThread; k++) {
+    const int tid = threadIdx.x + k * kConsumers, row = d.lo + tid;
+    prod[k] = 0.0;
+    if (row >= d.hi) continue;
     const int si = (row >> 5) - d.s0;
     const int sb = spp[si];
     const int base = sb - d.e0 + (row & 31);
@@ -912,10 +985,10 @@ __device__ __forceinline__ void spmv_tile_body(const SpmvArgs &a, int tile, cons
     a.q[row] = acc;
     const double pown = p_at<ZT>(a, row, first, beta);
     if (!std::is_same<ZT, void>::value) a.pnew[row] = pown;
-    prod = __dmul_rn(pown, acc);
+    prod[k] = __dmul_rn(pown, acc);
   }
-  const double tot = block_tree_nb<kTileThreads>(prod, ws, kBarConsumers);
-  if (tid == 0) a.part[tile] = tot;
+  const double tot = tile_tree_rows(prod, ws, kBarConsumers);
+  if (threadIdx.x == 0) a.part[tile] = tot;
 }
 
 __host__ __device__ inline StageLayout spmv_layout(const TileGeom &g) {
@@ -973,19 +1046,6 @@ __global__ void __launch_bounds__(kWsThreads) k_spmv_pq(const SpmvArgs a) {
       ring_release(R, st);
     }
   }
-  pdl_trigger();
-  finish_grid(a.st, 1, kStepPq, a.part, a.g.ntiles, ws);
-}
-
-template <int KS>
-__global__ void __launch_bounds__(kTileRows) k_spmv_direct(const SpmvArgs a) {
-  __shared__ double ws[32];
-  pdl_wait();
-  if (a.st->done) return;
-  const int tile = blockIdx.x;
-  const TileDesc d = a.td[tile];
-  spmv_tile<KS>(a, tile, d, a.scol + d.e0, a.sval + d.e0, a.sp + d.s0, a.meta + d.lo, a.pat, ws,
-                a.pnew == nullptr ? 0 : (a.st->branch == 1 ? 1 : 2), a.st->first != 0, a.st->beta);
   pdl_trigger();
   finish_grid(a.st, 1, kStepPq, a.part, a.g.ntiles, ws);
 }
@@ -1089,11 +1149,14 @@ __global__ void __launch_bounds__(kWsThreads) k_update_first(const PassArgs<T> a
       const TileDesc d = R.desc[st];
       const unsigned char *sb = smem + st * L.bytes;
       const bool ok = R.ok[st] != 0;
-      const int row = d.lo + static_cast<int>(threadIdx.x);
-      double sq = 0.0;
-      T rv = T(0);
-      if (row < d.hi) {
-        const int i = threadIdx.x;
+      double sq[kRowsPerThread];
+      T rv[kRowsPerThread];
+#pragma unroll
+      for (int k = 0; k < kRowsPerThread; k++) {
+        const int i = threadIdx.x + k * kConsumers, row = d.lo + i;
+        sq[k] = 0.0;
+        rv[k] = T(0);
+        if (row >= d.hi) continue;
         const double xv = ok ? staged(sb + L.v1, x, d.lo, d.hi)[i] : x[row];
         const double pv = ok ? staged(sb + L.v2, p, d.lo, d.hi)[i] : p[row];
         const double qv = ok ? staged(sb + L.v3, q, d.lo, d.hi)[i] : q[row];
@@ -1101,10 +1164,10 @@ __global__ void __launch_bounds__(kWsThreads) k_update_first(const PassArgs<T> a
         x[row] = __dadd_rn(xv, __dmul_rn(alpha, pv));
         const double rn = __dsub_rn(ro, __dmul_rn(alpha, qv));
         r[row] = rn;
-        sq = __dmul_rn(rn, rn);
-        rv = narrow_checked(a, rn, row, true);
+        sq[k] = __dmul_rn(rn, rn);
+        rv[k] = narrow_checked(a, rn, row, true);
       }
-      const double tot = block_tree_nb<kTileThreads>(sq, ws, kBarConsumers);
+      const double tot = tile_tree_rows(sq, ws, kBarConsumers);
       if (threadIdx.x == 0) a.part[tile] = tot;
       const bool scols = ok && a.g.cols && d.ngen > 0;
       const int *col = scols ? reinterpret_cast<const int *>(sb + L.col) : a.ib_col + d.ie0;
@@ -1117,34 +1180,6 @@ __global__ void __launch_bounds__(kWsThreads) k_update_first(const PassArgs<T> a
       ring_release(R, st);
     }
   }
-  pdl_trigger();
-  finish_grid(a.st, 2, kStepRrZ, a.part, a.g.ntiles, ws);
-}
-
-template <typename T>
-__global__ void __launch_bounds__(kTileRows) k_update_first_direct(const PassArgs<T> a, double *x, const double *p,
-                                                                     const double *q, double *r) {
-  __shared__ T s_w[kTileRows];
-  __shared__ double ws[32];
-  pdl_wait();
-  if (gated_off(a)) return;
-  const double alpha = a.st->alpha;
-  const int tile = blockIdx.x;
-  const TileDesc d = a.td[tile];
-  const int row = d.lo + static_cast<int>(threadIdx.x);
-  double sq = 0.0;
-  T rv = T(0);
-  if (row < d.hi) {
-    const double xv = x[row], pv = p[row], qv = q[row], ro = r[row];
-    x[row] = __dadd_rn(xv, __dmul_rn(alpha, pv));
-    const double rn = __dsub_rn(ro, __dmul_rn(alpha, qv));
-    r[row] = rn;
-    sq = __dmul_rn(rn, rn);
-    rv = narrow_checked(a, rn, row, true);
-  }
-  const double tot = block_tree_nb<kTileThreads>(sq, ws, kBarConsumers);
-  if (threadIdx.x == 0) a.part[tile] = tot;
-  bjac_first_body<T>(a, d, a.ib_col + d.ie0, a.ib_val + d.ie0, a.ib_sp + d.s0, a.meta + d.lo, rv, a.pat, s_w);
   pdl_trigger();
   finish_grid(a.st, 2, kStepRrZ, a.part, a.g.ntiles, ws);
 }
