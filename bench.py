@@ -241,7 +241,7 @@ def run_b200(args, world, rank, local):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    cs = problems.make_config(args.config)
+    cs = problems.make_config(args.config, device=True)   # GPU-side assembly (bit-identical)
     policy = args.policy or cs.policies[0]
     part = BlockPartition.fixed_size(cs.A.n, cs.block_rows)
     pp = PrecisionPolicy.parse(policy)

@@ -308,6 +308,22 @@ int mpb_profile_iteration_dist(mpb_handle *h, const mpb_plan *plan, const mpb_cs
                                int64_t workspace_bytes, int branch, int reps,
                                double *h_ms);
 
+/* ---- GPU-side problem assembly (setup; problems.py restated) ------------- */
+/* Entries of the 7-point finite-volume operator on an n^3 grid (7 n^3 - 6 n^2). */
+int64_t mpb_stencil_nnz(int64_t n);
+/* The operator of problems.py diffusion_matrix / stencil_csr from a device
+ * cell field kappa (n^3, x fastest): rows in order, entries zm ym xm diag xp
+ * yp zp, interior faces w*2ab/(a+b), boundary faces w*kappa, off-diagonals
+ * -(face*scale), diagonal ((((xm+xp)+ym)+yp)+zm)+zp)*scale.  Bit-identical
+ * to the host generator.  row_ptr (n^3+1), col_idx, values: device. */
+int mpb_assemble_stencil(mpb_handle *h, int64_t n, const double *kappa,
+                         double wx, double wy, double wz, double scale,
+                         int32_t *row_ptr, int32_t *col_idx, double *values);
+/* a * u_i + b for the first count SplitMix64 uniforms of seed
+ * (problems.py splitmix64_stream; a = 1, b = 0: the stream itself). */
+int mpb_splitmix64_uniform(mpb_handle *h, uint64_t seed, int64_t count,
+                           double a, double b, double *out);
+
 /* ||b - A x|| / r0_norm in device order.  Synchronous. */
 int mpb_true_relres(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A,
                     const double *x, const double *b, double r0_norm,

@@ -39,7 +39,8 @@ EXPORTED = (
     "mpb_plan_bind_sell", "mpb_plan_inblock_nnz", "mpb_plan_pack_inblock_f64",
     "mpb_plan_pack_inblock_f32", "mpb_comm_unique_id", "mpb_comm_create",
     "mpb_comm_destroy", "mpb_solve_workspace_bytes_dist", "mpb_pcg_solve_dist",
-    "mpb_profile_iteration_dist", "mpb_plan_layout_info",
+    "mpb_profile_iteration_dist", "mpb_plan_layout_info", "mpb_stencil_nnz",
+    "mpb_assemble_stencil", "mpb_splitmix64_uniform",
 )
 
 
@@ -100,6 +101,10 @@ def _declare(L):
         "mpb_plan_destroy": ([_P], C.c_int),
         "mpb_plan_info": ([_P, _I64P, C.POINTER(C.c_int), _I64P], C.c_int),
         "mpb_plan_layout_info": ([_P, C.POINTER(C.c_int), _I64P], C.c_int),
+        "mpb_stencil_nnz": ([_I64], C.c_int64),
+        "mpb_assemble_stencil": ([_P, _I64, _P, C.c_double, C.c_double, C.c_double, C.c_double, _P, _P, _P],
+                                 C.c_int),
+        "mpb_splitmix64_uniform": ([_P, C.c_uint64, _I64, C.c_double, C.c_double, _P], C.c_int),
         "mpb_csr_matvec_f64": ([_P, _I64, _P, _P, _P, _P, _P], C.c_int),
         "mpb_csr_matvec_f32": ([_P, _I64, _P, _P, _P, _P, _P], C.c_int),
         "mpb_block_jacobi_sweeps_f64": ([_P, _P, _P, _P, _P, _P, C.c_int, _P, _P, _P, _I64, _I64], C.c_int),

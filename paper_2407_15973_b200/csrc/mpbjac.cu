@@ -789,6 +789,29 @@ int mpb_plan_info(const mpb_plan *p, int64_t *h_ntiles, int *h_large, int64_t *h
   return MPB_OK;
 }
 
+// ---- GPU-side problem assembly -------------------------------------------
+int64_t mpb_stencil_nnz(int64_t n) { return n < 2 ? (n == 1 ? 1 : 0) : stencil_row_ptr(n * n * n, n); }
+
+int mpb_assemble_stencil(mpb_handle *h, int64_t n, const double *kappa, double wx, double wy, double wz,
+                         double scale, int32_t *row_ptr, int32_t *col_idx, double *values) {
+  if (!h || n < 2 || !kappa || !row_ptr || !col_idx || !values) return MPB_ERR_ARG;
+  if (n * n * n >= (int64_t(1) << 31) - 1 || mpb_stencil_nnz(n) >= (int64_t(1) << 31)) return MPB_ERR_INDEX32;
+  MPB_CUDA(cudaSetDevice(h->device));
+  k_stencil<<<elt_blocks(n * n * n), kEltThreads, 0, h->user>>>(n, kappa, wx, wy, wz, scale, row_ptr, col_idx,
+                                                                 values);
+  MPB_LAUNCHED(h);
+  return MPB_OK;
+}
+
+int mpb_splitmix64_uniform(mpb_handle *h, uint64_t seed, int64_t count, double a, double b, double *out) {
+  if (!h || count < 0 || (count > 0 && !out)) return MPB_ERR_ARG;
+  if (count == 0) return MPB_OK;
+  MPB_CUDA(cudaSetDevice(h->device));
+  k_splitmix64<<<elt_blocks(count), kEltThreads, 0, h->user>>>(seed, count, a, b, out);
+  MPB_LAUNCHED(h);
+  return MPB_OK;
+}
+
 int mpb_plan_layout_info(const mpb_plan *p, int *h_npat, int64_t *h_ngeneric) {
   if (!p || !p->bound) return MPB_ERR_ARG;
   if (h_npat) *h_npat = p->npat;

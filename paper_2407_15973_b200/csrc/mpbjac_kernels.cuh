@@ -1434,6 +1434,69 @@ __global__ void k_ib_pack(long long n, const int *sp, const int *scol, const int
 }
 
 // ---------------------------------------------------------------------------
+// GPU-side problem assembly (problems.py restated): the
+// 7-point finite-volume operator from a cell field kappa, and the SplitMix64
+// uniform stream.  Same IEEE operations in the same order as the host
+// generators (no FMA), so the matrices and vectors are bit-identical.
+// ---------------------------------------------------------------------------
+// entries of rows [0, p) of the n^3 7-point operator: 7 p minus the missing
+// neighbours of those rows (closed form: no scan)
+__host__ __device__ inline long long stencil_row_ptr(long long p, long long n) {
+  const long long n2 = n * n, L = p / n, P = p / n2, rem = p % n2;
+  const long long mx = 2 * L + (p % n > 0 ? 1 : 0);
+  const long long my = 2 * n * P + (rem < n ? rem : n) + (rem > n * (n - 1) ? rem - n * (n - 1) : 0);
+  const long long mz = (p < n2 ? p : n2) + (p > (n - 1) * n2 ? p - (n - 1) * n2 : 0);
+  return 7 * p - mx - my - mz;
+}
+
+__device__ __forceinline__ double harmonic_face(double w, double a, double b) {
+  return __dmul_rn(w, __ddiv_rn(__dmul_rn(__dmul_rn(2.0, a), b), __dadd_rn(a, b)));  // problems.py _harmonic
+}
+
+// Row p: entries zm, ym, xm, diag, xp, yp, zp (ascending column), the
+// off-diagonals -(face*scale), the diagonal ((((xm+xp)+ym)+yp)+zm)+zp)*scale.
+__global__ void k_stencil(long long n, const double *kap, double wx, double wy, double wz, double scale, int *rp,
+                          int *col, double *val) {
+  const long long N = n * n * n, n2 = n * n;
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < N; p += (long long)gridDim.x * blockDim.x) {
+    const long long i = p % n, j = (p / n) % n, k = p / n2;
+    const double kc = kap[p];
+    const double fxm = i > 0 ? harmonic_face(wx, kap[p - 1], kc) : __dmul_rn(wx, kc);
+    const double fxp = i < n - 1 ? harmonic_face(wx, kc, kap[p + 1]) : __dmul_rn(wx, kc);
+    const double fym = j > 0 ? harmonic_face(wy, kap[p - n], kc) : __dmul_rn(wy, kc);
+    const double fyp = j < n - 1 ? harmonic_face(wy, kc, kap[p + n]) : __dmul_rn(wy, kc);
+    const double fzm = k > 0 ? harmonic_face(wz, kap[p - n2], kc) : __dmul_rn(wz, kc);
+    const double fzp = k < n - 1 ? harmonic_face(wz, kc, kap[p + n2]) : __dmul_rn(wz, kc);
+    long long e = stencil_row_ptr(p, n);
+    rp[p] = static_cast<int>(e);
+    if (p == N - 1) rp[N] = static_cast<int>(stencil_row_ptr(N, n));
+    const double d = __dmul_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(fxm, fxp), fym), fyp), fzm), fzp),
+                               scale);
+    if (k > 0) { col[e] = static_cast<int>(p - n2); val[e++] = -__dmul_rn(fzm, scale); }
+    if (j > 0) { col[e] = static_cast<int>(p - n); val[e++] = -__dmul_rn(fym, scale); }
+    if (i > 0) { col[e] = static_cast<int>(p - 1); val[e++] = -__dmul_rn(fxm, scale); }
+    col[e] = static_cast<int>(p);
+    val[e++] = d;
+    if (i < n - 1) { col[e] = static_cast<int>(p + 1); val[e++] = -__dmul_rn(fxp, scale); }
+    if (j < n - 1) { col[e] = static_cast<int>(p + n); val[e++] = -__dmul_rn(fyp, scale); }
+    if (k < n - 1) { col[e] = static_cast<int>(p + n2); val[e] = -__dmul_rn(fzp, scale); }
+  }
+}
+
+// problems.py splitmix64_stream: state_i = seed + (i+1) gamma, mixed, top 53 bits / 2^53
+__global__ void k_splitmix64(unsigned long long seed, long long count, double a, double b, double *out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
+       i += (long long)gridDim.x * blockDim.x) {
+    unsigned long long z = seed + static_cast<unsigned long long>(i + 1) * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    const double u = __dmul_rn(static_cast<double>(z >> 11), 0x1.0p-53);
+    out[i] = a == 1.0 && b == 0.0 ? u : __dadd_rn(__dmul_rn(a, u), b);  // a*u + b (e.g. C1: 2u - 1)
+  }
+}
+
+// ---------------------------------------------------------------------------
 // reference backend kernels (plugin level; CSR; kernels_numba.py)
 // ---------------------------------------------------------------------------
 template <typename T>

@@ -21,6 +21,14 @@ no generator in the reference; they follow the recipe of SURVEY.md §8(d):
 Grid ordering everywhere: node (i, j, k) -> row p = i + j n + k n^2, cell
 arrays C-ordered [k, j, i]; h = 1/(n+1); face coefficient = harmonic mean
 (2a)b/(a+b) of the two cells, a boundary face takes the cell's own value.
+
+``device=True`` (make_config, diffusion_matrix, splitmix64_stream) assembles
+the 7-point operator and draws the uniform streams on the GPU
+(mpb_assemble_stencil / mpb_splitmix64_uniform: same IEEE operations, same
+order, bit-identical; tests/test_gpu_parity.py pins it), which turns the
+512^3 setup from minutes of numpy into a fraction of a second plus one
+device-to-host copy.  Cell fields (kappa: exp/log/cos/pow) stay on the host,
+where libm's correctly rounded results define them.
 """
 from __future__ import annotations
 
@@ -36,11 +44,26 @@ _M1 = np.uint64(0xBF58476D1CE4E5B9)
 _M2 = np.uint64(0x94D049BB133111EB)
 
 
-def splitmix64_stream(seed: int, count: int) -> np.ndarray:
+def _gpu():
+    from . import _lib
+    return _lib.Handle.get()
+
+
+def splitmix64_stream(seed: int, count: int, device: bool = False, a: float = 1.0,
+                      b: float = 0.0) -> np.ndarray:
     """First `count` uniforms in [0,1) of the SplitMix64 stream for seed:
-    state_i = seed + (i+1) gamma mod 2^64, mixed, top 53 bits scaled."""
+    state_i = seed + (i+1) gamma mod 2^64, mixed, top 53 bits scaled.
+    device=True: drawn on the GPU (a*u + b, as a host array)."""
     if count < 0:
         raise ValueError("count must be nonnegative")
+    if device:
+        import torch
+        from . import _lib
+        h = _gpu()
+        out = torch.empty(max(count, 1), dtype=torch.float64, device=f"cuda:{h.device}")
+        _lib.check(h.lib.mpb_splitmix64_uniform(h.ptr, seed & ((1 << 64) - 1), count, float(a),
+                                                float(b), _lib.ptr(out)), "splitmix64")
+        return out[:count].cpu().numpy()
     out = np.empty(count, np.float64)
     chunk = 1 << 24
     s = np.uint64(seed & ((1 << 64) - 1))
@@ -162,13 +185,38 @@ def family_kappa(n: int, family: Family, s: float = 1.0, seed: int = 0) -> np.nd
 
 
 def diffusion_matrix(n: int, kappa: np.ndarray, weights=(1.0, 1.0, 1.0),
-                     validate: bool = True) -> SparseMatrix:
+                     validate: bool = True, device: bool = False) -> SparseMatrix:
+    if device and n >= 2:
+        return _diffusion_matrix_gpu(n, kappa, weights)
     kap3 = np.asarray(kappa, np.float64).reshape(n, n, n)
     row_ptr, col, val = stencil_csr(n, face_arrays(kap3, weights), float((n + 1) ** 2))
     N = n ** 3
     if validate:
         return SparseMatrix(N, N, row_ptr, col, val)
     return SparseMatrix.trusted(N, N, row_ptr, col, val)
+
+
+def _diffusion_matrix_gpu(n: int, kappa, weights) -> SparseMatrix:
+    """diffusion_matrix assembled on the GPU; the host copy is fetched once
+    and the device CSR is kept as the matrix's GPU copy (no re-upload)."""
+    import torch
+    from . import _lib
+    from .device import DeviceCSR, default_device
+    h = _gpu()
+    dev = default_device()
+    N = n ** 3
+    nnz = int(h.lib.mpb_stencil_nnz(n))
+    kd = torch.from_numpy(np.ascontiguousarray(kappa, np.float64).ravel()).to(dev)
+    rp = torch.empty(N + 1, dtype=torch.int32, device=dev)
+    col = torch.empty(nnz, dtype=torch.int32, device=dev)
+    val = torch.empty(nnz, dtype=torch.float64, device=dev)
+    _lib.check(h.lib.mpb_assemble_stencil(h.ptr, n, _lib.ptr(kd), float(weights[0]), float(weights[1]),
+                                          float(weights[2]), float((n + 1) ** 2), _lib.ptr(rp),
+                                          _lib.ptr(col), _lib.ptr(val)), "assemble_stencil")
+    rp_h = rp.cpu().numpy().astype(np.int64)
+    A = SparseMatrix.trusted(N, N, rp_h, col.cpu().numpy(), val.cpu().numpy())
+    A._dev[str(dev)] = DeviceCSR(N, N, rp, col, val64=val, host_row_ptr=rp_h)
+    return A
 
 
 def family_matrix(n: int, family: Family, s: float = 1.0, seed: int = 0) -> SparseMatrix:
@@ -283,36 +331,39 @@ CONFIG_NAMES = ("c1", "c2", "c3", "c4", "c5")
 FULL_N = {"c1": 32, "c2": 128, "c3": 256, "c4": 128, "c5": 512}
 
 
-def make_config(name: str, n: int | None = None, validate: bool | None = None) -> ConfigSystem:
+def make_config(name: str, n: int | None = None, validate: bool | None = None,
+                device: bool = False) -> ConfigSystem:
     """Config name 'c1'..'c5' at its BASELINE.json size, or at grid size n
-    (same recipe, for parity tests).  Same seeds, fields, blocks, policies."""
+    (same recipe, for parity tests).  Same seeds, fields, blocks, policies.
+    device=True: 7-point operators and right-hand sides built on the GPU
+    (bit-identical; C4's 3-T coupling is assembled on the host)."""
     name = name.lower()
     n = FULL_N[name] if n is None else int(n)
     N = n ** 3
     if validate is None:
         validate = N <= 4_000_000
     if name == "c1":
-        A = diffusion_matrix(n, np.ones(N), validate=validate)
-        b = 2.0 * splitmix64_stream(0, N) - 1.0
+        A = diffusion_matrix(n, np.ones(N), validate=validate, device=device)
+        b = splitmix64_stream(0, N, device, 2.0, -1.0) if device else 2.0 * splitmix64_stream(0, N) - 1.0
         return ConfigSystem("c1", A, b, 64, ("uniform", "fixed-low"), 2, 2, 1e-10, n,
                             "3-D Poisson, 7-point, Dirichlet")
     if name == "c2":
-        A = diffusion_matrix(n, kappa_c2(n), validate=validate)
-        return ConfigSystem("c2", A, splitmix64_stream(1, N), 64, ("fixed-low",), 2, 2,
+        A = diffusion_matrix(n, kappa_c2(n), validate=validate, device=device)
+        return ConfigSystem("c2", A, splitmix64_stream(1, N, device), 64, ("fixed-low",), 2, 2,
                             1e-10, n, "lognormal kappa, sigma=2")
     if name == "c3":
         if n % 8:
             raise ValueError("config 3 needs n divisible by 8")
-        A = diffusion_matrix(n, kappa_c3(n), validate=validate)
-        return ConfigSystem("c3", A, splitmix64_stream(2, N), 64, ("adaptive-lh:1e-6",),
+        A = diffusion_matrix(n, kappa_c3(n), validate=validate, device=device)
+        return ConfigSystem("c3", A, splitmix64_stream(2, N, device), 64, ("adaptive-lh:1e-6",),
                             2, 2, 1e-10, n, "8^3-cell blocks, kappa 1e-3..1e3")
     if name == "c4":
         A = three_temperature(n, validate=validate)
-        return ConfigSystem("c4", A, splitmix64_stream(3, 3 * N), 96,
+        return ConfigSystem("c4", A, splitmix64_stream(3, 3 * N, device), 96,
                             ("fixed-low", "adaptive-hl:10"), 2, 2, 1e-10, n,
                             "3-temperature radiation-diffusion stand-in")
     if name == "c5":
-        A = diffusion_matrix(n, kappa_c5(n), validate=validate)
-        return ConfigSystem("c5", A, splitmix64_stream(4, N), 64, ("fixed-low",), 2, 3,
+        A = diffusion_matrix(n, kappa_c5(n), validate=validate, device=device)
+        return ConfigSystem("c5", A, splitmix64_stream(4, N, device), 64, ("fixed-low",), 2, 3,
                             1e-8, n, "layered multiscale kappa 1e-4/1e4")
     raise ValueError(f"unknown config {name!r}, expected one of {CONFIG_NAMES}")

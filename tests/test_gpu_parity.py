@@ -356,3 +356,25 @@ def test_row_patterns_and_generic_rows_bitwise(cuda, oracle):
         rep, orc = _solve_both(A, b, offs, pol, 2, 2, 1e-10, oracle)
         assert rep.iterations == orc["iterations"]
         np.testing.assert_array_equal(rep.x, orc["x"])
+
+
+def test_gpu_assembly_bitwise_vs_host(cuda):
+    """The 7-point operators and right-hand sides built on the GPU
+    (mpb_assemble_stencil, mpb_splitmix64_uniform) equal the host
+    generators bit for bit, boundary rows and weights included."""
+    from paper_2407_15973_b200 import problems
+    for name, n in (("c1", 12), ("c2", 16), ("c3", 24), ("c4", 8), ("c5", 20)):
+        h = problems.make_config(name, n)
+        d = problems.make_config(name, n, device=True)
+        np.testing.assert_array_equal(d.A.row_ptr, h.A.row_ptr, err_msg=name)
+        np.testing.assert_array_equal(d.A.col_idx, h.A.col_idx, err_msg=name)
+        np.testing.assert_array_equal(d.A.values, h.A.values, err_msg=name)
+        np.testing.assert_array_equal(d.b, h.b, err_msg=name)
+    kap = np.exp(np.sin(np.arange(7 ** 3)))
+    for wts in ((1.0, 1.0, 1.0), (1.0, 0.1, 0.1)):
+        a = problems.diffusion_matrix(7, kap, wts)
+        g = problems.diffusion_matrix(7, kap, wts, device=True)
+        np.testing.assert_array_equal(g.values, a.values)
+        np.testing.assert_array_equal(g.col_idx, a.col_idx)
+    np.testing.assert_array_equal(problems.splitmix64_stream(12345, 1000, device=True),
+                                  problems.splitmix64_stream(12345, 1000))
