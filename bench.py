@@ -370,7 +370,8 @@ def run_b200(args, world, rank, local):
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath) and world == 1:
         with open(tpath) as fh:
-            traffic = json.load(fh).get(cs.name, {}).get(dom)
+            tj = json.load(fh).get(cs.name, {})
+            traffic = tj.get({"spmv_p": "spmv_pq"}.get(dom, dom))
     roofline = {"bound": "hbm", "kernel": dom, "achieved": kernels[dom]["gbs"],
                 "peak": peak, "unit": "GB/s", "frac": kernels[dom]["frac"],
                 "traffic": traffic, "peak_source": peak_src,
