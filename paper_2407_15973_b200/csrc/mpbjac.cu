@@ -342,7 +342,7 @@ int launch_apply(mpb_handle *h, cudaStream_t s, const mpb_plan *p, const mpb_csr
                  const double *r64, const T *rT, T *zout, double *zout64, double *part,
                  unsigned long long *ovf_count, long long *ovf_first, SolverState *st, int want_branch,
                  const ApplyBufs<T> &bufs, const DistCtx *dc = nullptr, int from_pass = 0, int to_pass = 1 << 30,
-                 int z1_gate = 0) {
+                 int z1_gate = 0, int prefetch = 0) {
   PassArgs<T> a{};
   a.sp = A->sell->d_sp;
   a.scol = A->sell->d_col;
@@ -363,6 +363,7 @@ int launch_apply(mpb_handle *h, cudaStream_t s, const mpb_plan *p, const mpb_csr
   a.want_branch = want_branch;
   a.pdl = (st != nullptr && dc == nullptr) ? 1 : 0;  // captured single-GPU iteration
   a.gate = z1_gate;
+  a.prefetch = prefetch;
   for (int pass = from_pass; pass < std::min(k, to_pass); pass++) {
     const bool first = pass == 0, last = pass == k - 1;
     a.zin = first ? nullptr : ((pass - 1) & 1 ? bufs.zB : bufs.zA);
@@ -387,7 +388,8 @@ int launch_apply(mpb_handle *h, cudaStream_t s, const mpb_plan *p, const mpb_csr
 template <typename T>
 int launch_update_first(mpb_handle *h, cudaStream_t s, const mpb_plan *p, const mpb_csr *A, int t, T *z1,
                         double *x, const double *pv, const double *q, double *r, double *part,
-                        unsigned long long *ovf_count, long long *ovf_first, SolverState *st, int want_branch) {
+                        unsigned long long *ovf_count, long long *ovf_first, SolverState *st, int want_branch,
+                        int prefetch = 0) {
   PassArgs<T> a{};
   a.sp = A->sell->d_sp;
   a.scol = A->sell->d_col;
@@ -411,6 +413,7 @@ int launch_update_first(mpb_handle *h, cudaStream_t s, const mpb_plan *p, const 
   a.st = st;
   a.want_branch = want_branch;
   a.gate = 2;
+  a.prefetch = prefetch;
   const StageLayout L = update_first_layout<T>(a.g);
   a.g.ns = pick_stages(k_update_first<T>, L.bytes);
   const uint32_t dyn = a.g.ns * L.bytes;
@@ -1293,6 +1296,11 @@ static int enqueue_iteration(mpb_handle *h, cudaStream_t s, const mpb_plan *p, c
   const bool high = o->kind != MPB_FIXED_LOW, low = o->kind != MPB_UNIFORM;
   const unsigned nt = static_cast<unsigned>(p->ntiles);
   const bool fused = fused_mode(p, o, dc);
+  // fixed-branch policies may stream their first tiles' matrix data before
+  // the grid dependency wait (MPB_PREFETCH=1); measured 2 % slower on C2
+  // (the early copies compete with the previous kernel's last tiles), so off
+  static const bool use_pre = std::getenv("MPB_PREFETCH") != nullptr;
+  const int pre = (fused && !(high && low) && use_pre) ? 1 : 0;
   int rc;
   // adaptive policies: the branch may have changed, invalidating the fused z1
   if (fused && high && low && (rc = enqueue_first_passes(h, s, p, A, o, w))) return rc;
@@ -1300,13 +1308,13 @@ static int enqueue_iteration(mpb_handle *h, cudaStream_t s, const mpb_plan *p, c
   if (high) {
     ApplyBufs<double> bb{w.zA64, w.zB64, w.res64, w.dg64, w.wA64, w.wB64};
     rc = launch_apply<double>(h, s, p, A, o->k, o->t, w.r, nullptr, w.z64, nullptr, w.part, nullptr, nullptr, w.st,
-                              0, bb, dc, from);
+                              0, bb, dc, from, 1 << 30, 0, pre);
     if (rc) return rc;
   }
   if (low) {
     ApplyBufs<float> bb{w.zA32, w.zB32, w.res32, w.dg32, w.wA32, w.wB32};
     rc = launch_apply<float>(h, s, p, A, o->k, o->t, w.r, nullptr, w.z32, nullptr, w.part, &w.st->ovf_count,
-                             &w.st->ovf_first, w.st, 1, bb, dc, from);
+                             &w.st->ovf_first, w.st, 1, bb, dc, from, 1 << 30, 0, pre);
     if (rc) return rc;
   }
   if ((rc = dist_step(h, dc, w.st, kStepRho, 2, s))) return rc;
@@ -1319,6 +1327,7 @@ static int enqueue_iteration(mpb_handle *h, cudaStream_t s, const mpb_plan *p, c
     const double *pold = (it & 1) ? w.p2 : w.p;
     pcur = (it & 1) ? w.p : w.p2;
     sa = spmv_args(h, p, A, w, pold, pcur);
+    sa.prefetch = pre;
   } else {
     MPB_CUDA(launch_k(pdl, k_pupdate, persistent_grid(k_pupdate, 0, p->ntiles), kCtaThreads, 0, s,
                       static_cast<const TileDesc *>(p->d_td), static_cast<int>(nt), static_cast<const float *>(w.z32),
@@ -1336,10 +1345,10 @@ static int enqueue_iteration(mpb_handle *h, cudaStream_t s, const mpb_plan *p, c
   if ((rc = dist_step(h, dc, w.st, kStepPq, 2, s))) return rc;
   if (fused) {
     if (high && (rc = launch_update_first<double>(h, s, p, A, o->t, w.zA64, x, pcur, w.q, w.r, w.part, nullptr,
-                                                  nullptr, w.st, 0)))
+                                                  nullptr, w.st, 0, pre)))
       return rc;
     if (low && (rc = launch_update_first<float>(h, s, p, A, o->t, w.zA32, x, pcur, w.q, w.r, w.part,
-                                                &w.st->ovf_count, &w.st->ovf_first, w.st, 1)))
+                                                &w.st->ovf_count, &w.st->ovf_first, w.st, 1, pre)))
       return rc;
   } else {
     MPB_CUDA(launch_k(pdl, k_update, persistent_grid(k_update, 0, p->ntiles), kCtaThreads, 0, s,
@@ -1468,6 +1477,9 @@ static int solve_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, con
   init.dist = dc ? 1 : 0;
   *h->h_state = init;
   MPB_CUDA(cudaMemcpyAsync(w.st, h->h_state, sizeof(SolverState), cudaMemcpyHostToDevice, s));
+  // tile-claim counters start at zero (a launch gated off after prefetching
+  // claims leaves its counter dirty; only the end of a solve gates so)
+  MPB_CUDA(cudaMemsetAsync(h->d_ctr, 0, 16 * sizeof(unsigned int), s));
   k_fill<<<elt_blocks(opt->max_iter), kEltThreads, 0, s>>>(tr_true, opt->max_iter, NAN);
   MPB_LAUNCHED(h);
   if (!opt->has_x0) MPB_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * A->n, s));
@@ -1592,6 +1604,7 @@ static int solve_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, con
     if (h->h_state->done) break;
   }
   MPB_CUDA(cudaEventRecord(h->ev_t1, s));
+  MPB_CUDA(cudaMemsetAsync(h->d_ctr, 0, 16 * sizeof(unsigned int), s));
   const SolverState st = *h->h_state;
   if (st.error == kOk) {  // final true residual (solver.py:179-182)
     if ((rc = halo_exchange(dc, x, 8, A->n, s))) return rc;

@@ -314,31 +314,50 @@ __device__ __forceinline__ const E *staged(const unsigned char *region, const E 
 }
 
 // Producer: stage tile `tile` into ring slot st (thread = producer lane 0).
+// part: kFillAll, or kFillStatic (the matrix data: columns, values, slice
+// pointers, row metadata -- no arrive, so it may run before the grid
+// dependency wait) followed later by kFillDynamic (the vector slices + the
+// arrive that completes the stage).
+enum { kFillAll = 0, kFillStatic = 1, kFillDynamic = 2 };
+
 template <typename T, typename V0, typename V1, typename V2, bool IB = false, typename V3 = uint8_t>
 __device__ __forceinline__ void produce(Ring &R, int st, const TileDesc *td, int tile, const TileGeom &g,
                                         const StageLayout &L, unsigned char *stage, const int *sp, const int *scol,
                                         const T *sval, const uint16_t *meta, const V0 *v0, const V1 *v1,
-                                        const V2 *v2, const V3 *v3 = nullptr) {
-  const TileDesc d = td[tile];
-  R.desc[st] = d;
+                                        const V2 *v2, const V3 *v3 = nullptr, int part = kFillAll) {
+  TileDesc d;
+  if (part != kFillDynamic) {
+    d = td[tile];
+    R.desc[st] = d;
+  } else {
+    d = R.desc[st];
+  }
   const int e0 = IB ? d.ie0 : d.e0, e1 = IB ? d.ie1 : d.e1;
   const int nent = e1 - e0;
   const bool fits = nent <= g.cap_e && (d.s1 - d.s0) <= g.max_sl;
-  R.ok[st] = fits ? 1 : 0;
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (part != kFillDynamic) {
+    R.ok[st] = fits ? 1 : 0;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
   if (!fits) {
-    mbar_arrive(&R.full[st]);
+    if (part != kFillStatic) mbar_arrive(&R.full[st]);
     return;
   }
   const bool cols = g.cols && d.ngen > 0;  // pattern rows rebuild their columns
-  uint32_t bytes = static_cast<uint32_t>(nent) * ((cols ? 4u : 0u) + sizeof(T)) + window_bytes(sp, d.s0, d.s1 + 1) +
-                   window_bytes(meta, d.lo, d.hi) + window_bytes(v0, d.lo, d.hi) + window_bytes(v1, d.lo, d.hi) +
-                   window_bytes(v2, d.lo, d.hi) + window_bytes(v3, d.lo, d.hi);
-  mbar_arrive_expect_tx(&R.full[st], bytes);
-  if (cols) bulk_g2s(stage + L.col, scol + e0, static_cast<uint32_t>(nent) * 4u, &R.full[st]);
-  bulk_g2s(stage + L.val, sval + e0, static_cast<uint32_t>(nent) * sizeof(T), &R.full[st]);
-  tma_window(stage + L.sp, sp, d.s0, d.s1 + 1, &R.full[st]);
-  if (meta != nullptr) tma_window(stage + L.meta, meta, d.lo, d.hi, &R.full[st]);
+  const uint32_t sbytes = static_cast<uint32_t>(nent) * ((cols ? 4u : 0u) + sizeof(T)) +
+                          window_bytes(sp, d.s0, d.s1 + 1) + window_bytes(meta, d.lo, d.hi);
+  const uint32_t dbytes = window_bytes(v0, d.lo, d.hi) + window_bytes(v1, d.lo, d.hi) + window_bytes(v2, d.lo, d.hi) +
+                          window_bytes(v3, d.lo, d.hi);
+  if (part == kFillAll) mbar_arrive_expect_tx(&R.full[st], sbytes + dbytes);
+  if (part == kFillStatic) mbar_expect_tx(&R.full[st], sbytes);
+  if (part != kFillDynamic) {
+    if (cols) bulk_g2s(stage + L.col, scol + e0, static_cast<uint32_t>(nent) * 4u, &R.full[st]);
+    bulk_g2s(stage + L.val, sval + e0, static_cast<uint32_t>(nent) * sizeof(T), &R.full[st]);
+    tma_window(stage + L.sp, sp, d.s0, d.s1 + 1, &R.full[st]);
+    if (meta != nullptr) tma_window(stage + L.meta, meta, d.lo, d.hi, &R.full[st]);
+  }
+  if (part == kFillStatic) return;
+  if (part == kFillDynamic) mbar_arrive_expect_tx(&R.full[st], dbytes);
   if (v0 != nullptr) tma_window(stage + L.v0, v0, d.lo, d.hi, &R.full[st]);
   if (v1 != nullptr) tma_window(stage + L.v1, v1, d.lo, d.hi, &R.full[st]);
   if (v2 != nullptr) tma_window(stage + L.v2, v2, d.lo, d.hi, &R.full[st]);
@@ -351,27 +370,63 @@ __device__ __forceinline__ void produce(Ring &R, int st, const TileDesc *td, int
 // the consumers' walk with tile -1.  The globally last claim (ntiles +
 // gridDim claims in all) resets the counter for the next launch.  ctr ==
 // null: static walk blockIdx.x, +gridDim.x, ...
-template <typename F>
-__device__ __forceinline__ void producer_loop(Ring &R, int ntiles, int ns, unsigned int *ctr, F &&fill) {
-  int st = 0, rnd = 0;  // stage, and how often it has been filled before
+//
+// prefetch (fixed-branch solves): the matrix data of the first ns tiles is
+// requested before the grid dependency wait -- it does not depend on the
+// previous kernel -- so it streams while the previous kernel drains; the
+// vector slices follow after the wait.  gated() is evaluated after the wait;
+// a gated-off launch drains its prefetched copies and stops (the solve
+// resets the claim counters at its start and end).
+template <typename F, typename G>
+__device__ __forceinline__ void producer_loop(Ring &R, int ntiles, int ns, unsigned int *ctr, bool prefetch,
+                                              G &&gated, F &&fill) {
   int next = blockIdx.x;
-  for (;;) {
-    if (rnd > 0) mbar_wait_sleep(&R.empty[st], (rnd - 1) & 1);
-    int tile;
+  auto claim = [&]() -> int {
     if (ctr != nullptr) {
       const unsigned int v = atomicAdd(ctr, 1u);
       if (v == static_cast<unsigned int>(ntiles) + gridDim.x - 1u) atomicExch(ctr, 0u);
-      tile = v < static_cast<unsigned int>(ntiles) ? static_cast<int>(v) : -1;
-    } else {
-      tile = next < ntiles ? next : -1;
-      next += gridDim.x;
+      return v < static_cast<unsigned int>(ntiles) ? static_cast<int>(v) : -1;
     }
+    const int t = next < ntiles ? next : -1;
+    next += gridDim.x;
+    return t;
+  };
+  int npre = 0;
+  bool exhausted = false;
+  if (prefetch) {
+    for (; npre < ns; npre++) {
+      const int tile = claim();
+      R.tile[npre] = tile;
+      if (tile < 0) {
+        exhausted = true;
+        break;
+      }
+      fill(npre, tile, kFillStatic);
+    }
+  }
+  pdl_wait();
+  if (gated()) {
+    for (int i = 0; i < npre; i++) {  // let the copies land before the CTA exits
+      mbar_arrive(&R.full[i]);
+      mbar_wait(&R.full[i], 0);
+    }
+    return;
+  }
+  for (int i = 0; i < npre; i++) fill(i, R.tile[i], kFillDynamic);
+  if (exhausted) {
+    mbar_arrive(&R.full[npre]);
+    return;
+  }
+  int st = npre % ns, rnd = npre / ns;  // stage, and how often it has been filled before
+  for (;;) {
+    if (rnd > 0) mbar_wait_sleep(&R.empty[st], (rnd - 1) & 1);
+    const int tile = claim();
     R.tile[st] = tile;
     if (tile < 0) {
       mbar_arrive(&R.full[st]);
       return;
     }
-    fill(st, tile);
+    fill(st, tile, kFillAll);
     if (++st == ns) {
       st = 0;
       rnd++;
@@ -437,6 +492,7 @@ struct PassArgs {
   T *dbuf;
   SolverState *st;       // solve mode: gate + fused scalar step
   int want_branch;
+  int prefetch;          // stream the first tiles' matrix data before the grid dependency wait
   int gate;              // 0: st->branch; 1: also skip when the fused update ran this first pass;
                          // 2: st->upd_branch (fused update: the step inside may change st->branch)
   int pdl;               // host side: launch with programmatic serialization
@@ -747,21 +803,27 @@ __global__ void __launch_bounds__(kWsThreads) k_bjac_tile(const PassArgs<T> a) {
   const StageLayout L = bjac_layout<T, FIRST, R64>(a.g);
   load_patterns(s_pat, a.pat, a.g.npat);
   ring_init(R, ns);
-  pdl_wait();
-  if (gated_off(a)) return;
   if (threadIdx.x >= kConsumers) {  // producer warp
     using RT = typename std::conditional<R64, double, T>::type;
     const RT *rsrc = R64 ? reinterpret_cast<const RT *>(a.r64) : reinterpret_cast<const RT *>(a.rT);
     if (threadIdx.x == kConsumers)
-      producer_loop(R, a.g.ntiles, ns, a.ctr, [&](int st, int tile) {
-        if (kIB)
-          produce<T, RT, uint8_t, uint8_t, true>(R, st, a.td, tile, a.g, L, smem + st * L.bytes, a.ib_sp, a.ib_col,
-                                                 a.ib_val, a.meta, rsrc, nullptr, nullptr);
-        else
-          produce<T, RT, uint8_t, uint8_t>(R, st, a.td, tile, a.g, L, smem + st * L.bytes, a.sp, a.scol, a.sval,
-                                           a.meta, rsrc, nullptr, nullptr);
-      });
+      producer_loop(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, [&]() { return gated_off(a); },
+                    [&](int st, int tile, int part) {
+                      if (kIB)
+                        produce<T, RT, uint8_t, uint8_t, true>(R, st, a.td, tile, a.g, L, smem + st * L.bytes,
+                                                               a.ib_sp, a.ib_col, a.ib_val, a.meta, rsrc, nullptr,
+                                                               nullptr, static_cast<const uint8_t *>(nullptr), part);
+                      else
+                        produce<T, RT, uint8_t, uint8_t>(R, st, a.td, tile, a.g, L, smem + st * L.bytes, a.sp,
+                                                         a.scol, a.sval, a.meta, rsrc, nullptr, nullptr,
+                                                         static_cast<const uint8_t *>(nullptr), part);
+                    });
+    else
+      pdl_wait();
+    if (gated_off(a)) return;
   } else {
+    pdl_wait();
+    if (gated_off(a)) return;
     for (RingCursor cur;; cur.advance(ns)) {
       const int st = cur.st;
       mbar_wait(&R.full[st], cur.phase);
@@ -933,6 +995,7 @@ struct SpmvArgs {
   double *q;
   double *part;
   SolverState *st;
+  int prefetch;     // see PassArgs::prefetch
 };
 
 // p_j as the SpMV reads it: stored (ZT = void) or rebuilt from z (ZT = the
@@ -1015,18 +1078,23 @@ __global__ void __launch_bounds__(kWsThreads) k_spmv_pq(const SpmvArgs a) {
   const StageLayout L = spmv_layout(a.g);
   load_patterns(s_pat, a.pat, a.g.npat);
   ring_init(R, ns);
-  pdl_wait();
-  if (a.st->done) return;
-  const int mode = a.pnew == nullptr ? 0 : (a.st->branch == 1 ? 1 : 2);
-  const bool first = a.st->first != 0;
-  const double beta = a.st->beta;
   if (threadIdx.x >= kConsumers) {
     if (threadIdx.x == kConsumers)
-      producer_loop(R, a.g.ntiles, ns, a.ctr, [&](int st, int tile) {
-        produce<double, uint8_t, uint8_t, uint8_t>(R, st, a.td, tile, a.g, L, smem + st * L.bytes, a.sp, a.scol,
-                                                   a.sval, a.meta, nullptr, nullptr, nullptr);
-      });
+      producer_loop(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, [&]() { return a.st->done != 0; },
+                    [&](int st, int tile, int part) {
+                      produce<double, uint8_t, uint8_t, uint8_t, false, uint8_t>(R, st, a.td, tile, a.g, L, smem + st * L.bytes,
+                                                                 a.sp, a.scol, a.sval, a.meta, nullptr, nullptr,
+                                                                 nullptr, nullptr, part);
+                    });
+    else
+      pdl_wait();
+    if (a.st->done) return;
   } else {
+    pdl_wait();
+    if (a.st->done) return;
+    const int mode = a.pnew == nullptr ? 0 : (a.st->branch == 1 ? 1 : 2);
+    const bool first = a.st->first != 0;
+    const double beta = a.st->beta;
     for (RingCursor cur;; cur.advance(ns)) {
       const int st = cur.st;
       mbar_wait(&R.full[st], cur.phase);
@@ -1131,15 +1199,20 @@ __global__ void __launch_bounds__(kWsThreads) k_update_first(const PassArgs<T> a
   const StageLayout L = update_first_layout<T>(a.g);
   load_patterns(s_pat, a.pat, a.g.npat);
   ring_init(R, ns);
-  pdl_wait();
-  if (gated_off(a)) return;
   if (threadIdx.x >= kConsumers) {
     if (threadIdx.x == kConsumers)
-      producer_loop(R, a.g.ntiles, ns, a.ctr, [&](int st, int tile) {
-        produce<T, double, double, double, true, double>(R, st, a.td, tile, a.g, L, smem + st * L.bytes, a.ib_sp,
-                                                         a.ib_col, a.ib_val, a.meta, r, x, p, q);
-      });
+      producer_loop(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, [&]() { return gated_off(a); },
+                    [&](int st, int tile, int part) {
+                      produce<T, double, double, double, true, double>(R, st, a.td, tile, a.g, L,
+                                                                       smem + st * L.bytes, a.ib_sp, a.ib_col,
+                                                                       a.ib_val, a.meta, r, x, p, q, part);
+                    });
+    else
+      pdl_wait();
+    if (gated_off(a)) return;
   } else {
+    pdl_wait();
+    if (gated_off(a)) return;
     const double alpha = a.st->alpha;
     for (RingCursor cur;; cur.advance(ns)) {
       const int st = cur.st;
