@@ -422,6 +422,9 @@ def run_b200(args, world, rank, local):
 
 
 def main():
+    # NCCL's own log lines (e.g. "NCCL version ...") must not reach stdout,
+    # where the driver reads exactly one JSON line
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     args = parse()
     world, rank, local = dist_env()
     if args.impl == "reference":

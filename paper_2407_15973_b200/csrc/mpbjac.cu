@@ -389,7 +389,7 @@ template <typename T>
 int launch_update_first(mpb_handle *h, cudaStream_t s, const mpb_plan *p, const mpb_csr *A, int t, T *z1,
                         double *x, const double *pv, const double *q, double *r, double *part,
                         unsigned long long *ovf_count, long long *ovf_first, SolverState *st, int want_branch,
-                        int prefetch = 0) {
+                        int prefetch = 0, bool pdl = true) {
   PassArgs<T> a{};
   a.sp = A->sell->d_sp;
   a.scol = A->sell->d_col;
@@ -418,7 +418,7 @@ int launch_update_first(mpb_handle *h, cudaStream_t s, const mpb_plan *p, const 
   a.g.ns = pick_stages(k_update_first<T>, L.bytes);
   const uint32_t dyn = a.g.ns * L.bytes;
   const int grid = persistent_grid(k_update_first<T>, dyn, p->ntiles, kWsThreads);
-  MPB_CUDA(launch_k(true, k_update_first<T>, grid, kWsThreads, dyn, s, a, x, pv, q, r));
+  MPB_CUDA(launch_k(pdl, k_update_first<T>, grid, kWsThreads, dyn, s, a, x, pv, q, r));
   MPB_LAUNCHED(h);
   return MPB_OK;
 }
@@ -498,10 +498,10 @@ SolveWs carve(const mpb_plan *p, int64_t n, char *base, int64_t ng = 0) {
   w.q = (double *)take(d);
   w.p = (double *)take(dg);
   w.p2 = (double *)take(dg);
-  w.z64 = (double *)take(d);
+  w.z64 = (double *)take(dg);
   w.zA64 = (double *)take(dg);
   w.zB64 = (double *)take(dg);
-  w.z32 = (float *)take(f);
+  w.z32 = (float *)take(fg);
   w.zA32 = (float *)take(fg);
   w.zB32 = (float *)take(fg);
   if (p->large) {
@@ -1262,27 +1262,30 @@ static SpmvArgs spmv_args(const mpb_handle *h, const mpb_plan *p, const mpb_csr 
 // exchanges before every gathering kernel, all-reduced scalar steps.
 // Fused mode (single GPU, k >= 2, tile plan): the x/r update of iteration i
 // and the first BJAC pass of iteration i+1 are one kernel (k_update_first).
-static bool fused_mode(const mpb_plan *p, const mpb_solve_options *o, const DistCtx *dc) {
+// Multi-GPU: the fused iteration exchanges three halos (z after the last
+// pass and p after the SpMV -- both gathered by the SpMV's p rebuild -- and
+// z1 after the fused update), the unfused one two (z1, p).
+static bool fused_mode(const mpb_plan *p, const mpb_solve_options *o, const DistCtx *) {
   static const bool off = std::getenv("MPB_NO_FUSE") != nullptr;
-  return !off && o->k >= 2 && !p->large && dc == nullptr;
+  return !off && o->k >= 2 && !p->large;
 }
 
 // Standalone first passes of the policy's branches (gated on st->branch and,
 // z1_gate, on the fused update not having produced z1 already).
 static int enqueue_first_passes(mpb_handle *h, cudaStream_t s, const mpb_plan *p, const mpb_csr *A,
-                                const mpb_solve_options *o, const SolveWs &w) {
+                                const mpb_solve_options *o, const SolveWs &w, const DistCtx *dc) {
   const bool high = o->kind != MPB_FIXED_LOW, low = o->kind != MPB_UNIFORM;
   int rc;
   if (high) {
     ApplyBufs<double> bb{w.zA64, w.zB64, w.res64, w.dg64, w.wA64, w.wB64};
     rc = launch_apply<double>(h, s, p, A, o->k, o->t, w.r, nullptr, w.z64, nullptr, w.part, nullptr, nullptr, w.st,
-                              0, bb, nullptr, 0, 1, 1);
+                              0, bb, dc, 0, 1, 1);  // (the z1 halo included: pass 0 is not the last)
     if (rc) return rc;
   }
   if (low) {
     ApplyBufs<float> bb{w.zA32, w.zB32, w.res32, w.dg32, w.wA32, w.wB32};
     rc = launch_apply<float>(h, s, p, A, o->k, o->t, w.r, nullptr, w.z32, nullptr, w.part, &w.st->ovf_count,
-                             &w.st->ovf_first, w.st, 1, bb, nullptr, 0, 1, 1);
+                             &w.st->ovf_first, w.st, 1, bb, dc, 0, 1, 1);
     if (rc) return rc;
   }
   return MPB_OK;
@@ -1303,7 +1306,7 @@ static int enqueue_iteration(mpb_handle *h, cudaStream_t s, const mpb_plan *p, c
   const int pre = (fused && !(high && low) && use_pre) ? 1 : 0;
   int rc;
   // adaptive policies: the branch may have changed, invalidating the fused z1
-  if (fused && high && low && (rc = enqueue_first_passes(h, s, p, A, o, w))) return rc;
+  if (fused && high && low && (rc = enqueue_first_passes(h, s, p, A, o, w, dc))) return rc;
   const int from = fused ? 1 : 0;
   if (high) {
     ApplyBufs<double> bb{w.zA64, w.zB64, w.res64, w.dg64, w.wA64, w.wB64};
@@ -1316,6 +1319,10 @@ static int enqueue_iteration(mpb_handle *h, cudaStream_t s, const mpb_plan *p, c
     rc = launch_apply<float>(h, s, p, A, o->k, o->t, w.r, nullptr, w.z32, nullptr, w.part, &w.st->ovf_count,
                              &w.st->ovf_first, w.st, 1, bb, dc, from, 1 << 30, 0, pre);
     if (rc) return rc;
+  }
+  if (fused && dc) {  // the SpMV's p rebuild gathers z at ghost rows
+    if (low && (rc = halo_exchange(dc, w.z32, 4, A->n, s))) return rc;
+    if (high && (rc = halo_exchange(dc, w.z64, 8, A->n, s))) return rc;
   }
   if ((rc = dist_step(h, dc, w.st, kStepRho, 2, s))) return rc;
   const bool pdl = dc == nullptr;
@@ -1342,21 +1349,26 @@ static int enqueue_iteration(mpb_handle *h, cudaStream_t s, const mpb_plan *p, c
                       dyn, s, sa));
   }
   MPB_LAUNCHED(h);
+  if (fused && (rc = halo_exchange(dc, pcur, 8, A->n, s))) return rc;  // next iteration's p_old ghosts
   if ((rc = dist_step(h, dc, w.st, kStepPq, 2, s))) return rc;
   if (fused) {
     if (high && (rc = launch_update_first<double>(h, s, p, A, o->t, w.zA64, x, pcur, w.q, w.r, w.part, nullptr,
-                                                  nullptr, w.st, 0, pre)))
+                                                  nullptr, w.st, 0, pre, pdl)))
       return rc;
     if (low && (rc = launch_update_first<float>(h, s, p, A, o->t, w.zA32, x, pcur, w.q, w.r, w.part,
-                                                &w.st->ovf_count, &w.st->ovf_first, w.st, 1, pre)))
+                                                &w.st->ovf_count, &w.st->ovf_first, w.st, 1, pre, pdl)))
       return rc;
+    if (dc) {  // z1 ghosts for the next last pass
+      if (low && (rc = halo_exchange(dc, w.zA32, 4, A->n, s))) return rc;
+      if (high && (rc = halo_exchange(dc, w.zA64, 8, A->n, s))) return rc;
+    }
   } else {
     MPB_CUDA(launch_k(pdl, k_update, persistent_grid(k_update, 0, p->ntiles), kCtaThreads, 0, s,
                       static_cast<const TileDesc *>(p->d_td), static_cast<int>(nt), x,
                       static_cast<const double *>(w.p), static_cast<const double *>(w.q), w.r, w.part, w.st));
     MPB_LAUNCHED(h);
   }
-  if ((rc = dist_step(h, dc, w.st, kStepRr, 2, s))) return rc;
+  if ((rc = dist_step(h, dc, w.st, fused ? kStepRrZ : kStepRr, 2, s))) return rc;
   if (o->true_stride > 0) {
     if ((rc = halo_exchange(dc, x, 8, A->n, s))) return rc;
     k_resid<true><<<persistent_grid(k_resid<true>, 0, p->ntiles), kCtaThreads, 0, s>>>(
@@ -1588,7 +1600,7 @@ static int solve_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, con
   MPB_LAUNCHED(h);
   MPB_CUDA(cudaEventRecord(h->ev_t0, s));
   // fused mode: the first iteration's first pass runs ahead of the graph
-  if (fused_mode(plan, opt, dc) && (rc = enqueue_first_passes(h, s, plan, A, opt, w))) return rc;
+  if (fused_mode(plan, opt, dc) && (rc = enqueue_first_passes(h, s, plan, A, opt, w, dc))) return rc;
   h->h_state->cond = loop ? static_cast<unsigned long long>(h->cond) : 0ull;
   MPB_CUDA(cudaMemcpyAsync(&w.st->cond, &h->h_state->cond, sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
   for (;;) {
@@ -1637,15 +1649,27 @@ static int solve_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, con
   return MPB_OK;
 }
 
+static int profile_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, const mpb_solve_options *opt,
+                        int64_t ghosts, const double *b, double *x, void *workspace, int64_t workspace_bytes,
+                        int branch, int reps, double *h_ms, bool dist);
+
 int mpb_profile_iteration(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, const mpb_solve_options *opt,
                           const double *b, double *x, void *workspace, int64_t workspace_bytes, int branch, int reps,
                           double *h_ms) {
-  return mpb_profile_iteration_dist(h, plan, A, opt, 0, b, x, workspace, workspace_bytes, branch, reps, h_ms);
+  return profile_impl(h, plan, A, opt, 0, b, x, workspace, workspace_bytes, branch, reps, h_ms, false);
 }
 
+// the multi-GPU solve runs the unfused iteration (first pass, last pass,
+// p-update, SpMV, x/r update): those are the kernels timed here
 int mpb_profile_iteration_dist(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, const mpb_solve_options *opt,
                                int64_t ghosts, const double *b, double *x, void *workspace,
                                int64_t workspace_bytes, int branch, int reps, double *h_ms) {
+  return profile_impl(h, plan, A, opt, ghosts, b, x, workspace, workspace_bytes, branch, reps, h_ms, true);
+}
+
+static int profile_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, const mpb_solve_options *opt,
+                        int64_t ghosts, const double *b, double *x, void *workspace, int64_t workspace_bytes,
+                        int branch, int reps, double *h_ms, bool dist) {
   if (!opt || ghosts < 0) return MPB_ERR_ARG;
   int rc = check_sell(A, true, branch == 1);
   if (rc == MPB_OK) rc = check_bound(plan, A);
@@ -1751,7 +1775,7 @@ int mpb_profile_iteration_dist(mpb_handle *h, const mpb_plan *plan, const mpb_cs
   // fused mode (what the solve runs when k >= 2 on a tile plan): the SpMV
   // rebuilds p from z (no p-update kernel), the x/r update carries the next
   // first pass
-  const bool fused = opt->k >= 2 && !plan->large && std::getenv("MPB_NO_FUSE") == nullptr;
+  const bool fused = !dist && opt->k >= 2 && !plan->large && std::getenv("MPB_NO_FUSE") == nullptr;
   const SpmvArgs sa = fused ? spmv_args(h, plan, A, w, w.p, w.p2) : spmv_args(h, plan, A, w);
   const uint32_t sdyn = spmv_dyn_smem(plan);
   const int sgrid = persistent_grid(spmv_kernel(plan), sdyn, plan->ntiles, kWsThreads);

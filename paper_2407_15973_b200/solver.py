@@ -370,10 +370,16 @@ def profile_iteration(A: SparseMatrix, mp: MixedPreconditioner, *,
     opt.res_tol = float(config.res_tol)
     opt.max_iter = cap
     out = (C.c_double * 8)()
-    _lib.check(h.lib.mpb_profile_iteration_dist(
-        h.ptr, P.plan.ptr, C.byref(s), C.byref(opt), int(ghosts), _lib.ptr(bd), _lib.ptr(x),
-        _lib.ptr(ws), ws.numel(), 0 if branch == "high" else 1, int(reps), out),
-        "profile_iteration")
+    if n_global is None:    # one GPU: the kernels pcg_solve runs (fused iteration)
+        _lib.check(h.lib.mpb_profile_iteration(
+            h.ptr, P.plan.ptr, C.byref(s), C.byref(opt), _lib.ptr(bd), _lib.ptr(x),
+            _lib.ptr(ws), ws.numel(), 0 if branch == "high" else 1, int(reps), out),
+            "profile_iteration")
+    else:                   # a slab of a multi-GPU solve (unfused iteration)
+        _lib.check(h.lib.mpb_profile_iteration_dist(
+            h.ptr, P.plan.ptr, C.byref(s), C.byref(opt), int(ghosts), _lib.ptr(bd), _lib.ptr(x),
+            _lib.ptr(ws), ws.numel(), 0 if branch == "high" else 1, int(reps), out),
+            "profile_iteration")
     names = ("bjac_first", "bjac_middle", "bjac_last", "spmv_pq", "update",
              "update_first", "iteration", "pupdate")
     return {k: float(out[i]) for i, k in enumerate(names)}
