@@ -425,6 +425,8 @@ def main():
     # NCCL's own log lines (e.g. "NCCL version ...") must not reach stdout,
     # where the driver reads exactly one JSON line
     os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+        os.environ["NCCL_DEBUG"] = "WARN"
     args = parse()
     world, rank, local = dist_env()
     if args.impl == "reference":
