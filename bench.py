@@ -406,7 +406,7 @@ def run_b200(args, world, rank, local):
             "config": config_dict(cs, part, policy, {
                 "parallelism": (f"z-slabs over {world} GPU(s), NCCL halos + fp64 all-reduce"
                                 if sharded else "1 GPU"),
-                "graph": "CUDA graph of 8 iterations replayed until the device sets done",
+                "graph": "one CUDA graph per solve: a device-side while loop over 16-iteration bodies",
                 "row_patterns": plan.layout_info()}),
             "iterations": it_med, "time_to_solution_ms": ms_per_step,
             "converged": bool(rep.converged), "final_true_relres": rep.final_true_relres,

@@ -22,7 +22,7 @@ using namespace mpb;
 
 namespace {
 
-constexpr int kDefaultGraphIters = 8;
+constexpr int kDefaultGraphIters = 16;  // iterations per while-loop body (measured best: 16-32)
 constexpr int kEltThreads = 256;
 
 inline int status_of(cudaError_t e) { return e == cudaSuccess ? MPB_OK : static_cast<int>(e); }
@@ -92,6 +92,7 @@ struct mpb_handle {
   size_t scratch_bytes;
   SolverState *h_state;  // pinned
   unsigned int *d_ctr;   // tile-claim counters of the persistent kernels (reset by each launch)
+  unsigned long long *d_tl;  // MPB_TIMELINE diagnostics buffer
   int64_t launches;
   cudaGraphExec_t gexec;
   cudaGraphConditionalHandle cond;  // while node of gexec (device-side solve loop)
@@ -577,6 +578,7 @@ int mpb_destroy(mpb_handle *h) {
   if (h->scratch) cudaFree(h->scratch);
   cudaFreeHost(h->h_state);
   cudaFree(h->d_ctr);
+  cudaFree(h->d_tl);
   cudaEventDestroy(h->ev_in);
   cudaEventDestroy(h->ev_out);
   cudaEventDestroy(h->ev_t0);
@@ -1487,6 +1489,14 @@ static int solve_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, con
   init.tr_branch = tr_branch;
   init.tr_time = tr_time;
   init.dist = dc ? 1 : 0;
+  static const bool timeline = std::getenv("MPB_TIMELINE") != nullptr;
+  if (timeline) {  // diagnostics: per-iteration kernel timestamps (summary on stderr)
+    if (h->d_tl == nullptr) MPB_CUDA(cudaMalloc(&h->d_tl, sizeof(unsigned long long) * kTlIters * 12));
+    std::vector<unsigned long long> t0(kTlIters * 12);
+    for (int i = 0; i < kTlIters * 12; i++) t0[i] = (i % 4 == 0) ? ~0ull : 0ull;
+    MPB_CUDA(cudaMemcpy(h->d_tl, t0.data(), sizeof(unsigned long long) * t0.size(), cudaMemcpyHostToDevice));
+    init.tl = h->d_tl;
+  }
   *h->h_state = init;
   MPB_CUDA(cudaMemcpyAsync(w.st, h->h_state, sizeof(SolverState), cudaMemcpyHostToDevice, s));
   // tile-claim counters start at zero (a launch gated off after prefetching
@@ -1617,6 +1627,32 @@ static int solve_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, con
   }
   MPB_CUDA(cudaEventRecord(h->ev_t1, s));
   MPB_CUDA(cudaMemsetAsync(h->d_ctr, 0, 16 * sizeof(unsigned int), s));
+  if (timeline) {
+    MPB_CUDA(cudaStreamSynchronize(s));
+    std::vector<unsigned long long> t(kTlIters * 12);
+    MPB_CUDA(cudaMemcpy(t.data(), h->d_tl, sizeof(unsigned long long) * t.size(), cudaMemcpyDeviceToHost));
+    const long long last = std::min<long long>(h->h_state->last_it, kTlIters - 1);
+    double acc[3][3] = {};  // per kernel: gap (start - previous step), body (end - start), tail (step - end)
+    long long cnt = 0;
+    for (long long it = 5; it < last; it++) {
+      const unsigned long long *r = &t[it * 12];
+      const unsigned long long prev = (&t[(it - 1) * 12])[2 * 4 + 2];
+      const unsigned long long stp[3] = {prev, r[0 * 4 + 2], r[1 * 4 + 2]};
+      bool ok = prev != 0;
+      for (int k = 0; k < 3; k++) ok = ok && r[k * 4] != ~0ull && r[k * 4 + 1] && r[k * 4 + 2];
+      if (!ok) continue;
+      for (int k = 0; k < 3; k++) {
+        acc[k][0] += 1e-3 * double(r[k * 4] - stp[k]);
+        acc[k][1] += 1e-3 * double(r[k * 4 + 1] - r[k * 4]);
+        acc[k][2] += 1e-3 * double(r[k * 4 + 2] - r[k * 4 + 1]);
+      }
+      cnt++;
+    }
+    const char *nm[3] = {"last pass", "spmv+p", "update+first"};
+    for (int k = 0; k < 3 && cnt; k++)
+      std::fprintf(stderr, "[mpb timeline] %-12s gap %6.2f us  body %6.2f us  tail %6.2f us  (mean of %lld iterations)\n",
+                   nm[k], acc[k][0] / cnt, acc[k][1] / cnt, acc[k][2] / cnt, cnt);
+  }
   const SolverState st = *h->h_state;
   if (st.error == kOk) {  // final true residual (solver.py:179-182)
     if ((rc = halo_exchange(dc, x, 8, A->n, s))) return rc;

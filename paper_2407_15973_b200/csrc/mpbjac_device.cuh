@@ -64,7 +64,29 @@ struct SolverState {
   int upd_branch;  // branch of the iteration whose x/r update is pending (set at kStepPq)
   int pad;
   unsigned long long cond;  // while-node handle of the solve graph (0: host-polled loop)
+  unsigned long long *tl;   // diagnostics (MPB_TIMELINE): per-iteration kernel timestamps, or null
 };
+
+// MPB_TIMELINE: tl[(it % kTlIters) * 12 + kind * 4 + f], kind 0 last pass,
+// 1 SpMV, 2 fused update; f 0 first consumer start, 1 last consumer end,
+// 2 scalar step (globaltimer ns)
+constexpr int kTlIters = 1024;
+__device__ __forceinline__ unsigned long long globaltimer_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// compiled in only with -DMPB_TIMELINE (make EXTRA=-DMPB_TIMELINE): the
+// extra state load sits on the critical path of warp 0
+__device__ __forceinline__ void tl_mark(const SolverState *st, int kind, int f, bool is_max) {
+#ifndef MPB_TIMELINE
+  return;
+#endif
+  if (st == nullptr || st->tl == nullptr) return;
+  unsigned long long *p = st->tl + (st->it % kTlIters) * 12 + kind * 4 + f;
+  const unsigned long long t = globaltimer_now();
+  if (is_max) atomicMax(p, t); else atomicMin(p, t);
+}
 
 // ---------------------------------------------------------------------------
 // reductions in the order fixed by include/mpbjac_order.h

@@ -115,6 +115,7 @@ __device__ __noinline__ void scalar_step(int step, double tot, SolverState *st) 
       break;
     }
     case kStepRho: {
+      tl_mark(st, 0, 2, true);
       if (st->ovf_count != 0ull) {
         fail(st, kNarrowOverflow, 0.0);
         break;
@@ -126,6 +127,7 @@ __device__ __noinline__ void scalar_step(int step, double tot, SolverState *st) 
       break;
     }
     case kStepPq: {
+      tl_mark(st, 1, 2, true);
       st->pq = tot;
       if (tot <= 0.0) { fail(st, kIndefMatrix, tot); break; }
       st->alpha = st->rho / tot;
@@ -134,6 +136,7 @@ __device__ __noinline__ void scalar_step(int step, double tot, SolverState *st) 
     }
     case kStepRr:
     case kStepRrZ: {
+      tl_mark(st, 2, 2, true);
       const int old_branch = st->branch;
       const double rnorm = sqrt(tot);
       st->rnorm = rnorm;
@@ -824,6 +827,7 @@ __global__ void __launch_bounds__(kWsThreads) k_bjac_tile(const PassArgs<T> a) {
   } else {
     pdl_wait();
     if (gated_off(a)) return;
+    if (LAST && threadIdx.x == 0) tl_mark(a.st, 0, 0, false);
     for (RingCursor cur;; cur.advance(ns)) {
       const int st = cur.st;
       mbar_wait(&R.full[st], cur.phase);
@@ -867,6 +871,7 @@ __global__ void __launch_bounds__(kWsThreads) k_bjac_tile(const PassArgs<T> a) {
       }
       ring_release(R, st);
     }
+    if (LAST && threadIdx.x == 0) tl_mark(a.st, 0, 1, true);
   }
   pdl_trigger();  // dependents may launch into the SMs this grid drains
   if (LAST && a.part != nullptr) finish_grid(a.st, 0, kStepRho, a.part, a.g.ntiles, ws);
@@ -1092,6 +1097,7 @@ __global__ void __launch_bounds__(kWsThreads) k_spmv_pq(const SpmvArgs a) {
   } else {
     pdl_wait();
     if (a.st->done) return;
+    if (threadIdx.x == 0) tl_mark(a.st, 1, 0, false);
     const int mode = a.pnew == nullptr ? 0 : (a.st->branch == 1 ? 1 : 2);
     const bool first = a.st->first != 0;
     const double beta = a.st->beta;
@@ -1113,6 +1119,7 @@ __global__ void __launch_bounds__(kWsThreads) k_spmv_pq(const SpmvArgs a) {
       }
       ring_release(R, st);
     }
+    if (threadIdx.x == 0) tl_mark(a.st, 1, 1, true);
   }
   pdl_trigger();
   finish_grid(a.st, 1, kStepPq, a.part, a.g.ntiles, ws);
@@ -1213,6 +1220,7 @@ __global__ void __launch_bounds__(kWsThreads) k_update_first(const PassArgs<T> a
   } else {
     pdl_wait();
     if (gated_off(a)) return;
+    if (threadIdx.x == 0) tl_mark(a.st, 2, 0, false);
     const double alpha = a.st->alpha;
     for (RingCursor cur;; cur.advance(ns)) {
       const int st = cur.st;
@@ -1252,6 +1260,7 @@ __global__ void __launch_bounds__(kWsThreads) k_update_first(const PassArgs<T> a
         bjac_first_body<T>(a, d, col, a.ib_val + d.ie0, a.ib_sp + d.s0, a.meta + d.lo, rv, s_pat, s_w);
       ring_release(R, st);
     }
+    if (threadIdx.x == 0) tl_mark(a.st, 2, 1, true);
   }
   pdl_trigger();
   finish_grid(a.st, 2, kStepRrZ, a.part, a.g.ntiles, ws);
