@@ -1632,7 +1632,8 @@ static int solve_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, con
     std::vector<unsigned long long> t(kTlIters * 12);
     MPB_CUDA(cudaMemcpy(t.data(), h->d_tl, sizeof(unsigned long long) * t.size(), cudaMemcpyDeviceToHost));
     const long long last = std::min<long long>(h->h_state->last_it, kTlIters - 1);
-    double acc[3][3] = {};  // per kernel: gap (start - previous step), body (end - start), tail (step - end)
+    double acc[3][4] = {};  // per kernel: gap (start - previous step), body (end - start), tail (step - end),
+                            // of which the last CTA's reduction + step (step - last CTA known)
     long long cnt = 0;
     for (long long it = 5; it < last; it++) {
       const unsigned long long *r = &t[it * 12];
@@ -1645,13 +1646,16 @@ static int solve_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, con
         acc[k][0] += 1e-3 * double(r[k * 4] - stp[k]);
         acc[k][1] += 1e-3 * double(r[k * 4 + 1] - r[k * 4]);
         acc[k][2] += 1e-3 * double(r[k * 4 + 2] - r[k * 4 + 1]);
+        if (r[k * 4 + 3]) acc[k][3] += 1e-3 * double(r[k * 4 + 2] - r[k * 4 + 3]);
       }
       cnt++;
     }
     const char *nm[3] = {"last pass", "spmv+p", "update+first"};
     for (int k = 0; k < 3 && cnt; k++)
-      std::fprintf(stderr, "[mpb timeline] %-12s gap %6.2f us  body %6.2f us  tail %6.2f us  (mean of %lld iterations)\n",
-                   nm[k], acc[k][0] / cnt, acc[k][1] / cnt, acc[k][2] / cnt, cnt);
+      std::fprintf(stderr,
+                   "[mpb timeline] %-12s gap %6.2f us  body %6.2f us  tail %6.2f us (last-CTA sum+step %5.2f)"
+                   "  (mean of %lld iterations)\n",
+                   nm[k], acc[k][0] / cnt, acc[k][1] / cnt, acc[k][2] / cnt, acc[k][3] / cnt, cnt);
   }
   const SolverState st = *h->h_state;
   if (st.error == kOk) {  // final true residual (solver.py:179-182)

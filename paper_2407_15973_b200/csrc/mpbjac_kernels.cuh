@@ -193,6 +193,7 @@ __device__ __forceinline__ void finish_grid(SolverState *st, int ticket, int ste
                                             double *ws) {
   if (st == nullptr) return;
   if (!grid_last(&st->ticket[ticket])) return;
+  if (threadIdx.x == 0) tl_mark(st, step == kStepRho ? 0 : (step == kStepPq ? 1 : 2), 3, true);  // diagnostics
   const double tot = fin_sum(part, ntiles, ws);
   if (threadIdx.x == 0) {
     if (st->dist) {  // multi-GPU: all-reduce first, k_apply_step runs the step
