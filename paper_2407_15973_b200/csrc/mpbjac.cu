@@ -232,7 +232,7 @@ struct ApplyBufs {
   T *res, *dg, *wA, *wB;  // large-block path (plan->large)
 };
 
-template <typename T, bool F, bool L, bool R64, int KS>
+template <typename T, bool F, bool L, bool R64, int KS, bool GEN>
 int launch_tile_kernel(mpb_handle *h, cudaStream_t s, const mpb_plan *p, PassArgs<T> a) {
   if (F && !L) {  // first pass streams the in-block layout
     if (a.ib_val == nullptr) return MPB_ERR_LAYOUT;
@@ -241,10 +241,10 @@ int launch_tile_kernel(mpb_handle *h, cudaStream_t s, const mpb_plan *p, PassArg
     a.g.cap_e = std::min(p->max_tile_ib, kStageCap);
   }
   const StageLayout Ls = bjac_layout<T, F, R64>(a.g);
-  a.g.ns = pick_stages(k_bjac_tile<T, F, L, R64, KS>, Ls.bytes);
+  a.g.ns = pick_stages(k_bjac_tile<T, F, L, R64, KS, GEN>, Ls.bytes);
   const uint32_t dyn = a.g.ns * Ls.bytes;
-  const int grid = persistent_grid(k_bjac_tile<T, F, L, R64, KS>, dyn, p->ntiles, kWsThreads);
-  MPB_CUDA(launch_k(a.pdl != 0, k_bjac_tile<T, F, L, R64, KS>, grid, kWsThreads, dyn, s, a));
+  const int grid = persistent_grid(k_bjac_tile<T, F, L, R64, KS, GEN>, dyn, p->ntiles, kWsThreads);
+  MPB_CUDA(launch_k(a.pdl != 0, k_bjac_tile<T, F, L, R64, KS, GEN>, grid, kWsThreads, dyn, s, a));
   MPB_LAUNCHED(h);
   return MPB_OK;
 }
@@ -254,11 +254,15 @@ int launch_pass(mpb_handle *h, cudaStream_t s, const mpb_plan *p, PassArgs<T> a,
   const int nt = static_cast<int>(p->ntiles);
   if (!p->large) {
     if (p->ks == 7) {
-      if (a.r64 != nullptr) return launch_tile_kernel<T, F, L, true, 7>(h, s, p, a);
-      return launch_tile_kernel<T, F, L, false, 7>(h, s, p, a);
+      if (p->ngeneric > 0) {
+        if (a.r64 != nullptr) return launch_tile_kernel<T, F, L, true, 7, true>(h, s, p, a);
+        return launch_tile_kernel<T, F, L, false, 7, true>(h, s, p, a);
+      }
+      if (a.r64 != nullptr) return launch_tile_kernel<T, F, L, true, 7, false>(h, s, p, a);
+      return launch_tile_kernel<T, F, L, false, 7, false>(h, s, p, a);
     }
-    if (a.r64 != nullptr) return launch_tile_kernel<T, F, L, true, kSlots>(h, s, p, a);
-    return launch_tile_kernel<T, F, L, false, kSlots>(h, s, p, a);
+    if (a.r64 != nullptr) return launch_tile_kernel<T, F, L, true, kSlots, true>(h, s, p, a);
+    return launch_tile_kernel<T, F, L, false, kSlots, true>(h, s, p, a);
   }
   a.resbuf = bufs.res;
   a.dbuf = bufs.dg;
@@ -416,10 +420,11 @@ int launch_update_first(mpb_handle *h, cudaStream_t s, const mpb_plan *p, const 
   a.gate = 2;
   a.prefetch = prefetch;
   const StageLayout L = update_first_layout<T>(a.g);
-  a.g.ns = pick_stages(k_update_first<T>, L.bytes);
+  auto kern = p->ngeneric > 0 ? k_update_first<T, true> : k_update_first<T, false>;
+  a.g.ns = pick_stages(kern, L.bytes);
   const uint32_t dyn = a.g.ns * L.bytes;
-  const int grid = persistent_grid(k_update_first<T>, dyn, p->ntiles, kWsThreads);
-  MPB_CUDA(launch_k(pdl, k_update_first<T>, grid, kWsThreads, dyn, s, a, x, pv, q, r));
+  const int grid = persistent_grid(kern, dyn, p->ntiles, kWsThreads);
+  MPB_CUDA(launch_k(pdl, kern, grid, kWsThreads, dyn, s, a, x, pv, q, r));
   MPB_LAUNCHED(h);
   return MPB_OK;
 }
@@ -1221,7 +1226,11 @@ int64_t mpb_solve_workspace_bytes(const mpb_plan *plan, int64_t n) {
   return static_cast<int64_t>(carve(plan, n, nullptr).bytes);
 }
 
-static void (*spmv_kernel(const mpb_plan *p))(SpmvArgs) { return p->ks == 7 ? k_spmv_pq<7> : k_spmv_pq<kSlots>; }
+// KS = 7 (7-point stencils) with or without generic rows; KS = 9 (e.g. 3-T) always with
+static void (*spmv_kernel(const mpb_plan *p))(SpmvArgs) {
+  if (p->ks == 7) return p->ngeneric > 0 ? k_spmv_pq<7, true> : k_spmv_pq<7, false>;
+  return k_spmv_pq<kSlots, true>;
+}
 
 static TileGeom spmv_geom(const mpb_plan *p) {
   TileGeom g = geom_for<double>(p);

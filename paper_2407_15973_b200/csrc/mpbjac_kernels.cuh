@@ -607,7 +607,8 @@ struct PassRow {
 
 // A pass up to its first inner sweep for one row: res = r - A z_in (all
 // slots, stored order), d, w = res / d (written to the tile's s_w).
-template <typename T, bool FIRST, int KS>
+// GEN: the plan has generic rows (no row pattern); false compiles their path out
+template <typename T, bool FIRST, int KS, bool GEN>
 __device__ __forceinline__ void pass_row_init(PassRow<T> &q, const PassArgs<T> &a, const TileDesc &d, int tid,
                                               const int *col, const T *val, const int *spp, const uint16_t *mt,
                                               const double *r64t, const T *rTt, const int *s_pat, T *s_w) {
@@ -629,7 +630,7 @@ __device__ __forceinline__ void pass_row_init(PassRow<T> &q, const PassArgs<T> &
   const T rv = r64t != nullptr ? narrow_checked(a, r64t[tid], row, FIRST) : rTt[tid];
   const T *zr = FIRST ? nullptr : a.zin + row;
   if (!FIRST) q.zown = __ldg(zr);
-  if (q.m != kMetaGeneric) {
+  if (!GEN || q.m != kMetaGeneric) {
     q.P = s_pat + meta_pid(q.m) * kPatStride;
     const int hdr = q.P[0], len = pat_len(hdr);
     q.i0 = meta_i0(q.m);
@@ -656,12 +657,12 @@ __device__ __forceinline__ void pass_row_init(PassRow<T> &q, const PassArgs<T> &
 }
 
 // A_b w over the row's in-block entries (one inner sweep's sum)
-template <typename T>
+template <typename T, bool GEN>
 __device__ __forceinline__ T pass_row_sweep(const PassRow<T> &q, const PassArgs<T> &a, const TileDesc &d, int tid,
                                             const int *col, const T *val, const T *s_w) {
   T acc = T(0);
   if (!q.valid) return acc;
-  if (q.m != kMetaGeneric) {
+  if (!GEN || q.m != kMetaGeneric) {
 #pragma unroll 1
     for (int j = q.i0; j < q.i1; j++) acc = add_rn(acc, mul_rn(val[q.base + 32 * j], s_w[tid + q.P[1 + j]]));
   } else {
@@ -673,20 +674,20 @@ __device__ __forceinline__ T pass_row_sweep(const PassRow<T> &q, const PassArgs<
 // One tile of a fused (non-first-only) pass, consumer threads only.  col /
 // val / spp / mt are the shared stage or the global arrays offset to the
 // tile (same indexing); r64t / rTt the tile's residual slice.
-template <typename T, bool FIRST, bool LAST, int KS>
+template <typename T, bool FIRST, bool LAST, int KS, bool GEN>
 __device__ __forceinline__ void bjac_tile_body(const PassArgs<T> &a, int tile, const TileDesc &d, const int *col,
                                                const T *val, const int *spp, const uint16_t *mt, const double *r64t,
                                                const T *rTt, const int *s_pat, T *s_w, double *ws) {
   PassRow<T> q[kRowsPerThread];
 #pragma unroll
   for (int k = 0; k < kRowsPerThread; k++)
-    pass_row_init<T, FIRST, KS>(q[k], a, d, threadIdx.x + k * kConsumers, col, val, spp, mt, r64t, rTt, s_pat, s_w);
+    pass_row_init<T, FIRST, KS, GEN>(q[k], a, d, threadIdx.x + k * kConsumers, col, val, spp, mt, r64t, rTt, s_pat, s_w);
   for (int s = 1; s < a.t; s++) {  // inner sweeps, the tile's w in shared memory
     named_sync(kBarConsumers, kConsumers);
     T acc[kRowsPerThread];
 #pragma unroll
     for (int k = 0; k < kRowsPerThread; k++)
-      acc[k] = pass_row_sweep(q[k], a, d, threadIdx.x + k * kConsumers, col, val, s_w);
+      acc[k] = pass_row_sweep<T, GEN>(q[k], a, d, threadIdx.x + k * kConsumers, col, val, s_w);
     named_sync(kBarConsumers, kConsumers);
 #pragma unroll
     for (int k = 0; k < kRowsPerThread; k++) {
@@ -716,7 +717,7 @@ __device__ __forceinline__ void bjac_tile_body(const PassArgs<T> &a, int tile, c
 // in-block entries (plan's in-block SELL): y = r / d, then t-1 sweeps
 // y += (r - A_b y) / d over the in-block entries in ascending column order.
 // res[k]: row tid + k kConsumers's residual in T (valid rows).
-template <typename T>
+template <typename T, bool GEN>
 __device__ __forceinline__ void bjac_first_body(const PassArgs<T> &a, const TileDesc &d, const int *col,
                                                 const T *val, const int *spp, const uint16_t *mt,
                                                 const T (&res)[kRowsPerThread], const int *s_pat, T *s_w) {
@@ -738,7 +739,7 @@ __device__ __forceinline__ void bjac_first_body(const PassArgs<T> &a, const Tile
     const int sb = spp[si];
     base[k] = sb - d.ie0 + (row & 31);
     const uint16_t m = mt[tid];
-    pat[k] = m != kMetaGeneric;
+    pat[k] = !GEN || m != kMetaGeneric;
     if (pat[k]) {
       const int i0 = meta_i0(m);
       nib[k] = meta_i1(m) - i0;
@@ -795,7 +796,7 @@ __host__ __device__ inline StageLayout bjac_layout(const TileGeom &g) {
 }
 
 // Persistent, warp-specialised fused pass.
-template <typename T, bool FIRST, bool LAST, bool R64, int KS>
+template <typename T, bool FIRST, bool LAST, bool R64, int KS, bool GEN>
 __global__ void __launch_bounds__(kWsThreads) k_bjac_tile(const PassArgs<T> a) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ Ring R;
@@ -850,22 +851,22 @@ __global__ void __launch_bounds__(kWsThreads) k_bjac_tile(const PassArgs<T> a) {
           else rv[k] = ok ? staged(sb + L.v0, a.rT, d.lo, d.hi)[tid] : a.rT[row];
         }
         if (ok) {
-          bjac_first_body<T>(a, d, col, reinterpret_cast<const T *>(sb + L.val),
+          bjac_first_body<T, GEN>(a, d, col, reinterpret_cast<const T *>(sb + L.val),
                              staged(sb + L.sp, a.ib_sp, d.s0, d.s1 + 1), staged(sb + L.meta, a.meta, d.lo, d.hi), rv,
                              s_pat, s_w);
         } else {
-          bjac_first_body<T>(a, d, col, a.ib_val + d.ie0, a.ib_sp + d.s0, a.meta + d.lo, rv, s_pat, s_w);
+          bjac_first_body<T, GEN>(a, d, col, a.ib_val + d.ie0, a.ib_sp + d.s0, a.meta + d.lo, rv, s_pat, s_w);
         }
       } else {
         const int *col = scols ? reinterpret_cast<const int *>(sb + L.col) : a.scol + d.e0;
         if (ok) {
-          bjac_tile_body<T, FIRST, LAST, KS>(a, tile, d, col, reinterpret_cast<const T *>(sb + L.val),
+          bjac_tile_body<T, FIRST, LAST, KS, GEN>(a, tile, d, col, reinterpret_cast<const T *>(sb + L.val),
                                              staged(sb + L.sp, a.sp, d.s0, d.s1 + 1),
                                              staged(sb + L.meta, a.meta, d.lo, d.hi),
                                              R64 ? staged(sb + L.v0, a.r64, d.lo, d.hi) : nullptr,
                                              R64 ? nullptr : staged(sb + L.v0, a.rT, d.lo, d.hi), s_pat, s_w, ws);
         } else {
-          bjac_tile_body<T, FIRST, LAST, KS>(a, tile, d, col, a.sval + d.e0, a.sp + d.s0, a.meta + d.lo,
+          bjac_tile_body<T, FIRST, LAST, KS, GEN>(a, tile, d, col, a.sval + d.e0, a.sp + d.s0, a.meta + d.lo,
                                              R64 ? a.r64 + d.lo : nullptr, R64 ? nullptr : a.rT + d.lo, s_pat, s_w,
                                              ws);
         }
@@ -1017,7 +1018,7 @@ __device__ __forceinline__ double p_at(const SpmvArgs &a, int c, bool first, dou
   }
 }
 
-template <int KS, typename ZT>
+template <int KS, typename ZT, bool GEN>
 __device__ __forceinline__ void spmv_tile_body(const SpmvArgs &a, int tile, const TileDesc &d, const int *col,
                                                const double *val, const int *spp, const uint16_t *mt,
                                                const int *s_pat, double *ws, bool first, double beta) {
@@ -1032,7 +1033,7 @@ __device__ __forceinline__ void spmv_tile_body(const SpmvArgs &a, int tile, cons
     const int base = sb - d.e0 + (row & 31);
     const uint16_t m = mt[tid];
     double acc = 0.0;
-    if (m != kMetaGeneric) {
+    if (!GEN || m != kMetaGeneric) {
       const int *P = s_pat + meta_pid(m) * kPatStride;
       const int len = pat_len(P[0]);
       double vv[KS], pv[KS];
@@ -1065,16 +1066,16 @@ __host__ __device__ inline StageLayout spmv_layout(const TileGeom &g) {
 }
 
 // one tile of the SpMV with p stored or rebuilt (branch of the iteration)
-template <int KS>
+template <int KS, bool GEN>
 __device__ __forceinline__ void spmv_tile(const SpmvArgs &a, int tile, const TileDesc &d, const int *col,
                                           const double *val, const int *spp, const uint16_t *mt, const int *s_pat,
                                           double *ws, int mode, bool first, double beta) {
-  if (mode == 0) spmv_tile_body<KS, void>(a, tile, d, col, val, spp, mt, s_pat, ws, first, beta);
-  else if (mode == 1) spmv_tile_body<KS, float>(a, tile, d, col, val, spp, mt, s_pat, ws, first, beta);
-  else spmv_tile_body<KS, double>(a, tile, d, col, val, spp, mt, s_pat, ws, first, beta);
+  if (mode == 0) spmv_tile_body<KS, void, GEN>(a, tile, d, col, val, spp, mt, s_pat, ws, first, beta);
+  else if (mode == 1) spmv_tile_body<KS, float, GEN>(a, tile, d, col, val, spp, mt, s_pat, ws, first, beta);
+  else spmv_tile_body<KS, double, GEN>(a, tile, d, col, val, spp, mt, s_pat, ws, first, beta);
 }
 
-template <int KS>
+template <int KS, bool GEN>
 __global__ void __launch_bounds__(kWsThreads) k_spmv_pq(const SpmvArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ Ring R;
@@ -1111,11 +1112,11 @@ __global__ void __launch_bounds__(kWsThreads) k_spmv_pq(const SpmvArgs a) {
       const unsigned char *sb = smem + st * L.bytes;
       if (R.ok[st]) {
         const int *col = (a.g.cols && d.ngen > 0) ? reinterpret_cast<const int *>(sb + L.col) : a.scol + d.e0;
-        spmv_tile<KS>(a, tile, d, col, reinterpret_cast<const double *>(sb + L.val),
+        spmv_tile<KS, GEN>(a, tile, d, col, reinterpret_cast<const double *>(sb + L.val),
                       staged(sb + L.sp, a.sp, d.s0, d.s1 + 1), staged(sb + L.meta, a.meta, d.lo, d.hi), s_pat, ws,
                       mode, first, beta);
       } else {
-        spmv_tile<KS>(a, tile, d, a.scol + d.e0, a.sval + d.e0, a.sp + d.s0, a.meta + d.lo, s_pat, ws, mode, first,
+        spmv_tile<KS, GEN>(a, tile, d, a.scol + d.e0, a.sval + d.e0, a.sp + d.s0, a.meta + d.lo, s_pat, ws, mode, first,
                       beta);
       }
       ring_release(R, st);
@@ -1195,7 +1196,7 @@ __host__ __device__ inline StageLayout update_first_layout(const TileGeom &g) {
   return stage_layout(g.cap_e, sizeof(T), g.max_sl, g.cols != 0, true, 8, 8, 8, 8);
 }
 
-template <typename T>
+template <typename T, bool GEN>
 __global__ void __launch_bounds__(kWsThreads) k_update_first(const PassArgs<T> a, double *x, const double *p,
                                                                const double *q, double *r) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -1254,11 +1255,11 @@ __global__ void __launch_bounds__(kWsThreads) k_update_first(const PassArgs<T> a
       const bool scols = ok && a.g.cols && d.ngen > 0;
       const int *col = scols ? reinterpret_cast<const int *>(sb + L.col) : a.ib_col + d.ie0;
       if (ok)
-        bjac_first_body<T>(a, d, col, reinterpret_cast<const T *>(sb + L.val),
+        bjac_first_body<T, GEN>(a, d, col, reinterpret_cast<const T *>(sb + L.val),
                            staged(sb + L.sp, a.ib_sp, d.s0, d.s1 + 1), staged(sb + L.meta, a.meta, d.lo, d.hi), rv,
                            s_pat, s_w);
       else
-        bjac_first_body<T>(a, d, col, a.ib_val + d.ie0, a.ib_sp + d.s0, a.meta + d.lo, rv, s_pat, s_w);
+        bjac_first_body<T, GEN>(a, d, col, a.ib_val + d.ie0, a.ib_sp + d.s0, a.meta + d.lo, rv, s_pat, s_w);
       ring_release(R, st);
     }
     if (threadIdx.x == 0) tl_mark(a.st, 2, 1, true);
