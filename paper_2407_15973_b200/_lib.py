@@ -11,7 +11,9 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmpbjac.so")
+# MPB_LIB: an alternative build of the same library (A/B timing of compile-time
+# variants, tools/ab.py); it must still be an in-tree build
+LIB_PATH = os.environ.get("MPB_LIB") or os.path.join(_HERE, "libmpbjac.so")
 
 MPB_UNIFORM, MPB_FIXED_LOW, MPB_ADAPTIVE_HL, MPB_ADAPTIVE_LH = 0, 1, 2, 3
 

@@ -197,6 +197,8 @@ int pick_stages(K kernel, uint32_t stage_bytes) {
 template <typename K>
 int persistent_grid(K kernel, uint32_t dyn_smem, int64_t ntiles, int threads = kCtaThreads) {
   cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn_smem));
+  static const int carve = std::getenv("MPB_CARVEOUT") ? std::atoi(std::getenv("MPB_CARVEOUT")) : -1;
+  if (carve >= 0) cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, dyn_smem) != cudaSuccess ||
       per_sm < 1)
@@ -1500,9 +1502,9 @@ static int solve_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, con
   init.dist = dc ? 1 : 0;
   static const bool timeline = std::getenv("MPB_TIMELINE") != nullptr;
   if (timeline) {  // diagnostics: per-iteration kernel timestamps (summary on stderr)
-    if (h->d_tl == nullptr) MPB_CUDA(cudaMalloc(&h->d_tl, sizeof(unsigned long long) * kTlIters * 12));
-    std::vector<unsigned long long> t0(kTlIters * 12);
-    for (int i = 0; i < kTlIters * 12; i++) t0[i] = (i % 4 == 0) ? ~0ull : 0ull;
+    if (h->d_tl == nullptr) MPB_CUDA(cudaMalloc(&h->d_tl, sizeof(unsigned long long) * kTlIters * kTlStride));
+    std::vector<unsigned long long> t0(kTlIters * kTlStride);
+    for (int i = 0; i < kTlIters * kTlStride; i++) t0[i] = (i % 4 == 0) ? ~0ull : 0ull;
     MPB_CUDA(cudaMemcpy(h->d_tl, t0.data(), sizeof(unsigned long long) * t0.size(), cudaMemcpyHostToDevice));
     init.tl = h->d_tl;
   }
@@ -1638,21 +1640,31 @@ static int solve_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, con
   MPB_CUDA(cudaMemsetAsync(h->d_ctr, 0, 16 * sizeof(unsigned int), s));
   if (timeline) {
     MPB_CUDA(cudaStreamSynchronize(s));
-    std::vector<unsigned long long> t(kTlIters * 12);
+    std::vector<unsigned long long> t(kTlIters * kTlStride);
     MPB_CUDA(cudaMemcpy(t.data(), h->d_tl, sizeof(unsigned long long) * t.size(), cudaMemcpyDeviceToHost));
     const long long last = std::min<long long>(h->h_state->last_it, kTlIters - 1);
     double acc[3][4] = {};  // per kernel: gap (start - previous step), body (end - start), tail (step - end),
                             // of which the last CTA's reduction + step (step - last CTA known)
     long long cnt = 0;
+    std::vector<double> gaps[3];
+    double ent[3] = {};
+    long long ent_n = 0;  // per kernel, for the median (graph-body boundaries skew the mean)
     for (long long it = 5; it < last; it++) {
-      const unsigned long long *r = &t[it * 12];
-      const unsigned long long prev = (&t[(it - 1) * 12])[2 * 4 + 2];
+      const unsigned long long *r = &t[it * kTlStride];
+      const unsigned long long prev = (&t[(it - 1) * kTlStride])[2 * 4 + 2];
       const unsigned long long stp[3] = {prev, r[0 * 4 + 2], r[1 * 4 + 2]};
       bool ok = prev != 0;
       for (int k = 0; k < 3; k++) ok = ok && r[k * 4] != ~0ull && r[k * 4 + 1] && r[k * 4 + 2];
       if (!ok) continue;
       for (int k = 0; k < 3; k++) {
         acc[k][0] += 1e-3 * double(r[k * 4] - stp[k]);
+        gaps[k].push_back(1e-3 * double(r[k * 4] - stp[k]));
+        if (k == 0 && r[12] != ~0ull && r[13] && r[15]) {  // last pass CTA entries relative to the previous step
+          ent[0] += 1e-3 * (double(r[12]) - double(prev));
+          ent[1] += 1e-3 * (double(r[13]) - double(prev));
+          ent[2] += 1e-3 * (double(r[15]) - double(prev));
+          ent_n++;
+        }
         acc[k][1] += 1e-3 * double(r[k * 4 + 1] - r[k * 4]);
         acc[k][2] += 1e-3 * double(r[k * 4 + 2] - r[k * 4 + 1]);
         if (r[k * 4 + 3]) acc[k][3] += 1e-3 * double(r[k * 4 + 2] - r[k * 4 + 3]);
@@ -1660,11 +1672,17 @@ static int solve_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, con
       cnt++;
     }
     const char *nm[3] = {"last pass", "spmv+p", "update+first"};
-    for (int k = 0; k < 3 && cnt; k++)
+    if (ent_n)
+      std::fprintf(stderr, "[mpb timeline] last pass CTA entry after the previous step: first %6.2f us, last %6.2f us;"
+                           " last CTA past its grid wait %6.2f us\n", ent[0] / ent_n, ent[1] / ent_n, ent[2] / ent_n);
+    for (int k = 0; k < 3 && cnt; k++) {
+      std::sort(gaps[k].begin(), gaps[k].end());
       std::fprintf(stderr,
-                   "[mpb timeline] %-12s gap %6.2f us  body %6.2f us  tail %6.2f us (last-CTA sum+step %5.2f)"
-                   "  (mean of %lld iterations)\n",
-                   nm[k], acc[k][0] / cnt, acc[k][1] / cnt, acc[k][2] / cnt, acc[k][3] / cnt, cnt);
+                   "[mpb timeline] %-12s gap %6.2f us (median %5.2f, max %6.2f)  body %6.2f us  tail %6.2f us "
+                   "(last-CTA sum+step %5.2f)  (mean of %lld iterations)\n",
+                   nm[k], acc[k][0] / cnt, gaps[k][gaps[k].size() / 2], gaps[k].back(), acc[k][1] / cnt,
+                   acc[k][2] / cnt, acc[k][3] / cnt, cnt);
+    }
   }
   const SolverState st = *h->h_state;
   if (st.error == kOk) {  // final true residual (solver.py:179-182)

@@ -67,10 +67,11 @@ struct SolverState {
   unsigned long long *tl;   // diagnostics (MPB_TIMELINE): per-iteration kernel timestamps, or null
 };
 
-// MPB_TIMELINE: tl[(it % kTlIters) * 12 + kind * 4 + f], kind 0 last pass,
+// MPB_TIMELINE: tl[(it % kTlIters) * kTlStride + kind * 4 + f], kind 0 last pass,
 // 1 SpMV, 2 fused update; f 0 first consumer start, 1 last consumer end,
 // 2 scalar step (globaltimer ns)
 constexpr int kTlIters = 1024;
+constexpr int kTlStride = 16;  // kinds 0-2 as above; kind 3: last-pass CTA entry min / max, post-wait max
 __device__ __forceinline__ unsigned long long globaltimer_now() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -83,8 +84,17 @@ __device__ __forceinline__ void tl_mark(const SolverState *st, int kind, int f, 
   return;
 #endif
   if (st == nullptr || st->tl == nullptr) return;
-  unsigned long long *p = st->tl + (st->it % kTlIters) * 12 + kind * 4 + f;
+  unsigned long long *p = st->tl + (st->it % kTlIters) * kTlStride + kind * 4 + f;
   const unsigned long long t = globaltimer_now();
+  if (is_max) atomicMax(p, t); else atomicMin(p, t);
+}
+// the same with a time taken earlier (e.g. at CTA entry, before st->it is final)
+__device__ __forceinline__ void tl_mark_at(const SolverState *st, int kind, int f, bool is_max, unsigned long long t) {
+#ifndef MPB_TIMELINE
+  return;
+#endif
+  if (st == nullptr || st->tl == nullptr) return;
+  unsigned long long *p = st->tl + (st->it % kTlIters) * kTlStride + kind * 4 + f;
   if (is_max) atomicMax(p, t); else atomicMin(p, t);
 }
 

@@ -43,6 +43,19 @@ constexpr int kConsumers = kCtaThreads / kRowsPerThread;  // compute threads of 
 constexpr int kWsThreads = kConsumers + 32;    // + one TMA producer warp
 static_assert(kWsThreads >= kFinThreads, "the last CTA's fin_sum uses kFinThreads threads");
 constexpr int kMaxStages = 4;
+// MPB_MINB_PASS / MPB_MINB_SPMV=n (experiments): compile the warp-specialised
+// kernels for n co-resident CTAs per SM (caps their registers).  Unset: no
+// minimum (not the same as 1 -- ptxas then picks the register budget itself)
+#ifdef MPB_MINB_PASS
+#define MPB_WS_BOUNDS_PASS __launch_bounds__(kWsThreads, MPB_MINB_PASS)
+#else
+#define MPB_WS_BOUNDS_PASS __launch_bounds__(kWsThreads)
+#endif
+#ifdef MPB_MINB_SPMV
+#define MPB_WS_BOUNDS_SPMV __launch_bounds__(kWsThreads, MPB_MINB_SPMV)
+#else
+#define MPB_WS_BOUNDS_SPMV __launch_bounds__(kWsThreads)
+#endif
 constexpr int kBarConsumers = 1;               // named barrier id among consumers
 constexpr uint16_t kMetaGeneric = 0xFFFFu;
 
@@ -86,9 +99,12 @@ __device__ __forceinline__ int choose_branch(int kind, double tol, double relres
   return relres >= tol ? 1 : 0;
 }
 
-// the solve graph's device-side loop continues while the solve is not done
+// the solve graph's device-side loop continues while the solve is not done.
+// The while condition is 1 from the graph launch on (cudaGraphCondAssignDefault)
+// and only ever needs clearing: cudaGraphSetConditional delays the grid's
+// completion by ~2.5 us, so it is called once, when the solve is done.
 __device__ __forceinline__ void set_loop(const SolverState *st) {
-  if (st->cond != 0ull) cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(st->cond), st->done ? 0u : 1u);
+  if (st->cond != 0ull && st->done) cudaGraphSetConditional(static_cast<cudaGraphConditionalHandle>(st->cond), 0u);
 }
 
 __device__ __forceinline__ void fail(SolverState *st, int code, double val) {
@@ -186,21 +202,59 @@ __device__ __noinline__ void scalar_step(int step, double tot, SolverState *st) 
   }
 }
 
+// The scalar steps run on a register/local copy of the state: one batch of
+// independent loads instead of a chain of dependent global round trips (the
+// step sits on the critical path between two kernels).  state_store writes
+// back what a step may change: the scalars (rho .. ovf_first) and the flags
+// (dist .. pad) -- not the trace pointers, tickets, all-reduce buffers, loop
+// handle or diagnostics pointer.
+constexpr int kStWords = static_cast<int>(sizeof(SolverState) / 8);
+static_assert(sizeof(SolverState) % 8 == 0, "state words");
+static_assert(offsetof(SolverState, tr_relres) % 8 == 0 && offsetof(SolverState, dist) % 8 == 0 &&
+                  offsetof(SolverState, cond) % 8 == 0,
+              "state write-back ranges");
+__device__ __forceinline__ void state_store(SolverState *g, const SolverState &L) {
+  const unsigned long long *s = reinterpret_cast<const unsigned long long *>(&L);
+  unsigned long long *d = reinterpret_cast<unsigned long long *>(g);
+#pragma unroll
+  for (int i = 0; i < static_cast<int>(offsetof(SolverState, tr_relres) / 8); i++) d[i] = s[i];
+#pragma unroll
+  for (int i = static_cast<int>(offsetof(SolverState, dist) / 8); i < static_cast<int>(offsetof(SolverState, cond) / 8);
+       i++)
+    d[i] = s[i];
+}
+__device__ __forceinline__ void state_load(SolverState &L, const SolverState *g) {
+  const unsigned long long *s = reinterpret_cast<const unsigned long long *>(g);
+  unsigned long long *d = reinterpret_cast<unsigned long long *>(&L);
+#pragma unroll
+  for (int i = 0; i < kStWords; i++) d[i] = __ldcg(s + i);
+}
+
 // After a kernel's CTAs have written all tile partials: the CTA that
 // finishes last reduces them in the fixed order and runs the scalar step.
+// The state is fetched into shared memory while the partials are summed.
 // Called by all threads of the CTA.
 __device__ __forceinline__ void finish_grid(SolverState *st, int ticket, int step, const double *part, int ntiles,
                                             double *ws) {
   if (st == nullptr) return;
   if (!grid_last(&st->ticket[ticket])) return;
+  __shared__ __align__(16) unsigned long long s_state[kStWords];
+  if (threadIdx.x < kStWords) s_state[threadIdx.x] = __ldcg(reinterpret_cast<const unsigned long long *>(st) + threadIdx.x);
   if (threadIdx.x == 0) tl_mark(st, step == kStepRho ? 0 : (step == kStepPq ? 1 : 2), 3, true);  // diagnostics
-  const double tot = fin_sum(part, ntiles, ws);
+  const double tot = fin_sum(part, ntiles, ws);  // (its barriers publish s_state)
   if (threadIdx.x == 0) {
-    if (st->dist) {  // multi-GPU: all-reduce first, k_apply_step runs the step
+    SolverState L;
+    {
+      unsigned long long *d = reinterpret_cast<unsigned long long *>(&L);
+#pragma unroll
+      for (int i = 0; i < kStWords; i++) d[i] = s_state[i];
+    }
+    if (L.dist) {  // multi-GPU: all-reduce first, k_apply_step runs the step
       st->red_local[0] = tot;
-      st->red_local[1] = static_cast<double>(st->ovf_count);
+      st->red_local[1] = static_cast<double>(L.ovf_count);
     } else {
-      scalar_step(step, tot, st);
+      scalar_step(step, tot, &L);
+      state_store(st, L);
     }
     st->ticket[ticket] = 0u;
   }
@@ -210,10 +264,13 @@ __device__ __forceinline__ void finish_grid(SolverState *st, int ticket, int ste
 // same state from the same global values)
 __global__ void k_apply_step(int step, SolverState *st, int gate) {
   if (threadIdx.x != 0) return;
-  if (gate == 1 && !st->true_pending) return;
-  if (gate == 2 && st->done) return;
-  if (step == kStepRho) st->ovf_count = static_cast<unsigned long long>(st->red_global[1]);
-  scalar_step(step, st->red_global[0], st);
+  SolverState L;
+  state_load(L, st);
+  if (gate == 1 && !L.true_pending) return;
+  if (gate == 2 && L.done) return;
+  if (step == kStepRho) L.ovf_count = static_cast<unsigned long long>(L.red_global[1]);
+  scalar_step(step, L.red_global[0], &L);
+  state_store(st, L);
 }
 
 // U independent tile sums at once (same order as block_tree<kTileThreads>
@@ -797,12 +854,15 @@ __host__ __device__ inline StageLayout bjac_layout(const TileGeom &g) {
 
 // Persistent, warp-specialised fused pass.
 template <typename T, bool FIRST, bool LAST, bool R64, int KS, bool GEN>
-__global__ void __launch_bounds__(kWsThreads) k_bjac_tile(const PassArgs<T> a) {
+__global__ void MPB_WS_BOUNDS_PASS k_bjac_tile(const PassArgs<T> a) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ Ring R;
   __shared__ T s_w[kTileRows];
   __shared__ double ws[32];
   __shared__ int s_pat[kPatMax * kPatStride];
+#ifdef MPB_TIMELINE
+  const unsigned long long t_entry = globaltimer_now();
+#endif
   const int ns = a.g.ns;
   constexpr bool kIB = FIRST && !LAST;  // first pass alone: in-block entries only
   const StageLayout L = bjac_layout<T, FIRST, R64>(a.g);
@@ -829,7 +889,14 @@ __global__ void __launch_bounds__(kWsThreads) k_bjac_tile(const PassArgs<T> a) {
   } else {
     pdl_wait();
     if (gated_off(a)) return;
-    if (LAST && threadIdx.x == 0) tl_mark(a.st, 0, 0, false);
+    if (LAST && threadIdx.x == 0) {
+      tl_mark(a.st, 0, 0, false);
+#ifdef MPB_TIMELINE
+      tl_mark_at(a.st, 3, 0, false, t_entry);
+      tl_mark_at(a.st, 3, 1, true, t_entry);
+      tl_mark(a.st, 3, 3, true);
+#endif
+    }
     for (RingCursor cur;; cur.advance(ns)) {
       const int st = cur.st;
       mbar_wait(&R.full[st], cur.phase);
@@ -1076,7 +1143,7 @@ __device__ __forceinline__ void spmv_tile(const SpmvArgs &a, int tile, const Til
 }
 
 template <int KS, bool GEN>
-__global__ void __launch_bounds__(kWsThreads) k_spmv_pq(const SpmvArgs a) {
+__global__ void MPB_WS_BOUNDS_SPMV k_spmv_pq(const SpmvArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ Ring R;
   __shared__ double ws[32];
@@ -1197,7 +1264,7 @@ __host__ __device__ inline StageLayout update_first_layout(const TileGeom &g) {
 }
 
 template <typename T, bool GEN>
-__global__ void __launch_bounds__(kWsThreads) k_update_first(const PassArgs<T> a, double *x, const double *p,
+__global__ void MPB_WS_BOUNDS_PASS k_update_first(const PassArgs<T> a, double *x, const double *p,
                                                                const double *q, double *r) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ Ring R;
@@ -1314,7 +1381,12 @@ __global__ void __launch_bounds__(kCtaThreads)
 
 // one-thread scalar step (solve start: wall-clock origin of the trace)
 __global__ void k_scalar_start(SolverState *st) {
-  if (threadIdx.x == 0) scalar_step(kStepStart, 0.0, st);
+  if (threadIdx.x == 0) {
+    SolverState L;
+    state_load(L, st);
+    scalar_step(kStepStart, 0.0, &L);
+    state_store(st, L);
+  }
 }
 
 __global__ void k_fill(double *p, long long n, double v) {
