@@ -158,18 +158,21 @@ __device__ __forceinline__ R block_tree_nb(R v, R *ws, int bar) {
 // kFinThreads contribute nothing); result valid in thread 0.  Partials are
 // read through L2 (__ldcg): other SMs wrote them in the same kernel.  Loads
 // are issued in batches of 8 before the (ordered) adds.
+// B: loads in flight per lane (16 halves the L2 round trips of 8; kernels
+// whose register budget it would raise keep 8)
+template <int B = 16>
 __device__ __forceinline__ double fin_sum(const double *part, long long count, double *ws) {
   double acc = 0.0;
   if (threadIdx.x < kFinThreads) {
-    for (long long i0 = threadIdx.x; i0 < count; i0 += 8LL * kFinThreads) {
-      double v[8];
+    for (long long i0 = threadIdx.x; i0 < count; i0 += (long long)B * kFinThreads) {
+      double v[B];
 #pragma unroll
-      for (int u = 0; u < 8; u++) {
+      for (int u = 0; u < B; u++) {
         const long long i = i0 + (long long)u * kFinThreads;
         v[u] = i < count ? __ldcg(part + i) : 0.0;
       }
 #pragma unroll
-      for (int u = 0; u < 8; u++)
+      for (int u = 0; u < B; u++)
         if (i0 + (long long)u * kFinThreads < count) acc = __dadd_rn(acc, v[u]);
     }
   }
@@ -179,14 +182,25 @@ __device__ __forceinline__ double fin_sum(const double *part, long long count, d
 // Grid-wide "last CTA" detection: thread 0 fences (its tile partials become
 // visible) and takes a ticket; true in every thread of the CTA that finished
 // last among the kernel's gridDim.x CTAs.  Must be called by all threads.
+// The ticket is one acq_rel atomic: release publishes the CTA's writes
+// (ordered before it by the barrier, cumulatively), acquire makes every other
+// CTA's released writes visible to the last one.  MPB_FENCED_TICKET=1 restores
+// the fence / atomic / fence sequence.
 __device__ __forceinline__ bool grid_last(unsigned int *ticket) {
   __shared__ int am_last;
+  __syncthreads();
   if (threadIdx.x == 0) {
+#ifdef MPB_FENCED_TICKET
     __threadfence();
     am_last = atomicAdd(ticket, 1u) == gridDim.x - 1u;
+    if (am_last) __threadfence();
+#else
+    unsigned int old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(ticket) : "memory");
+    am_last = old == gridDim.x - 1u;
+#endif
   }
   __syncthreads();
-  if (am_last) __threadfence();
   return am_last != 0;
 }
 

@@ -234,6 +234,7 @@ __device__ __forceinline__ void state_load(SolverState &L, const SolverState *g)
 // finishes last reduces them in the fixed order and runs the scalar step.
 // The state is fetched into shared memory while the partials are summed.
 // Called by all threads of the CTA.
+template <int B = 16>
 __device__ __forceinline__ void finish_grid(SolverState *st, int ticket, int step, const double *part, int ntiles,
                                             double *ws) {
   if (st == nullptr) return;
@@ -241,7 +242,7 @@ __device__ __forceinline__ void finish_grid(SolverState *st, int ticket, int ste
   __shared__ __align__(16) unsigned long long s_state[kStWords];
   if (threadIdx.x < kStWords) s_state[threadIdx.x] = __ldcg(reinterpret_cast<const unsigned long long *>(st) + threadIdx.x);
   if (threadIdx.x == 0) tl_mark(st, step == kStepRho ? 0 : (step == kStepPq ? 1 : 2), 3, true);  // diagnostics
-  const double tot = fin_sum(part, ntiles, ws);  // (its barriers publish s_state)
+  const double tot = fin_sum<B>(part, ntiles, ws);  // (its barriers publish s_state)
   if (threadIdx.x == 0) {
     SolverState L;
     {
@@ -1332,7 +1333,7 @@ __global__ void MPB_WS_BOUNDS_PASS k_update_first(const PassArgs<T> a, double *x
     if (threadIdx.x == 0) tl_mark(a.st, 2, 1, true);
   }
   pdl_trigger();
-  finish_grid(a.st, 2, kStepRrZ, a.part, a.g.ntiles, ws);
+  finish_grid<8>(a.st, 2, kStepRrZ, a.part, a.g.ntiles, ws);  // 16 would cost it a CTA per SM
 }
 
 // res = b - A x (or b), optionally stored; res.res partial; the last CTA runs
