@@ -116,7 +116,9 @@ __device__ __forceinline__ void fail(SolverState *st, int code, double val) {
 }
 
 // Executed by one thread once the global sum `tot` of a step is known.
-__device__ __noinline__ void scalar_step(int step, double tot, SolverState *st) {
+// Inlined where the step is a constant (the switch folds), on a state copy
+// in shared memory (finish_grid) or registers.
+__device__ __forceinline__ void scalar_step_body(int step, double tot, SolverState *st) {
   switch (step) {
     case kStepR0: {
       st->r0 = sqrt(tot);
@@ -202,6 +204,8 @@ __device__ __noinline__ void scalar_step(int step, double tot, SolverState *st) 
   }
 }
 
+__device__ __noinline__ void scalar_step(int step, double tot, SolverState *st) { scalar_step_body(step, tot, st); }
+
 // The scalar steps run on a register/local copy of the state: one batch of
 // independent loads instead of a chain of dependent global round trips (the
 // step sits on the critical path between two kernels).  state_store writes
@@ -243,21 +247,26 @@ __device__ __forceinline__ void finish_grid(SolverState *st, int ticket, int ste
   if (threadIdx.x < kStWords) s_state[threadIdx.x] = __ldcg(reinterpret_cast<const unsigned long long *>(st) + threadIdx.x);
   if (threadIdx.x == 0) tl_mark(st, step == kStepRho ? 0 : (step == kStepPq ? 1 : 2), 3, true);  // diagnostics
   const double tot = fin_sum<B>(part, ntiles, ws);  // (its barriers publish s_state)
+  SolverState *L = reinterpret_cast<SolverState *>(s_state);
+  const bool dist = L->dist != 0;
   if (threadIdx.x == 0) {
-    SolverState L;
-    {
-      unsigned long long *d = reinterpret_cast<unsigned long long *>(&L);
-#pragma unroll
-      for (int i = 0; i < kStWords; i++) d[i] = s_state[i];
-    }
-    if (L.dist) {  // multi-GPU: all-reduce first, k_apply_step runs the step
+    if (dist) {  // multi-GPU: all-reduce first, k_apply_step runs the step
       st->red_local[0] = tot;
-      st->red_local[1] = static_cast<double>(L.ovf_count);
+      st->red_local[1] = static_cast<double>(L->ovf_count);
     } else {
-      scalar_step(step, tot, &L);
-      state_store(st, L);
+      scalar_step_body(step, tot, L);
     }
     st->ticket[ticket] = 0u;
+  }
+  if (!dist && threadIdx.x < 32) {  // warp 0 writes the changed state back (state_store's ranges)
+    __syncwarp();
+    unsigned long long *d = reinterpret_cast<unsigned long long *>(st);
+    constexpr int a1 = static_cast<int>(offsetof(SolverState, tr_relres) / 8);
+    constexpr int b0 = static_cast<int>(offsetof(SolverState, dist) / 8), b1 = static_cast<int>(offsetof(SolverState, cond) / 8);
+    for (int i = threadIdx.x; i < a1 + (b1 - b0); i += 32) {
+      const int w = i < a1 ? i : b0 + (i - a1);
+      d[w] = s_state[w];
+    }
   }
 }
 
