@@ -171,7 +171,15 @@ double orc_tree_sum(i64 ntiles, const i64 *tile_lo, const double *vals) {
   OMP_FOR for (i64 t = 0; t < ntiles; t++)
     part[t] = lane_tree(tile_lo[t + 1] - tile_lo[t], MPB_TILE_THREADS,
                         vals + tile_lo[t]);
-  double total = lane_tree(ntiles, MPB_FIN_THREADS, part);
+  /* two-level global sum: chunk sums, then the sum of the chunk sums */
+  i64 nch = (ntiles + MPB_CHUNK_TILES - 1) / MPB_CHUNK_TILES;
+  double *csum = (double *)malloc(sizeof(double) * (nch > 0 ? nch : 1));
+  for (i64 c = 0; c < nch; c++) {
+    i64 t0 = c * MPB_CHUNK_TILES, t1 = t0 + MPB_CHUNK_TILES < ntiles ? t0 + MPB_CHUNK_TILES : ntiles;
+    csum[c] = lane_tree(t1 - t0, MPB_CHUNK_TILES, part + t0);
+  }
+  double total = lane_tree(nch, MPB_FIN_THREADS, csum);
+  free(csum);
   free(part);
   return total;
 }

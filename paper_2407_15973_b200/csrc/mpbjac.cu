@@ -157,6 +157,13 @@ TileGeom geom_for(const mpb_plan *p) {
   return g;
 }
 
+// The chunk sums follow the tile partials in the solve workspace (carve);
+// kernels launched with a solve state find them from the partials pointer.
+double *chunk_sum_of(const mpb_plan *p, double *part) {
+  return part ? reinterpret_cast<double *>(reinterpret_cast<char *>(part) + al256(sizeof(double) * (p->ntiles + 1)))
+              : nullptr;
+}
+
 int g_num_sms = 0;
 int num_sms() {
   if (g_num_sms == 0) {
@@ -367,6 +374,7 @@ int launch_apply(mpb_handle *h, cudaStream_t s, const mpb_plan *p, const mpb_csr
   a.ovf_count = ovf_count;
   a.ovf_first = ovf_first;
   a.st = st;
+  a.csum = st ? chunk_sum_of(p, part) : nullptr;
   a.want_branch = want_branch;
   a.pdl = (st != nullptr && dc == nullptr) ? 1 : 0;  // captured single-GPU iteration
   a.gate = z1_gate;
@@ -418,6 +426,7 @@ int launch_update_first(mpb_handle *h, cudaStream_t s, const mpb_plan *p, const 
   a.ovf_count = ovf_count;
   a.ovf_first = ovf_first;
   a.st = st;
+  a.csum = st ? chunk_sum_of(p, part) : nullptr;
   a.want_branch = want_branch;
   a.gate = 2;
   a.prefetch = prefetch;
@@ -486,6 +495,7 @@ struct SolveWs {
   double *res64, *dg64, *wA64, *wB64;
   float *res32, *dg32, *wA32, *wB32;
   double *part;
+  double *csum;        // chunk sums of the two-level dot sums (part: all slots kPartEmpty between kernels)
   SolverState *st;
   size_t bytes;
 };
@@ -523,10 +533,13 @@ SolveWs carve(const mpb_plan *p, int64_t n, char *base, int64_t ng = 0) {
     w.wB32 = (float *)take(f);
   }
   w.part = (double *)take(sizeof(double) * (p->ntiles + 1));
+  w.csum = (double *)take(sizeof(double) * ((p->ntiles + kChunkTiles - 1) / kChunkTiles + 1));
   w.st = (SolverState *)take(sizeof(SolverState));
   w.bytes = off;
   return w;
 }
+
+
 
 }  // namespace
 
@@ -879,6 +892,22 @@ int mpb_block_jacobi_sweeps_f32(mpb_handle *h, const int32_t *row_ptr, const int
   return sweeps_impl<float>(h, row_ptr, col_idx, val, in_block, diag, t, r, y, tmp, row_start, row_end);
 }
 
+// Global sum of nt tile partials in the two-level order: chunk sums into
+// csum (nt/256 + 1 entries of scratch), then the final level into *out.
+template <typename ACC>
+static int launch_fin(mpb_handle *h, const ACC *part, int64_t nt, ACC *csum, ACC *out) {
+  const int64_t nch = (nt + kChunkTiles - 1) / kChunkTiles;
+  const int per = kTileThreads / 32;
+  if (nch > 0) {
+    k_chunk_sums<ACC><<<static_cast<unsigned>((nch + per - 1) / per), kTileThreads, 0, h->user>>>(part, nt, csum);
+    MPB_LAUNCHED(h);
+  }
+  k_fin<ACC><<<1, kFinThreads, 0, h->user>>>(csum, nch, out);
+  MPB_LAUNCHED(h);
+  return MPB_OK;
+}
+static size_t chunk_scratch(size_t es, int64_t nt) { return al256(es * ((nt + kChunkTiles - 1) / kChunkTiles + 1)); }
+
 template <typename T, typename ACC, bool SQ>
 static int tile_reduce(mpb_handle *h, const mpb_plan *plan, int64_t n, const T *x, const T *y, ACC *h_out) {
   if (!h || !h_out || n < 0) return MPB_ERR_ARG;
@@ -888,15 +917,15 @@ static int tile_reduce(mpb_handle *h, const mpb_plan *plan, int64_t n, const T *
   }
   if (plan && plan->n != n) return MPB_ERR_SHAPE;
   const int64_t nt = plan ? plan->ntiles : (n + kTileRows - 1) / kTileRows;
-  int rc = ensure_scratch(h, al256(sizeof(ACC) * (nt + 1)) + 256);
+  int rc = ensure_scratch(h, al256(sizeof(ACC) * (nt + 1)) + chunk_scratch(sizeof(ACC), nt) + 256);
   if (rc) return rc;
   ACC *part = static_cast<ACC *>(h->scratch);
-  ACC *res = reinterpret_cast<ACC *>(static_cast<char *>(h->scratch) + al256(sizeof(ACC) * (nt + 1)));
+  ACC *csum = reinterpret_cast<ACC *>(static_cast<char *>(h->scratch) + al256(sizeof(ACC) * (nt + 1)));
+  ACC *res = reinterpret_cast<ACC *>(reinterpret_cast<char *>(csum) + chunk_scratch(sizeof(ACC), nt));
   k_tile_dot<T, ACC, SQ><<<static_cast<unsigned>(nt), kTileThreads, 0, h->user>>>(n, plan ? plan->d_tile_lo : nullptr,
                                                                                  x, y, part);
   MPB_LAUNCHED(h);
-  k_fin<ACC><<<1, kFinThreads, 0, h->user>>>(part, nt, res);
-  MPB_LAUNCHED(h);
+  if ((rc = launch_fin<ACC>(h, part, nt, csum, res))) return rc;
   MPB_CUDA(cudaMemcpyAsync(h_out, res, sizeof(ACC), cudaMemcpyDeviceToHost, h->user));
   MPB_CUDA(cudaStreamSynchronize(h->user));
   return MPB_OK;
@@ -1265,6 +1294,7 @@ static SpmvArgs spmv_args(const mpb_handle *h, const mpb_plan *p, const mpb_csr 
   sa.q = w.q;
   sa.part = w.part;
   sa.st = w.st;
+  sa.csum = w.csum;
   return sa;
 }
 
@@ -1378,7 +1408,7 @@ static int enqueue_iteration(mpb_handle *h, cudaStream_t s, const mpb_plan *p, c
   } else {
     MPB_CUDA(launch_k(pdl, k_update, persistent_grid(k_update, 0, p->ntiles), kCtaThreads, 0, s,
                       static_cast<const TileDesc *>(p->d_td), static_cast<int>(nt), x,
-                      static_cast<const double *>(w.p), static_cast<const double *>(w.q), w.r, w.part, w.st));
+                      static_cast<const double *>(w.p), static_cast<const double *>(w.q), w.r, w.part, w.st, w.csum));
     MPB_LAUNCHED(h);
   }
   if ((rc = dist_step(h, dc, w.st, fused ? kStepRrZ : kStepRr, 2, s))) return rc;
@@ -1386,7 +1416,7 @@ static int enqueue_iteration(mpb_handle *h, cudaStream_t s, const mpb_plan *p, c
     if ((rc = halo_exchange(dc, x, 8, A->n, s))) return rc;
     k_resid<true><<<persistent_grid(k_resid<true>, 0, p->ntiles), kCtaThreads, 0, s>>>(
         A->sell->d_sp, A->sell->d_col, A->sell_val64, p->d_td, static_cast<int>(nt), b, x, nullptr, w.part, w.st, 1,
-        kStepTrue);
+        kStepTrue, w.csum);
     MPB_LAUNCHED(h);
     if ((rc = dist_step(h, dc, w.st, kStepTrue, 1, s))) return rc;
   }
@@ -1513,6 +1543,7 @@ static int solve_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, con
   // tile-claim counters start at zero (a launch gated off after prefetching
   // claims leaves its counter dirty; only the end of a solve gates so)
   MPB_CUDA(cudaMemsetAsync(h->d_ctr, 0, 16 * sizeof(unsigned int), s));
+  MPB_CUDA(cudaMemsetAsync(w.part, 0xFF, sizeof(double) * plan->ntiles, s));  // every slot kPartEmpty
   k_fill<<<elt_blocks(opt->max_iter), kEltThreads, 0, s>>>(tr_true, opt->max_iter, NAN);
   MPB_LAUNCHED(h);
   if (!opt->has_x0) MPB_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * A->n, s));
@@ -1521,11 +1552,11 @@ static int solve_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, con
     if ((rc = halo_exchange(dc, x, 8, A->n, s))) return rc;
     k_resid<true><<<persistent_grid(k_resid<true>, 0, plan->ntiles), kCtaThreads, 0, s>>>(
                                               A->sell->d_sp, A->sell->d_col, A->sell_val64, plan->d_td, static_cast<int>(nt), b, x, w.r, w.part, w.st, 0,
-                                              kStepR0);
+                                              kStepR0, w.csum);
   } else {
     k_resid<false><<<persistent_grid(k_resid<false>, 0, plan->ntiles), kCtaThreads, 0, s>>>(
                                                A->sell->d_sp, A->sell->d_col, A->sell_val64, plan->d_td, static_cast<int>(nt), b, nullptr, w.r, w.part, w.st,
-                                               0, kStepR0);
+                                               0, kStepR0, w.csum);
   }
   MPB_LAUNCHED(h);
   if ((rc = dist_step(h, dc, w.st, kStepR0, 0, s))) return rc;
@@ -1689,7 +1720,7 @@ static int solve_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, con
     if ((rc = halo_exchange(dc, x, 8, A->n, s))) return rc;
     k_resid<true><<<persistent_grid(k_resid<true>, 0, plan->ntiles), kCtaThreads, 0, s>>>(
                                               A->sell->d_sp, A->sell->d_col, A->sell_val64, plan->d_td, static_cast<int>(nt), b, x, nullptr, w.part, w.st, 0,
-                                              kStepFinal);
+                                              kStepFinal, w.csum);
     MPB_LAUNCHED(h);
     if ((rc = dist_step(h, dc, w.st, kStepFinal, 0, s))) return rc;
     MPB_CUDA(cudaMemcpyAsync(h->h_state, w.st, sizeof(SolverState), cudaMemcpyDeviceToHost, s));
@@ -1768,6 +1799,7 @@ static int profile_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, c
   mid.tr_branch = reinterpret_cast<int *>(w.zB64);
   mid.tr_time = reinterpret_cast<double *>(w.zB64) + 8;
   *h->h_state = mid;
+  MPB_CUDA(cudaMemsetAsync(w.part, 0xFF, sizeof(double) * plan->ntiles, s));  // every slot kPartEmpty
   auto reset = [&]() -> cudaError_t {
     return cudaMemcpyAsync(w.st, h->h_state, sizeof(SolverState), cudaMemcpyHostToDevice, s);
   };
@@ -1804,6 +1836,7 @@ static int profile_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, c
       a.t = opt->t;
       a.r64 = w.r;
       a.st = w.st;
+      a.csum = w.csum;
       a.want_branch = want;
       a.zin = first ? nullptr : ((pass - 1) & 1 ? zB : zA);
       a.zout = last ? zfinal : (pass & 1 ? zB : zA);
@@ -1864,7 +1897,7 @@ static int profile_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, c
   if (rc) return rc;
   rc = timed(4, [&]() -> int {
     k_update<<<ugrid, kCtaThreads, 0, s>>>(plan->d_td, static_cast<int>(nt), x, w.p, w.q, w.r, w.part,
-                                         w.st);
+                                         w.st, w.csum);
     MPB_LAUNCHED(h);
     return MPB_OK;
   });
@@ -1895,16 +1928,16 @@ int mpb_true_relres(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, const
   if (!h || !plan || !x || !b || !h_out) return MPB_ERR_ARG;
   if (plan->n != A->n) return MPB_ERR_PARTITION;
   const int64_t nt = plan->ntiles;
-  rc = ensure_scratch(h, al256(sizeof(double) * (nt + 1)) + 256);
+  rc = ensure_scratch(h, al256(sizeof(double) * (nt + 1)) + chunk_scratch(sizeof(double), nt) + 256);
   if (rc) return rc;
   double *part = static_cast<double *>(h->scratch);
-  double *out = reinterpret_cast<double *>(static_cast<char *>(h->scratch) + al256(sizeof(double) * (nt + 1)));
+  double *csum = reinterpret_cast<double *>(static_cast<char *>(h->scratch) + al256(sizeof(double) * (nt + 1)));
+  double *out = reinterpret_cast<double *>(reinterpret_cast<char *>(csum) + chunk_scratch(sizeof(double), nt));
   k_resid<true><<<persistent_grid(k_resid<true>, 0, nt), kCtaThreads, 0, h->user>>>(
       A->sell->d_sp, A->sell->d_col, A->sell_val64, plan->d_td, static_cast<int>(nt), b, x, nullptr,
-      part, nullptr, 0, kStepFinal);
+      part, nullptr, 0, kStepFinal, nullptr);
   MPB_LAUNCHED(h);
-  k_fin<double><<<1, kFinThreads, 0, h->user>>>(part, nt, out);
-  MPB_LAUNCHED(h);
+  if ((rc = launch_fin<double>(h, part, nt, csum, out))) return rc;
   double v;
   MPB_CUDA(cudaMemcpyAsync(&v, out, sizeof(double), cudaMemcpyDeviceToHost, h->user));
   MPB_CUDA(cudaStreamSynchronize(h->user));

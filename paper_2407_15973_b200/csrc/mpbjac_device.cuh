@@ -179,6 +179,121 @@ __device__ __forceinline__ double fin_sum(const double *part, long long count, d
   return block_tree<kFinThreads>(acc, ws);
 }
 
+// ---- two-level global sums (include/mpbjac_order.h) -------------------------
+constexpr int kChunkTiles = MPB_CHUNK_TILES;
+static_assert(kChunkTiles == 8 * 32, "a chunk sum is one warp emulating 8 warps of 32 lanes");
+
+// C_c = the tile-sum order over chunk c's partials (lane j of 256 holds
+// P[c*256 + j] or +0), computed by one warp: the 8 virtual warps'
+// butterflies, then the butterfly of their sums padded with +0.  All lanes
+// return C_c.  Partials written by other CTAs in this kernel: read via L2.
+template <typename R>
+__device__ __forceinline__ R chunk_sum_warp(const R *part, long long c, long long ntiles) {
+  const int lane = threadIdx.x & 31;
+  const long long base = c * kChunkTiles;
+  R v[kChunkTiles / 32];
+#pragma unroll
+  for (int w = 0; w < kChunkTiles / 32; w++) {
+    const long long i = base + 32 * w + lane;
+    v[w] = i < ntiles ? __ldcg(part + i) : R(0);
+  }
+#pragma unroll
+  for (int w = 0; w < kChunkTiles / 32; w++) v[w] = warp_bfly(v[w]);
+  R r = R(0);
+#pragma unroll
+  for (int w = 0; w < kChunkTiles / 32; w++)
+    if (lane == w) r = v[w];
+  return warp_bfly(r);
+}
+
+// Chunk sums while the kernel runs, without per-tile fences: a tile partial
+// is its own completion flag.  The partials array holds kPartEmpty (all
+// bits set, a NaN no tile sum is stored as) in every slot between kernels;
+// a tile's partial is one 8-byte relaxed store; the warp that owns chunk c
+// (the CTA that claimed the chunk's last tile) polls the chunk's slots with
+// relaxed loads until none is empty, sums them (chunk_sum order), stores
+// csum[c] and empties the slots for the next launch.  The kernel's final
+// CTA reads csum after the grid ticket (acq_rel).
+constexpr unsigned long long kPartEmpty = ~0ull;
+__device__ __forceinline__ void put_part(double *p, double v) {
+  unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
+  if (b == kPartEmpty) b = 0x7ff8000000000000ull;  // (still a NaN; the empty pattern stays unique)
+  asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(b) : "memory");
+}
+__device__ __forceinline__ unsigned long long get_part_bits(const double *p) {
+  unsigned long long b;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(b) : "l"(p) : "memory");
+  return b;
+}
+
+struct ChunkCtx {
+  double *csum;  // null: no chunk bookkeeping (plugin-level launch)
+  double *part;
+  int ntiles;
+};
+__device__ __forceinline__ bool chunk_final(int tile, int ntiles) {
+  return tile % kChunkTiles == kChunkTiles - 1 || tile == ntiles - 1;
+}
+// One warp; chunk c's slots polled once (block: until complete).  On
+// completion the chunk sum is stored and the slots emptied; returns whether
+// it completed.
+__device__ __forceinline__ bool chunk_poll(const ChunkCtx &ck, int c, bool block) {
+  const int lane = threadIdx.x & 31;
+  const int base = c * kChunkTiles + lane;  // (tile indices are int32)
+  const double *pb = ck.part + base;
+  const int lim = ck.ntiles - base;         // slot w is a tile iff 32 w < lim
+  for (;;) {
+    unsigned long long b[kChunkTiles / 32];
+    bool full = true;
+#pragma unroll
+    for (int w = 0; w < kChunkTiles / 32; w++) {
+      b[w] = 32 * w < lim ? get_part_bits(pb + 32 * w) : 0ull;  // (+0.0 beyond the last tile)
+      full = full && b[w] != kPartEmpty;
+    }
+    if (__all_sync(0xffffffffu, full)) {
+      double v[kChunkTiles / 32];
+#pragma unroll
+      for (int w = 0; w < kChunkTiles / 32; w++) v[w] = warp_bfly(__longlong_as_double(static_cast<long long>(b[w])));
+      double r = 0.0;
+#pragma unroll
+      for (int w = 0; w < kChunkTiles / 32; w++)
+        if (lane == w) r = v[w];
+      r = warp_bfly(r);
+      if (lane == 0) ck.csum[c] = r;
+#pragma unroll
+      for (int w = 0; w < kChunkTiles / 32; w++)
+        if (32 * w < lim) reinterpret_cast<unsigned long long *>(const_cast<double *>(pb))[32 * w] = kPartEmpty;
+      return true;
+    }
+    if (!block) return false;
+    __nanosleep(200);
+  }
+}
+// All chunks by the CTA that took the grid's last ticket (kernels whose
+// grid may exceed residency, so no CTA may wait for another): warps take
+// chunks round-robin; the slots are emptied.  Called by all threads.
+__device__ __forceinline__ void chunk_all_in_cta(const ChunkCtx &ck) {
+  if (ck.csum == nullptr) return;
+  const int nch = (ck.ntiles + kChunkTiles - 1) / kChunkTiles;
+  for (int c = threadIdx.x >> 5; c < nch; c += blockDim.x >> 5) {
+    const double v = chunk_sum_warp(static_cast<const double *>(ck.part), c, ck.ntiles);
+    if ((threadIdx.x & 31) == 0) ck.csum[c] = v;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < ck.ntiles; i += blockDim.x) reinterpret_cast<unsigned long long *>(ck.part)[i] = kPartEmpty;
+  __syncthreads();
+}
+// Non-warp-specialised persistent kernels (static walk tile0, tile0 +
+// stride, ...): after its tiles, warp 0 owns the chunks whose last tile it
+// processed.  Called by all threads.
+__device__ __forceinline__ void chunk_duties_strided(const ChunkCtx &ck, int tile0, int stride) {
+  if (ck.csum == nullptr) return;
+  __syncthreads();
+  if (threadIdx.x >= 32) return;
+  for (int t = tile0; t < ck.ntiles; t += stride)
+    if (chunk_final(t, ck.ntiles)) chunk_poll(ck, t / kChunkTiles, true);
+}
+
 // Grid-wide "last CTA" detection: thread 0 fences (its tile partials become
 // visible) and takes a ticket; true in every thread of the CTA that finished
 // last among the kernel's gridDim.x CTAs.  Must be called by all threads.
@@ -229,6 +344,17 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
       "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// non-blocking: has the phase with this parity completed?
+__device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
       " selp.u32 %0, 1, 0, p;\n}\n"
       : "=r"(ok)
       : "r"(smem_u32(bar)), "r"(parity)

@@ -43,6 +43,7 @@ constexpr int kConsumers = kCtaThreads / kRowsPerThread;  // compute threads of 
 constexpr int kWsThreads = kConsumers + 32;    // + one TMA producer warp
 static_assert(kWsThreads >= kFinThreads, "the last CTA's fin_sum uses kFinThreads threads");
 constexpr int kMaxStages = 4;
+constexpr int kMaxPend = 4;  // owned chunks a producer keeps pending
 // MPB_MINB_PASS / MPB_MINB_SPMV=n (experiments): compile the warp-specialised
 // kernels for n co-resident CTAs per SM (caps their registers).  Unset: no
 // minimum (not the same as 1 -- ptxas then picks the register budget itself)
@@ -51,6 +52,9 @@ constexpr int kMaxStages = 4;
 #else
 #define MPB_WS_BOUNDS_PASS __launch_bounds__(kWsThreads)
 #endif
+// the fused update is compiled for 5 CTAs per SM (its consumer path needs
+// 40 registers; the producer's chunk polling alone would raise the budget)
+#define MPB_WS_BOUNDS_UPDATE __launch_bounds__(kWsThreads, 5)
 #ifdef MPB_MINB_SPMV
 #define MPB_WS_BOUNDS_SPMV __launch_bounds__(kWsThreads, MPB_MINB_SPMV)
 #else
@@ -238,15 +242,20 @@ __device__ __forceinline__ void state_load(SolverState &L, const SolverState *g)
 // finishes last reduces them in the fixed order and runs the scalar step.
 // The state is fetched into shared memory while the partials are summed.
 // Called by all threads of the CTA.
+// The chunk sums of the two-level order are in ck.csum: their owners stored
+// them before their CTAs took the ticket (chunks_in_cta: the last CTA sums
+// them here).
 template <int B = 16>
-__device__ __forceinline__ void finish_grid(SolverState *st, int ticket, int step, const double *part, int ntiles,
-                                            double *ws) {
+__device__ __forceinline__ void finish_grid(SolverState *st, int ticket, int step, const ChunkCtx &ck, double *ws,
+                                            bool chunks_in_cta = false) {
   if (st == nullptr) return;
   if (!grid_last(&st->ticket[ticket])) return;
   __shared__ __align__(16) unsigned long long s_state[kStWords];
   if (threadIdx.x < kStWords) s_state[threadIdx.x] = __ldcg(reinterpret_cast<const unsigned long long *>(st) + threadIdx.x);
+  if (chunks_in_cta) chunk_all_in_cta(ck);
   if (threadIdx.x == 0) tl_mark(st, step == kStepRho ? 0 : (step == kStepPq ? 1 : 2), 3, true);  // diagnostics
-  const double tot = fin_sum<B>(part, ntiles, ws);  // (its barriers publish s_state)
+  const int nch = (ck.ntiles + kChunkTiles - 1) / kChunkTiles;
+  const double tot = fin_sum<B>(ck.csum, nch, ws);  // (its barriers publish s_state)
   SolverState *L = reinterpret_cast<SolverState *>(s_state);
   const bool dist = L->dist != 0;
   if (threadIdx.x == 0) {
@@ -364,6 +373,7 @@ struct Ring {
   int ok[kMaxStages];          // tile fitted and was staged
   int tile[kMaxStages];        // tile in the stage, -1: no more tiles
   TileDesc desc[kMaxStages];
+  int pend[kMaxPend];          // producer: owned chunks not yet summed
 };
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
@@ -448,61 +458,92 @@ __device__ __forceinline__ void produce(Ring &R, int st, const TileDesc *td, int
 // vector slices follow after the wait.  gated() is evaluated after the wait;
 // a gated-off launch drains its prefetched copies and stops (the solve
 // resets the claim counters at its start and end).
+//
+// The whole producer warp runs the loop (lane 0 claims and issues the
+// copies).  Chunk duties (ck.csum != null): claiming the last tile of a
+// chunk makes this warp the chunk's owner (chunk_poll).  Pending chunks are
+// polled while the producer would otherwise wait for a stage to come back,
+// and blocking after the last claim.  (Owners polling from a consumer warp
+// stall their CTA: measured slower.)
 template <typename F, typename G>
 __device__ __forceinline__ void producer_loop(Ring &R, int ntiles, int ns, unsigned int *ctr, bool prefetch,
-                                              G &&gated, F &&fill) {
+                                              G &&gated, F &&fill, const ChunkCtx &ck) {
+  const int lane = threadIdx.x & 31;
   int next = blockIdx.x;
   auto claim = [&]() -> int {
-    if (ctr != nullptr) {
-      const unsigned int v = atomicAdd(ctr, 1u);
-      if (v == static_cast<unsigned int>(ntiles) + gridDim.x - 1u) atomicExch(ctr, 0u);
-      return v < static_cast<unsigned int>(ntiles) ? static_cast<int>(v) : -1;
+    int t = -1;
+    if (lane == 0) {
+      if (ctr != nullptr) {
+        const unsigned int v = atomicAdd(ctr, 1u);
+        if (v == static_cast<unsigned int>(ntiles) + gridDim.x - 1u) atomicExch(ctr, 0u);
+        t = v < static_cast<unsigned int>(ntiles) ? static_cast<int>(v) : -1;
+      } else {
+        t = next < ntiles ? next : -1;
+      }
     }
-    const int t = next < ntiles ? next : -1;
     next += gridDim.x;
-    return t;
+    return __shfl_sync(0xffffffffu, t, 0);
+  };
+  // owned chunks not yet summed: a FIFO in shared memory, [phead, ptail)
+  int phead = 0, ptail = 0;
+  auto own = [&](int tile) {
+    if (ck.csum == nullptr || !chunk_final(tile, ntiles)) return;
+    if (ptail - phead == kMaxPend) chunk_poll(ck, R.pend[phead++ % kMaxPend], true);
+    if (lane == 0) R.pend[ptail % kMaxPend] = tile / kChunkTiles;
+    __syncwarp();
+    ptail++;
+  };
+  auto poll_oldest = [&](bool block) {
+    if (phead != ptail && chunk_poll(ck, R.pend[phead % kMaxPend], block)) phead++;
   };
   int npre = 0;
   bool exhausted = false;
   if (prefetch) {
     for (; npre < ns; npre++) {
       const int tile = claim();
-      R.tile[npre] = tile;
+      if (lane == 0) R.tile[npre] = tile;
       if (tile < 0) {
         exhausted = true;
         break;
       }
-      fill(npre, tile, kFillStatic);
+      if (lane == 0) fill(npre, tile, kFillStatic);
+      own(tile);
     }
   }
   pdl_wait();
   if (gated()) {
-    for (int i = 0; i < npre; i++) {  // let the copies land before the CTA exits
-      mbar_arrive(&R.full[i]);
-      mbar_wait(&R.full[i], 0);
+    if (lane == 0) {
+      for (int i = 0; i < npre; i++) {  // let the copies land before the CTA exits
+        mbar_arrive(&R.full[i]);
+        mbar_wait(&R.full[i], 0);
+      }
     }
+    __syncwarp();
     return;
   }
-  for (int i = 0; i < npre; i++) fill(i, R.tile[i], kFillDynamic);
-  if (exhausted) {
-    mbar_arrive(&R.full[npre]);
-    return;
-  }
+  if (lane == 0)
+    for (int i = 0; i < npre; i++) fill(i, R.tile[i], kFillDynamic);
   int st = npre % ns, rnd = npre / ns;  // stage, and how often it has been filled before
-  for (;;) {
-    if (rnd > 0) mbar_wait_sleep(&R.empty[st], (rnd - 1) & 1);
-    const int tile = claim();
-    R.tile[st] = tile;
-    if (tile < 0) {
-      mbar_arrive(&R.full[st]);
-      return;
-    }
-    fill(st, tile, kFillAll);
-    if (++st == ns) {
-      st = 0;
-      rnd++;
+  if (!exhausted) {
+    for (;;) {
+      if (rnd > 0) {
+        if (phead != ptail && !mbar_test(&R.empty[st], (rnd - 1) & 1)) poll_oldest(false);
+        mbar_wait_sleep(&R.empty[st], (rnd - 1) & 1);
+      }
+      const int tile = claim();
+      if (lane == 0) R.tile[st] = tile;
+      if (tile < 0) break;
+      if (lane == 0) fill(st, tile, kFillAll);
+      own(tile);
+      if (++st == ns) {
+        st = 0;
+        rnd++;
+      }
     }
   }
+  if (lane == 0) mbar_arrive(&R.full[st]);  // stage st holds the end marker (-1)
+  __syncwarp();
+  while (phead != ptail) poll_oldest(true);
 }
 
 // consumer-side ring cursor: stage and mbarrier parity of the i-th tile
@@ -562,6 +603,7 @@ struct PassArgs {
   T *resbuf;             // large-block path
   T *dbuf;
   SolverState *st;       // solve mode: gate + fused scalar step
+  double *csum;          // solve mode: chunk sums of the two-level r.z sum (ChunkCtx)
   int want_branch;
   int prefetch;          // stream the first tiles' matrix data before the grid dependency wait
   int gate;              // 0: st->branch; 1: also skip when the fused update ran this first pass;
@@ -776,7 +818,7 @@ __device__ __forceinline__ void bjac_tile_body(const PassArgs<T> &a, int tile, c
   }
   if (LAST && a.part != nullptr) {
     const double tot = tile_tree_rows(prod, ws, kBarConsumers);
-    if (threadIdx.x == 0) a.part[tile] = tot;
+    if (threadIdx.x == 0) put_part(a.part + tile, tot);
   }
 }
 
@@ -881,8 +923,8 @@ __global__ void MPB_WS_BOUNDS_PASS k_bjac_tile(const PassArgs<T> a) {
   if (threadIdx.x >= kConsumers) {  // producer warp
     using RT = typename std::conditional<R64, double, T>::type;
     const RT *rsrc = R64 ? reinterpret_cast<const RT *>(a.r64) : reinterpret_cast<const RT *>(a.rT);
-    if (threadIdx.x == kConsumers)
-      producer_loop(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, [&]() { return gated_off(a); },
+    const ChunkCtx ck{(LAST && a.part != nullptr && a.st != nullptr) ? a.csum : nullptr, a.part, a.g.ntiles};
+    producer_loop(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, [&]() { return gated_off(a); },
                     [&](int st, int tile, int part) {
                       if (kIB)
                         produce<T, RT, uint8_t, uint8_t, true>(R, st, a.td, tile, a.g, L, smem + st * L.bytes,
@@ -892,9 +934,7 @@ __global__ void MPB_WS_BOUNDS_PASS k_bjac_tile(const PassArgs<T> a) {
                         produce<T, RT, uint8_t, uint8_t>(R, st, a.td, tile, a.g, L, smem + st * L.bytes, a.sp,
                                                          a.scol, a.sval, a.meta, rsrc, nullptr, nullptr,
                                                          static_cast<const uint8_t *>(nullptr), part);
-                    });
-    else
-      pdl_wait();
+                    }, ck);
     if (gated_off(a)) return;
   } else {
     pdl_wait();
@@ -953,7 +993,8 @@ __global__ void MPB_WS_BOUNDS_PASS k_bjac_tile(const PassArgs<T> a) {
     if (LAST && threadIdx.x == 0) tl_mark(a.st, 0, 1, true);
   }
   pdl_trigger();  // dependents may launch into the SMs this grid drains
-  if (LAST && a.part != nullptr) finish_grid(a.st, 0, kStepRho, a.part, a.g.ntiles, ws);
+  if (LAST && a.part != nullptr)
+    finish_grid(a.st, 0, kStepRho, ChunkCtx{a.csum, a.part, a.g.ntiles}, ws);
 }
 
 // ---- large blocks (> kTileRows rows): one launch per inner sweep ----------
@@ -1014,8 +1055,9 @@ __global__ void __launch_bounds__(kCtaThreads) k_big_finish(const PassArgs<T> a,
   }
   if (LAST && a.part != nullptr) {
     const double tot = block_tree<kTileThreads>(prod, ws);
-    if (threadIdx.x == 0) a.part[tile] = tot;
-    finish_grid(a.st, 0, kStepRho, a.part, a.g.ntiles, ws);
+    if (threadIdx.x == 0) put_part(a.part + tile, tot);
+    // one CTA per tile (grid may exceed residency): the last CTA sums the chunks
+    finish_grid(a.st, 0, kStepRho, ChunkCtx{a.st != nullptr ? a.csum : nullptr, a.part, a.g.ntiles}, ws, true);
   }
 }
 
@@ -1079,6 +1121,7 @@ struct SpmvArgs {
   double *q;
   double *part;
   SolverState *st;
+  double *csum;        // chunk sums of the two-level p.q sum (ChunkCtx)
   int prefetch;     // see PassArgs::prefetch
 };
 
@@ -1135,7 +1178,7 @@ __device__ __forceinline__ void spmv_tile_body(const SpmvArgs &a, int tile, cons
     prod[k] = __dmul_rn(pown, acc);
   }
   const double tot = tile_tree_rows(prod, ws, kBarConsumers);
-  if (threadIdx.x == 0) a.part[tile] = tot;
+  if (threadIdx.x == 0) put_part(a.part + tile, tot);
 }
 
 __host__ __device__ inline StageLayout spmv_layout(const TileGeom &g) {
@@ -1163,15 +1206,13 @@ __global__ void MPB_WS_BOUNDS_SPMV k_spmv_pq(const SpmvArgs a) {
   load_patterns(s_pat, a.pat, a.g.npat);
   ring_init(R, ns);
   if (threadIdx.x >= kConsumers) {
-    if (threadIdx.x == kConsumers)
-      producer_loop(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, [&]() { return a.st->done != 0; },
+    const ChunkCtx ck{a.csum, a.part, a.g.ntiles};
+    producer_loop(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, [&]() { return a.st->done != 0; },
                     [&](int st, int tile, int part) {
                       produce<double, uint8_t, uint8_t, uint8_t, false, uint8_t>(R, st, a.td, tile, a.g, L, smem + st * L.bytes,
                                                                  a.sp, a.scol, a.sval, a.meta, nullptr, nullptr,
                                                                  nullptr, nullptr, part);
-                    });
-    else
-      pdl_wait();
+                    }, ck);
     if (a.st->done) return;
   } else {
     pdl_wait();
@@ -1201,7 +1242,7 @@ __global__ void MPB_WS_BOUNDS_SPMV k_spmv_pq(const SpmvArgs a) {
     if (threadIdx.x == 0) tl_mark(a.st, 1, 1, true);
   }
   pdl_trigger();
-  finish_grid(a.st, 1, kStepPq, a.part, a.g.ntiles, ws);
+  finish_grid(a.st, 1, kStepPq, ChunkCtx{a.csum, a.part, a.g.ntiles}, ws);
 }
 
 // x += alpha p ; r -= alpha q ; r.r partial   (solver.py:160-165)
@@ -1209,7 +1250,7 @@ __global__ void MPB_WS_BOUNDS_SPMV k_spmv_pq(const SpmvArgs a) {
 // issued up front and one barrier pair for their tile sums.
 __global__ void __launch_bounds__(kCtaThreads)
     k_update(const TileDesc *td, int ntiles, double *x, const double *p, const double *q, double *r, double *part,
-             SolverState *st) {
+             SolverState *st, double *csum) {
   pdl_wait();
   if (st->done) return;
   __shared__ double ws[kStreamTiles][32];
@@ -1253,12 +1294,14 @@ __global__ void __launch_bounds__(kCtaThreads)
 #pragma unroll
       for (int u = 0; u < U; u++) {
         const int tile = t0 + u * gridDim.x;
-        if (tile < ntiles) part[tile] = sq[u];
+        if (tile < ntiles) put_part(part + tile, sq[u]);
       }
     }
   }
   pdl_trigger();
-  finish_grid(st, 2, kStepRr, part, ntiles, wsf);
+  const ChunkCtx ck{csum, part, ntiles};
+  chunk_duties_strided(ck, blockIdx.x, gridDim.x);
+  finish_grid(st, 2, kStepRr, ck, wsf);
 }
 
 // Fused x/r update + the next iteration's first BJAC pass (solver.py:160-165
@@ -1274,7 +1317,7 @@ __host__ __device__ inline StageLayout update_first_layout(const TileGeom &g) {
 }
 
 template <typename T, bool GEN>
-__global__ void MPB_WS_BOUNDS_PASS k_update_first(const PassArgs<T> a, double *x, const double *p,
+__global__ void MPB_WS_BOUNDS_UPDATE k_update_first(const PassArgs<T> a, double *x, const double *p,
                                                                const double *q, double *r) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ Ring R;
@@ -1286,15 +1329,13 @@ __global__ void MPB_WS_BOUNDS_PASS k_update_first(const PassArgs<T> a, double *x
   load_patterns(s_pat, a.pat, a.g.npat);
   ring_init(R, ns);
   if (threadIdx.x >= kConsumers) {
-    if (threadIdx.x == kConsumers)
-      producer_loop(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, [&]() { return gated_off(a); },
+    const ChunkCtx ck{a.csum, a.part, a.g.ntiles};
+    producer_loop(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, [&]() { return gated_off(a); },
                     [&](int st, int tile, int part) {
                       produce<T, double, double, double, true, double>(R, st, a.td, tile, a.g, L,
                                                                        smem + st * L.bytes, a.ib_sp, a.ib_col,
                                                                        a.ib_val, a.meta, r, x, p, q, part);
-                    });
-    else
-      pdl_wait();
+                    }, ck);
     if (gated_off(a)) return;
   } else {
     pdl_wait();
@@ -1328,7 +1369,7 @@ __global__ void MPB_WS_BOUNDS_PASS k_update_first(const PassArgs<T> a, double *x
         rv[k] = narrow_checked(a, rn, row, true);
       }
       const double tot = tile_tree_rows(sq, ws, kBarConsumers);
-      if (threadIdx.x == 0) a.part[tile] = tot;
+      if (threadIdx.x == 0) put_part(a.part + tile, tot);
       const bool scols = ok && a.g.cols && d.ngen > 0;
       const int *col = scols ? reinterpret_cast<const int *>(sb + L.col) : a.ib_col + d.ie0;
       if (ok)
@@ -1342,7 +1383,7 @@ __global__ void MPB_WS_BOUNDS_PASS k_update_first(const PassArgs<T> a, double *x
     if (threadIdx.x == 0) tl_mark(a.st, 2, 1, true);
   }
   pdl_trigger();
-  finish_grid<8>(a.st, 2, kStepRrZ, a.part, a.g.ntiles, ws);  // 16 would cost it a CTA per SM
+  finish_grid<8>(a.st, 2, kStepRrZ, ChunkCtx{a.csum, a.part, a.g.ntiles}, ws);  // 16: a CTA per SM less
 }
 
 // res = b - A x (or b), optionally stored; res.res partial; the last CTA runs
@@ -1351,7 +1392,7 @@ __global__ void MPB_WS_BOUNDS_PASS k_update_first(const PassArgs<T> a, double *x
 template <bool HAS_X>
 __global__ void __launch_bounds__(kCtaThreads)
     k_resid(const int *sp, const int *scol, const double *sval, const TileDesc *td, int ntiles, const double *b,
-            const double *x, double *rout, double *part, SolverState *st, int gate, int step) {
+            const double *x, double *rout, double *part, SolverState *st, int gate, int step, double *csum) {
   if (gate == 1 && (st == nullptr || !st->true_pending)) return;
   __shared__ double ws[32];
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -1384,9 +1425,11 @@ __global__ void __launch_bounds__(kCtaThreads)
       sq = __dmul_rn(res, res);
     }
     const double tot = block_tree<kTileThreads>(sq, ws);
-    if (threadIdx.x == 0) part[tile] = tot;
+    if (threadIdx.x == 0) put_part(part + tile, tot);
   }
-  finish_grid(st, 3, step, part, ntiles, ws);
+  const ChunkCtx ck{st != nullptr ? csum : nullptr, part, ntiles};
+  chunk_duties_strided(ck, blockIdx.x, gridDim.x);
+  finish_grid(st, 3, step, ck, ws);
 }
 
 // one-thread scalar step (solve start: wall-clock origin of the trace)
@@ -1746,6 +1789,17 @@ __global__ void __launch_bounds__(kTileThreads)
   if (threadIdx.x == 0) part[blockIdx.x] = tot;
 }
 
+// chunk sums of the two-level order (include/mpbjac_order.h): one warp per chunk
+template <typename ACC>
+__global__ void __launch_bounds__(kTileThreads) k_chunk_sums(const ACC *part, long long nparts, ACC *csum) {
+  const long long c = (long long)blockIdx.x * (kTileThreads / 32) + (threadIdx.x >> 5);
+  const long long nch = (nparts + kChunkTiles - 1) / kChunkTiles;
+  if (c >= nch) return;
+  const ACC v = chunk_sum_warp(part, c, nparts);
+  if ((threadIdx.x & 31) == 0) csum[c] = v;
+}
+
+// the final level over `nparts` values (chunk sums)
 template <typename ACC>
 __global__ void __launch_bounds__(kFinThreads) k_fin(const ACC *part, long long nparts, ACC *out) {
   __shared__ ACC ws[32];

@@ -304,6 +304,25 @@ def test_pcg_many_tiles_per_cta_bitwise(cuda, oracle, pol):
     np.testing.assert_array_equal([r.implicit_relres for r in rep.trace], orc["relres"])
 
 
+@pytest.mark.parametrize("k,pol", ((2, "fixed-low"), (1, "uniform"), (2, "adaptive-lh:1e-6")))
+def test_pcg_two_level_sums_partial_chunk_bitwise(cuda, oracle, k, pol):
+    """n = 50: 489 tiles = one full 256-tile chunk and a partial one, so the
+    two-level dot sums (chunk sums ticked while the kernels run, then the
+    final level) cover a ragged last chunk; k = 1 runs the unfused
+    iteration (x/r update kernel), stride 3 and x0 the residual kernel."""
+    from paper_2407_15973_b200 import problems
+    cs = problems.make_config("c2", 50)
+    offs = np.append(np.arange(0, cs.A.n, 64), cs.A.n)
+    x0 = np.cos(np.arange(cs.A.n) * 0.01)
+    rep, orc = _solve_both(cs.A, cs.b, offs, pol, k, 2, 1e-8, oracle, stride=3, x0=x0)
+    assert rep.iterations == orc["iterations"]
+    np.testing.assert_array_equal(rep.x, orc["x"])
+    np.testing.assert_array_equal([r.implicit_relres for r in rep.trace], orc["relres"])
+    tr = np.array([np.nan if r.true_relres is None else r.true_relres for r in rep.trace])
+    np.testing.assert_array_equal(tr, orc["true_relres"])
+    assert rep.final_true_relres == orc["final_true_relres"]
+
+
 @pytest.mark.parametrize("pol", ("fixed-low", "adaptive-hl:1e-3"))
 def test_slab_solver_single_rank_matches_single_gpu(cuda, oracle, pol):
     """The multi-GPU path (NCCL communicator, all-reduced scalar steps
