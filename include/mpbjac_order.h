@@ -28,14 +28,16 @@
  *      MPB_TILE_THREADS == MPB_TILE_MAX_ROWS every lane owns at most one row);
  *   2. each warp butterflies (xor 16, 8, 4, 2, 1) -> lane 0 holds W_w;
  *   3. warp 0 butterflies W_0..W_{nw-1} padded with +0.0 to 32 lanes.
- * Global sum of the tile partials P[0..T), two levels:
- *   chunk c = tiles [c*MPB_CHUNK_TILES, min(T, (c+1)*MPB_CHUNK_TILES)):
- *     C_c = steps 1-3 with MPB_CHUNK_TILES lanes over the chunk's partials
- *     (lane j holds P[c*MPB_CHUNK_TILES + j] or +0.0);
- *   total = steps 1-3 with MPB_FIN_THREADS lanes over C[0..ceil(T/MPB_CHUNK_TILES)).
- *   (T <= MPB_CHUNK_TILES: total = C_0, the one-level sum of earlier rounds.)
- *   Chunks are summed while the kernel runs, by whichever CTA completes a
- *   chunk's last tile, so the kernel's final CTA only adds T/256 values.
+ * Global sum of the tile partials P[0..T):
+ *   T <= MPB_ONE_LEVEL_TILES: steps 1-3 with MPB_FIN_THREADS lanes over P.
+ *   Larger T, two levels: chunk c = tiles [c*MPB_CHUNK_TILES,
+ *     min(T, (c+1)*MPB_CHUNK_TILES)); C_c = steps 1-3 with MPB_CHUNK_TILES
+ *     lanes over the chunk's partials (lane j holds P[c*MPB_CHUNK_TILES + j]
+ *     or +0.0); total = steps 1-3 with MPB_FIN_THREADS lanes over the C_c.
+ *   The chunks are summed while the kernel runs, by the CTA that claimed a
+ *   chunk's last tile, so the kernel's final CTA adds T/256 values instead of
+ *   T (C3: 65,536 partials, C5: 524,288).  Up to MPB_ONE_LEVEL_TILES the
+ *   final CTA's one-level sum (two rounds of loads) is the faster one.
  * Multi-GPU: each rank's global sum is combined by an fp64 all-reduce.
  */
 #ifndef MPBJAC_ORDER_H
@@ -46,5 +48,6 @@
 #define MPB_TILE_PACK_NNZ  2048
 #define MPB_FIN_THREADS    256
 #define MPB_CHUNK_TILES    256
+#define MPB_ONE_LEVEL_TILES 8192
 
 #endif

@@ -171,6 +171,11 @@ double orc_tree_sum(i64 ntiles, const i64 *tile_lo, const double *vals) {
   OMP_FOR for (i64 t = 0; t < ntiles; t++)
     part[t] = lane_tree(tile_lo[t + 1] - tile_lo[t], MPB_TILE_THREADS,
                         vals + tile_lo[t]);
+  if (ntiles <= MPB_ONE_LEVEL_TILES) {
+    double total1 = lane_tree(ntiles, MPB_FIN_THREADS, part);
+    free(part);
+    return total1;
+  }
   /* two-level global sum: chunk sums, then the sum of the chunk sums */
   i64 nch = (ntiles + MPB_CHUNK_TILES - 1) / MPB_CHUNK_TILES;
   double *csum = (double *)malloc(sizeof(double) * (nch > 0 ? nch : 1));

@@ -145,6 +145,10 @@ bool sell_slice_ptrs(int64_t n, const int64_t *h_rp, std::vector<int> &sp) {
 
 constexpr int kStageCap = 4096;  // staged SELL entries per tile (2 stages per CTA)
 
+// the two-level sum order applies (and chunk owners poll) above
+// MPB_ONE_LEVEL_TILES tiles
+bool owners_poll(int64_t ntiles) { return two_level(ntiles); }
+
 template <typename T>
 TileGeom geom_for(const mpb_plan *p) {
   TileGeom g;
@@ -154,6 +158,7 @@ TileGeom geom_for(const mpb_plan *p) {
   g.ns = 2;
   g.cols = p->ngeneric > 0 ? 1 : 0;
   g.npat = p->npat;
+  g.poll = owners_poll(p->ntiles) ? 1 : 0;
   return g;
 }
 
@@ -250,10 +255,12 @@ int launch_tile_kernel(mpb_handle *h, cudaStream_t s, const mpb_plan *p, PassArg
     a.g.cap_e = std::min(p->max_tile_ib, kStageCap);
   }
   const StageLayout Ls = bjac_layout<T, F, R64>(a.g);
-  a.g.ns = pick_stages(k_bjac_tile<T, F, L, R64, KS, GEN>, Ls.bytes);
+  // the last pass carries the r.z sum: two-level order above MPB_ONE_LEVEL_TILES
+  auto kern = (L && a.g.poll) ? k_bjac_tile<T, F, L, R64, KS, GEN, L> : k_bjac_tile<T, F, L, R64, KS, GEN, false>;
+  a.g.ns = pick_stages(kern, Ls.bytes);
   const uint32_t dyn = a.g.ns * Ls.bytes;
-  const int grid = persistent_grid(k_bjac_tile<T, F, L, R64, KS, GEN>, dyn, p->ntiles, kWsThreads);
-  MPB_CUDA(launch_k(a.pdl != 0, k_bjac_tile<T, F, L, R64, KS, GEN>, grid, kWsThreads, dyn, s, a));
+  const int grid = persistent_grid(kern, dyn, p->ntiles, kWsThreads);
+  MPB_CUDA(launch_k(a.pdl != 0, kern, grid, kWsThreads, dyn, s, a));
   MPB_LAUNCHED(h);
   return MPB_OK;
 }
@@ -431,7 +438,8 @@ int launch_update_first(mpb_handle *h, cudaStream_t s, const mpb_plan *p, const 
   a.gate = 2;
   a.prefetch = prefetch;
   const StageLayout L = update_first_layout<T>(a.g);
-  auto kern = p->ngeneric > 0 ? k_update_first<T, true> : k_update_first<T, false>;
+  auto kern = two_level(p->ntiles) ? (p->ngeneric > 0 ? k_update_first_two<T, true> : k_update_first_two<T, false>)
+                                    : (p->ngeneric > 0 ? k_update_first<T, true> : k_update_first<T, false>);
   a.g.ns = pick_stages(kern, L.bytes);
   const uint32_t dyn = a.g.ns * L.bytes;
   const int grid = persistent_grid(kern, dyn, p->ntiles, kWsThreads);
@@ -892,16 +900,20 @@ int mpb_block_jacobi_sweeps_f32(mpb_handle *h, const int32_t *row_ptr, const int
   return sweeps_impl<float>(h, row_ptr, col_idx, val, in_block, diag, t, r, y, tmp, row_start, row_end);
 }
 
-// Global sum of nt tile partials in the two-level order: chunk sums into
-// csum (nt/256 + 1 entries of scratch), then the final level into *out.
+// Global sum of nt tile partials in the order of include/mpbjac_order.h:
+// one level, or chunk sums into csum (nt/256 + 1 entries of scratch) and
+// the final level over them, into *out.
 template <typename ACC>
 static int launch_fin(mpb_handle *h, const ACC *part, int64_t nt, ACC *csum, ACC *out) {
+  if (!two_level(nt)) {
+    k_fin<ACC><<<1, kFinThreads, 0, h->user>>>(part, nt, out);
+    MPB_LAUNCHED(h);
+    return MPB_OK;
+  }
   const int64_t nch = (nt + kChunkTiles - 1) / kChunkTiles;
   const int per = kTileThreads / 32;
-  if (nch > 0) {
-    k_chunk_sums<ACC><<<static_cast<unsigned>((nch + per - 1) / per), kTileThreads, 0, h->user>>>(part, nt, csum);
-    MPB_LAUNCHED(h);
-  }
+  k_chunk_sums<ACC><<<static_cast<unsigned>((nch + per - 1) / per), kTileThreads, 0, h->user>>>(part, nt, csum);
+  MPB_LAUNCHED(h);
   k_fin<ACC><<<1, kFinThreads, 0, h->user>>>(csum, nch, out);
   MPB_LAUNCHED(h);
   return MPB_OK;
@@ -1259,6 +1271,10 @@ int64_t mpb_solve_workspace_bytes(const mpb_plan *plan, int64_t n) {
 
 // KS = 7 (7-point stencils) with or without generic rows; KS = 9 (e.g. 3-T) always with
 static void (*spmv_kernel(const mpb_plan *p))(SpmvArgs) {
+  if (two_level(p->ntiles)) {
+    if (p->ks == 7) return p->ngeneric > 0 ? k_spmv_pq<7, true, true> : k_spmv_pq<7, false, true>;
+    return k_spmv_pq<kSlots, true, true>;
+  }
   if (p->ks == 7) return p->ngeneric > 0 ? k_spmv_pq<7, true> : k_spmv_pq<7, false>;
   return k_spmv_pq<kSlots, true>;
 }
@@ -1408,7 +1424,7 @@ static int enqueue_iteration(mpb_handle *h, cudaStream_t s, const mpb_plan *p, c
   } else {
     MPB_CUDA(launch_k(pdl, k_update, persistent_grid(k_update, 0, p->ntiles), kCtaThreads, 0, s,
                       static_cast<const TileDesc *>(p->d_td), static_cast<int>(nt), x,
-                      static_cast<const double *>(w.p), static_cast<const double *>(w.q), w.r, w.part, w.st, w.csum));
+                      static_cast<const double *>(w.p), static_cast<const double *>(w.q), w.r, w.part, w.st, w.csum, owners_poll(p->ntiles) ? 1 : 0));
     MPB_LAUNCHED(h);
   }
   if ((rc = dist_step(h, dc, w.st, fused ? kStepRrZ : kStepRr, 2, s))) return rc;
@@ -1416,7 +1432,7 @@ static int enqueue_iteration(mpb_handle *h, cudaStream_t s, const mpb_plan *p, c
     if ((rc = halo_exchange(dc, x, 8, A->n, s))) return rc;
     k_resid<true><<<persistent_grid(k_resid<true>, 0, p->ntiles), kCtaThreads, 0, s>>>(
         A->sell->d_sp, A->sell->d_col, A->sell_val64, p->d_td, static_cast<int>(nt), b, x, nullptr, w.part, w.st, 1,
-        kStepTrue, w.csum);
+        kStepTrue, w.csum, owners_poll(p->ntiles) ? 1 : 0);
     MPB_LAUNCHED(h);
     if ((rc = dist_step(h, dc, w.st, kStepTrue, 1, s))) return rc;
   }
@@ -1552,11 +1568,11 @@ static int solve_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, con
     if ((rc = halo_exchange(dc, x, 8, A->n, s))) return rc;
     k_resid<true><<<persistent_grid(k_resid<true>, 0, plan->ntiles), kCtaThreads, 0, s>>>(
                                               A->sell->d_sp, A->sell->d_col, A->sell_val64, plan->d_td, static_cast<int>(nt), b, x, w.r, w.part, w.st, 0,
-                                              kStepR0, w.csum);
+                                              kStepR0, w.csum, owners_poll(plan->ntiles) ? 1 : 0);
   } else {
     k_resid<false><<<persistent_grid(k_resid<false>, 0, plan->ntiles), kCtaThreads, 0, s>>>(
                                                A->sell->d_sp, A->sell->d_col, A->sell_val64, plan->d_td, static_cast<int>(nt), b, nullptr, w.r, w.part, w.st,
-                                               0, kStepR0, w.csum);
+                                               0, kStepR0, w.csum, owners_poll(plan->ntiles) ? 1 : 0);
   }
   MPB_LAUNCHED(h);
   if ((rc = dist_step(h, dc, w.st, kStepR0, 0, s))) return rc;
@@ -1720,7 +1736,7 @@ static int solve_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, con
     if ((rc = halo_exchange(dc, x, 8, A->n, s))) return rc;
     k_resid<true><<<persistent_grid(k_resid<true>, 0, plan->ntiles), kCtaThreads, 0, s>>>(
                                               A->sell->d_sp, A->sell->d_col, A->sell_val64, plan->d_td, static_cast<int>(nt), b, x, nullptr, w.part, w.st, 0,
-                                              kStepFinal, w.csum);
+                                              kStepFinal, w.csum, owners_poll(plan->ntiles) ? 1 : 0);
     MPB_LAUNCHED(h);
     if ((rc = dist_step(h, dc, w.st, kStepFinal, 0, s))) return rc;
     MPB_CUDA(cudaMemcpyAsync(h->h_state, w.st, sizeof(SolverState), cudaMemcpyDeviceToHost, s));
@@ -1897,7 +1913,7 @@ static int profile_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, c
   if (rc) return rc;
   rc = timed(4, [&]() -> int {
     k_update<<<ugrid, kCtaThreads, 0, s>>>(plan->d_td, static_cast<int>(nt), x, w.p, w.q, w.r, w.part,
-                                         w.st, w.csum);
+                                         w.st, w.csum, owners_poll(plan->ntiles) ? 1 : 0);
     MPB_LAUNCHED(h);
     return MPB_OK;
   });
@@ -1935,7 +1951,7 @@ int mpb_true_relres(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, const
   double *out = reinterpret_cast<double *>(reinterpret_cast<char *>(csum) + chunk_scratch(sizeof(double), nt));
   k_resid<true><<<persistent_grid(k_resid<true>, 0, nt), kCtaThreads, 0, h->user>>>(
       A->sell->d_sp, A->sell->d_col, A->sell_val64, plan->d_td, static_cast<int>(nt), b, x, nullptr,
-      part, nullptr, 0, kStepFinal, nullptr);
+      part, nullptr, 0, kStepFinal, nullptr, 0);
   MPB_LAUNCHED(h);
   if ((rc = launch_fin<double>(h, part, nt, csum, out))) return rc;
   double v;

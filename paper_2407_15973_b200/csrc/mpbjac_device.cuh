@@ -218,7 +218,11 @@ constexpr unsigned long long kPartEmpty = ~0ull;
 __device__ __forceinline__ void put_part(double *p, double v) {
   unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
   if (b == kPartEmpty) b = 0x7ff8000000000000ull;  // (still a NaN; the empty pattern stays unique)
+#ifdef MPB_EXP_WEAK_PART
+  *reinterpret_cast<unsigned long long *>(p) = b;
+#else
   asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(b) : "memory");
+#endif
 }
 __device__ __forceinline__ unsigned long long get_part_bits(const double *p) {
   unsigned long long b;
@@ -226,10 +230,14 @@ __device__ __forceinline__ unsigned long long get_part_bits(const double *p) {
   return b;
 }
 
+// Two-level sums only above MPB_ONE_LEVEL_TILES tiles (include/mpbjac_order.h).
+__host__ __device__ inline bool two_level(long long ntiles) { return ntiles > MPB_ONE_LEVEL_TILES; }
+
 struct ChunkCtx {
   double *csum;  // null: no chunk bookkeeping (plugin-level launch)
   double *part;
   int ntiles;
+  int poll;      // two-level order: chunk owners poll (two_level(ntiles))
 };
 __device__ __forceinline__ bool chunk_final(int tile, int ntiles) {
   return tile % kChunkTiles == kChunkTiles - 1 || tile == ntiles - 1;
@@ -269,9 +277,11 @@ __device__ __forceinline__ bool chunk_poll(const ChunkCtx &ck, int c, bool block
     __nanosleep(200);
   }
 }
-// All chunks by the CTA that took the grid's last ticket (kernels whose
-// grid may exceed residency, so no CTA may wait for another): warps take
-// chunks round-robin; the slots are emptied.  Called by all threads.
+
+// All chunks by the CTA that took the grid's last ticket, warps taking
+// chunks round-robin (two-level kernels whose grid may exceed residency, so
+// that no CTA may wait for another); the slots are emptied.  Called by all
+// threads.
 __device__ __forceinline__ void chunk_all_in_cta(const ChunkCtx &ck) {
   if (ck.csum == nullptr) return;
   const int nch = (ck.ntiles + kChunkTiles - 1) / kChunkTiles;
@@ -283,11 +293,12 @@ __device__ __forceinline__ void chunk_all_in_cta(const ChunkCtx &ck) {
   for (int i = threadIdx.x; i < ck.ntiles; i += blockDim.x) reinterpret_cast<unsigned long long *>(ck.part)[i] = kPartEmpty;
   __syncthreads();
 }
+
 // Non-warp-specialised persistent kernels (static walk tile0, tile0 +
 // stride, ...): after its tiles, warp 0 owns the chunks whose last tile it
 // processed.  Called by all threads.
 __device__ __forceinline__ void chunk_duties_strided(const ChunkCtx &ck, int tile0, int stride) {
-  if (ck.csum == nullptr) return;
+  if (ck.csum == nullptr || !ck.poll) return;
   __syncthreads();
   if (threadIdx.x >= 32) return;
   for (int t = tile0; t < ck.ntiles; t += stride)

@@ -52,9 +52,6 @@ constexpr int kMaxPend = 4;  // owned chunks a producer keeps pending
 #else
 #define MPB_WS_BOUNDS_PASS __launch_bounds__(kWsThreads)
 #endif
-// the fused update is compiled for 5 CTAs per SM (its consumer path needs
-// 40 registers; the producer's chunk polling alone would raise the budget)
-#define MPB_WS_BOUNDS_UPDATE __launch_bounds__(kWsThreads, 5)
 #ifdef MPB_MINB_SPMV
 #define MPB_WS_BOUNDS_SPMV __launch_bounds__(kWsThreads, MPB_MINB_SPMV)
 #else
@@ -245,17 +242,22 @@ __device__ __forceinline__ void state_load(SolverState &L, const SolverState *g)
 // The chunk sums of the two-level order are in ck.csum: their owners stored
 // them before their CTAs took the ticket (chunks_in_cta: the last CTA sums
 // them here).
+// One-level order (!ck.poll): the final CTA sums all tile partials.  Two
+// levels: the chunk sums are in ck.csum, stored by their owners before their
+// CTAs took the ticket (in_cta: grids that may exceed residency have no
+// owners; the final CTA sums the chunks here).
 template <int B = 16>
 __device__ __forceinline__ void finish_grid(SolverState *st, int ticket, int step, const ChunkCtx &ck, double *ws,
-                                            bool chunks_in_cta = false) {
+                                            bool in_cta = false) {
   if (st == nullptr) return;
   if (!grid_last(&st->ticket[ticket])) return;
   __shared__ __align__(16) unsigned long long s_state[kStWords];
   if (threadIdx.x < kStWords) s_state[threadIdx.x] = __ldcg(reinterpret_cast<const unsigned long long *>(st) + threadIdx.x);
-  if (chunks_in_cta) chunk_all_in_cta(ck);
+  if (ck.poll && in_cta) chunk_all_in_cta(ck);
   if (threadIdx.x == 0) tl_mark(st, step == kStepRho ? 0 : (step == kStepPq ? 1 : 2), 3, true);  // diagnostics
   const int nch = (ck.ntiles + kChunkTiles - 1) / kChunkTiles;
-  const double tot = fin_sum<B>(ck.csum, nch, ws);  // (its barriers publish s_state)
+  const double tot = ck.poll ? fin_sum<B>(ck.csum, nch, ws)
+                             : fin_sum<B>(ck.part, ck.ntiles, ws);  // (their barriers publish s_state)
   SolverState *L = reinterpret_cast<SolverState *>(s_state);
   const bool dist = L->dist != 0;
   if (threadIdx.x == 0) {
@@ -329,6 +331,7 @@ struct TileDesc {
 
 struct TileGeom {
   int ntiles;
+  int poll;    // two-level sums: chunk owners poll (ChunkCtx::poll)
   int cap_e;   // staged SELL entries per tile (max over tiles, capped)
   int max_sl;  // max slices per tile
   int ns;      // shared-memory stages (prefetch depth)
@@ -544,6 +547,65 @@ __device__ __forceinline__ void producer_loop(Ring &R, int ntiles, int ns, unsig
   if (lane == 0) mbar_arrive(&R.full[st]);  // stage st holds the end marker (-1)
   __syncwarp();
   while (phead != ptail) poll_oldest(true);
+}
+
+// Single-lane producer (lane 0 of the producer warp) for kernels without
+// chunk owners: the same walk as producer_loop.
+template <typename F, typename G>
+__device__ __forceinline__ void producer_loop_single(Ring &R, int ntiles, int ns, unsigned int *ctr, bool prefetch,
+                                              G &&gated, F &&fill) {
+  int next = blockIdx.x;
+  auto claim = [&]() -> int {
+    if (ctr != nullptr) {
+      const unsigned int v = atomicAdd(ctr, 1u);
+      if (v == static_cast<unsigned int>(ntiles) + gridDim.x - 1u) atomicExch(ctr, 0u);
+      return v < static_cast<unsigned int>(ntiles) ? static_cast<int>(v) : -1;
+    }
+    const int t = next < ntiles ? next : -1;
+    next += gridDim.x;
+    return t;
+  };
+  int npre = 0;
+  bool exhausted = false;
+  if (prefetch) {
+    for (; npre < ns; npre++) {
+      const int tile = claim();
+      R.tile[npre] = tile;
+      if (tile < 0) {
+        exhausted = true;
+        break;
+      }
+      fill(npre, tile, kFillStatic);
+    }
+  }
+  pdl_wait();
+  if (gated()) {
+    for (int i = 0; i < npre; i++) {  // let the copies land before the CTA exits
+      mbar_arrive(&R.full[i]);
+      mbar_wait(&R.full[i], 0);
+    }
+    return;
+  }
+  for (int i = 0; i < npre; i++) fill(i, R.tile[i], kFillDynamic);
+  if (exhausted) {
+    mbar_arrive(&R.full[npre]);
+    return;
+  }
+  int st = npre % ns, rnd = npre / ns;  // stage, and how often it has been filled before
+  for (;;) {
+    if (rnd > 0) mbar_wait_sleep(&R.empty[st], (rnd - 1) & 1);
+    const int tile = claim();
+    R.tile[st] = tile;
+    if (tile < 0) {
+      mbar_arrive(&R.full[st]);
+      return;
+    }
+    fill(st, tile, kFillAll);
+    if (++st == ns) {
+      st = 0;
+      rnd++;
+    }
+  }
 }
 
 // consumer-side ring cursor: stage and mbarrier parity of the i-th tile
@@ -904,8 +966,9 @@ __host__ __device__ inline StageLayout bjac_layout(const TileGeom &g) {
   return stage_layout(g.cap_e, sizeof(T), g.max_sl, g.cols != 0, true, R64 ? 8 : sizeof(T), 0, 0);
 }
 
-// Persistent, warp-specialised fused pass.
-template <typename T, bool FIRST, bool LAST, bool R64, int KS, bool GEN>
+// Persistent, warp-specialised fused pass.  TWO: the two-level dot-sum order
+// (chunk owners in the producer warp); false compiles that machinery out.
+template <typename T, bool FIRST, bool LAST, bool R64, int KS, bool GEN, bool TWO = false>
 __global__ void MPB_WS_BOUNDS_PASS k_bjac_tile(const PassArgs<T> a) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ Ring R;
@@ -923,18 +986,24 @@ __global__ void MPB_WS_BOUNDS_PASS k_bjac_tile(const PassArgs<T> a) {
   if (threadIdx.x >= kConsumers) {  // producer warp
     using RT = typename std::conditional<R64, double, T>::type;
     const RT *rsrc = R64 ? reinterpret_cast<const RT *>(a.r64) : reinterpret_cast<const RT *>(a.rT);
-    const ChunkCtx ck{(LAST && a.part != nullptr && a.st != nullptr) ? a.csum : nullptr, a.part, a.g.ntiles};
-    producer_loop(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, [&]() { return gated_off(a); },
-                    [&](int st, int tile, int part) {
-                      if (kIB)
-                        produce<T, RT, uint8_t, uint8_t, true>(R, st, a.td, tile, a.g, L, smem + st * L.bytes,
-                                                               a.ib_sp, a.ib_col, a.ib_val, a.meta, rsrc, nullptr,
-                                                               nullptr, static_cast<const uint8_t *>(nullptr), part);
-                      else
-                        produce<T, RT, uint8_t, uint8_t>(R, st, a.td, tile, a.g, L, smem + st * L.bytes, a.sp,
-                                                         a.scol, a.sval, a.meta, rsrc, nullptr, nullptr,
-                                                         static_cast<const uint8_t *>(nullptr), part);
-                    }, ck);
+    const ChunkCtx ck{(TWO && LAST && a.part != nullptr && a.st != nullptr) ? a.csum : nullptr, a.part, a.g.ntiles,
+                      TWO ? a.g.poll : 0};
+    auto fill = [&](int st, int tile, int part) {
+      if (kIB)
+        produce<T, RT, uint8_t, uint8_t, true>(R, st, a.td, tile, a.g, L, smem + st * L.bytes, a.ib_sp, a.ib_col,
+                                               a.ib_val, a.meta, rsrc, nullptr, nullptr,
+                                               static_cast<const uint8_t *>(nullptr), part);
+      else
+        produce<T, RT, uint8_t, uint8_t>(R, st, a.td, tile, a.g, L, smem + st * L.bytes, a.sp, a.scol, a.sval,
+                                         a.meta, rsrc, nullptr, nullptr, static_cast<const uint8_t *>(nullptr), part);
+    };
+    auto gated = [&]() { return gated_off(a); };
+    if (TWO && ck.csum != nullptr && ck.poll)
+      producer_loop(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, gated, fill, ck);
+    else if (threadIdx.x == kConsumers)
+      producer_loop_single(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, gated, fill);
+    else
+      pdl_wait();
     if (gated_off(a)) return;
   } else {
     pdl_wait();
@@ -994,7 +1063,7 @@ __global__ void MPB_WS_BOUNDS_PASS k_bjac_tile(const PassArgs<T> a) {
   }
   pdl_trigger();  // dependents may launch into the SMs this grid drains
   if (LAST && a.part != nullptr)
-    finish_grid(a.st, 0, kStepRho, ChunkCtx{a.csum, a.part, a.g.ntiles}, ws);
+    finish_grid(a.st, 0, kStepRho, ChunkCtx{a.csum, a.part, a.g.ntiles, TWO ? a.g.poll : 0}, ws);
 }
 
 // ---- large blocks (> kTileRows rows): one launch per inner sweep ----------
@@ -1057,7 +1126,7 @@ __global__ void __launch_bounds__(kCtaThreads) k_big_finish(const PassArgs<T> a,
     const double tot = block_tree<kTileThreads>(prod, ws);
     if (threadIdx.x == 0) put_part(a.part + tile, tot);
     // one CTA per tile (grid may exceed residency): the last CTA sums the chunks
-    finish_grid(a.st, 0, kStepRho, ChunkCtx{a.st != nullptr ? a.csum : nullptr, a.part, a.g.ntiles}, ws, true);
+    finish_grid(a.st, 0, kStepRho, ChunkCtx{a.st != nullptr ? a.csum : nullptr, a.part, a.g.ntiles, a.g.poll}, ws, true);
   }
 }
 
@@ -1195,7 +1264,7 @@ __device__ __forceinline__ void spmv_tile(const SpmvArgs &a, int tile, const Til
   else spmv_tile_body<KS, double, GEN>(a, tile, d, col, val, spp, mt, s_pat, ws, first, beta);
 }
 
-template <int KS, bool GEN>
+template <int KS, bool GEN, bool TWO = false>
 __global__ void MPB_WS_BOUNDS_SPMV k_spmv_pq(const SpmvArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ Ring R;
@@ -1206,13 +1275,19 @@ __global__ void MPB_WS_BOUNDS_SPMV k_spmv_pq(const SpmvArgs a) {
   load_patterns(s_pat, a.pat, a.g.npat);
   ring_init(R, ns);
   if (threadIdx.x >= kConsumers) {
-    const ChunkCtx ck{a.csum, a.part, a.g.ntiles};
-    producer_loop(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, [&]() { return a.st->done != 0; },
-                    [&](int st, int tile, int part) {
-                      produce<double, uint8_t, uint8_t, uint8_t, false, uint8_t>(R, st, a.td, tile, a.g, L, smem + st * L.bytes,
-                                                                 a.sp, a.scol, a.sval, a.meta, nullptr, nullptr,
-                                                                 nullptr, nullptr, part);
-                    }, ck);
+    const ChunkCtx ck{a.csum, a.part, a.g.ntiles, TWO ? a.g.poll : 0};
+    auto fill = [&](int st, int tile, int part) {
+      produce<double, uint8_t, uint8_t, uint8_t, false, uint8_t>(R, st, a.td, tile, a.g, L, smem + st * L.bytes, a.sp,
+                                                                 a.scol, a.sval, a.meta, nullptr, nullptr, nullptr,
+                                                                 nullptr, part);
+    };
+    auto gated = [&]() { return a.st->done != 0; };
+    if (TWO && ck.poll)
+      producer_loop(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, gated, fill, ck);
+    else if (threadIdx.x == kConsumers)
+      producer_loop_single(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, gated, fill);
+    else
+      pdl_wait();
     if (a.st->done) return;
   } else {
     pdl_wait();
@@ -1242,7 +1317,7 @@ __global__ void MPB_WS_BOUNDS_SPMV k_spmv_pq(const SpmvArgs a) {
     if (threadIdx.x == 0) tl_mark(a.st, 1, 1, true);
   }
   pdl_trigger();
-  finish_grid(a.st, 1, kStepPq, ChunkCtx{a.csum, a.part, a.g.ntiles}, ws);
+  finish_grid(a.st, 1, kStepPq, ChunkCtx{a.csum, a.part, a.g.ntiles, TWO ? a.g.poll : 0}, ws);
 }
 
 // x += alpha p ; r -= alpha q ; r.r partial   (solver.py:160-165)
@@ -1250,7 +1325,7 @@ __global__ void MPB_WS_BOUNDS_SPMV k_spmv_pq(const SpmvArgs a) {
 // issued up front and one barrier pair for their tile sums.
 __global__ void __launch_bounds__(kCtaThreads)
     k_update(const TileDesc *td, int ntiles, double *x, const double *p, const double *q, double *r, double *part,
-             SolverState *st, double *csum) {
+             SolverState *st, double *csum, int poll) {
   pdl_wait();
   if (st->done) return;
   __shared__ double ws[kStreamTiles][32];
@@ -1299,7 +1374,7 @@ __global__ void __launch_bounds__(kCtaThreads)
     }
   }
   pdl_trigger();
-  const ChunkCtx ck{csum, part, ntiles};
+  const ChunkCtx ck{csum, part, ntiles, poll};
   chunk_duties_strided(ck, blockIdx.x, gridDim.x);
   finish_grid(st, 2, kStepRr, ck, wsf);
 }
@@ -1316,9 +1391,9 @@ __host__ __device__ inline StageLayout update_first_layout(const TileGeom &g) {
   return stage_layout(g.cap_e, sizeof(T), g.max_sl, g.cols != 0, true, 8, 8, 8, 8);
 }
 
-template <typename T, bool GEN>
-__global__ void MPB_WS_BOUNDS_UPDATE k_update_first(const PassArgs<T> a, double *x, const double *p,
-                                                               const double *q, double *r) {
+template <typename T, bool GEN, bool TWO>
+__device__ __forceinline__ void update_first_body(const PassArgs<T> &a, double *x, const double *p, const double *q,
+                                                  double *r) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ Ring R;
   __shared__ T s_w[kTileRows];
@@ -1329,13 +1404,18 @@ __global__ void MPB_WS_BOUNDS_UPDATE k_update_first(const PassArgs<T> a, double 
   load_patterns(s_pat, a.pat, a.g.npat);
   ring_init(R, ns);
   if (threadIdx.x >= kConsumers) {
-    const ChunkCtx ck{a.csum, a.part, a.g.ntiles};
-    producer_loop(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, [&]() { return gated_off(a); },
-                    [&](int st, int tile, int part) {
-                      produce<T, double, double, double, true, double>(R, st, a.td, tile, a.g, L,
-                                                                       smem + st * L.bytes, a.ib_sp, a.ib_col,
-                                                                       a.ib_val, a.meta, r, x, p, q, part);
-                    }, ck);
+    const ChunkCtx ck{a.csum, a.part, a.g.ntiles, TWO ? a.g.poll : 0};
+    auto fill = [&](int st, int tile, int part) {
+      produce<T, double, double, double, true, double>(R, st, a.td, tile, a.g, L, smem + st * L.bytes, a.ib_sp,
+                                                       a.ib_col, a.ib_val, a.meta, r, x, p, q, part);
+    };
+    auto gated = [&]() { return gated_off(a); };
+    if (TWO && ck.poll)
+      producer_loop(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, gated, fill, ck);
+    else if (threadIdx.x == kConsumers)
+      producer_loop_single(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, gated, fill);
+    else
+      pdl_wait();
     if (gated_off(a)) return;
   } else {
     pdl_wait();
@@ -1383,7 +1463,22 @@ __global__ void MPB_WS_BOUNDS_UPDATE k_update_first(const PassArgs<T> a, double 
     if (threadIdx.x == 0) tl_mark(a.st, 2, 1, true);
   }
   pdl_trigger();
-  finish_grid<8>(a.st, 2, kStepRrZ, ChunkCtx{a.csum, a.part, a.g.ntiles}, ws);  // 16: a CTA per SM less
+  finish_grid<8>(a.st, 2, kStepRrZ, ChunkCtx{a.csum, a.part, a.g.ntiles, TWO ? a.g.poll : 0}, ws);  // 16: a CTA per SM less
+}
+
+// One-level order: ptxas' own register budget (40, 5 CTAs per SM; an
+// explicit minimum of 5 measured 1 % slower).  Two-level: the owners'
+// polling code would raise the budget, so the one-level occupancy (5 CTAs
+// per SM in fp32, 4 in fp64) is imposed.
+template <typename T, bool GEN>
+__global__ void __launch_bounds__(kWsThreads) k_update_first(const PassArgs<T> a, double *x, const double *p,
+                                                             const double *q, double *r) {
+  update_first_body<T, GEN, false>(a, x, p, q, r);
+}
+template <typename T, bool GEN>
+__global__ void __launch_bounds__(kWsThreads, sizeof(T) == 4 ? 5 : 4)
+    k_update_first_two(const PassArgs<T> a, double *x, const double *p, const double *q, double *r) {
+  update_first_body<T, GEN, true>(a, x, p, q, r);
 }
 
 // res = b - A x (or b), optionally stored; res.res partial; the last CTA runs
@@ -1392,7 +1487,8 @@ __global__ void MPB_WS_BOUNDS_UPDATE k_update_first(const PassArgs<T> a, double 
 template <bool HAS_X>
 __global__ void __launch_bounds__(kCtaThreads)
     k_resid(const int *sp, const int *scol, const double *sval, const TileDesc *td, int ntiles, const double *b,
-            const double *x, double *rout, double *part, SolverState *st, int gate, int step, double *csum) {
+            const double *x, double *rout, double *part, SolverState *st, int gate, int step, double *csum,
+            int poll) {
   if (gate == 1 && (st == nullptr || !st->true_pending)) return;
   __shared__ double ws[32];
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -1427,7 +1523,7 @@ __global__ void __launch_bounds__(kCtaThreads)
     const double tot = block_tree<kTileThreads>(sq, ws);
     if (threadIdx.x == 0) put_part(part + tile, tot);
   }
-  const ChunkCtx ck{st != nullptr ? csum : nullptr, part, ntiles};
+  const ChunkCtx ck{st != nullptr ? csum : nullptr, part, ntiles, poll};
   chunk_duties_strided(ck, blockIdx.x, gridDim.x);
   finish_grid(st, 3, step, ck, ws);
 }

@@ -304,17 +304,20 @@ def test_pcg_many_tiles_per_cta_bitwise(cuda, oracle, pol):
     np.testing.assert_array_equal([r.implicit_relres for r in rep.trace], orc["relres"])
 
 
-@pytest.mark.parametrize("k,pol", ((2, "fixed-low"), (1, "uniform"), (2, "adaptive-lh:1e-6")))
-def test_pcg_two_level_sums_partial_chunk_bitwise(cuda, oracle, k, pol):
-    """n = 50: 489 tiles = one full 256-tile chunk and a partial one, so the
-    two-level dot sums (chunk sums ticked while the kernels run, then the
-    final level) cover a ragged last chunk; k = 1 runs the unfused
-    iteration (x/r update kernel), stride 3 and x0 the residual kernel."""
+@pytest.mark.parametrize("n,k,pol,tol", ((50, 2, "fixed-low", 1e-8), (50, 1, "uniform", 1e-8),
+                                         (130, 2, "fixed-low", 1e-6), (130, 1, "uniform", 1e-6),
+                                         (130, 2, "adaptive-lh:1e-4", 1e-6)))
+def test_pcg_dot_sum_orders_bitwise(cuda, oracle, n, k, pol, tol):
+    """n = 50: 489 tiles, the one-level sum in the kernels' final CTA.
+    n = 130: 8,583 tiles > MPB_ONE_LEVEL_TILES, the two-level sum (33 full
+    chunks and a ragged one) whose chunks the CTAs that claimed their last
+    tiles sum while the kernels run.  k = 1 runs the unfused iteration (x/r
+    update kernel), stride 3 and x0 the residual kernel."""
     from paper_2407_15973_b200 import problems
-    cs = problems.make_config("c2", 50)
+    cs = problems.make_config("c2", n)
     offs = np.append(np.arange(0, cs.A.n, 64), cs.A.n)
     x0 = np.cos(np.arange(cs.A.n) * 0.01)
-    rep, orc = _solve_both(cs.A, cs.b, offs, pol, k, 2, 1e-8, oracle, stride=3, x0=x0)
+    rep, orc = _solve_both(cs.A, cs.b, offs, pol, k, 2, tol, oracle, stride=3, x0=x0)
     assert rep.iterations == orc["iterations"]
     np.testing.assert_array_equal(rep.x, orc["x"])
     np.testing.assert_array_equal([r.implicit_relres for r in rep.trace], orc["relres"])
