@@ -257,12 +257,15 @@ int mpb_pcg_solve(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A,
  * bracketing every launch with CUDA events, using the buffers of a prior
  * mpb_pcg_solve with the same arguments (the solver state is reset to a
  * mid-solve state before each launch).  branch: 0 fp64 / 1 fp32 instance.
- * h_ms[8] receives the mean ms per launch of: 0 first BJAC pass,
+ * h_ms[16] receives the mean ms per launch of: 0 first BJAC pass,
  * 1 middle passes (all of them, 0 when k < 3), 2 last BJAC pass,
  * 3 SpMV q = A p with the fused p.q step, 4 x/r update (fused relres
  * step), 5 x/r update fused with the next iteration's first pass (what the
  * solve runs when k >= 2 on one GPU; 0 otherwise), 6 whole iteration (sum of
- * the kernels the solve runs), 7 p-update p = z + beta p. */
+ * the kernels the solve runs), 7 p-update p = z + beta p; each launched
+ * alone between two events ("cold").  h_ms[8 + i]: the same kernels, `reps`
+ * launches back to back with programmatic dependent launch as the solve
+ * graph chains them ("chained"). */
 int mpb_profile_iteration(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A,
                           const mpb_solve_options *opt, const double *b, double *x,
                           void *workspace, int64_t workspace_bytes, int branch,

@@ -1819,8 +1819,14 @@ static int profile_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, c
   auto reset = [&]() -> cudaError_t {
     return cudaMemcpyAsync(w.st, h->h_state, sizeof(SolverState), cudaMemcpyHostToDevice, s);
   };
-  for (int i = 0; i < 8; i++) h_ms[i] = 0.0;  // 7: p-update
+  for (int i = 0; i < 16; i++) h_ms[i] = 0.0;  // 7: p-update; 8..15: the same, chained
   const unsigned nt = static_cast<unsigned>(plan->ntiles);
+  // h_ms[slot]: one launch between two events (cold: launch latency, ramp
+  // and drain included); h_ms[8 + slot]: `reps` launches back to back with
+  // programmatic dependent launch, as the solve graph chains its kernels
+  // (each launch's prologue overlaps the previous one's drain), per launch.
+  // Within the chain the scalar steps advance the state as in a solve (the
+  // mid-solve state keeps them finite; res_tol 0 keeps the launches live).
   auto timed = [&](int slot, auto &&launch) -> int {
     float total = 0.f;
     for (int r = 0; r < reps; r++) {
@@ -1835,6 +1841,17 @@ static int profile_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, c
       total += ms;
     }
     h_ms[slot] += total / reps;
+    MPB_CUDA(reset());
+    MPB_CUDA(cudaEventRecord(h->ev_t0, s));
+    for (int r = 0; r < reps; r++) {
+      int lrc = launch();
+      if (lrc) return lrc;
+    }
+    MPB_CUDA(cudaEventRecord(h->ev_t1, s));
+    MPB_CUDA(cudaEventSynchronize(h->ev_t1));
+    float ms = 0.f;
+    MPB_CUDA(cudaEventElapsedTime(&ms, h->ev_t0, h->ev_t1));
+    h_ms[8 + slot] += ms / reps;
     return MPB_OK;
   };
   // BJAC passes of the requested instance, one pass at a time
@@ -1906,7 +1923,7 @@ static int profile_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, c
     if (rc) return rc;
   }
   rc = timed(3, [&]() -> int {
-    spmv_kernel(plan)<<<sgrid, kWsThreads, sdyn, s>>>(sa);
+    MPB_CUDA(launch_k(!dist, spmv_kernel(plan), sgrid, kWsThreads, sdyn, s, sa));
     MPB_LAUNCHED(h);
     return MPB_OK;
   });
@@ -1930,8 +1947,11 @@ static int profile_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, c
     });
     if (rc) return rc;
   }
-  const double passes = h_ms[1] * (opt->k > 2 ? opt->k - 2 : 0) + h_ms[2];
-  h_ms[6] = fused ? passes + h_ms[3] + h_ms[5] + h_ms[7] : h_ms[0] + passes + h_ms[3] + h_ms[4] + h_ms[7];
+  for (int c = 0; c < 16; c += 8) {
+    double *m = h_ms + c;
+    const double passes = m[1] * (opt->k > 2 ? opt->k - 2 : 0) + m[2];
+    m[6] = fused ? passes + m[3] + m[5] + m[7] : m[0] + passes + m[3] + m[4] + m[7];
+  }
   MPB_CUDA(cudaEventRecord(h->ev_out, s));
   MPB_CUDA(cudaStreamWaitEvent(h->user, h->ev_out, 0));
   return MPB_OK;

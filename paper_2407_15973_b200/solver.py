@@ -354,7 +354,9 @@ def profile_iteration(A: SparseMatrix, mp: MixedPreconditioner, *,
                       config: SolveConfig = SolveConfig(), branch: str = "low",
                       reps: int = 20, ghosts: int = 0, n_global=None) -> dict:
     """Mean CUDA-event time (ms) per launch of each kernel of one PCG
-    iteration, on the buffers pcg_solve uses (mpb_profile_iteration).
+    iteration, on the buffers pcg_solve uses (mpb_profile_iteration): each
+    kernel launched alone ("<name>") and chained back to back with
+    programmatic dependent launch as in the solve graph ("<name>_chained").
     Call after at least one pcg_solve with the same A / mp / config.
     ghosts > 0: a slab of a multi-GPU solve (local kernels only)."""
     D, s = _dev_struct(A, mp)
@@ -369,7 +371,7 @@ def profile_iteration(A: SparseMatrix, mp: MixedPreconditioner, *,
     opt.k, opt.t = P.k, P.t
     opt.res_tol = float(config.res_tol)
     opt.max_iter = cap
-    out = (C.c_double * 8)()
+    out = (C.c_double * 16)()
     if n_global is None:    # one GPU: the kernels pcg_solve runs (fused iteration)
         _lib.check(h.lib.mpb_profile_iteration(
             h.ptr, P.plan.ptr, C.byref(s), C.byref(opt), _lib.ptr(bd), _lib.ptr(x),
@@ -382,4 +384,6 @@ def profile_iteration(A: SparseMatrix, mp: MixedPreconditioner, *,
             "profile_iteration")
     names = ("bjac_first", "bjac_middle", "bjac_last", "spmv_pq", "update",
              "update_first", "iteration", "pupdate")
-    return {k: float(out[i]) for i, k in enumerate(names)}
+    res = {k: float(out[i]) for i, k in enumerate(names)}
+    res.update({k + "_chained": float(out[8 + i]) for i, k in enumerate(names)})
+    return res
