@@ -845,16 +845,43 @@ __device__ __forceinline__ T pass_row_sweep(const PassRow<T> &q, const PassArgs<
 // One tile of a fused (non-first-only) pass, consumer threads only.  col /
 // val / spp / mt are the shared stage or the global arrays offset to the
 // tile (same indexing); r64t / rTt the tile's residual slice.
+// Deferred tile sums (MPB_DEFER_TREE, on unless 0): with inner sweeps, the
+// warps store their warp sums of tile i and move on; warp 0 finishes tile
+// i's sum after the first sweep barrier of the CTA's next tile (which every
+// warp passes only after storing), so the tile sum needs no barriers of its
+// own.  Same arithmetic as tile_tree_rows.  dt: the pending tile (-1 none)
+// and the ws slot (0/1) it occupies.
+#ifndef MPB_DEFER_TREE
+#define MPB_DEFER_TREE 1
+#endif
+struct DeferredTree {
+  int tile = -1, slot = 0;
+};
+__device__ __forceinline__ void deferred_tree_finish(DeferredTree &dt, double *part, const double *ws) {
+  if (dt.tile < 0) return;
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    double r = lane < kTileThreads / 32 ? ws[dt.slot * 8 + lane] : 0.0;
+    r = warp_bfly(r);
+    if (lane == 0) put_part(part + dt.tile, r);
+  }
+  dt.tile = -1;
+}
+
 template <typename T, bool FIRST, bool LAST, int KS, bool GEN>
 __device__ __forceinline__ void bjac_tile_body(const PassArgs<T> &a, int tile, const TileDesc &d, const int *col,
                                                const T *val, const int *spp, const uint16_t *mt, const double *r64t,
-                                               const T *rTt, const int *s_pat, T *s_w, double *ws) {
+                                               const T *rTt, const int *s_pat, T *s_w, double *ws,
+                                               DeferredTree &dt) {
+  static_assert(kRowsPerThread == 1 || !MPB_DEFER_TREE, "deferred tile sums: one row per thread");
+  const bool defer = MPB_DEFER_TREE && LAST && a.part != nullptr && a.t >= 2;
   PassRow<T> q[kRowsPerThread];
 #pragma unroll
   for (int k = 0; k < kRowsPerThread; k++)
     pass_row_init<T, FIRST, KS, GEN>(q[k], a, d, threadIdx.x + k * kConsumers, col, val, spp, mt, r64t, rTt, s_pat, s_w);
   for (int s = 1; s < a.t; s++) {  // inner sweeps, the tile's w in shared memory
     named_sync(kBarConsumers, kConsumers);
+    if (defer && s == 1) deferred_tree_finish(dt, a.part, ws);
     T acc[kRowsPerThread];
 #pragma unroll
     for (int k = 0; k < kRowsPerThread; k++)
@@ -878,7 +905,12 @@ __device__ __forceinline__ void bjac_tile_body(const PassArgs<T> &a, int tile, c
     if (a.zout64 != nullptr) a.zout64[row] = static_cast<double>(zo);
     if (LAST && a.part != nullptr) prod[k] = __dmul_rn(r64t[tid], static_cast<double>(zo));
   }
-  if (LAST && a.part != nullptr) {
+  if (defer) {
+    const double w = warp_bfly(prod[0]);
+    dt.slot ^= 1;
+    if ((threadIdx.x & 31) == 0) ws[dt.slot * 8 + (threadIdx.x >> 5)] = w;
+    dt.tile = tile;
+  } else if (LAST && a.part != nullptr) {
     const double tot = tile_tree_rows(prod, ws, kBarConsumers);
     if (threadIdx.x == 0) put_part(a.part + tile, tot);
   }
@@ -1016,6 +1048,7 @@ __global__ void MPB_WS_BOUNDS_PASS k_bjac_tile(const PassArgs<T> a) {
       tl_mark(a.st, 3, 3, true);
 #endif
     }
+    DeferredTree dt;
     for (RingCursor cur;; cur.advance(ns)) {
       const int st = cur.st;
       mbar_wait(&R.full[st], cur.phase);
@@ -1050,14 +1083,18 @@ __global__ void MPB_WS_BOUNDS_PASS k_bjac_tile(const PassArgs<T> a) {
                                              staged(sb + L.sp, a.sp, d.s0, d.s1 + 1),
                                              staged(sb + L.meta, a.meta, d.lo, d.hi),
                                              R64 ? staged(sb + L.v0, a.r64, d.lo, d.hi) : nullptr,
-                                             R64 ? nullptr : staged(sb + L.v0, a.rT, d.lo, d.hi), s_pat, s_w, ws);
+                                             R64 ? nullptr : staged(sb + L.v0, a.rT, d.lo, d.hi), s_pat, s_w, ws, dt);
         } else {
           bjac_tile_body<T, FIRST, LAST, KS, GEN>(a, tile, d, col, a.sval + d.e0, a.sp + d.s0, a.meta + d.lo,
                                              R64 ? a.r64 + d.lo : nullptr, R64 ? nullptr : a.rT + d.lo, s_pat, s_w,
-                                             ws);
+                                             ws, dt);
         }
       }
       ring_release(R, st);
+    }
+    if (dt.tile >= 0) {  // the last tile's deferred sum: every warp has stored its share
+      named_sync(kBarConsumers, kConsumers);
+      deferred_tree_finish(dt, a.part, ws);
     }
     if (LAST && threadIdx.x == 0) tl_mark(a.st, 0, 1, true);
   }
