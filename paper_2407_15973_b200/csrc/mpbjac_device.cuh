@@ -154,29 +154,51 @@ __device__ __forceinline__ R block_tree_nb(R v, R *ws, int bar) {
 }
 
 // Global sum of tile partials, steps 1-3 with kFinThreads lanes.  Called by
-// all threads of a CTA with at least kFinThreads threads (threads beyond
-// kFinThreads contribute nothing); result valid in thread 0.  Partials are
-// read through L2 (__ldcg): other SMs wrote them in the same kernel.  Loads
-// are issued in batches of 8 before the (ordered) adds.
+// all threads of a CTA; RPT lanes per thread (lanes t + k * kFinThreads/RPT,
+// for CTAs with fewer than kFinThreads compute threads), threads beyond
+// contribute nothing; result valid in thread 0.  Partials are read through
+// L2 (__ldcg): other SMs wrote them in the same kernel.
 // B: loads in flight per lane (16 halves the L2 round trips of 8; kernels
 // whose register budget it would raise keep 8)
-template <int B = 16>
+template <int B = 16, int RPT = 1>
 __device__ __forceinline__ double fin_sum(const double *part, long long count, double *ws) {
-  double acc = 0.0;
-  if (threadIdx.x < kFinThreads) {
-    for (long long i0 = threadIdx.x; i0 < count; i0 += (long long)B * kFinThreads) {
-      double v[B];
+  constexpr int NT = kFinThreads / RPT;
+  double acc[RPT];
 #pragma unroll
-      for (int u = 0; u < B; u++) {
-        const long long i = i0 + (long long)u * kFinThreads;
-        v[u] = i < count ? __ldcg(part + i) : 0.0;
+  for (int k = 0; k < RPT; k++) acc[k] = 0.0;
+  if (threadIdx.x < NT) {
+#pragma unroll
+    for (int k = 0; k < RPT; k++) {
+      for (long long i0 = threadIdx.x + k * NT; i0 < count; i0 += (long long)B * kFinThreads) {
+        double v[B];
+#pragma unroll
+        for (int u = 0; u < B; u++) {
+          const long long i = i0 + (long long)u * kFinThreads;
+          v[u] = i < count ? __ldcg(part + i) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < B; u++)
+          if (i0 + (long long)u * kFinThreads < count) acc[k] = __dadd_rn(acc[k], v[u]);
       }
-#pragma unroll
-      for (int u = 0; u < B; u++)
-        if (i0 + (long long)u * kFinThreads < count) acc = __dadd_rn(acc, v[u]);
     }
   }
-  return block_tree<kFinThreads>(acc, ws);
+  if (RPT == 1) return block_tree<kFinThreads>(acc[0], ws);
+  // virtual warps (lane t + k NT), then warp 0 over the kFinThreads/32 warp sums
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < RPT; k++) acc[k] = warp_bfly(acc[k]);
+  __syncthreads();
+  if (lane == 0 && threadIdx.x < NT) {
+#pragma unroll
+    for (int k = 0; k < RPT; k++) ws[warp + k * (NT / 32)] = acc[k];
+  }
+  __syncthreads();
+  double r = 0.0;
+  if (warp == 0) {
+    r = lane < kFinThreads / 32 ? ws[lane] : 0.0;
+    r = warp_bfly(r);
+  }
+  return r;
 }
 
 // ---- two-level global sums (include/mpbjac_order.h) -------------------------

@@ -38,10 +38,15 @@
 namespace mpb {
 
 constexpr int kSlots = 9;                      // register-resident row entries (stencils, 3-T rows)
-constexpr int kRowsPerThread = 1;              // tile rows per consumer thread (2 measured slower: fewer warps per SM)
+#ifndef MPB_ROWS_PER_THREAD
+#define MPB_ROWS_PER_THREAD 1
+#endif
+constexpr int kRowsPerThread = MPB_ROWS_PER_THREAD;  // tile rows per consumer thread
 constexpr int kConsumers = kCtaThreads / kRowsPerThread;  // compute threads of the warp-specialised kernels
 constexpr int kWsThreads = kConsumers + 32;    // + one TMA producer warp
-static_assert(kWsThreads >= kFinThreads, "the last CTA's fin_sum uses kFinThreads threads");
+// final sums of the warp-specialised kernels: lanes per consumer thread
+constexpr int kFinRptWs = kConsumers >= kFinThreads ? 1 : kFinThreads / kConsumers;
+static_assert(kConsumers * kFinRptWs >= kFinThreads, "fin_sum lanes");
 constexpr int kMaxStages = 4;
 constexpr int kMaxPend = 4;  // owned chunks a producer keeps pending
 // MPB_MINB_PASS / MPB_MINB_SPMV=n (experiments): compile the warp-specialised
@@ -246,7 +251,7 @@ __device__ __forceinline__ void state_load(SolverState &L, const SolverState *g)
 // levels: the chunk sums are in ck.csum, stored by their owners before their
 // CTAs took the ticket (in_cta: grids that may exceed residency have no
 // owners; the final CTA sums the chunks here).
-template <int B = 16>
+template <int B = 16, int RPT = 1>
 __device__ __forceinline__ void finish_grid(SolverState *st, int ticket, int step, const ChunkCtx &ck, double *ws,
                                             bool in_cta = false) {
   if (st == nullptr) return;
@@ -256,8 +261,8 @@ __device__ __forceinline__ void finish_grid(SolverState *st, int ticket, int ste
   if (ck.poll && in_cta) chunk_all_in_cta(ck);
   if (threadIdx.x == 0) tl_mark(st, step == kStepRho ? 0 : (step == kStepPq ? 1 : 2), 3, true);  // diagnostics
   const int nch = (ck.ntiles + kChunkTiles - 1) / kChunkTiles;
-  const double tot = ck.poll ? fin_sum<B>(ck.csum, nch, ws)
-                             : fin_sum<B>(ck.part, ck.ntiles, ws);  // (their barriers publish s_state)
+  const double tot = ck.poll ? fin_sum<B, RPT>(ck.csum, nch, ws)
+                             : fin_sum<B, RPT>(ck.part, ck.ntiles, ws);  // (their barriers publish s_state)
   SolverState *L = reinterpret_cast<SolverState *>(s_state);
   const bool dist = L->dist != 0;
   if (threadIdx.x == 0) {
@@ -873,7 +878,6 @@ __device__ __forceinline__ void bjac_tile_body(const PassArgs<T> &a, int tile, c
                                                const T *val, const int *spp, const uint16_t *mt, const double *r64t,
                                                const T *rTt, const int *s_pat, T *s_w, double *ws,
                                                DeferredTree &dt) {
-  static_assert(kRowsPerThread == 1 || !MPB_DEFER_TREE, "deferred tile sums: one row per thread");
   const bool defer = MPB_DEFER_TREE && LAST && a.part != nullptr && a.t >= 2;
   PassRow<T> q[kRowsPerThread];
 #pragma unroll
@@ -906,9 +910,12 @@ __device__ __forceinline__ void bjac_tile_body(const PassArgs<T> &a, int tile, c
     if (LAST && a.part != nullptr) prod[k] = __dmul_rn(r64t[tid], static_cast<double>(zo));
   }
   if (defer) {
-    const double w = warp_bfly(prod[0]);
     dt.slot ^= 1;
-    if ((threadIdx.x & 31) == 0) ws[dt.slot * 8 + (threadIdx.x >> 5)] = w;
+#pragma unroll
+    for (int k = 0; k < kRowsPerThread; k++) {  // virtual warp (threadIdx.x >> 5) + k * kConsumers / 32
+      const double w = warp_bfly(prod[k]);
+      if ((threadIdx.x & 31) == 0) ws[dt.slot * 8 + (threadIdx.x >> 5) + k * (kConsumers / 32)] = w;
+    }
     dt.tile = tile;
   } else if (LAST && a.part != nullptr) {
     const double tot = tile_tree_rows(prod, ws, kBarConsumers);
@@ -1100,7 +1107,7 @@ __global__ void MPB_WS_BOUNDS_PASS k_bjac_tile(const PassArgs<T> a) {
   }
   pdl_trigger();  // dependents may launch into the SMs this grid drains
   if (LAST && a.part != nullptr)
-    finish_grid(a.st, 0, kStepRho, ChunkCtx{a.csum, a.part, a.g.ntiles, TWO ? a.g.poll : 0}, ws);
+    finish_grid<16, kFinRptWs>(a.st, 0, kStepRho, ChunkCtx{a.csum, a.part, a.g.ntiles, TWO ? a.g.poll : 0}, ws);
 }
 
 // ---- large blocks (> kTileRows rows): one launch per inner sweep ----------
@@ -1354,7 +1361,7 @@ __global__ void MPB_WS_BOUNDS_SPMV k_spmv_pq(const SpmvArgs a) {
     if (threadIdx.x == 0) tl_mark(a.st, 1, 1, true);
   }
   pdl_trigger();
-  finish_grid(a.st, 1, kStepPq, ChunkCtx{a.csum, a.part, a.g.ntiles, TWO ? a.g.poll : 0}, ws);
+  finish_grid<16, kFinRptWs>(a.st, 1, kStepPq, ChunkCtx{a.csum, a.part, a.g.ntiles, TWO ? a.g.poll : 0}, ws);
 }
 
 // x += alpha p ; r -= alpha q ; r.r partial   (solver.py:160-165)
@@ -1500,7 +1507,7 @@ __device__ __forceinline__ void update_first_body(const PassArgs<T> &a, double *
     if (threadIdx.x == 0) tl_mark(a.st, 2, 1, true);
   }
   pdl_trigger();
-  finish_grid<8>(a.st, 2, kStepRrZ, ChunkCtx{a.csum, a.part, a.g.ntiles, TWO ? a.g.poll : 0}, ws);  // 16: a CTA per SM less
+  finish_grid<8, kFinRptWs>(a.st, 2, kStepRrZ, ChunkCtx{a.csum, a.part, a.g.ntiles, TWO ? a.g.poll : 0}, ws);  // 16: a CTA per SM less
 }
 
 // One-level order: ptxas' own register budget (40, 5 CTAs per SM; an
