@@ -240,11 +240,7 @@ constexpr unsigned long long kPartEmpty = ~0ull;
 __device__ __forceinline__ void put_part(double *p, double v) {
   unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
   if (b == kPartEmpty) b = 0x7ff8000000000000ull;  // (still a NaN; the empty pattern stays unique)
-#ifdef MPB_EXP_WEAK_PART
-  *reinterpret_cast<unsigned long long *>(p) = b;
-#else
   asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(b) : "memory");
-#endif
 }
 __device__ __forceinline__ unsigned long long get_part_bits(const double *p) {
   unsigned long long b;
