@@ -327,6 +327,42 @@ int mpb_assemble_stencil(mpb_handle *h, int64_t n, const double *kappa,
 int mpb_splitmix64_uniform(mpb_handle *h, uint64_t seed, int64_t count,
                            double a, double b, double *out);
 
+/* ---- row features (features.py:41-211 on the device) --------------------- */
+/* Per row of a CSR matrix (device row_ptr (n+1), col_idx, values: exactly one
+ * of val64 / val32): tau = max/min |a_ij| over stored nonzero off-diagonals
+ * (NaN when undefined: none, or a non-finite maximum), dom = |a_ii| /
+ * sum_{j!=i} |a_ij| (inf when that sum is 0), row_sum = sum a_ij, abs_sum =
+ * sum |a_ij|, diag = stored a_ii (0 if missing); all in fp64, sums in
+ * numpy's add.reduceat order (bit-identical to the reference).  Any output
+ * may be NULL.  Replaces features.py:27-55 / 127-152 / 190-196. */
+int mpb_row_features(mpb_handle *h, int64_t n, const int32_t *row_ptr,
+                     const int32_t *col_idx, const double *val64,
+                     const float *val32, double *tau, double *dom,
+                     double *row_sum, double *abs_sum, double *diag);
+/* Lower-inclusive histogram of the non-NaN tau over h_edges (ascending,
+ * <= 64 host values; the last bin unbounded) and the NaN (undefined) count
+ * (features.py:94-113).  Synchronous. */
+int mpb_tau_histogram(mpb_handle *h, int64_t n, const double *tau,
+                      const double *h_edges, int nedges, int64_t *h_counts,
+                      int64_t *h_undefined);
+/* min, median (mean of the middle two for even n), max of x with numpy's NaN
+ * propagation, and the count of x > thresh (features.py:144-152).
+ * Synchronous. */
+int mpb_vector_stats(mpb_handle *h, int64_t n, const double *x, double thresh,
+                     double *h_min, double *h_median, double *h_max,
+                     int64_t *h_count_gt);
+/* The first k (<= 1024) violations in index order of an M-matrix sign check
+ * (features.py:182-203): kind 0 rows with !(a_i > 0) (a = diag); kind 1 rows
+ * with a_i < -(tol * b_i) (a = row sums, b = absolute row sums); kind 2
+ * entries (n = nnz) off the diagonal with a value > 0 (row_ptr / nrows /
+ * col_idx / values of the matrix).  *h_found = how many were written.
+ * Synchronous. */
+int mpb_first_violations(mpb_handle *h, int kind, int64_t n, const double *a,
+                         const double *b, double tol, const int32_t *row_ptr,
+                         int64_t nrows, const int32_t *col_idx,
+                         const double *val64, const float *val32, int k,
+                         int64_t *h_idx, int64_t *h_found);
+
 /* ||b - A x|| / r0_norm in device order.  Synchronous. */
 int mpb_true_relres(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A,
                     const double *x, const double *b, double r0_norm,

@@ -43,6 +43,8 @@ EXPORTED = (
     "mpb_comm_destroy", "mpb_solve_workspace_bytes_dist", "mpb_pcg_solve_dist",
     "mpb_profile_iteration_dist", "mpb_plan_layout_info", "mpb_stencil_nnz",
     "mpb_assemble_stencil", "mpb_splitmix64_uniform",
+    "mpb_row_features", "mpb_tau_histogram", "mpb_vector_stats",
+    "mpb_first_violations",
 )
 
 
@@ -107,6 +109,13 @@ def _declare(L):
         "mpb_assemble_stencil": ([_P, _I64, _P, C.c_double, C.c_double, C.c_double, C.c_double, _P, _P, _P],
                                  C.c_int),
         "mpb_splitmix64_uniform": ([_P, C.c_uint64, _I64, C.c_double, C.c_double, _P], C.c_int),
+        "mpb_row_features": ([_P, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P], C.c_int),
+        "mpb_tau_histogram": ([_P, _I64, _P, C.POINTER(C.c_double), C.c_int, C.POINTER(C.c_int64),
+                               C.POINTER(C.c_int64)], C.c_int),
+        "mpb_vector_stats": ([_P, _I64, _P, C.c_double, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                              C.POINTER(C.c_double), C.POINTER(C.c_int64)], C.c_int),
+        "mpb_first_violations": ([_P, C.c_int, _I64, _P, _P, C.c_double, _P, _I64, _P, _P, _P, C.c_int,
+                                  C.POINTER(C.c_int64), C.POINTER(C.c_int64)], C.c_int),
         "mpb_csr_matvec_f64": ([_P, _I64, _P, _P, _P, _P, _P], C.c_int),
         "mpb_csr_matvec_f32": ([_P, _I64, _P, _P, _P, _P, _P], C.c_int),
         "mpb_block_jacobi_sweeps_f64": ([_P, _P, _P, _P, _P, _P, C.c_int, _P, _P, _P, _I64, _I64], C.c_int),

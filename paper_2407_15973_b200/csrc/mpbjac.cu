@@ -16,6 +16,9 @@
 
 #include "../../include/mpbjac.h"
 #include "mpbjac_kernels.cuh"
+#include "mpbjac_features.cuh"
+
+#include <cub/device/device_radix_sort.cuh>
 #include "mpbjac_nccl.h"
 
 using namespace mpb;
@@ -1980,3 +1983,121 @@ int mpb_true_relres(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, const
   *h_out = std::sqrt(v) / r0_norm;
   return MPB_OK;
 }
+
+// ---- row features (features.py restated on the device) ---------------------
+int mpb_row_features(mpb_handle *h, int64_t n, const int32_t *row_ptr, const int32_t *col_idx, const double *val64,
+                     const float *val32, double *tau, double *dom, double *row_sum, double *abs_sum, double *diag) {
+  if (!h || n < 0 || !row_ptr || !col_idx || (val64 == nullptr) == (val32 == nullptr)) return MPB_ERR_ARG;
+  if (n == 0) return MPB_OK;
+  MPB_CUDA(cudaSetDevice(h->device));
+  if (val64)
+    k_row_features<double><<<elt_blocks(n), kEltThreads, 0, h->user>>>(n, row_ptr, col_idx, val64, tau, dom, row_sum,
+                                                                       abs_sum, diag);
+  else
+    k_row_features<float><<<elt_blocks(n), kEltThreads, 0, h->user>>>(n, row_ptr, col_idx, val32, tau, dom, row_sum,
+                                                                      abs_sum, diag);
+  MPB_LAUNCHED(h);
+  return MPB_OK;
+}
+
+int mpb_tau_histogram(mpb_handle *h, int64_t n, const double *tau, const double *h_edges, int nedges,
+                      int64_t *h_counts, int64_t *h_undefined) {
+  if (!h || n < 0 || (n > 0 && !tau) || !h_edges || nedges < 1 || nedges > kMaxEdges || !h_counts || !h_undefined)
+    return MPB_ERR_ARG;
+  MPB_CUDA(cudaSetDevice(h->device));
+  int rc = ensure_scratch(h, 2 * al256(sizeof(double) * (kMaxEdges + 1)));
+  if (rc) return rc;
+  unsigned long long *cnt = static_cast<unsigned long long *>(h->scratch);
+  double *edges = reinterpret_cast<double *>(static_cast<char *>(h->scratch) + al256(sizeof(double) * (kMaxEdges + 1)));
+  MPB_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * (nedges + 1), h->user));
+  MPB_CUDA(cudaMemcpyAsync(edges, h_edges, sizeof(double) * nedges, cudaMemcpyHostToDevice, h->user));
+  if (n > 0) {
+    k_tau_histogram<<<std::min(elt_blocks(n), 4 * num_sms()), kEltThreads, 0, h->user>>>(n, tau, edges, nedges, cnt);
+    MPB_LAUNCHED(h);
+  }
+  std::vector<unsigned long long> hc(nedges + 1);
+  MPB_CUDA(cudaMemcpyAsync(hc.data(), cnt, sizeof(unsigned long long) * (nedges + 1), cudaMemcpyDeviceToHost, h->user));
+  MPB_CUDA(cudaStreamSynchronize(h->user));
+  for (int j = 0; j < nedges; j++) h_counts[j] = static_cast<int64_t>(hc[j]);
+  *h_undefined = static_cast<int64_t>(hc[nedges]);
+  return MPB_OK;
+}
+
+int mpb_vector_stats(mpb_handle *h, int64_t n, const double *x, double thresh, double *h_min, double *h_median,
+                     double *h_max, int64_t *h_count_gt) {
+  if (!h || n < 1 || !x || !h_min || !h_median || !h_max || !h_count_gt) return MPB_ERR_ARG;
+  MPB_CUDA(cudaSetDevice(h->device));
+  size_t sort_bytes = 0;
+  MPB_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, sort_bytes, static_cast<const double *>(nullptr),
+                                          static_cast<double *>(nullptr), static_cast<int>(n)));
+  const size_t acc_b = 256, vec_b = al256(sizeof(double) * n);
+  int rc = ensure_scratch(h, acc_b + vec_b + al256(sort_bytes));
+  if (rc) return rc;
+  char *base = static_cast<char *>(h->scratch);
+  unsigned long long *acc = reinterpret_cast<unsigned long long *>(base);
+  double *sorted = reinterpret_cast<double *>(base + acc_b);
+  void *tmp = base + acc_b + vec_b;
+  const unsigned long long init[4] = {~0ull, 0ull, 0ull, 0ull};
+  MPB_CUDA(cudaMemcpyAsync(acc, init, sizeof(init), cudaMemcpyHostToDevice, h->user));
+  k_vector_stats<<<std::min(elt_blocks(n), 4 * num_sms()), kEltThreads, 0, h->user>>>(n, x, thresh, acc);
+  MPB_LAUNCHED(h);
+  unsigned long long ha[4];
+  MPB_CUDA(cudaMemcpyAsync(ha, acc, sizeof(ha), cudaMemcpyDeviceToHost, h->user));
+  MPB_CUDA(cudaStreamSynchronize(h->user));
+  *h_count_gt = static_cast<int64_t>(ha[3]);
+  if (ha[2]) {  // numpy: min, max and median of an array holding NaN are NaN
+    *h_min = *h_max = *h_median = NAN;
+    return MPB_OK;
+  }
+  *h_min = dkey_inv(ha[0]);
+  *h_max = dkey_inv(ha[1]);
+  // median (np.median: the middle value, or the mean of the middle two)
+  MPB_CUDA(cub::DeviceRadixSort::SortKeys(tmp, sort_bytes, x, sorted, static_cast<int>(n), 0, 64, h->user));
+  MPB_LAUNCHED(h);
+  double mid[2] = {0.0, 0.0};
+  const int64_t m0 = (n - 1) / 2;
+  MPB_CUDA(cudaMemcpyAsync(mid, sorted + m0, sizeof(double) * (n % 2 ? 1 : 2), cudaMemcpyDeviceToHost, h->user));
+  MPB_CUDA(cudaStreamSynchronize(h->user));
+  *h_median = n % 2 ? mid[0] : (mid[0] + mid[1]) / 2.0;
+  return MPB_OK;
+}
+
+int mpb_first_violations(mpb_handle *h, int kind, int64_t n, const double *a, const double *b, double tol,
+                         const int32_t *row_ptr, int64_t nrows, const int32_t *col_idx, const double *val64,
+                         const float *val32, int k, int64_t *h_idx, int64_t *h_found) {
+  if (!h || n < 0 || k < 1 || k > 1024 || !h_idx || !h_found || kind < 0 || kind > 2) return MPB_ERR_ARG;
+  if ((kind == 0 && !a) || (kind == 1 && (!a || !b)) ||
+      (kind == 2 && (!row_ptr || !col_idx || nrows < 1 || (val64 == nullptr) == (val32 == nullptr))))
+    return MPB_ERR_ARG;
+  *h_found = 0;
+  if (n == 0) return MPB_OK;
+  MPB_CUDA(cudaSetDevice(h->device));
+  constexpr int kChunkBlocks = 4096;  // items per round: 4096 * kFlagBlock
+  const size_t out_b = al256(sizeof(long long) * kChunkBlocks * k), cnt_b = al256(sizeof(int) * kChunkBlocks);
+  int rc = ensure_scratch(h, out_b + cnt_b);
+  if (rc) return rc;
+  long long *out = static_cast<long long *>(h->scratch);
+  int *cnt = reinterpret_cast<int *>(static_cast<char *>(h->scratch) + out_b);
+  std::vector<long long> ho(static_cast<size_t>(kChunkBlocks) * k);
+  std::vector<int> hcnt(kChunkBlocks);
+  int64_t found = 0;
+  for (long long base = 0; base < n && found < k; base += (long long)kChunkBlocks * kFlagBlock) {
+    const long long items = std::min<long long>(n - base, (long long)kChunkBlocks * kFlagBlock);
+    const int blocks = static_cast<int>((items + kFlagBlock - 1) / kFlagBlock);
+    if (kind == 2 && val32)
+      k_first_flags<float><<<blocks, 256, 0, h->user>>>(kind, n, base, a, b, tol, row_ptr, nrows, col_idx, val32, k,
+                                                        out, cnt);
+    else
+      k_first_flags<double><<<blocks, 256, 0, h->user>>>(kind, n, base, a, b, tol, row_ptr, nrows, col_idx, val64, k,
+                                                         out, cnt);
+    MPB_LAUNCHED(h);
+    MPB_CUDA(cudaMemcpyAsync(hcnt.data(), cnt, sizeof(int) * blocks, cudaMemcpyDeviceToHost, h->user));
+    MPB_CUDA(cudaMemcpyAsync(ho.data(), out, sizeof(long long) * blocks * k, cudaMemcpyDeviceToHost, h->user));
+    MPB_CUDA(cudaStreamSynchronize(h->user));
+    for (int blk = 0; blk < blocks && found < k; blk++)
+      for (int j = 0; j < std::min(hcnt[blk], k) && found < k; j++) h_idx[found++] = ho[static_cast<size_t>(blk) * k + j];
+  }
+  *h_found = found;
+  return MPB_OK;
+}
+
