@@ -18,35 +18,41 @@
 
 namespace mpb {
 
+// numpy pairwise_sum for n <= 128 (no recursion; inlined)
 template <typename F>
-__device__ double np_pairwise(const F &f, long long i0, long long n) {
+__device__ __forceinline__ double np_pairwise_small(const F &f, long long i0, long long n) {
   if (n < 8) {
     double r = -0.0;
     for (long long i = 0; i < n; i++) r = __dadd_rn(r, f(i0 + i));
     return r;
   }
-  if (n <= 128) {
-    double r[8];
+  double r[8];
 #pragma unroll
-    for (int j = 0; j < 8; j++) r[j] = f(i0 + j);
-    long long i = 8;
-    for (; i < n - (n % 8); i += 8) {
+  for (int j = 0; j < 8; j++) r[j] = f(i0 + j);
+  long long i = 8;
+  for (; i < n - (n % 8); i += 8) {
 #pragma unroll
-      for (int j = 0; j < 8; j++) r[j] = __dadd_rn(r[j], f(i0 + i + j));
-    }
-    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-    for (; i < n; i++) res = __dadd_rn(res, f(i0 + i));
-    return res;
+    for (int j = 0; j < 8; j++) r[j] = __dadd_rn(r[j], f(i0 + i + j));
   }
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (; i < n; i++) res = __dadd_rn(res, f(i0 + i));
+  return res;
+}
+// the recursive split for longer segments (rare: rows of more than 129 entries)
+template <typename F>
+__device__ __noinline__ double np_pairwise_big(const F &f, long long i0, long long n) {
   long long n2 = n / 2;
   n2 -= n2 % 8;
-  return __dadd_rn(np_pairwise(f, i0, n2), np_pairwise(f, i0 + n2, n - n2));
+  const double a = n2 <= 128 ? np_pairwise_small(f, i0, n2) : np_pairwise_big(f, i0, n2);
+  const double b = n - n2 <= 128 ? np_pairwise_small(f, i0 + n2, n - n2) : np_pairwise_big(f, i0 + n2, n - n2);
+  return __dadd_rn(a, b);
 }
 // np.add.reduceat of one nonempty segment [lo, lo + m)
 template <typename F>
-__device__ double np_segment_sum(const F &f, long long lo, long long m) {
-  return __dadd_rn(f(lo), np_pairwise(f, lo + 1, m - 1));
+__device__ __forceinline__ double np_segment_sum(const F &f, long long lo, long long m) {
+  const double rest = m - 1 <= 128 ? np_pairwise_small(f, lo + 1, m - 1) : np_pairwise_big(f, lo + 1, m - 1);
+  return __dadd_rn(f(lo), rest);
 }
 
 // One thread per row (features.py:41-55 multiscale_profile, :127-152
