@@ -416,6 +416,22 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// The same for data read once per kernel (matrix values / columns): L2
+// evict-first, so the streamed matrix does not push the iteration's vectors
+// (gathered by the next kernels) out of L2.  MPB_NO_EVICT_FIRST=1: plain.
+__device__ __forceinline__ void bulk_g2s_stream(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+#ifdef MPB_NO_EVICT_FIRST
+  bulk_g2s(dst, src, bytes, bar);
+#else
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+#endif
+}
 
 // Programmatic dependent launch: a kernel launched with programmatic stream
 // serialization may start while its predecessor drains; everything before

@@ -440,8 +440,8 @@ __device__ __forceinline__ void produce(Ring &R, int st, const TileDesc *td, int
   if (part == kFillAll) mbar_arrive_expect_tx(&R.full[st], sbytes + dbytes);
   if (part == kFillStatic) mbar_expect_tx(&R.full[st], sbytes);
   if (part != kFillDynamic) {
-    if (cols) bulk_g2s(stage + L.col, scol + e0, static_cast<uint32_t>(nent) * 4u, &R.full[st]);
-    bulk_g2s(stage + L.val, sval + e0, static_cast<uint32_t>(nent) * sizeof(T), &R.full[st]);
+    if (cols) bulk_g2s_stream(stage + L.col, scol + e0, static_cast<uint32_t>(nent) * 4u, &R.full[st]);
+    bulk_g2s_stream(stage + L.val, sval + e0, static_cast<uint32_t>(nent) * sizeof(T), &R.full[st]);
     tma_window(stage + L.sp, sp, d.s0, d.s1 + 1, &R.full[st]);
     if (meta != nullptr) tma_window(stage + L.meta, meta, d.lo, d.hi, &R.full[st]);
   }
