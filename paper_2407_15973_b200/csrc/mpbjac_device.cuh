@@ -416,6 +416,16 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// global store with an L2 evict-first policy (data not read again soon)
+__device__ __forceinline__ void st_evict_first(double *p, double v) {
+#ifdef MPB_NO_EVICT_FIRST
+  *p = v;
+#else
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+#endif
+}
 // The same for data read once per kernel (matrix values / columns): L2
 // evict-first, so the streamed matrix does not push the iteration's vectors
 // (gathered by the next kernels) out of L2.  MPB_NO_EVICT_FIRST=1: plain.

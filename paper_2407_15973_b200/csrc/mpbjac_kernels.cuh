@@ -389,9 +389,11 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 }
 
 template <typename E>
-__device__ __forceinline__ void tma_window(unsigned char *dst, const E *base, int lo, int hi, uint64_t *bar) {
+__device__ __forceinline__ void tma_window(unsigned char *dst, const E *base, int lo, int hi, uint64_t *bar,
+                                           bool last_use = false) {
   const Window w = window_of(base, lo, hi);
-  bulk_g2s(dst, reinterpret_cast<const void *>(w.g0), w.bytes, bar);
+  if (last_use) bulk_g2s_stream(dst, reinterpret_cast<const void *>(w.g0), w.bytes, bar);
+  else bulk_g2s(dst, reinterpret_cast<const void *>(w.g0), w.bytes, bar);
 }
 template <typename E>
 __device__ __forceinline__ uint32_t window_bytes(const E *base, int lo, int hi) {
@@ -409,7 +411,10 @@ __device__ __forceinline__ const E *staged(const unsigned char *region, const E 
 // arrive that completes the stage).
 enum { kFillAll = 0, kFillStatic = 1, kFillDynamic = 2 };
 
-template <typename T, typename V0, typename V1, typename V2, bool IB = false, typename V3 = uint8_t>
+// LAST_USE: bit i set = vector slice vi is read for the last time this
+// iteration (streamed evict-first, like the matrix data)
+template <typename T, typename V0, typename V1, typename V2, bool IB = false, typename V3 = uint8_t,
+          unsigned LAST_USE = 0u>
 __device__ __forceinline__ void produce(Ring &R, int st, const TileDesc *td, int tile, const TileGeom &g,
                                         const StageLayout &L, unsigned char *stage, const int *sp, const int *scol,
                                         const T *sval, const uint16_t *meta, const V0 *v0, const V1 *v1,
@@ -447,10 +452,10 @@ __device__ __forceinline__ void produce(Ring &R, int st, const TileDesc *td, int
   }
   if (part == kFillStatic) return;
   if (part == kFillDynamic) mbar_arrive_expect_tx(&R.full[st], dbytes);
-  if (v0 != nullptr) tma_window(stage + L.v0, v0, d.lo, d.hi, &R.full[st]);
-  if (v1 != nullptr) tma_window(stage + L.v1, v1, d.lo, d.hi, &R.full[st]);
-  if (v2 != nullptr) tma_window(stage + L.v2, v2, d.lo, d.hi, &R.full[st]);
-  if (v3 != nullptr) tma_window(stage + L.v3, v3, d.lo, d.hi, &R.full[st]);
+  if (v0 != nullptr) tma_window(stage + L.v0, v0, d.lo, d.hi, &R.full[st], LAST_USE & 1u);
+  if (v1 != nullptr) tma_window(stage + L.v1, v1, d.lo, d.hi, &R.full[st], LAST_USE & 2u);
+  if (v2 != nullptr) tma_window(stage + L.v2, v2, d.lo, d.hi, &R.full[st], LAST_USE & 4u);
+  if (v3 != nullptr) tma_window(stage + L.v3, v3, d.lo, d.hi, &R.full[st], LAST_USE & 8u);
 }
 
 // Producer loop (producer warp, lane 0): claims tiles from the launch's
@@ -1450,8 +1455,9 @@ __device__ __forceinline__ void update_first_body(const PassArgs<T> &a, double *
   if (threadIdx.x >= kConsumers) {
     const ChunkCtx ck{a.csum, a.part, a.g.ntiles, TWO ? a.g.poll : 0};
     auto fill = [&](int st, int tile, int part) {
-      produce<T, double, double, double, true, double>(R, st, a.td, tile, a.g, L, smem + st * L.bytes, a.ib_sp,
-                                                       a.ib_col, a.ib_val, a.meta, r, x, p, q, part);
+      // x (v1) and q (v3) are not read again before the next x/r update
+      produce<T, double, double, double, true, double, 0xAu>(R, st, a.td, tile, a.g, L, smem + st * L.bytes,
+                                                             a.ib_sp, a.ib_col, a.ib_val, a.meta, r, x, p, q, part);
     };
     auto gated = [&]() { return gated_off(a); };
     if (TWO && ck.poll)
@@ -1486,7 +1492,7 @@ __device__ __forceinline__ void update_first_body(const PassArgs<T> &a, double *
         const double pv = ok ? staged(sb + L.v2, p, d.lo, d.hi)[i] : p[row];
         const double qv = ok ? staged(sb + L.v3, q, d.lo, d.hi)[i] : q[row];
         const double ro = ok ? staged(sb + L.v0, r, d.lo, d.hi)[i] : r[row];
-        x[row] = __dadd_rn(xv, __dmul_rn(alpha, pv));
+        st_evict_first(x + row, __dadd_rn(xv, __dmul_rn(alpha, pv)));  // (read again by the next update only)
         const double rn = __dsub_rn(ro, __dmul_rn(alpha, qv));
         r[row] = rn;
         sq[k] = __dmul_rn(rn, rn);
