@@ -855,14 +855,15 @@ __device__ __forceinline__ T pass_row_sweep(const PassRow<T> &q, const PassArgs<
 // One tile of a fused (non-first-only) pass, consumer threads only.  col /
 // val / spp / mt are the shared stage or the global arrays offset to the
 // tile (same indexing); r64t / rTt the tile's residual slice.
-// Deferred tile sums (MPB_DEFER_TREE, on unless 0): with inner sweeps, the
+// Deferred tile sums (MPB_DEFER_TREE=1; off: C2 -0.3 %, but the C4 last pass
+// +27 % and C3 / C5 +1 %): with inner sweeps, the
 // warps store their warp sums of tile i and move on; warp 0 finishes tile
 // i's sum after the first sweep barrier of the CTA's next tile (which every
 // warp passes only after storing), so the tile sum needs no barriers of its
 // own.  Same arithmetic as tile_tree_rows.  dt: the pending tile (-1 none)
 // and the ws slot (0/1) it occupies.
 #ifndef MPB_DEFER_TREE
-#define MPB_DEFER_TREE 1
+#define MPB_DEFER_TREE 0
 #endif
 struct DeferredTree {
   int tile = -1, slot = 0;
