@@ -187,13 +187,13 @@ int num_sms() {
 // that keeps the co-resident CTA count registers and threads allow
 // (MPB_STAGES=n forces n; MPB_VERBOSE=1 reports the choice).
 template <typename K>
-int pick_stages(K kernel, uint32_t stage_bytes) {
+int pick_stages(K kernel, uint32_t stage_bytes, int threads = kWsThreads) {
   auto per_sm = [&](int ns) {
     const uint32_t dyn = ns * stage_bytes;
     if (dyn > 220u * 1024u) return 0;
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn));
     int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, kWsThreads, dyn) != cudaSuccess) n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, dyn) != cudaSuccess) n = 0;
     return n;
   };
   static const int forced = std::getenv("MPB_STAGES") ? std::atoi(std::getenv("MPB_STAGES")) : 0;
@@ -258,12 +258,16 @@ int launch_tile_kernel(mpb_handle *h, cudaStream_t s, const mpb_plan *p, PassArg
     a.g.cap_e = std::min(p->max_tile_ib, kStageCap);
   }
   const StageLayout Ls = bjac_layout<T, F, R64>(a.g);
-  // the last pass carries the r.z sum: two-level order above MPB_ONE_LEVEL_TILES
-  auto kern = (L && a.g.poll) ? k_bjac_tile<T, F, L, R64, KS, GEN, L> : k_bjac_tile<T, F, L, R64, KS, GEN, false>;
-  a.g.ns = pick_stages(kern, Ls.bytes);
+  // the last pass carries the r.z sum: two-level order above MPB_ONE_LEVEL_TILES;
+  // a pass that is not the first runs kLastRpt rows per consumer thread
+  constexpr int RPT = (!F) ? kLastRpt : kRowsPerThread;
+  constexpr int threads = kTileThreads / RPT + 32;
+  auto kern = (L && a.g.poll) ? k_bjac_tile<T, F, L, R64, KS, GEN, L, RPT>
+                              : k_bjac_tile<T, F, L, R64, KS, GEN, false, RPT>;
+  a.g.ns = pick_stages(kern, Ls.bytes, threads);
   const uint32_t dyn = a.g.ns * Ls.bytes;
-  const int grid = persistent_grid(kern, dyn, p->ntiles, kWsThreads);
-  MPB_CUDA(launch_k(a.pdl != 0, kern, grid, kWsThreads, dyn, s, a));
+  const int grid = persistent_grid(kern, dyn, p->ntiles, threads);
+  MPB_CUDA(launch_k(a.pdl != 0, kern, grid, threads, dyn, s, a));
   MPB_LAUNCHED(h);
   return MPB_OK;
 }

@@ -44,6 +44,13 @@ constexpr int kSlots = 9;                      // register-resident row entries 
 constexpr int kRowsPerThread = MPB_ROWS_PER_THREAD;  // tile rows per consumer thread
 constexpr int kConsumers = kCtaThreads / kRowsPerThread;  // compute threads of the warp-specialised kernels
 constexpr int kWsThreads = kConsumers + 32;    // + one TMA producer warp
+// rows per consumer thread of the BJAC passes after the first (MPB_LAST_RPT=2:
+// 4 consumer warps per CTA, 6 CTAs per SM; measured 0.8 % slower on C2 and
+// 1.6 % on C4 than 1 row per thread, whose tails are shorter)
+#ifndef MPB_LAST_RPT
+#define MPB_LAST_RPT 1
+#endif
+constexpr int kLastRpt = MPB_LAST_RPT;
 // final sums of the warp-specialised kernels: lanes per consumer thread
 constexpr int kFinRptWs = kConsumers >= kFinThreads ? 1 : kFinThreads / kConsumers;
 static_assert(kConsumers * kFinRptWs >= kFinThreads, "fin_sum lanes");
@@ -629,11 +636,11 @@ struct RingCursor {
   }
 };
 
-__device__ __forceinline__ void ring_init(Ring &R, int ns) {
+__device__ __forceinline__ void ring_init(Ring &R, int ns, int consumers = kConsumers) {
   if (threadIdx.x == 0) {
     for (int st = 0; st < ns; st++) {
       mbar_init(&R.full[st], 1);
-      mbar_init(&R.empty[st], kConsumers / 32);
+      mbar_init(&R.empty[st], consumers / 32);
     }
   }
   __syncthreads();
@@ -753,20 +760,20 @@ __device__ __forceinline__ T generic_row_sweep(const PassArgs<T> &a, const TileD
 // Tile sum of kRowsPerThread values per consumer thread in the fixed order:
 // virtual lane t + k kConsumers, virtual warps butterfly, warp 0 butterflies
 // the kTileThreads/32 warp sums padded with +0.  Result valid in thread 0.
-template <typename R>
-__device__ __forceinline__ R tile_tree_rows(const R (&v)[kRowsPerThread], R *ws, int bar) {
-  constexpr int kWarps = kConsumers / 32;
-  static_assert(kConsumers * kRowsPerThread == kTileThreads, "tile lanes");
-  R s[kRowsPerThread];
+template <typename R, int RPT = kRowsPerThread>
+__device__ __forceinline__ R tile_tree_rows(const R (&v)[RPT], R *ws, int bar) {
+  constexpr int NC = kTileThreads / RPT;  // consumer threads
+  constexpr int kWarps = NC / 32;
+  R s[RPT];
 #pragma unroll
-  for (int k = 0; k < kRowsPerThread; k++) s[k] = warp_bfly(v[k]);
+  for (int k = 0; k < RPT; k++) s[k] = warp_bfly(v[k]);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  named_sync(bar, kConsumers);
+  named_sync(bar, NC);
   if (lane == 0) {
 #pragma unroll
-    for (int k = 0; k < kRowsPerThread; k++) ws[warp + k * kWarps] = s[k];
+    for (int k = 0; k < RPT; k++) ws[warp + k * kWarps] = s[k];
   }
-  named_sync(bar, kConsumers);
+  named_sync(bar, NC);
   R r = R(0);
   if (warp == 0) {
     r = lane < kTileThreads / 32 ? ws[lane] : R(0);
@@ -879,37 +886,38 @@ __device__ __forceinline__ void deferred_tree_finish(DeferredTree &dt, double *p
   dt.tile = -1;
 }
 
-template <typename T, bool FIRST, bool LAST, int KS, bool GEN>
+template <typename T, bool FIRST, bool LAST, int KS, bool GEN, int RPT = kRowsPerThread>
 __device__ __forceinline__ void bjac_tile_body(const PassArgs<T> &a, int tile, const TileDesc &d, const int *col,
                                                const T *val, const int *spp, const uint16_t *mt, const double *r64t,
                                                const T *rTt, const int *s_pat, T *s_w, double *ws,
                                                DeferredTree &dt) {
   const bool defer = MPB_DEFER_TREE && LAST && a.part != nullptr && a.t >= 2;
-  PassRow<T> q[kRowsPerThread];
+  constexpr int NC = kTileThreads / RPT;
+  PassRow<T> q[RPT];
 #pragma unroll
-  for (int k = 0; k < kRowsPerThread; k++)
-    pass_row_init<T, FIRST, KS, GEN>(q[k], a, d, threadIdx.x + k * kConsumers, col, val, spp, mt, r64t, rTt, s_pat, s_w);
+  for (int k = 0; k < RPT; k++)
+    pass_row_init<T, FIRST, KS, GEN>(q[k], a, d, threadIdx.x + k * NC, col, val, spp, mt, r64t, rTt, s_pat, s_w);
   for (int s = 1; s < a.t; s++) {  // inner sweeps, the tile's w in shared memory
-    named_sync(kBarConsumers, kConsumers);
+    named_sync(kBarConsumers, NC);
     if (defer && s == 1) deferred_tree_finish(dt, a.part, ws);
-    T acc[kRowsPerThread];
+    T acc[RPT];
 #pragma unroll
-    for (int k = 0; k < kRowsPerThread; k++)
-      acc[k] = pass_row_sweep<T, GEN>(q[k], a, d, threadIdx.x + k * kConsumers, col, val, s_w);
-    named_sync(kBarConsumers, kConsumers);
+    for (int k = 0; k < RPT; k++)
+      acc[k] = pass_row_sweep<T, GEN>(q[k], a, d, threadIdx.x + k * NC, col, val, s_w);
+    named_sync(kBarConsumers, NC);
 #pragma unroll
-    for (int k = 0; k < kRowsPerThread; k++) {
+    for (int k = 0; k < RPT; k++) {
       if (!q[k].valid) continue;
       q[k].w = add_rn(q[k].w, div_rn(sub_rn(q[k].res, acc[k]), q[k].dd));
-      s_w[threadIdx.x + k * kConsumers] = q[k].w;
+      s_w[threadIdx.x + k * NC] = q[k].w;
     }
   }
-  double prod[kRowsPerThread];
+  double prod[RPT];
 #pragma unroll
-  for (int k = 0; k < kRowsPerThread; k++) {
+  for (int k = 0; k < RPT; k++) {
     prod[k] = 0.0;
     if (!q[k].valid) continue;
-    const int tid = threadIdx.x + k * kConsumers, row = d.lo + tid;
+    const int tid = threadIdx.x + k * NC, row = d.lo + tid;
     const T zo = FIRST ? q[k].w : add_rn(q[k].zown, q[k].w);
     if (a.zout != nullptr) a.zout[row] = zo;
     if (a.zout64 != nullptr) a.zout64[row] = static_cast<double>(zo);
@@ -918,13 +926,13 @@ __device__ __forceinline__ void bjac_tile_body(const PassArgs<T> &a, int tile, c
   if (defer) {
     dt.slot ^= 1;
 #pragma unroll
-    for (int k = 0; k < kRowsPerThread; k++) {  // virtual warp (threadIdx.x >> 5) + k * kConsumers / 32
+    for (int k = 0; k < RPT; k++) {  // virtual warp (threadIdx.x >> 5) + k * NC / 32
       const double w = warp_bfly(prod[k]);
-      if ((threadIdx.x & 31) == 0) ws[dt.slot * 8 + (threadIdx.x >> 5) + k * (kConsumers / 32)] = w;
+      if ((threadIdx.x & 31) == 0) ws[dt.slot * 8 + (threadIdx.x >> 5) + k * (NC / 32)] = w;
     }
     dt.tile = tile;
   } else if (LAST && a.part != nullptr) {
-    const double tot = tile_tree_rows(prod, ws, kBarConsumers);
+    const double tot = tile_tree_rows<double, RPT>(prod, ws, kBarConsumers);
     if (threadIdx.x == 0) put_part(a.part + tile, tot);
   }
 }
@@ -933,17 +941,18 @@ __device__ __forceinline__ void bjac_tile_body(const PassArgs<T> &a, int tile, c
 // in-block entries (plan's in-block SELL): y = r / d, then t-1 sweeps
 // y += (r - A_b y) / d over the in-block entries in ascending column order.
 // res[k]: row tid + k kConsumers's residual in T (valid rows).
-template <typename T, bool GEN>
+template <typename T, bool GEN, int RPT = kRowsPerThread>
 __device__ __forceinline__ void bjac_first_body(const PassArgs<T> &a, const TileDesc &d, const int *col,
                                                 const T *val, const int *spp, const uint16_t *mt,
-                                                const T (&res)[kRowsPerThread], const int *s_pat, T *s_w) {
-  T dd[kRowsPerThread], w[kRowsPerThread];
-  const int *P[kRowsPerThread];
-  int base[kRowsPerThread], nib[kRowsPerThread];
-  bool pat[kRowsPerThread], valid[kRowsPerThread];
+                                                const T (&res)[RPT], const int *s_pat, T *s_w) {
+  constexpr int NC = kTileThreads / RPT;
+  T dd[RPT], w[RPT];
+  const int *P[RPT];
+  int base[RPT], nib[RPT];
+  bool pat[RPT], valid[RPT];
 #pragma unroll
-  for (int k = 0; k < kRowsPerThread; k++) {
-    const int tid = threadIdx.x + k * kConsumers, row = d.lo + tid;
+  for (int k = 0; k < RPT; k++) {
+    const int tid = threadIdx.x + k * NC, row = d.lo + tid;
     dd[k] = T(1);
     w[k] = T(0);
     P[k] = s_pat;
@@ -974,11 +983,11 @@ __device__ __forceinline__ void bjac_first_body(const PassArgs<T> &a, const Tile
     s_w[tid] = w[k];
   }
   for (int s = 1; s < a.t; s++) {
-    named_sync(kBarConsumers, kConsumers);
-    T acc[kRowsPerThread];
+    named_sync(kBarConsumers, NC);
+    T acc[RPT];
 #pragma unroll
-    for (int k = 0; k < kRowsPerThread; k++) {
-      const int tid = threadIdx.x + k * kConsumers;
+    for (int k = 0; k < RPT; k++) {
+      const int tid = threadIdx.x + k * NC;
       acc[k] = T(0);
       if (pat[k]) {
 #pragma unroll 1
@@ -988,18 +997,18 @@ __device__ __forceinline__ void bjac_first_body(const PassArgs<T> &a, const Tile
           acc[k] = add_rn(acc[k], mul_rn(val[base[k] + 32 * j], s_w[col[base[k] + 32 * j] - d.lo]));
       }
     }
-    named_sync(kBarConsumers, kConsumers);
+    named_sync(kBarConsumers, NC);
 #pragma unroll
-    for (int k = 0; k < kRowsPerThread; k++) {
+    for (int k = 0; k < RPT; k++) {
       if (!valid[k]) continue;
       w[k] = add_rn(w[k], div_rn(sub_rn(res[k], acc[k]), dd[k]));
-      s_w[threadIdx.x + k * kConsumers] = w[k];
+      s_w[threadIdx.x + k * NC] = w[k];
     }
   }
 #pragma unroll
-  for (int k = 0; k < kRowsPerThread; k++) {
+  for (int k = 0; k < RPT; k++) {
     if (!valid[k]) continue;
-    const int row = d.lo + threadIdx.x + k * kConsumers;
+    const int row = d.lo + threadIdx.x + k * NC;
     if (a.zout != nullptr) a.zout[row] = w[k];
     if (a.zout64 != nullptr) a.zout64[row] = static_cast<double>(w[k]);
   }
@@ -1013,8 +1022,12 @@ __host__ __device__ inline StageLayout bjac_layout(const TileGeom &g) {
 
 // Persistent, warp-specialised fused pass.  TWO: the two-level dot-sum order
 // (chunk owners in the producer warp); false compiles that machinery out.
-template <typename T, bool FIRST, bool LAST, bool R64, int KS, bool GEN, bool TWO = false>
-__global__ void MPB_WS_BOUNDS_PASS k_bjac_tile(const PassArgs<T> a) {
+// RPT: tile rows per consumer thread (kTileThreads / RPT consumer threads +
+// the producer warp per CTA)
+template <typename T, bool FIRST, bool LAST, bool R64, int KS, bool GEN, bool TWO = false, int RPT = kRowsPerThread>
+__global__ void __launch_bounds__(kTileThreads / RPT + 32) k_bjac_tile(const PassArgs<T> a) {
+  constexpr int NC = kTileThreads / RPT;
+  constexpr int kFinRpt = NC >= kFinThreads ? 1 : kFinThreads / NC;
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ Ring R;
   __shared__ T s_w[kTileRows];
@@ -1027,8 +1040,8 @@ __global__ void MPB_WS_BOUNDS_PASS k_bjac_tile(const PassArgs<T> a) {
   constexpr bool kIB = FIRST && !LAST;  // first pass alone: in-block entries only
   const StageLayout L = bjac_layout<T, FIRST, R64>(a.g);
   load_patterns(s_pat, a.pat, a.g.npat);
-  ring_init(R, ns);
-  if (threadIdx.x >= kConsumers) {  // producer warp
+  ring_init(R, ns, NC);
+  if (threadIdx.x >= NC) {  // producer warp
     using RT = typename std::conditional<R64, double, T>::type;
     const RT *rsrc = R64 ? reinterpret_cast<const RT *>(a.r64) : reinterpret_cast<const RT *>(a.rT);
     const ChunkCtx ck{(TWO && LAST && a.part != nullptr && a.st != nullptr) ? a.csum : nullptr, a.part, a.g.ntiles,
@@ -1045,7 +1058,7 @@ __global__ void MPB_WS_BOUNDS_PASS k_bjac_tile(const PassArgs<T> a) {
     auto gated = [&]() { return gated_off(a); };
     if (TWO && ck.csum != nullptr && ck.poll)
       producer_loop(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, gated, fill, ck);
-    else if (threadIdx.x == kConsumers)
+    else if (threadIdx.x == NC)
       producer_loop_single(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, gated, fill);
     else
       pdl_wait();
@@ -1073,32 +1086,32 @@ __global__ void MPB_WS_BOUNDS_PASS k_bjac_tile(const PassArgs<T> a) {
       const bool scols = ok && a.g.cols && d.ngen > 0;
       if (kIB) {
         const int *col = scols ? reinterpret_cast<const int *>(sb + L.col) : a.ib_col + d.ie0;
-        T rv[kRowsPerThread];
+        T rv[RPT];
 #pragma unroll
-        for (int k = 0; k < kRowsPerThread; k++) {
-          const int tid = threadIdx.x + k * kConsumers, row = d.lo + tid;
+        for (int k = 0; k < RPT; k++) {
+          const int tid = threadIdx.x + k * NC, row = d.lo + tid;
           rv[k] = T(0);
           if (row >= d.hi) continue;
           if (R64) rv[k] = narrow_checked(a, ok ? staged(sb + L.v0, a.r64, d.lo, d.hi)[tid] : a.r64[row], row, true);
           else rv[k] = ok ? staged(sb + L.v0, a.rT, d.lo, d.hi)[tid] : a.rT[row];
         }
         if (ok) {
-          bjac_first_body<T, GEN>(a, d, col, reinterpret_cast<const T *>(sb + L.val),
+          bjac_first_body<T, GEN, RPT>(a, d, col, reinterpret_cast<const T *>(sb + L.val),
                              staged(sb + L.sp, a.ib_sp, d.s0, d.s1 + 1), staged(sb + L.meta, a.meta, d.lo, d.hi), rv,
                              s_pat, s_w);
         } else {
-          bjac_first_body<T, GEN>(a, d, col, a.ib_val + d.ie0, a.ib_sp + d.s0, a.meta + d.lo, rv, s_pat, s_w);
+          bjac_first_body<T, GEN, RPT>(a, d, col, a.ib_val + d.ie0, a.ib_sp + d.s0, a.meta + d.lo, rv, s_pat, s_w);
         }
       } else {
         const int *col = scols ? reinterpret_cast<const int *>(sb + L.col) : a.scol + d.e0;
         if (ok) {
-          bjac_tile_body<T, FIRST, LAST, KS, GEN>(a, tile, d, col, reinterpret_cast<const T *>(sb + L.val),
+          bjac_tile_body<T, FIRST, LAST, KS, GEN, RPT>(a, tile, d, col, reinterpret_cast<const T *>(sb + L.val),
                                              staged(sb + L.sp, a.sp, d.s0, d.s1 + 1),
                                              staged(sb + L.meta, a.meta, d.lo, d.hi),
                                              R64 ? staged(sb + L.v0, a.r64, d.lo, d.hi) : nullptr,
                                              R64 ? nullptr : staged(sb + L.v0, a.rT, d.lo, d.hi), s_pat, s_w, ws, dt);
         } else {
-          bjac_tile_body<T, FIRST, LAST, KS, GEN>(a, tile, d, col, a.sval + d.e0, a.sp + d.s0, a.meta + d.lo,
+          bjac_tile_body<T, FIRST, LAST, KS, GEN, RPT>(a, tile, d, col, a.sval + d.e0, a.sp + d.s0, a.meta + d.lo,
                                              R64 ? a.r64 + d.lo : nullptr, R64 ? nullptr : a.rT + d.lo, s_pat, s_w,
                                              ws, dt);
         }
@@ -1106,14 +1119,14 @@ __global__ void MPB_WS_BOUNDS_PASS k_bjac_tile(const PassArgs<T> a) {
       ring_release(R, st);
     }
     if (dt.tile >= 0) {  // the last tile's deferred sum: every warp has stored its share
-      named_sync(kBarConsumers, kConsumers);
+      named_sync(kBarConsumers, NC);
       deferred_tree_finish(dt, a.part, ws);
     }
     if (LAST && threadIdx.x == 0) tl_mark(a.st, 0, 1, true);
   }
   pdl_trigger();  // dependents may launch into the SMs this grid drains
   if (LAST && a.part != nullptr)
-    finish_grid<16, kFinRptWs>(a.st, 0, kStepRho, ChunkCtx{a.csum, a.part, a.g.ntiles, TWO ? a.g.poll : 0}, ws);
+    finish_grid<16, kFinRpt>(a.st, 0, kStepRho, ChunkCtx{a.csum, a.part, a.g.ntiles, TWO ? a.g.poll : 0}, ws);
 }
 
 // ---- large blocks (> kTileRows rows): one launch per inner sweep ----------
