@@ -426,6 +426,24 @@ __device__ __forceinline__ void st_evict_first(double *p, double v) {
   asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
 #endif
 }
+// global store with an L2 evict-last policy (a vector the next kernels
+// gather; MPB_EVICT_LAST=1 enables it, else a plain store)
+template <typename T>
+__device__ __forceinline__ void st_keep(T *p, T v) {
+#ifdef MPB_EVICT_LAST
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  if constexpr (sizeof(T) == 8)
+    asm volatile("st.global.L2::cache_hint.b64 [%0], %1, %2;" ::"l"(p), "l"(*reinterpret_cast<unsigned long long *>(&v)),
+                 "l"(pol)
+                 : "memory");
+  else
+    asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "r"(*reinterpret_cast<unsigned *>(&v)), "l"(pol)
+                 : "memory");
+#else
+  *p = v;
+#endif
+}
 // The same for data read once per kernel (matrix values / columns): L2
 // evict-first, so the streamed matrix does not push the iteration's vectors
 // (gathered by the next kernels) out of L2.  MPB_NO_EVICT_FIRST=1: plain.

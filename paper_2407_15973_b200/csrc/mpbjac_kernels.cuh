@@ -919,7 +919,7 @@ __device__ __forceinline__ void bjac_tile_body(const PassArgs<T> &a, int tile, c
     if (!q[k].valid) continue;
     const int tid = threadIdx.x + k * NC, row = d.lo + tid;
     const T zo = FIRST ? q[k].w : add_rn(q[k].zown, q[k].w);
-    if (a.zout != nullptr) a.zout[row] = zo;
+    if (a.zout != nullptr) st_keep(a.zout + row, zo);
     if (a.zout64 != nullptr) a.zout64[row] = static_cast<double>(zo);
     if (LAST && a.part != nullptr) prod[k] = __dmul_rn(r64t[tid], static_cast<double>(zo));
   }
@@ -1009,7 +1009,7 @@ __device__ __forceinline__ void bjac_first_body(const PassArgs<T> &a, const Tile
   for (int k = 0; k < RPT; k++) {
     if (!valid[k]) continue;
     const int row = d.lo + threadIdx.x + k * NC;
-    if (a.zout != nullptr) a.zout[row] = w[k];
+    if (a.zout != nullptr) st_keep(a.zout + row, w[k]);
     if (a.zout64 != nullptr) a.zout64[row] = static_cast<double>(w[k]);
   }
 }
@@ -1181,7 +1181,7 @@ __global__ void __launch_bounds__(kCtaThreads) k_big_finish(const PassArgs<T> a,
   double prod = 0.0;
   if (row < d.hi) {
     const T zo = FIRST ? w[row] : add_rn(a.zin[row], w[row]);
-    if (a.zout != nullptr) a.zout[row] = zo;
+    if (a.zout != nullptr) st_keep(a.zout + row, zo);
     if (a.zout64 != nullptr) a.zout64[row] = static_cast<double>(zo);
     if (LAST && a.part != nullptr) prod = __dmul_rn(a.r64[row], static_cast<double>(zo));
   }
@@ -1306,7 +1306,7 @@ __device__ __forceinline__ void spmv_tile_body(const SpmvArgs &a, int tile, cons
     }
     a.q[row] = acc;
     const double pown = p_at<ZT>(a, row, first, beta);
-    if (!std::is_same<ZT, void>::value) a.pnew[row] = pown;
+    if (!std::is_same<ZT, void>::value) st_keep(a.pnew + row, pown);
     prod[k] = __dmul_rn(pown, acc);
   }
   const double tot = tile_tree_rows(prod, ws, kBarConsumers);
