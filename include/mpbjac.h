@@ -95,6 +95,12 @@ typedef struct mpb_csr {
    * (mpb_plan_pack_inblock_*); read by the first BJAC pass */
   const double *ib_val64;
   const float *ib_val32;
+  /* the solved operator's fp64 values in SELL-32 when they differ from the
+   * fp64 preconditioner values above (a preconditioner set up from another
+   * matrix of the same structure, e.g. diag_augment(A, p)): the outer SpMV
+   * and the true residuals read these (solver.py:154, 93-98).  NULL: the
+   * operator is sell_val64. */
+  const double *op_sell_val64;
 } mpb_csr;
 
 typedef struct mpb_solve_options {

@@ -234,6 +234,11 @@ typedef struct {
   int order; /* 0: sequential (reference numba), 1: device tile-tree */
   i64 ntiles;
   const i64 *tile_lo;
+  /* fp64 preconditioner values when the preconditioner was set up from
+   * another matrix of the same structure (policies.build_mixed(A2, ..) used
+   * to solve A); NULL: val64.  The outer SpMV and true residuals always use
+   * val64 (solver.py:154, 93-98). */
+  const double *pval64;
 } orc_problem;
 
 typedef struct {
@@ -311,7 +316,7 @@ int orc_pcg_solve(const orc_problem *P, const double *b, int has_x0, double *x,
     int branch = choose_branch(P->kind, P->adp_tol, relres, &bad);
     if (bad) { res->error = E_BAD_RELRES; res->err_it = it; res->err_val = relres; goto done; }
     if (branch == 0) {
-      orc_bjac_apply_f64(n, P->rp, P->ci, P->val64, P->in_block, P->diag64,
+      orc_bjac_apply_f64(n, P->rp, P->ci, P->pval64 ? P->pval64 : P->val64, P->in_block, P->diag64,
                          P->k, P->t, r, z, work64);
     } else {
       i64 fb;

@@ -48,6 +48,7 @@ class _Problem(C.Structure):
         ("kind", C.c_int), ("adp_tol", C.c_double), ("res_tol", C.c_double),
         ("cap", C.c_int64), ("stride", C.c_int64), ("order", C.c_int),
         ("ntiles", C.c_int64), ("tile_lo", C.c_void_p),
+        ("pval64", C.c_void_p),
     ]
 
 
@@ -233,23 +234,27 @@ def tree_dot(tile_lo, x, y):
 
 def pcg_solve(row_ptr, col_idx, values, b, offsets, kind="uniform",
               adp_tol=None, k=2, t=2, res_tol=1e-10, max_iter=None,
-              stride=0, order="sequential", x0=None, threads=None):
+              stride=0, order="sequential", x0=None, threads=None,
+              prec_values=None):
     """Oracle solve.  order='sequential' replays the reference (numba) dot
-    order, order='device' the GPU tile-tree order.  Returns a dict."""
+    order, order='device' the GPU tile-tree order.  Returns a dict.
+    prec_values: the preconditioner's source values (same structure), when
+    it was set up from another matrix than the solved one."""
     row_ptr = np.ascontiguousarray(row_ptr, np.int64)
     col_idx = np.ascontiguousarray(col_idx, np.int32)
     values = np.ascontiguousarray(values, np.float64)
     b = np.ascontiguousarray(b, np.float64)
     n = b.size
     offsets = np.ascontiguousarray(offsets, np.int64)
-    diag64, diag32, val32, in_block = setup_arrays(row_ptr, col_idx, values,
+    pvals = values if prec_values is None else np.ascontiguousarray(prec_values, np.float64)
+    diag64, diag32, val32, in_block = setup_arrays(row_ptr, col_idx, pvals,
                                                    offsets)
     tile_lo, _ = plan_tiles(offsets, row_ptr)
     cap = int(max_iter) if max_iter is not None else min(10 * n, 20000)
     if adp_tol is None:
         adp_tol = {"adaptive-hl": 10.0, "adaptive-lh": 1e-5}.get(kind, 0.0)
     P = _Problem()
-    keep = (row_ptr, col_idx, values, val32, diag64, diag32, in_block, tile_lo)
+    keep = (row_ptr, col_idx, values, val32, diag64, diag32, in_block, tile_lo, pvals)
     P.n = n
     P.rp, P.ci, P.val64, P.val32 = (a.ctypes.data for a in keep[:4])
     P.diag64, P.diag32, P.in_block = (a.ctypes.data for a in keep[4:7])
@@ -262,6 +267,7 @@ def pcg_solve(row_ptr, col_idx, values, b, offsets, kind="uniform",
     P.order = 0 if order == "sequential" else 1
     P.ntiles = tile_lo.size - 1
     P.tile_lo = tile_lo.ctypes.data
+    P.pval64 = None if prec_values is None else pvals.ctypes.data
     x = np.zeros(n) if x0 is None else np.array(x0, np.float64)
     rel = np.zeros(cap)
     tru = np.full(cap, np.nan)

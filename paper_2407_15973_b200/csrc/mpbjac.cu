@@ -44,7 +44,7 @@ inline int status_of(cudaError_t e) { return e == cudaSuccess ? MPB_OK : static_
   } while (0)
 
 struct GraphKey {
-  const void *plan, *rp, *sell, *v64, *v32, *b, *x, *trr, *trt, *trb, *trw, *ws, *comm;
+  const void *plan, *rp, *sell, *v64, *v32, *vop, *b, *x, *trr, *trt, *trb, *trw, *ws, *comm;
   int kind, k, t, iters, loop;
   long long stride, n;
   bool operator==(const GraphKey &o) const { return std::memcmp(this, &o, sizeof(GraphKey)) == 0; }
@@ -301,6 +301,9 @@ int launch_pass(mpb_handle *h, cudaStream_t s, const mpb_plan *p, PassArgs<T> a,
   MPB_LAUNCHED(h);
   return MPB_OK;
 }
+
+// the operator of the outer SpMV and the true residuals (solver.py:154, 93-98)
+static const double *op_vals(const mpb_csr *A) { return A->op_sell_val64 ? A->op_sell_val64 : A->sell_val64; }
 
 template <typename T>
 const T *sell_vals(const mpb_csr *A);
@@ -1303,7 +1306,7 @@ static SpmvArgs spmv_args(const mpb_handle *h, const mpb_plan *p, const mpb_csr 
   SpmvArgs sa{};
   sa.sp = A->sell->d_sp;
   sa.scol = A->sell->d_col;
-  sa.sval = A->sell_val64;
+  sa.sval = op_vals(A);
   sa.meta = p->d_meta;
   sa.pat = p->d_pat;
   sa.td = p->d_td;
@@ -1438,7 +1441,7 @@ static int enqueue_iteration(mpb_handle *h, cudaStream_t s, const mpb_plan *p, c
   if (o->true_stride > 0) {
     if ((rc = halo_exchange(dc, x, 8, A->n, s))) return rc;
     k_resid<true><<<persistent_grid(k_resid<true>, 0, p->ntiles), kCtaThreads, 0, s>>>(
-        A->sell->d_sp, A->sell->d_col, A->sell_val64, p->d_td, static_cast<int>(nt), b, x, nullptr, w.part, w.st, 1,
+        A->sell->d_sp, A->sell->d_col, op_vals(A), p->d_td, static_cast<int>(nt), b, x, nullptr, w.part, w.st, 1,
         kStepTrue, w.csum, owners_poll(p->ntiles) ? 1 : 0);
     MPB_LAUNCHED(h);
     if ((rc = dist_step(h, dc, w.st, kStepTrue, 1, s))) return rc;
@@ -1574,11 +1577,11 @@ static int solve_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, con
   if (opt->has_x0) {
     if ((rc = halo_exchange(dc, x, 8, A->n, s))) return rc;
     k_resid<true><<<persistent_grid(k_resid<true>, 0, plan->ntiles), kCtaThreads, 0, s>>>(
-                                              A->sell->d_sp, A->sell->d_col, A->sell_val64, plan->d_td, static_cast<int>(nt), b, x, w.r, w.part, w.st, 0,
+                                              A->sell->d_sp, A->sell->d_col, op_vals(A), plan->d_td, static_cast<int>(nt), b, x, w.r, w.part, w.st, 0,
                                               kStepR0, w.csum, owners_poll(plan->ntiles) ? 1 : 0);
   } else {
     k_resid<false><<<persistent_grid(k_resid<false>, 0, plan->ntiles), kCtaThreads, 0, s>>>(
-                                               A->sell->d_sp, A->sell->d_col, A->sell_val64, plan->d_td, static_cast<int>(nt), b, nullptr, w.r, w.part, w.st,
+                                               A->sell->d_sp, A->sell->d_col, op_vals(A), plan->d_td, static_cast<int>(nt), b, nullptr, w.r, w.part, w.st,
                                                0, kStepR0, w.csum, owners_poll(plan->ntiles) ? 1 : 0);
   }
   MPB_LAUNCHED(h);
@@ -1603,6 +1606,7 @@ static int solve_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, con
   key.rp = A->row_ptr;
   key.sell = A->sell;
   key.v64 = A->sell_val64;
+  key.vop = A->op_sell_val64;
   key.v32 = A->sell_val32;
   key.b = b;
   key.x = x;
@@ -1742,7 +1746,7 @@ static int solve_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, con
   if (st.error == kOk) {  // final true residual (solver.py:179-182)
     if ((rc = halo_exchange(dc, x, 8, A->n, s))) return rc;
     k_resid<true><<<persistent_grid(k_resid<true>, 0, plan->ntiles), kCtaThreads, 0, s>>>(
-                                              A->sell->d_sp, A->sell->d_col, A->sell_val64, plan->d_td, static_cast<int>(nt), b, x, nullptr, w.part, w.st, 0,
+                                              A->sell->d_sp, A->sell->d_col, op_vals(A), plan->d_td, static_cast<int>(nt), b, x, nullptr, w.part, w.st, 0,
                                               kStepFinal, w.csum, owners_poll(plan->ntiles) ? 1 : 0);
     MPB_LAUNCHED(h);
     if ((rc = dist_step(h, dc, w.st, kStepFinal, 0, s))) return rc;
@@ -1758,10 +1762,17 @@ static int solve_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, con
   res->err_iteration = fin.error ? fin.err_it : 0;
   res->err_value = fin.err_val;
   res->final_true_relres = fin.error ? NAN : fin.final_true;
+  // ovf_count is global (all-reduced on the multi-GPU path); ovf_first is
+  // this rank's own first local row, INT64_MAX when the overflow happened on
+  // another rank (the caller all-reduces the global first index,
+  // distributed.SlabSolver).  Only a row this rank owns is dereferenced.
+  const bool local_ovf = fin.ovf_count && fin.ovf_first >= 0 && fin.ovf_first < A->n;
   res->overflow_count = static_cast<int64_t>(fin.ovf_count);
-  res->overflow_index = fin.ovf_count ? fin.ovf_first : -1;
-  if (fin.error == kNarrowOverflow && fin.ovf_count) {  // the offending r entry
-    MPB_CUDA(cudaMemcpy(&res->err_value, w.r + fin.ovf_first, sizeof(double), cudaMemcpyDeviceToHost));
+  res->overflow_index = local_ovf ? fin.ovf_first : -1;
+  if (fin.error == kNarrowOverflow) {  // the offending r entry
+    res->err_value = NAN;
+    if (local_ovf)
+      MPB_CUDA(cudaMemcpy(&res->err_value, w.r + fin.ovf_first, sizeof(double), cudaMemcpyDeviceToHost));
   }
   res->device_seconds = 1e-3 * ms;
   res->kernel_launches = h->launches - launches0;
@@ -1977,7 +1988,7 @@ int mpb_true_relres(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, const
   double *csum = reinterpret_cast<double *>(static_cast<char *>(h->scratch) + al256(sizeof(double) * (nt + 1)));
   double *out = reinterpret_cast<double *>(reinterpret_cast<char *>(csum) + chunk_scratch(sizeof(double), nt));
   k_resid<true><<<persistent_grid(k_resid<true>, 0, nt), kCtaThreads, 0, h->user>>>(
-      A->sell->d_sp, A->sell->d_col, A->sell_val64, plan->d_td, static_cast<int>(nt), b, x, nullptr,
+      A->sell->d_sp, A->sell->d_col, op_vals(A), plan->d_td, static_cast<int>(nt), b, x, nullptr,
       part, nullptr, 0, kStepFinal, nullptr, 0);
   MPB_LAUNCHED(h);
   if ((rc = launch_fin<double>(h, part, nt, csum, out))) return rc;

@@ -127,6 +127,25 @@ def extract_slab(row_ptr, col_idx, values, partition: BlockPartition, bounds, ra
                 np.asarray(values)[e0:e1], local_offs, recv_lo, recv_hi, send_lo, send_hi)
 
 
+def global_first_overflow(lo: int, local_index: int, local_value: float):
+    """(global row, value) of the first narrowing overflow over all ranks:
+    a MIN all-reduce of the global row (ranks without a local overflow offer
+    2^62), then the owner's value by a SUM all-reduce (the others add 0)."""
+    import torch
+    import torch.distributed as dist
+    dev = torch.device("cuda", torch.cuda.current_device()) \
+        if dist.get_backend() == "nccl" else torch.device("cpu")
+    none = 1 << 62
+    g = lo + local_index if local_index >= 0 else none
+    t = torch.tensor([g], dtype=torch.int64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    gmin = int(t.item())
+    mine = g == gmin and gmin != none
+    v = torch.tensor([local_value if mine else 0.0], dtype=torch.float64, device=dev)
+    dist.all_reduce(v, op=dist.ReduceOp.SUM)
+    return (gmin if gmin != none else -1), float(v.item())
+
+
 class SlabSolver:
     """Distributed drop-in for ``pcg_solve`` on one rank (one process per
     GPU; torch.distributed must be initialised — the NCCL unique id travels
@@ -169,8 +188,19 @@ class SlabSolver:
         from .solver import SolveConfig, _run_solve
         config = config or SolveConfig()
         return _run_solve(self.A_loc, b_local, self.mp, config, x0_local,
-                          dist=(self.comm, self.slab.halo(), self.slab.ghosts),
+                          dist=(self.comm, self.slab.halo(), self.slab.ghosts,
+                                self._global_overflow),
                           n_global=self.bounds[-1][1])
+
+    def _global_overflow(self, res) -> None:
+        """After a narrowing overflow (the count is already global): every
+        rank reports the globally first offending row and its value, as the
+        one-GPU solve would (sparse.py:207-213).  res.overflow_index is the
+        local row on the rank that saw an overflow itself, else -1."""
+        g, v = global_first_overflow(self.slab.lo, int(res.overflow_index),
+                                     float(res.err_value))
+        res.overflow_index = g
+        res.err_value = v
 
     def profile_iteration(self, config=None, branch: str = "low", reps: int = 20) -> dict:
         """Per-kernel times of one iteration on this slab (no communication)."""

@@ -224,6 +224,28 @@ def family_matrix(n: int, family: Family, s: float = 1.0, seed: int = 0) -> Spar
     return diffusion_matrix(n, family_kappa(n, family, s, seed), weights)
 
 
+def diag_augment(A: SparseMatrix, p_diag: float) -> SparseMatrix:
+    """A with p_diag * (row's absolute sum, diagonal included) added to each
+    diagonal entry (pkg/src/mpcg/problems.py:259-281): a preconditioner
+    source of A's structure with other values.  The row sums use numpy's
+    add.reduceat like the reference, so the result is bit-identical;
+    p_diag = 0 gives a bitwise copy."""
+    if p_diag < 0:
+        raise ValueError("p_diag must be nonnegative")
+    rows = np.repeat(np.arange(A.n), np.diff(A.row_ptr))
+    diag_pos = np.flatnonzero(rows == A.col_idx)
+    if diag_pos.size != A.n:
+        have = np.zeros(A.n, dtype=bool)
+        have[rows[diag_pos]] = True
+        raise ValueError(f"row {int(np.flatnonzero(~have)[0])} has no stored diagonal entry")
+    sums = np.zeros(A.n, dtype=A.values.dtype)
+    nonempty = np.flatnonzero(np.diff(A.row_ptr) > 0)
+    sums[nonempty] = np.add.reduceat(np.abs(A.values), A.row_ptr[nonempty])
+    values = A.values.copy()
+    values[diag_pos] = values[diag_pos] + A.values.dtype.type(p_diag) * sums
+    return SparseMatrix(A.n, A.m, A.row_ptr, A.col_idx, values)
+
+
 # ---------------------------------------------------------------------------
 # BASELINE.json configs
 # ---------------------------------------------------------------------------

@@ -26,7 +26,7 @@ import numpy as np
 from . import _lib
 from .device import dtype_name, is_tensor, to_device, to_host
 from .policies import KIND_CODE, MixedPreconditioner, PrecisionPolicy
-from .sparse import NarrowingOverflowError, SparseMatrix, _narrow_error
+from .sparse import NarrowingOverflowError, PrecisionMismatchError, SparseMatrix, _narrow_error
 
 #: smallest positive normal float64; zero residuals clamp here before log10
 TINY = float(np.finfo(np.float64).tiny)
@@ -101,26 +101,39 @@ class SolveReport:
 def _dev_struct(A: SparseMatrix, mp: MixedPreconditioner):
     """Device CSR shared by the SpMV and both preconditioner instances."""
     P = mp.any
+    if A.values.dtype != np.float64:
+        # the reference's spmv(A, p) with an fp32 A (sparse.py:50-54, 178)
+        raise PrecisionMismatchError(
+            f"spmv: operands mix precisions (float32, float64)")
+    D = P.dcsr
+    op = None  # the operator's SELL values when they are not the preconditioner's
     if P.source is not A:
         same = (P.source.n == A.n and np.array_equal(P.source.row_ptr, A.row_ptr)
                 and np.array_equal(P.source.col_idx, A.col_idx))
-        if same and mp.p_high is not None:
-            same = np.array_equal(P.source.values.astype(np.float64),
-                                  A.values.astype(np.float64))
         if not same:
             raise NotImplementedError(
-                "GPU pcg_solve needs the preconditioner set up from the same "
-                "matrix that is being solved")
-    D = P.dcsr
+                "GPU pcg_solve needs the preconditioner set up from a matrix "
+                "with the solved matrix's sparsity structure")
+        # The outer SpMV and the true residuals always multiply by the A
+        # passed in (solver.py:154, 93-98); the preconditioner keeps the
+        # values it was set up from.  Same structure: A's fp64 values are
+        # packed into the preconditioner's SELL-32 layout once and cached.
+        cache = A.__dict__.setdefault("_op_sell", {})
+        hit = cache.get(id(D))
+        if hit is None or hit[0] is not D:
+            v = to_device(A.values, device=D.device)
+            hit = (D, v, D.sell_values(v))
+            cache[id(D)] = hit
+        op = hit[2]
     val64 = mp.p_high.dvalues if mp.p_high is not None else None
     if val64 is None:
-        if A.values.dtype != np.float64:
-            raise ValueError("solver matrix must hold float64 values")
         if D.val64 is None:
-            D.val64 = to_device(A.values, device=D.device)
+            D.val64 = to_device(P.source.values.astype(np.float64), device=D.device)
         val64 = D.val64
     val32 = mp.p_low.dvalues if mp.p_low is not None else None
-    return D, D.c_struct(val64=val64, val32=val32, plan=P.plan)
+    s = D.c_struct(val64=val64, val32=val32, plan=P.plan)
+    s.op_sell_val64 = op.data_ptr() if op is not None else None
+    return D, s
 
 
 def true_relres(A: SparseMatrix, x, b, r0_norm: float) -> float:
@@ -229,13 +242,15 @@ def _run_solve(A: SparseMatrix, b, mp: MixedPreconditioner, config: SolveConfig,
             _lib.ptr(tr[0]), _lib.ptr(tr[1]), _lib.ptr(trb), _lib.ptr(tr[2]),
             _lib.ptr(ws), ws.numel(), C.byref(res)), "pcg_solve")
     else:
-        comm, halo, _ = dist
+        comm, halo = dist[0], dist[1]
         _lib.check(h.lib.mpb_pcg_solve_dist(
             h.ptr, comm, C.byref(halo), P.plan.ptr, C.byref(s), C.byref(opt), _lib.ptr(bd),
             _lib.ptr(x_ext), _lib.ptr(tr[0]), _lib.ptr(tr[1]), _lib.ptr(trb), _lib.ptr(tr[2]),
             _lib.ptr(ws), ws.numel(), C.byref(res)), "pcg_solve_dist")
     it = int(res.iterations)
     err = int(res.error)
+    if err == _lib.SOLVE_NARROW_OVERFLOW and dist is not None and len(dist) > 3:
+        dist[3](res)   # global first overflow index and value (multi-GPU)
     if err:
         _raise_solve_error(err, res)
     stats = {"device_seconds": float(res.device_seconds),

@@ -260,3 +260,35 @@ def test_two_rank_solve_matches_rank_split_reference(tmp_path, kind, adp_tol):
     full = O.pcg_solve(cs.A.row_ptr, cs.A.col_idx, cs.A.values, cs.b, part.offsets, kind=kind,
                        adp_tol=adp_tol, k=cs.k, t=cs.t, res_tol=cs.res_tol, order="device")
     assert abs(full["iterations"] - tr_ref.size) <= 2
+
+
+def _ovf_worker(rank, nranks, port, out):
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=nranks)
+    from paper_2407_15973_b200.distributed import global_first_overflow
+    # rank 0 owns rows [0, 100) without an overflow; rank 1 owns [100, 250)
+    # and overflowed at its local row 7 (value 1e300); rank 2 at local row 3
+    lo = (0, 100, 250)[rank]
+    local = (-1, 7, 3)[rank]
+    val = (float("nan"), 1e300, -2e300)[rank]
+    g, v = global_first_overflow(lo, local, val)
+    np.save(os.path.join(out, f"ovf{rank}.npy"), np.array([g, v]))
+    dist.destroy_process_group()
+
+
+def test_global_first_overflow_three_ranks(tmp_path):
+    """Multi-GPU narrowing overflow: every rank reports the globally first
+    offending row and its value (ovf_first was rank-local)."""
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    procs = [ctx.Process(target=_ovf_worker, args=(r, 3, port, str(tmp_path))) for r in range(3)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    for r in range(3):
+        g, v = np.load(tmp_path / f"ovf{r}.npy")
+        assert int(g) == 107 and v == 1e300

@@ -400,3 +400,45 @@ def test_gpu_assembly_bitwise_vs_host(cuda):
         np.testing.assert_array_equal(g.col_idx, a.col_idx)
     np.testing.assert_array_equal(problems.splitmix64_stream(12345, 1000, device=True),
                                   problems.splitmix64_stream(12345, 1000))
+
+
+@pytest.mark.parametrize("pol", ("fixed-low", "uniform", "adaptive-hl:1e-3", "adaptive-lh:1e-4"))
+def test_pcg_preconditioner_from_other_matrix(cuda, oracle, pol):
+    """The outer SpMV and the true residuals multiply by the A passed to
+    pcg_solve, the preconditioner keeps the values it was set up from
+    (solver.py:154): solving A with build_mixed(diag_augment(A, p)) matches
+    the oracle bit for bit, and the reference's run within the band."""
+    import os
+    from paper_2407_15973_b200 import SparseMatrix
+    from paper_2407_15973_b200.bjac import BlockPartition
+    from paper_2407_15973_b200.policies import PrecisionPolicy, build_mixed
+    from paper_2407_15973_b200.problems import diag_augment
+    from paper_2407_15973_b200.solver import SolveConfig, pcg_solve
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "augment_golden.npz")
+    with np.load(path) as z:
+        g = {k: z[k] for k in z.files}
+    for name in sorted({k.split("/")[0] for k in g}):
+        rp, ci, v = (g[f"{name}/{s}"] for s in ("row_ptr", "col_idx", "values"))
+        pd, k, t, tol = g[f"{name}/meta"]
+        A = SparseMatrix(rp.size - 1, rp.size - 1, rp, ci, v)
+        A2 = diag_augment(A, float(pd))
+        offs, b = g[f"{name}/offsets"], g[f"{name}/b"]
+        pp = PrecisionPolicy.parse(pol)
+        mp = build_mixed(A2, pp, k=int(k), t=int(t), partition=BlockPartition(offs))
+        cfg = SolveConfig(res_tol=float(tol), record_true_residual_every=4)
+        for _ in range(2):   # also after A2's own solve (cached graph / values)
+            rep = pcg_solve(A, b, mp, cfg)
+            orc = oracle.pcg_solve(rp, ci, v, b, offs, kind=pp.kind.value, adp_tol=pp.adp_tol,
+                                   k=int(k), t=int(t), res_tol=float(tol), stride=4,
+                                   order="device", prec_values=A2.values)
+            assert rep.iterations == orc["iterations"], name
+            np.testing.assert_array_equal(rep.x, orc["x"], err_msg=name)
+            np.testing.assert_array_equal([r.implicit_relres for r in rep.trace], orc["relres"])
+            assert rep.final_true_relres == orc["final_true_relres"]
+            assert abs(rep.iterations - int(g[f"{name}/{pol}/iterations"])) <= 2
+            # the preconditioner's own matrix solves differently
+            rep2 = pcg_solve(A2, b, mp, cfg)
+            orc2 = oracle.pcg_solve(rp, ci, A2.values, b, offs, kind=pp.kind.value,
+                                    adp_tol=pp.adp_tol, k=int(k), t=int(t), res_tol=float(tol),
+                                    stride=4, order="device")
+            np.testing.assert_array_equal(rep2.x, orc2["x"], err_msg=name)

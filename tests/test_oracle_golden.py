@@ -102,3 +102,40 @@ def test_device_order_differs_only_in_dots(golden, oracle):
         out = oracle.pcg_solve(rp, ci, v, golden[f"{name}/b"], offs, kind="fixed-low",
                                k=int(k), t=int(t), res_tol=tol, order="device")
         assert abs(out["iterations"] - int(golden[f"{name}/pcg/fixed-low/iterations"])) <= 2
+
+
+AUG_POLICIES = ("fixed-low", "uniform", "adaptive-hl:1e-3", "adaptive-lh:1e-4")
+
+
+@pytest.fixture(scope="module")
+def augment_golden():
+    import os
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "augment_golden.npz")
+    with np.load(path) as z:
+        return {k: z[k] for k in z.files}
+
+
+@pytest.mark.parametrize("pol", AUG_POLICIES)
+def test_oracle_preconditioner_from_other_matrix(augment_golden, oracle, pol):
+    """pcg_solve(A, b, build_mixed(diag_augment(A, p), ..)): the reference
+    multiplies by A and preconditions with the augmented values
+    (tests/golden/make_augment_golden.py); the oracle's prec_values path
+    reproduces it bit for bit."""
+    g = augment_golden
+    from paper_2407_15973_b200 import SparseMatrix
+    from paper_2407_15973_b200.problems import diag_augment
+    for name in sorted({k.split("/")[0] for k in g}):
+        rp, ci, v, pv = (g[f"{name}/{s}"] for s in ("row_ptr", "col_idx", "values", "prec_values"))
+        pd, k, t, tol = g[f"{name}/meta"]
+        mine = diag_augment(SparseMatrix(rp.size - 1, rp.size - 1, rp, ci, v), float(pd))
+        np.testing.assert_array_equal(mine.values, pv)
+        kind, _, tolstr = pol.partition(":")
+        out = oracle.pcg_solve(rp, ci, v, g[f"{name}/b"], g[f"{name}/offsets"], kind=kind,
+                               adp_tol=float(tolstr) if tolstr else None, k=int(k), t=int(t),
+                               res_tol=tol, stride=4, order="sequential", prec_values=pv)
+        key = f"{name}/{pol}"
+        assert out["iterations"] == int(g[f"{key}/iterations"]), name
+        np.testing.assert_array_equal(out["relres"], g[f"{key}/relres"])
+        np.testing.assert_array_equal(out["x"], g[f"{key}/x"])
+        np.testing.assert_array_equal(out["true_relres"], g[f"{key}/true"])
+        assert out["final_true_relres"] == float(g[f"{key}/final_true"])
