@@ -36,9 +36,15 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-#: iterations of the reference-order solve to rtol (oracle, sequential dot
-#: order, measured in the build container; the GPU run reports its own)
-REF_ITERS = {"c1": 63, "c2": 386}
+def ref_iterations(cfg: str, policy: str):
+    """Iterations of the reference-order (sequential dot) solve to rtol,
+    from the oracle fixtures of tools/make_fullsize_golden.py; None when no
+    fixture exists for this (config, policy)."""
+    path = os.path.join(ROOT, "tests", "golden", "fullsize", f"{cfg}_{policy.replace(':', '_')}.npz")
+    if not os.path.exists(path):
+        return None
+    with np.load(path) as z:
+        return int(z["seq_iterations"]) if "seq_iterations" in z.files else None
 
 
 def parse():
@@ -51,8 +57,11 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
     ap.add_argument("--cpu-iters", type=int, default=40,
                     help="iterations of the bounded CPU-baseline sample")
+    ap.add_argument("--ref-budget", type=float, default=40.0,
+                    help="--impl reference: seconds a whole solve may take before steps "
+                         "become capped samples extrapolated to the known iteration count")
     ap.add_argument("--ref-iters", type=int, default=60,
-                    help="iterations per --impl reference step")
+                    help="--impl reference: iterations of a capped sample step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sharded", action="store_true",
                     help="use the multi-GPU slab path even at N=1 (always on for N>1)")
@@ -184,6 +193,13 @@ def config_dict(cs, part, policy, extra=None):
 
 
 def run_reference(args, world, rank):
+    """The reference's CPU implementation of the path (the oracle port of
+    kernels_numba.py / bjac.py / solver.py, reference dot order, all host
+    threads) on rank 0.  A step is one whole solve to rtol when that fits
+    --ref-budget seconds (C1, C2 on a 16-core host); otherwise a capped
+    sample scaled by the reference-order iteration count of the oracle
+    fixtures -- and no line at all (an "unavailable" line) when that count is
+    unknown."""
     from paper_2407_15973_b200 import problems
     from paper_2407_15973_b200.bjac import BlockPartition
     if rank != 0:
@@ -192,27 +208,45 @@ def run_reference(args, world, rank):
     policy = args.policy or cs.policies[0]
     part = BlockPartition.fixed_size(cs.A.n, cs.block_rows)
     threads = os.cpu_count() or 1
-    it_full = REF_ITERS.get(cs.name)
-    for _ in range(args.warmup):
-        cpu_sample(cs, part, policy, args.ref_iters, threads)
-    times = []
+    it_full = ref_iterations(cs.name, policy)
+    # probe: a short capped solve gives the per-iteration cost
+    dt, its = cpu_sample(cs, part, policy, 10, threads)
+    est = dt / max(its, 1) * (it_full or 10 ** 9)
+    whole = est <= args.ref_budget
+    if not whole and it_full is None:
+        print(json.dumps({"impl": "reference", "unavailable":
+                          f"no reference-order iteration count for {cs.name}/{policy} and a whole "
+                          f"solve exceeds the {args.ref_budget:g} s budget"}), flush=True)
+        return
+    cap = None if whole else args.ref_iters
+    for _ in range(args.warmup):   # warm-up: short capped solves (page cache, thread pool)
+        cpu_sample(cs, part, policy, 10, threads)
+    times, iters = [], []
     for _ in range(args.steps):
-        dt, its = cpu_sample(cs, part, policy, args.ref_iters, threads)
-        times.append(dt / its)
-    per_it = float(np.mean(times))
-    if it_full is None:
-        it_full = args.ref_iters
-    solve_s = per_it * it_full
+        dt, its = cpu_sample(cs, part, policy, cap, threads)
+        times.append(dt)
+        iters.append(its)
+    if whole:
+        step_s = float(np.mean(times))
+        solve_s = step_s
+        sample = (f"{cs.name.upper()}: whole solves to rtol {cs.res_tol:g} ({iters[0]} iterations; "
+                  f"oracle restatement of the reference, reference dot order, {threads} OpenMP threads)")
+    else:
+        step_s = float(np.mean(times))
+        solve_s = float(np.mean([t / i for t, i in zip(times, iters)])) * it_full
+        sample = (f"{cs.name.upper()} solve capped at {args.ref_iters} iterations per step "
+                  f"(oracle restatement of the reference, reference dot order, {threads} OpenMP "
+                  f"threads), scaled to the {it_full}-iteration reference-order solve "
+                  f"(tests/golden/fullsize); ms_per_step is the solve time, step_s the sample")
     value = 1.0 / solve_s
-    sample = (f"{cs.name.upper()} solve capped at {args.ref_iters} iterations per step "
-              f"(oracle restatement of the reference, reference dot order, {threads} OpenMP "
-              f"threads), extrapolated to the {it_full}-iteration solve to rtol")
     line = {"impl": "reference", "metric": metric_name(cs), "value": value,
             "unit": "solve/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * solve_s,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64 CG / f32 preconditioner", "data": "synthetic (seeded SplitMix64)",
             "config": config_dict(cs, part, policy, {"parallelism": "1 CPU process"}),
+            "iterations": iters[0] if whole else it_full, "whole_solves": whole,
+            "step_s": step_s,
             "cpu_baseline": {"value": value, "unit": "solve/s", "cores": threads,
                              "kind": "port", "sample": sample},
             "e2e": {"value": value, "unit": "solve/s", "h2d_bytes_per_step": 0,
@@ -370,7 +404,8 @@ def run_b200(args, world, rank, local):
         fgbs = fb[name] / (t_ms * 1e-3) / 1e9
         kernels[name] = {"ms": round(t_ms, 5), "bytes": kb[name], "gbs": round(gbs, 1),
                          "frac": round(gbs / peak, 4), "format_bytes": fb[name],
-                         "format_gbs": round(fgbs, 1), "ms_cold": round(t_cold, 5),
+                         "format_gbs": round(fgbs, 1), "format_frac": round(fgbs / peak, 4),
+                         "ms_cold": round(t_cold, 5),
                          "frac_cold": round(kb[name] / (t_cold * 1e-3) / 1e9 / peak, 4)}
     per_iter_share = {k: v["ms"] for k, v in kernels.items()}
     dom = max(kernels, key=lambda k: per_iter_share[k])
@@ -380,12 +415,21 @@ def run_b200(args, world, rank, local):
         with open(tpath) as fh:
             tj = json.load(fh).get(cs.name, {})
             traffic = tj.get({"spmv_p": "spmv_pq"}.get(dom, dom))
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": kernels[dom]["gbs"],
-                "peak": peak, "unit": "GB/s", "frac": kernels[dom]["frac"],
-                "traffic": traffic, "peak_source": peak_src,
-                "bytes_per_launch": kb[dom], "bytes_model": "SURVEY.md 8(d) CSR model",
-                "format_bytes_per_launch": fb[dom],
-                "format_frac": round(kernels[dom]["format_gbs"] / peak, 4),
+    t_dom = kernels[dom]["ms"] * 1e-3
+    roofline = {"bound": "hbm", "kernel": dom,
+                # headline: the bytes this layout has to move per launch (SELL
+                # values, 2-byte row metadata, vectors; pattern rows carry no
+                # column index), DESIGN.md §4
+                "achieved": kernels[dom]["format_gbs"], "peak": peak, "unit": "GB/s",
+                "frac": round(kernels[dom]["format_gbs"] / peak, 4),
+                "bytes_per_launch": fb[dom], "bytes": "format bytes (DESIGN.md §4)",
+                "traffic": traffic,
+                "traffic_frac": round(traffic / t_dom / 1e9 / peak, 4) if traffic else None,
+                "peak_source": peak_src,
+                # SURVEY.md §8(d) CSR model: counts the column indices the
+                # row-pattern layout never reads, so it can exceed 1
+                "model_bytes_per_launch": kb[dom], "model_achieved": kernels[dom]["gbs"],
+                "model_frac": kernels[dom]["frac"],
                 "timing": "CUDA events around back-to-back launches chained by programmatic dependent "
                           "launch (as in the solve graph); kernels.*.ms_cold: one launch between two events"}
     it_med = int(np.median(iters))
@@ -398,13 +442,16 @@ def run_b200(args, world, rank, local):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         dt, its = cpu_sample(cs, part, policy, args.cpu_iters, 1)
-        it_full = REF_ITERS.get(cs.name, it_med)
+        it_full = ref_iterations(cs.name, policy)
+        src = "the reference-order iteration count of tests/golden/fullsize"
+        if it_full is None:
+            it_full, src = it_med, "the GPU's iteration count (no reference-order fixture)"
         cpu_solve = dt / its * it_full
         cpu = {"value": 1.0 / cpu_solve, "unit": "solve/s", "cores": 1, "kind": "port",
                "sample": f"{cs.name.upper()} solve capped at {its} iterations "
                          f"({dt:.1f} s; oracle restatement of the reference, reference dot "
                          f"order, 1 thread like the reference's numba kernels), "
-                         f"extrapolated to the {it_full}-iteration solve",
+                         f"scaled to the {it_full}-iteration solve ({src})",
                "host_cores": os.cpu_count()}
     if rank == 0:
         line = {
@@ -420,6 +467,9 @@ def run_b200(args, world, rank, local):
                 "row_patterns": plan.layout_info()}),
             "iterations": it_med, "time_to_solution_ms": ms_per_step,
             "converged": bool(rep.converged), "final_true_relres": rep.final_true_relres,
+            # north_star: final true fp64 relres at or below the tolerance
+            # (C3 ends at 1.10e-9 > 1e-10, as the reference's own order does)
+            "true_relres_met": bool(rep.final_true_relres <= cs.res_tol),
             "solve_gbs": round(solve_gbs, 1),
             "roofline": roofline, "kernels": kernels,
             "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": launches,

@@ -1,0 +1,170 @@
+"""Full-size parity on the GPU: every BASELINE config at its BASELINE size,
+and the reference's own n=128 acceptance problems on its default nb=32
+partition.
+
+Fixtures (tests/golden/fullsize/*.npz) come from tools/make_fullsize_golden.py,
+which runs the CPU oracle (pinned bit for bit to the reference by
+tests/test_oracle_golden.py) in two dot orders:
+
+  * device order: the GPU solve must match it BIT FOR BIT -- iteration count,
+    implicit relres trace, branches, final true relres and x (its SHA-256,
+    plus a strided sample for a readable failure);
+  * the reference's sequential order: the GPU iteration count must lie
+    within +-2 of it (SURVEY.md §8(c) band).
+
+The acceptance checks mirror pkg/tests/test_acceptance.py:226-317 (numbers
+in pkg/test_output.txt:27-33: Const 150/167, Ani(1000) 345/345, adaptive-hl
+tolerance sweep -> 150 or 167) on the GPU.
+"""
+import glob
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+FIXTURES = sorted(glob.glob(os.path.join(HERE, "golden", "fullsize", "*.npz")))
+
+
+def _policy_of(path):
+    stem = os.path.basename(path)[:-4]
+    cfg, _, pol = stem.partition("_nb32_") if "_nb32_" in stem else stem.partition("_")
+    if "_nb32_" in stem:
+        cfg += "_nb32"
+    kind, _, tol = pol.partition("_")
+    return cfg, kind + (":" + tol if tol else "")
+
+
+_SYSTEMS = {}
+
+
+def _system(cfg):
+    """(A, b, partition, k, t, res_tol) built on the GPU where the generator
+    can (bit-identical to the host generator, test_gpu_parity.py)."""
+    if cfg in _SYSTEMS:
+        return _SYSTEMS[cfg]
+    _SYSTEMS.clear()          # one full-size system resident at a time
+    from paper_2407_15973_b200 import problems
+    from paper_2407_15973_b200.bjac import BlockPartition
+    if cfg.endswith("_nb32"):
+        fam = problems.Family.CONST if cfg.startswith("const") else problems.Family.ANI
+        A = problems.family_matrix(128, fam, 1.0 if fam is problems.Family.CONST else 1000.0)
+        sysm = (A, np.ones(A.n), BlockPartition.equal_split(A.n, 32), 2, 2, 1e-10)
+    else:
+        cs = problems.make_config(cfg, device=cfg != "c4")
+        sysm = (cs.A, cs.b, BlockPartition.fixed_size(cs.A.n, cs.block_rows), cs.k, cs.t, cs.res_tol)
+    _SYSTEMS[cfg] = sysm
+    return sysm
+
+
+def _solve(cfg, pol, **cfg_kw):
+    from paper_2407_15973_b200.policies import PrecisionPolicy, build_mixed
+    from paper_2407_15973_b200.solver import SolveConfig, pcg_solve
+    A, b, part, k, t, tol = _system(cfg)
+    mp = build_mixed(A, PrecisionPolicy.parse(pol), k=k, t=t, partition=part)
+    return pcg_solve(A, b, mp, SolveConfig(res_tol=tol, **cfg_kw))
+
+
+def _x_host(x):
+    return x.cpu().numpy() if hasattr(x, "cpu") else np.asarray(x)
+
+
+@pytest.mark.parametrize("path", FIXTURES, ids=[os.path.basename(p)[:-4] for p in FIXTURES])
+def test_fullsize_bitwise_vs_oracle(cuda, path):
+    cfg, pol = _policy_of(path)
+    with np.load(path) as z:
+        fx = {k: z[k] for k in z.files}
+    rep = _solve(cfg, pol)
+    A = _system(cfg)[0]
+    assert (A.n, A.nnz) == (int(fx["meta"][0]), int(fx["meta"][1]))
+    assert rep.iterations == int(fx["iterations"]), (cfg, pol, rep.iterations)
+    np.testing.assert_array_equal([r.implicit_relres for r in rep.trace], fx["relres"])
+    np.testing.assert_array_equal([r.branch == "low" for r in rep.trace], fx["branch"].astype(bool))
+    assert rep.final_true_relres == float(fx["final_true"])
+    x = _x_host(rep.x)
+    np.testing.assert_array_equal(x[fx["x_sample_idx"]], fx["x_sample"])
+    assert hashlib.sha256(np.ascontiguousarray(x).tobytes()).hexdigest() == str(fx["x_sha256"])
+    assert rep.converged == bool(fx["converged"])
+    # the reference's own (sequential) dot order: within the band
+    if "seq_iterations" in fx:
+        assert abs(rep.iterations - int(fx["seq_iterations"])) <= 2
+
+
+# ---- the reference's acceptance criteria at n=128, nb=32 (on the GPU) ----
+
+def test_acceptance_06_convergence_delay(cuda):
+    """test_acceptance.py:226-237; published 150 / 167 (test_output.txt:27)."""
+    u = _solve("const128_nb32", "uniform")
+    lo = _solve("const128_nb32", "fixed-low")
+    assert u.converged and lo.converged
+    assert abs(u.iterations - 148) <= 0.20 * 148 and abs(lo.iterations - 165) <= 0.20 * 165
+    assert lo.iterations / u.iterations > 1.05
+    assert abs(u.iterations - 150) <= 2 and abs(lo.iterations - 167) <= 2
+
+
+def test_acceptance_07_no_delay_on_anisotropic(cuda):
+    """test_acceptance.py:240-250; published 345 / 345 (test_output.txt:29)."""
+    u = _solve("ani128_nb32", "uniform")
+    lo = _solve("ani128_nb32", "fixed-low")
+    assert u.converged and lo.converged
+    assert lo.iterations == u.iterations
+    assert abs(u.iterations - 327) <= 0.20 * 327 and abs(u.iterations - 345) <= 2
+
+
+def test_acceptance_08_adaptive_rescues_delay(cuda):
+    """test_acceptance.py:253-274: adaptive-hl at 1e-1..1e-5 takes the
+    uniform count, at 10 and 5 the fixed-low count."""
+    u = _solve("const128_nb32", "uniform").iterations
+    lo = _solve("const128_nb32", "fixed-low").iterations
+    for tol in ("1e-1", "1e-2", "1e-3", "1e-4", "1e-5"):
+        rep = _solve("const128_nb32", f"adaptive-hl:{tol}")
+        assert rep.converged and rep.iterations == u, (tol, rep.iterations, u)
+    for tol in ("10", "5"):
+        rep = _solve("const128_nb32", f"adaptive-hl:{tol}")
+        assert rep.converged and rep.iterations == lo, (tol, rep.iterations, lo)
+
+
+def test_acceptance_09_diagonal_dominance_trend(cuda):
+    """test_acceptance.py:277-290: diagonal augmentation at n=64 shrinks the
+    fixed-low / uniform iteration ratio (the preconditioner is built from
+    the augmented matrix, which is also the solved one)."""
+    from paper_2407_15973_b200 import problems
+    from paper_2407_15973_b200.policies import PrecisionPolicy, build_mixed
+    from paper_2407_15973_b200.solver import SolveConfig, pcg_solve
+    base = problems.family_matrix(64, problems.Family.CONST)
+    ratios = {}
+    for pd in (0.0, 1.0, 2.0, 8.0):
+        A = problems.diag_augment(base, pd) if pd else base
+        its = {}
+        for pol in ("uniform", "fixed-low"):
+            mp = build_mixed(A, PrecisionPolicy.parse(pol), nb=32)
+            rep = pcg_solve(A, np.ones(A.n), mp, SolveConfig(res_tol=1e-10))
+            assert rep.converged
+            its[pol] = rep.iterations
+        ratios[pd] = its["fixed-low"] / its["uniform"]
+    assert ratios[8.0] <= ratios[0.0]
+
+
+def test_acceptance_10_rerun_determinism(cuda, tmp_path):
+    """test_acceptance.py:293-317: rebuilt and re-solved systems give
+    byte-identical trace files."""
+    from paper_2407_15973_b200 import problems
+    from paper_2407_15973_b200.policies import PrecisionPolicy, build_mixed
+    from paper_2407_15973_b200.solver import SolveConfig, pcg_solve, trace_to_csv
+
+    def one_round(tag):
+        A = problems.family_matrix(8, problems.Family.DIS, 1000.0)
+        b = problems.splitmix64_stream(7, A.n)
+        blobs = []
+        for pol in ("uniform", "fixed-low", "adaptive-hl:10"):
+            rep = pcg_solve(A, b, build_mixed(A, PrecisionPolicy.parse(pol), nb=8),
+                            SolveConfig(res_tol=1e-10))
+            path = tmp_path / f"{tag}-{pol.replace(':', '-')}.csv"
+            trace_to_csv(rep, path)
+            blobs.append(path.read_bytes())
+        return blobs
+
+    assert one_round("a") == one_round("b")
