@@ -249,6 +249,45 @@ struct ApplyBufs {
   T *res, *dg, *wA, *wB;  // large-block path (plan->large)
 };
 
+// Warp-per-tile passes (k_bjac_wt / k_update_first_wt) for plans without
+// generic rows: an experiment, off by default (MPB_WT=1 turns it on).  On C2
+// the last pass took 47 us against 37 us for the CTA-per-tile k_bjac_tile:
+// too few warps per SM (two shared-memory stages per warp) for its serial
+// eight rows per lane (profiles/r02_notes.md).
+bool use_wt() {
+  static const bool on = std::getenv("MPB_WT") && std::atoi(std::getenv("MPB_WT")) != 0;
+  return on;
+}
+
+// Ring depth (stages per consumer warp) of a warp-per-tile kernel: the
+// deepest ring up to MPB_WT_DEPTH (default 2) that keeps the resident CTA
+// count of the shallowest one.
+template <typename K>
+int pick_wt_depth(K kernel, uint32_t stage_bytes, int threads) {
+  auto per_sm = [&](int depth) {
+    const uint32_t dyn = depth * kWtWarps * stage_bytes;
+    if (depth * kWtWarps > kWtMaxStages || dyn > 220u * 1024u) return 0;
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn));
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, dyn) != cudaSuccess) n = 0;
+    return n;
+  };
+  static const int forced = std::getenv("MPB_WT_DEPTH") ? std::atoi(std::getenv("MPB_WT_DEPTH")) : 0;
+  int depth = 1;
+  if (forced > 0) {
+    while (depth < forced && per_sm(depth + 1) > 0) depth++;
+  } else {  // at least two stages per warp (one in use, one loading), then deeper while the CTA count holds
+    if (per_sm(2) > 0) depth = 2;
+    const int base = per_sm(depth);
+    while (depth < 4 && per_sm(depth + 1) >= base) depth++;
+  }
+  static const bool verbose = std::getenv("MPB_VERBOSE") != nullptr;
+  if (verbose)
+    std::fprintf(stderr, "[mpb] wt stage %u B: %d warps x depth %d, %d CTAs/SM\n", stage_bytes, kWtWarps, depth,
+                 per_sm(depth));
+  return depth;
+}
+
 template <typename T, bool F, bool L, bool R64, int KS, bool GEN>
 int launch_tile_kernel(mpb_handle *h, cudaStream_t s, const mpb_plan *p, PassArgs<T> a) {
   if (F && !L) {  // first pass streams the in-block layout
@@ -258,6 +297,23 @@ int launch_tile_kernel(mpb_handle *h, cudaStream_t s, const mpb_plan *p, PassArg
     a.g.cap_e = std::min(p->max_tile_ib, kStageCap);
   }
   const StageLayout Ls = bjac_layout<T, F, R64>(a.g);
+  static const bool flat = std::getenv("MPB_FLAT") && std::atoi(std::getenv("MPB_FLAT")) != 0;
+  if (!GEN && flat && R64 && !(F && !L) && !a.g.poll) {
+    auto kern = k_bjac_flat<T, F, L, KS>;
+    MPB_CUDA(launch_k(a.pdl != 0, kern, static_cast<unsigned>(p->ntiles), kTileRows, 0, s, a));
+    MPB_LAUNCHED(h);
+    return MPB_OK;
+  }
+  if (!GEN && use_wt()) {
+    constexpr int threads = kWtWarps * 32 + 32;
+    auto kern = (L && a.g.poll) ? k_bjac_wt<T, F, L, R64, KS, L> : k_bjac_wt<T, F, L, R64, KS, false>;
+    a.g.ns = pick_wt_depth(kern, Ls.bytes, threads) * kWtWarps;
+    const uint32_t dyn = a.g.ns * Ls.bytes;
+    const int grid = persistent_grid(kern, dyn, p->ntiles, threads);
+    MPB_CUDA(launch_k(a.pdl != 0, kern, grid, threads, dyn, s, a));
+    MPB_LAUNCHED(h);
+    return MPB_OK;
+  }
   // the last pass carries the r.z sum: two-level order above MPB_ONE_LEVEL_TILES;
   // a pass that is not the first runs kLastRpt rows per consumer thread
   constexpr int RPT = (!F) ? kLastRpt : kRowsPerThread;
@@ -448,6 +504,16 @@ int launch_update_first(mpb_handle *h, cudaStream_t s, const mpb_plan *p, const 
   a.gate = 2;
   a.prefetch = prefetch;
   const StageLayout L = update_first_layout<T>(a.g);
+  if (p->ngeneric == 0 && use_wt()) {
+    constexpr int threads = kWtWarps * 32 + 32;
+    auto kern = two_level(p->ntiles) ? k_update_first_wt<T, true> : k_update_first_wt<T, false>;
+    a.g.ns = pick_wt_depth(kern, L.bytes, threads) * kWtWarps;
+    const uint32_t dyn = a.g.ns * L.bytes;
+    const int grid = persistent_grid(kern, dyn, p->ntiles, threads);
+    MPB_CUDA(launch_k(pdl, kern, grid, threads, dyn, s, a, x, pv, q, r));
+    MPB_LAUNCHED(h);
+    return MPB_OK;
+  }
   auto kern = two_level(p->ntiles) ? (p->ngeneric > 0 ? k_update_first_two<T, true> : k_update_first_two<T, false>)
                                     : (p->ngeneric > 0 ? k_update_first<T, true> : k_update_first<T, false>);
   a.g.ns = pick_stages(kern, L.bytes);

@@ -461,6 +461,23 @@ __device__ __forceinline__ void bulk_g2s_stream(void *dst, const void *src, uint
 #endif
 }
 
+// streaming loads (read once per kernel): L1 no-allocate, L2 evict-first
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ float ld_stream(const float *p, uint64_t pol) {
+  float v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ld_stream(const double *p, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
 // Programmatic dependent launch: a kernel launched with programmatic stream
 // serialization may start while its predecessor drains; everything before
 // pdl_wait() must touch only data the predecessor does not write.

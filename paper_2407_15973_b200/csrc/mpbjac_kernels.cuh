@@ -382,14 +382,16 @@ __host__ __device__ inline StageLayout stage_layout(int cap_e, int es, int max_s
 }
 
 // Ring of shared-memory stages filled by the producer warp.
-struct Ring {
-  uint64_t full[kMaxStages];   // TMA bytes landed
-  uint64_t empty[kMaxStages];  // consumers done with the stage
-  int ok[kMaxStages];          // tile fitted and was staged
-  int tile[kMaxStages];        // tile in the stage, -1: no more tiles
-  TileDesc desc[kMaxStages];
-  int pend[kMaxPend];          // producer: owned chunks not yet summed
+template <int MS>
+struct RingT {
+  uint64_t full[MS];   // TMA bytes landed
+  uint64_t empty[MS];  // consumers done with the stage
+  int ok[MS];          // tile fitted and was staged
+  int tile[MS];        // tile in the stage, -1: no more tiles
+  TileDesc desc[MS];
+  int pend[kMaxPend];  // producer: owned chunks not yet summed
 };
+using Ring = RingT<kMaxStages>;
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -421,8 +423,8 @@ enum { kFillAll = 0, kFillStatic = 1, kFillDynamic = 2 };
 // LAST_USE: bit i set = vector slice vi is read for the last time this
 // iteration (streamed evict-first, like the matrix data)
 template <typename T, typename V0, typename V1, typename V2, bool IB = false, typename V3 = uint8_t,
-          unsigned LAST_USE = 0u>
-__device__ __forceinline__ void produce(Ring &R, int st, const TileDesc *td, int tile, const TileGeom &g,
+          unsigned LAST_USE = 0u, class RG>
+__device__ __forceinline__ void produce(RG &R, int st, const TileDesc *td, int tile, const TileGeom &g,
                                         const StageLayout &L, unsigned char *stage, const int *sp, const int *scol,
                                         const T *sval, const uint16_t *meta, const V0 *v0, const V1 *v1,
                                         const V2 *v2, const V3 *v3 = nullptr, int part = kFillAll) {
@@ -485,9 +487,27 @@ __device__ __forceinline__ void produce(Ring &R, int st, const TileDesc *td, int
 // polled while the producer would otherwise wait for a stage to come back,
 // and blocking after the last claim.  (Owners polling from a consumer warp
 // stall their CTA: measured slower.)
-template <typename F, typename G>
-__device__ __forceinline__ void producer_loop(Ring &R, int ntiles, int ns, unsigned int *ctr, bool prefetch,
-                                              G &&gated, F &&fill, const ChunkCtx &ck) {
+// End markers (one thread): stage st (free) and the next nterm - 1 stages
+// get tile -1, so that each of nterm consumer warps sees one (warp-per-tile
+// kernels consume the stages round-robin, stage i by warp i % nterm).
+template <class RG>
+__device__ __forceinline__ void ring_end(RG &R, int st, int rnd, int ns, int nterm) {
+  R.tile[st] = -1;
+  mbar_arrive(&R.full[st]);
+  for (int i = 1; i < nterm; i++) {
+    if (++st == ns) {
+      st = 0;
+      rnd++;
+    }
+    if (rnd > 0) mbar_wait_sleep(&R.empty[st], (rnd - 1) & 1);
+    R.tile[st] = -1;
+    mbar_arrive(&R.full[st]);
+  }
+}
+
+template <typename F, typename G, class RG>
+__device__ __forceinline__ void producer_loop(RG &R, int ntiles, int ns, unsigned int *ctr, bool prefetch,
+                                              G &&gated, F &&fill, const ChunkCtx &ck, int nterm = 1) {
   const int lane = threadIdx.x & 31;
   int next = blockIdx.x;
   auto claim = [&]() -> int {
@@ -561,16 +581,16 @@ __device__ __forceinline__ void producer_loop(Ring &R, int ntiles, int ns, unsig
       }
     }
   }
-  if (lane == 0) mbar_arrive(&R.full[st]);  // stage st holds the end marker (-1)
+  if (lane == 0) ring_end(R, st, rnd, ns, nterm);  // stage st holds the (first) end marker
   __syncwarp();
   while (phead != ptail) poll_oldest(true);
 }
 
 // Single-lane producer (lane 0 of the producer warp) for kernels without
 // chunk owners: the same walk as producer_loop.
-template <typename F, typename G>
-__device__ __forceinline__ void producer_loop_single(Ring &R, int ntiles, int ns, unsigned int *ctr, bool prefetch,
-                                              G &&gated, F &&fill) {
+template <typename F, typename G, class RG>
+__device__ __forceinline__ void producer_loop_single(RG &R, int ntiles, int ns, unsigned int *ctr, bool prefetch,
+                                              G &&gated, F &&fill, int nterm = 1) {
   int next = blockIdx.x;
   auto claim = [&]() -> int {
     if (ctr != nullptr) {
@@ -605,7 +625,7 @@ __device__ __forceinline__ void producer_loop_single(Ring &R, int ntiles, int ns
   }
   for (int i = 0; i < npre; i++) fill(i, R.tile[i], kFillDynamic);
   if (exhausted) {
-    mbar_arrive(&R.full[npre]);
+    ring_end(R, npre, 0, ns, nterm);
     return;
   }
   int st = npre % ns, rnd = npre / ns;  // stage, and how often it has been filled before
@@ -614,7 +634,7 @@ __device__ __forceinline__ void producer_loop_single(Ring &R, int ntiles, int ns
     const int tile = claim();
     R.tile[st] = tile;
     if (tile < 0) {
-      mbar_arrive(&R.full[st]);
+      ring_end(R, st, rnd, ns, nterm);
       return;
     }
     fill(st, tile, kFillAll);
@@ -636,7 +656,8 @@ struct RingCursor {
   }
 };
 
-__device__ __forceinline__ void ring_init(Ring &R, int ns, int consumers = kConsumers) {
+template <class RG>
+__device__ __forceinline__ void ring_init(RG &R, int ns, int consumers = kConsumers) {
   if (threadIdx.x == 0) {
     for (int st = 0; st < ns; st++) {
       mbar_init(&R.full[st], 1);
@@ -647,7 +668,8 @@ __device__ __forceinline__ void ring_init(Ring &R, int ns, int consumers = kCons
 }
 
 // consumer warp releases its use of a stage (one arrive per warp)
-__device__ __forceinline__ void ring_release(Ring &R, int st) {
+template <class RG>
+__device__ __forceinline__ void ring_release(RG &R, int st) {
   __syncwarp();
   if ((threadIdx.x & 31) == 0) mbar_arrive(&R.empty[st]);
 }
@@ -1129,6 +1151,346 @@ __global__ void __launch_bounds__(kTileThreads / RPT + 32) k_bjac_tile(const Pas
     finish_grid<16, kFinRpt>(a.st, 0, kStepRho, ChunkCtx{a.csum, a.part, a.g.ntiles, TWO ? a.g.poll : 0}, ws);
 }
 
+// ---------------------------------------------------------------------------
+// Warp-per-tile fused BJAC pass.  Each consumer warp owns a whole tile, 8
+// rows per lane (row lane + 32 k), so the inner sweeps need only __syncwarp
+// (the tile's w lives in a warp-private shared array) and the tile's r.z
+// sum is the same tree as include/mpbjac_order.h's (virtual warp k = rows
+// 32k..32k+31 butterflied, then the 8 warp sums butterflied with +0 padding)
+// without any CTA barrier.  Warps run their tiles independently, each with
+// 8 rows x up to 7 z_in gathers of memory-level parallelism, where the CTA-
+// wide version stalled all warps at every sweep barrier.  Consumer warp c
+// takes ring stages c, c + W, c + 2W, ... (ns = W x depth stages); the
+// producer ends the walk with one end marker per warp (ring_end).
+// Plans with generic rows keep k_bjac_tile.
+// ---------------------------------------------------------------------------
+constexpr int kWtRows = kTileRows / 32;  // rows per lane
+#ifndef MPB_WT_WARPS
+#define MPB_WT_WARPS 4
+#endif
+constexpr int kWtWarps = MPB_WT_WARPS;   // consumer warps per CTA
+constexpr int kWtMaxStages = 16;
+constexpr int kWtBatch = 4;              // rows per lane whose gathers are in flight together
+
+// tile sum of one value per row (prod[k] = row lane + 32 k) in the fixed
+// order; the result is valid in every lane
+__device__ __forceinline__ double wt_tile_sum(const double (&prod)[kWtRows]) {
+  const int lane = threadIdx.x & 31;
+  double r = 0.0;
+#pragma unroll
+  for (int k = 0; k < kWtRows; k++) {
+    const double wsum = warp_bfly(prod[k]);
+    if (lane == k) r = wsum;
+  }
+  return warp_bfly(r);
+}
+
+// One tile of a pass that reads the full rows (not the in-block-only first
+// pass): z_out = z_in + D_b^{-1}(r - A z_in), the in-block sweeps in s_w.
+template <typename T, bool FIRST, bool LAST, int KS>
+__device__ __forceinline__ void wt_pass_tile(const PassArgs<T> &a, int tile, const TileDesc &d, const T *val,
+                                             const int *spp, const uint16_t *mt, const double *r64t, const T *rTt,
+                                             const int *s_pat, T *s_w) {
+  const int lane = threadIdx.x & 31;
+  T res[kWtRows], dd[kWtRows], w[kWtRows], zown[kWtRows];
+#pragma unroll
+  for (int kb = 0; kb < kWtRows; kb += kWtBatch) {
+    T g[kWtBatch][KS], v[kWtBatch][KS];
+    int len[kWtBatch];
+#pragma unroll
+    for (int q = 0; q < kWtBatch; q++) {  // issue every gather of the batch first
+      const int k = kb + q, i = lane + 32 * k, row = d.lo + i;
+      const bool valid = row < d.hi;
+      const int ii = valid ? i : 0;
+      const int *P = s_pat + meta_pid(mt[ii]) * kPatStride;
+      const int base = spp[((d.lo + ii) >> 5) - d.s0] - d.e0 + ((d.lo + ii) & 31);
+      len[q] = valid ? pat_len(P[0]) : 0;
+      dd[k] = valid ? val[base + 32 * pat_dpos(P[0])] : T(1);
+      const T *zr = FIRST ? nullptr : a.zin + d.lo + ii;
+      if (!FIRST) zown[k] = __ldg(zr);
+#pragma unroll
+      for (int u = 0; u < KS; u++) {
+        v[q][u] = u < len[q] ? val[base + 32 * u] : T(0);
+        if (!FIRST) g[q][u] = __ldg(zr + P[1 + u]);  // offsets past len are 0
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kWtBatch; q++) {
+      const int k = kb + q, i = lane + 32 * k, row = d.lo + i;
+      if (row >= d.hi) {
+        res[k] = T(0);
+        w[k] = T(0);
+        continue;
+      }
+      const T rv = r64t != nullptr ? narrow_checked(a, r64t[i], row, FIRST) : rTt[i];
+      T az = T(0);
+      if (!FIRST) {
+#pragma unroll
+        for (int u = 0; u < KS; u++)
+          if (u < len[q]) az = add_rn(az, mul_rn(v[q][u], g[q][u]));
+      }
+      res[k] = FIRST ? rv : sub_rn(rv, az);
+      w[k] = div_rn(res[k], dd[k]);
+      s_w[i] = w[k];
+    }
+  }
+  for (int s = 1; s < a.t; s++) {  // inner sweeps over the in-block entries
+    __syncwarp();
+    T acc[kWtRows];
+#pragma unroll
+    for (int k = 0; k < kWtRows; k++) {
+      const int i = lane + 32 * k, row = d.lo + i;
+      acc[k] = T(0);
+      if (row >= d.hi) continue;
+      const uint16_t m = mt[i];
+      const int *P = s_pat + meta_pid(m) * kPatStride + 1;
+      const int base = spp[(row >> 5) - d.s0] - d.e0 + (row & 31);
+#pragma unroll 1
+      for (int j = meta_i0(m); j < meta_i1(m); j++) acc[k] = add_rn(acc[k], mul_rn(val[base + 32 * j], s_w[i + P[j]]));
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < kWtRows; k++) {
+      const int i = lane + 32 * k;
+      if (d.lo + i >= d.hi) continue;
+      w[k] = add_rn(w[k], div_rn(sub_rn(res[k], acc[k]), dd[k]));
+      s_w[i] = w[k];
+    }
+  }
+  double prod[kWtRows];
+#pragma unroll
+  for (int k = 0; k < kWtRows; k++) {
+    const int i = lane + 32 * k, row = d.lo + i;
+    prod[k] = 0.0;
+    if (row >= d.hi) continue;
+    const T zo = FIRST ? w[k] : add_rn(zown[k], w[k]);
+    if (a.zout != nullptr) st_keep(a.zout + row, zo);
+    if (a.zout64 != nullptr) a.zout64[row] = static_cast<double>(zo);
+    if (LAST && a.part != nullptr) prod[k] = __dmul_rn(r64t[i], static_cast<double>(zo));
+  }
+  if (LAST && a.part != nullptr) {
+    const double tot = wt_tile_sum(prod);
+    if (lane == 0) put_part(a.part + tile, tot);
+  }
+  __syncwarp();  // s_w is reused by the warp's next tile
+}
+
+// One tile of the in-block-only first pass (z1 = D_b^{-1} r): values and slice
+// pointers of the plan's in-block SELL layout; res[k] = the row's residual.
+template <typename T>
+__device__ __forceinline__ void wt_first_tile(const PassArgs<T> &a, const TileDesc &d, const T *val, const int *spp,
+                                              const uint16_t *mt, const T (&res)[kWtRows], const int *s_pat,
+                                              T *s_w) {
+  const int lane = threadIdx.x & 31;
+  T dd[kWtRows], w[kWtRows];
+#pragma unroll
+  for (int k = 0; k < kWtRows; k++) {
+    const int i = lane + 32 * k, row = d.lo + i;
+    dd[k] = T(1);
+    w[k] = T(0);
+    if (row >= d.hi) continue;
+    const uint16_t m = mt[i];
+    const int *P = s_pat + meta_pid(m) * kPatStride;
+    const int base = spp[(row >> 5) - d.s0] - d.ie0 + (row & 31);
+    dd[k] = val[base + 32 * (pat_dpos(P[0]) - meta_i0(m))];
+    w[k] = div_rn(res[k], dd[k]);
+    s_w[i] = w[k];
+  }
+  for (int s = 1; s < a.t; s++) {
+    __syncwarp();
+    T acc[kWtRows];
+#pragma unroll
+    for (int k = 0; k < kWtRows; k++) {
+      const int i = lane + 32 * k, row = d.lo + i;
+      acc[k] = T(0);
+      if (row >= d.hi) continue;
+      const uint16_t m = mt[i];
+      const int i0 = meta_i0(m), nib = meta_i1(m) - i0;
+      const int *P = s_pat + meta_pid(m) * kPatStride + 1 + i0;
+      const int base = spp[(row >> 5) - d.s0] - d.ie0 + (row & 31);
+#pragma unroll 1
+      for (int j = 0; j < nib; j++) acc[k] = add_rn(acc[k], mul_rn(val[base + 32 * j], s_w[i + P[j]]));
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < kWtRows; k++) {
+      const int i = lane + 32 * k;
+      if (d.lo + i >= d.hi) continue;
+      w[k] = add_rn(w[k], div_rn(sub_rn(res[k], acc[k]), dd[k]));
+      s_w[i] = w[k];
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kWtRows; k++) {
+    const int row = d.lo + lane + 32 * k;
+    if (row >= d.hi) continue;
+    if (a.zout != nullptr) st_keep(a.zout + row, w[k]);
+    if (a.zout64 != nullptr) a.zout64[row] = static_cast<double>(w[k]);
+  }
+  __syncwarp();
+}
+
+template <typename T, bool FIRST, bool LAST, bool R64, int KS, bool TWO>
+__global__ void __launch_bounds__(kWtWarps * 32 + 32) k_bjac_wt(const PassArgs<T> a) {
+  constexpr int NC = kWtWarps * 32;
+  constexpr int kFinRpt = NC >= kFinThreads ? 1 : kFinThreads / NC;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ RingT<kWtMaxStages> R;
+  __shared__ T s_w[kWtWarps][kTileRows];
+  __shared__ double ws[32];
+  __shared__ int s_pat[kPatMax * kPatStride];
+  const int ns = a.g.ns;
+  constexpr bool kIB = FIRST && !LAST;  // first pass alone: in-block entries only
+  const StageLayout L = bjac_layout<T, FIRST, R64>(a.g);
+  load_patterns(s_pat, a.pat, a.g.npat);
+  ring_init(R, ns, 32);  // one consumer warp per stage
+  if (threadIdx.x >= NC) {  // producer warp
+    using RT = typename std::conditional<R64, double, T>::type;
+    const RT *rsrc = R64 ? reinterpret_cast<const RT *>(a.r64) : reinterpret_cast<const RT *>(a.rT);
+    const ChunkCtx ck{(TWO && LAST && a.part != nullptr && a.st != nullptr) ? a.csum : nullptr, a.part, a.g.ntiles,
+                      TWO ? a.g.poll : 0};
+    auto fill = [&](int st, int tile, int part) {
+      if (kIB)
+        produce<T, RT, uint8_t, uint8_t, true>(R, st, a.td, tile, a.g, L, smem + st * L.bytes, a.ib_sp, a.ib_col,
+                                               a.ib_val, a.meta, rsrc, nullptr, nullptr,
+                                               static_cast<const uint8_t *>(nullptr), part);
+      else
+        produce<T, RT, uint8_t, uint8_t>(R, st, a.td, tile, a.g, L, smem + st * L.bytes, a.sp, a.scol, a.sval,
+                                         a.meta, rsrc, nullptr, nullptr, static_cast<const uint8_t *>(nullptr), part);
+    };
+    auto gated = [&]() { return gated_off(a); };
+    if (TWO && ck.csum != nullptr && ck.poll)
+      producer_loop(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, gated, fill, ck, kWtWarps);
+    else if (threadIdx.x == NC)
+      producer_loop_single(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, gated, fill, kWtWarps);
+    else
+      pdl_wait();
+    if (gated_off(a)) return;
+  } else {
+    pdl_wait();
+    if (gated_off(a)) return;
+    const int c = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    T *sw = s_w[c];
+    int st = c, phase = 0;
+    for (;;) {
+      mbar_wait(&R.full[st], phase);
+      const int tile = R.tile[st];
+      if (tile < 0) break;
+      const TileDesc d = R.desc[st];
+      const unsigned char *sb = smem + st * L.bytes;
+      const bool ok = R.ok[st] != 0;
+      if (kIB) {
+        const T *val = ok ? reinterpret_cast<const T *>(sb + L.val) : a.ib_val + d.ie0;
+        const int *spp = ok ? staged(sb + L.sp, a.ib_sp, d.s0, d.s1 + 1) : a.ib_sp + d.s0;
+        const uint16_t *mt = ok ? staged(sb + L.meta, a.meta, d.lo, d.hi) : a.meta + d.lo;
+        T rv[kWtRows];
+#pragma unroll
+        for (int k = 0; k < kWtRows; k++) {
+          const int i = lane + 32 * k, row = d.lo + i;
+          rv[k] = T(0);
+          if (row >= d.hi) continue;
+          if (R64) rv[k] = narrow_checked(a, ok ? staged(sb + L.v0, a.r64, d.lo, d.hi)[i] : a.r64[row], row, true);
+          else rv[k] = ok ? staged(sb + L.v0, a.rT, d.lo, d.hi)[i] : a.rT[row];
+        }
+        wt_first_tile<T>(a, d, val, spp, mt, rv, s_pat, sw);
+      } else {
+        const T *val = ok ? reinterpret_cast<const T *>(sb + L.val) : a.sval + d.e0;
+        const int *spp = ok ? staged(sb + L.sp, a.sp, d.s0, d.s1 + 1) : a.sp + d.s0;
+        const uint16_t *mt = ok ? staged(sb + L.meta, a.meta, d.lo, d.hi) : a.meta + d.lo;
+        const double *r64t = R64 ? (ok ? staged(sb + L.v0, a.r64, d.lo, d.hi) : a.r64 + d.lo) : nullptr;
+        const T *rTt = R64 ? nullptr : (ok ? staged(sb + L.v0, a.rT, d.lo, d.hi) : a.rT + d.lo);
+        wt_pass_tile<T, FIRST, LAST, KS>(a, tile, d, val, spp, mt, r64t, rTt, s_pat, sw);
+      }
+      if (lane == 0) mbar_arrive(&R.empty[st]);
+      st += kWtWarps;
+      if (st >= ns) {
+        st -= ns;
+        phase ^= 1;
+      }
+    }
+  }
+  pdl_trigger();  // dependents may launch into the SMs this grid drains
+  if (LAST && a.part != nullptr)
+    finish_grid<16, kFinRpt>(a.st, 0, kStepRho, ChunkCtx{a.csum, a.part, a.g.ntiles, TWO ? a.g.poll : 0}, ws);
+}
+
+// ---------------------------------------------------------------------------
+// Flat (non-persistent) BJAC pass, no TMA ring: one CTA per tile, one row per
+// thread, operands loaded straight from global memory (matrix values and
+// row metadata before the grid dependency wait -- they do not depend on the
+// previous kernel -- then the residual and the z_in gathers).  Many small
+// resident CTAs (8 per SM) hide each other's load latency and barriers.
+// Pattern rows only; one-level sums (<= MPB_ONE_LEVEL_TILES tiles).
+// ---------------------------------------------------------------------------
+template <typename T, bool FIRST, bool LAST, int KS>
+__global__ void __launch_bounds__(kTileRows) k_bjac_flat(const PassArgs<T> a) {
+  __shared__ T s_w[kTileRows];
+  __shared__ double ws[32];
+  __shared__ int s_pat[kPatMax * kPatStride];
+  const int tile = blockIdx.x;
+  const TileDesc d = a.td[tile];
+  const int i = threadIdx.x, row = d.lo + i;
+  const bool valid = row < d.hi;
+  const int rr = valid ? row : d.lo;
+  const uint16_t m = __ldg(a.meta + rr);
+  const int sb = __ldg(a.sp + (rr >> 5));
+  const int width = (__ldg(a.sp + (rr >> 5) + 1) - sb) >> 5;
+  const int base = sb + (rr & 31);
+  T v[KS];
+  const uint64_t pol = policy_evict_first();
+#pragma unroll
+  for (int u = 0; u < KS; u++) v[u] = u < width ? ld_stream(a.sval + base + 32 * u, pol) : T(0);
+  load_patterns(s_pat, a.pat, a.g.npat);
+  __syncthreads();
+  pdl_wait();
+  if (gated_off(a)) return;
+  const int *P = s_pat + meta_pid(m) * kPatStride;
+  const int hdr = P[0], len = pat_len(hdr);
+  const T rv = narrow_checked(a, a.r64[rr], rr, FIRST);
+  T az = T(0), zown = T(0);
+  if (!FIRST) {
+    const T *zr = a.zin + rr;
+    zown = __ldg(zr);
+    T g[KS];
+#pragma unroll
+    for (int u = 0; u < KS; u++) g[u] = __ldg(zr + P[1 + u]);
+#pragma unroll
+    for (int u = 0; u < KS; u++)
+      if (u < len) az = add_rn(az, mul_rn(v[u], g[u]));
+  }
+  T dd = T(1);
+#pragma unroll
+  for (int u = 0; u < KS; u++)
+    if (u == pat_dpos(hdr)) dd = v[u];
+  const T res = FIRST ? rv : sub_rn(rv, az);
+  T w = div_rn(res, dd);
+  s_w[i] = w;
+  const int i0 = meta_i0(m), i1 = meta_i1(m);
+  for (int s = 1; s < a.t; s++) {
+    __syncthreads();
+    T acc = T(0);
+#pragma unroll
+    for (int u = 0; u < KS; u++)
+      if (u >= i0 && u < i1) acc = add_rn(acc, mul_rn(v[u], s_w[i + P[1 + u]]));
+    __syncthreads();
+    w = add_rn(w, div_rn(sub_rn(res, acc), dd));
+    s_w[i] = w;
+  }
+  double prod = 0.0;
+  if (valid) {
+    const T zo = FIRST ? w : add_rn(zown, w);
+    if (a.zout != nullptr) st_keep(a.zout + row, zo);
+    if (a.zout64 != nullptr) a.zout64[row] = static_cast<double>(zo);
+    if (LAST && a.part != nullptr) prod = __dmul_rn(a.r64[row], static_cast<double>(zo));
+  }
+  if (LAST && a.part != nullptr) {
+    const double tot = block_tree<kTileThreads>(prod, ws);
+    if (threadIdx.x == 0) put_part(a.part + tile, tot);
+  }
+  pdl_trigger();
+  if (LAST && a.part != nullptr) finish_grid<16, 1>(a.st, 0, kStepRho, ChunkCtx{nullptr, a.part, a.g.ntiles, 0}, ws);
+}
+
 // ---- large blocks (> kTileRows rows): one launch per inner sweep ----------
 // pass prologue: res = r - A z_in, d = diag, w0 = res / d
 template <typename T, bool FIRST>
@@ -1543,6 +1905,88 @@ template <typename T, bool GEN>
 __global__ void __launch_bounds__(kWsThreads, sizeof(T) == 4 ? 5 : 4)
     k_update_first_two(const PassArgs<T> a, double *x, const double *p, const double *q, double *r) {
   update_first_body<T, GEN, true>(a, x, p, q, r);
+}
+
+// Warp-per-tile fused x/r update + next first pass (same arithmetic and
+// tile order as update_first_body; see k_bjac_wt for the warp-per-tile
+// scheme).  Plans with generic rows keep k_update_first.
+template <typename T, bool TWO>
+__global__ void __launch_bounds__(kWtWarps * 32 + 32)
+    k_update_first_wt(const PassArgs<T> a, double *x, const double *p, const double *q, double *r) {
+  constexpr int NC = kWtWarps * 32;
+  constexpr int kFinRpt = NC >= kFinThreads ? 1 : kFinThreads / NC;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ RingT<kWtMaxStages> R;
+  __shared__ T s_w[kWtWarps][kTileRows];
+  __shared__ double ws[32];
+  __shared__ int s_pat[kPatMax * kPatStride];
+  const int ns = a.g.ns;
+  const StageLayout L = update_first_layout<T>(a.g);
+  load_patterns(s_pat, a.pat, a.g.npat);
+  ring_init(R, ns, 32);
+  if (threadIdx.x >= NC) {
+    const ChunkCtx ck{a.csum, a.part, a.g.ntiles, TWO ? a.g.poll : 0};
+    auto fill = [&](int st, int tile, int part) {
+      // x (v1) and q (v3) are not read again before the next x/r update
+      produce<T, double, double, double, true, double, 0xAu>(R, st, a.td, tile, a.g, L, smem + st * L.bytes,
+                                                             a.ib_sp, a.ib_col, a.ib_val, a.meta, r, x, p, q, part);
+    };
+    auto gated = [&]() { return gated_off(a); };
+    if (TWO && ck.poll)
+      producer_loop(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, gated, fill, ck, kWtWarps);
+    else if (threadIdx.x == NC)
+      producer_loop_single(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, gated, fill, kWtWarps);
+    else
+      pdl_wait();
+    if (gated_off(a)) return;
+  } else {
+    pdl_wait();
+    if (gated_off(a)) return;
+    const double alpha = a.st->alpha;
+    const int c = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    T *sw = s_w[c];
+    int st = c, phase = 0;
+    for (;;) {
+      mbar_wait(&R.full[st], phase);
+      const int tile = R.tile[st];
+      if (tile < 0) break;
+      const TileDesc d = R.desc[st];
+      const unsigned char *sb = smem + st * L.bytes;
+      const bool ok = R.ok[st] != 0;
+      const double *xs = ok ? staged(sb + L.v1, x, d.lo, d.hi) : x + d.lo;
+      const double *ps = ok ? staged(sb + L.v2, p, d.lo, d.hi) : p + d.lo;
+      const double *qs = ok ? staged(sb + L.v3, q, d.lo, d.hi) : q + d.lo;
+      const double *rs = ok ? staged(sb + L.v0, r, d.lo, d.hi) : r + d.lo;
+      double sq[kWtRows];
+      T rv[kWtRows];
+#pragma unroll
+      for (int k = 0; k < kWtRows; k++) {
+        const int i = lane + 32 * k, row = d.lo + i;
+        sq[k] = 0.0;
+        rv[k] = T(0);
+        if (row >= d.hi) continue;
+        st_evict_first(x + row, __dadd_rn(xs[i], __dmul_rn(alpha, ps[i])));  // (read again by the next update only)
+        const double rn = __dsub_rn(rs[i], __dmul_rn(alpha, qs[i]));
+        r[row] = rn;
+        sq[k] = __dmul_rn(rn, rn);
+        rv[k] = narrow_checked(a, rn, row, true);
+      }
+      const double tot = wt_tile_sum(sq);
+      if (lane == 0) put_part(a.part + tile, tot);
+      const T *val = ok ? reinterpret_cast<const T *>(sb + L.val) : a.ib_val + d.ie0;
+      const int *spp = ok ? staged(sb + L.sp, a.ib_sp, d.s0, d.s1 + 1) : a.ib_sp + d.s0;
+      const uint16_t *mt = ok ? staged(sb + L.meta, a.meta, d.lo, d.hi) : a.meta + d.lo;
+      wt_first_tile<T>(a, d, val, spp, mt, rv, s_pat, sw);
+      if (lane == 0) mbar_arrive(&R.empty[st]);
+      st += kWtWarps;
+      if (st >= ns) {
+        st -= ns;
+        phase ^= 1;
+      }
+    }
+  }
+  pdl_trigger();
+  finish_grid<8, kFinRpt>(a.st, 2, kStepRrZ, ChunkCtx{a.csum, a.part, a.g.ntiles, TWO ? a.g.poll : 0}, ws);
 }
 
 // res = b - A x (or b), optionally stored; res.res partial; the last CTA runs
