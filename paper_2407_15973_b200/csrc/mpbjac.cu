@@ -65,10 +65,12 @@ struct mpb_plan {
   int *d_ib_sp, *d_ib_col;  // in-block SELL layout (first passes)
   int64_t ib_nnz;
   int max_tile_ib;
+  int max_ib_row;           // most in-block entries of a row (the sweeps' unroll bound)
   const int *d_pat;         // the bound SELL's row-pattern table (not owned)
   int npat;
   int ks;                   // compile-time slot count of the hot kernels (7 or 9)
   int64_t ngeneric;         // rows without a usable pattern (kMetaGeneric)
+  WinSet win;               // z_in gather windows of the passes after the first (n == 0: none)
 };
 
 struct mpb_comm {
@@ -162,6 +164,7 @@ TileGeom geom_for(const mpb_plan *p) {
   g.cols = p->ngeneric > 0 ? 1 : 0;
   g.npat = p->npat;
   g.poll = owners_poll(p->ntiles) ? 1 : 0;
+  g.kib = p->max_ib_row;
   return g;
 }
 
@@ -249,6 +252,13 @@ struct ApplyBufs {
   T *res, *dg, *wA, *wB;  // large-block path (plan->large)
 };
 
+// Tile-claim counter i of the persistent kernels (dynamic scheduling), or
+// null for the static walk blockIdx.x, +gridDim.x, ... (MPB_STATIC=1)
+unsigned int *claim_ctr(const mpb_handle *h, int i) {
+  static const bool stat = std::getenv("MPB_STATIC") && std::atoi(std::getenv("MPB_STATIC")) != 0;
+  return stat ? nullptr : h->d_ctr + i;
+}
+
 // Warp-per-tile passes (k_bjac_wt / k_update_first_wt) for plans without
 // generic rows: an experiment, off by default (MPB_WT=1 turns it on).  On C2
 // the last pass took 47 us against 37 us for the CTA-per-tile k_bjac_tile:
@@ -303,6 +313,21 @@ int launch_tile_kernel(mpb_handle *h, cudaStream_t s, const mpb_plan *p, PassArg
     MPB_CUDA(launch_k(a.pdl != 0, kern, static_cast<unsigned>(p->ntiles), kTileRows, 0, s, a));
     MPB_LAUNCHED(h);
     return MPB_OK;
+  }
+  if constexpr (!F && !GEN) {
+    if (a.win.n > 0 && (reinterpret_cast<uintptr_t>(a.zin) & 15) == 0 && !use_wt()) {
+    constexpr int RPT = kLastRpt;
+    constexpr int threads = kTileThreads / RPT + 32;
+    const StageLayout Lw = bjac_layout_win<T, F, R64>(a.g, a.win);
+    auto kern = (L && a.g.poll) ? k_bjac_tile<T, F, L, R64, KS, GEN, L, RPT, true>
+                                : k_bjac_tile<T, F, L, R64, KS, GEN, false, RPT, true>;
+    a.g.ns = pick_stages(kern, Lw.bytes, threads);
+    const uint32_t dyn = a.g.ns * Lw.bytes;
+    const int grid = persistent_grid(kern, dyn, p->ntiles, threads);
+    MPB_CUDA(launch_k(a.pdl != 0, kern, grid, threads, dyn, s, a));
+    MPB_LAUNCHED(h);
+    return MPB_OK;
+    }
   }
   if (!GEN && use_wt()) {
     constexpr int threads = kWtWarps * 32 + 32;
@@ -438,7 +463,7 @@ int launch_apply(mpb_handle *h, cudaStream_t s, const mpb_plan *p, const mpb_csr
   a.meta = p->d_meta;
   a.pat = p->d_pat;
   a.td = p->d_td;
-  a.ctr = h->d_ctr + 0;
+  a.ctr = claim_ctr(h, 0);
   a.boff = p->d_boff;
   a.g = geom_for<T>(p);
   a.t = t;
@@ -452,6 +477,10 @@ int launch_apply(mpb_handle *h, cudaStream_t s, const mpb_plan *p, const mpb_csr
   a.pdl = (st != nullptr && dc == nullptr) ? 1 : 0;  // captured single-GPU iteration
   a.gate = z1_gate;
   a.prefetch = prefetch;
+  if (dc == nullptr) {  // gather windows: one GPU (slabs' ghost columns are not row + offset)
+    a.win = p->win;
+    a.win.zlen = static_cast<int>(A->n);
+  }
   for (int pass = from_pass; pass < std::min(k, to_pass); pass++) {
     const bool first = pass == 0, last = pass == k - 1;
     a.zin = first ? nullptr : ((pass - 1) & 1 ? bufs.zB : bufs.zA);
@@ -489,7 +518,7 @@ int launch_update_first(mpb_handle *h, cudaStream_t s, const mpb_plan *p, const 
   a.meta = p->d_meta;
   a.pat = p->d_pat;
   a.td = p->d_td;
-  a.ctr = h->d_ctr + 1;
+  a.ctr = claim_ctr(h, 1);
   a.boff = p->d_boff;
   a.g = geom_for<T>(p);
   a.g.cap_e = std::min(p->max_tile_ib, kStageCap);
@@ -827,6 +856,8 @@ int mpb_plan_bind_sell(mpb_handle *h, mpb_plan *p, const mpb_sell *sell) {
   MPB_CUDA(cudaMemcpyAsync(cnt.data(), d_cnt, sizeof(int) * n, cudaMemcpyDeviceToHost, h->user));
   MPB_CUDA(cudaStreamSynchronize(h->user));
   cudaFree(d_cnt);
+  p->max_ib_row = 0;
+  for (int64_t r = 0; r < n; r++) p->max_ib_row = std::max(p->max_ib_row, cnt[r]);
   std::vector<int> ib_sp(ns + 1);
   int64_t acc = 0;
   for (int64_t sl = 0; sl < ns; sl++) {
@@ -866,6 +897,53 @@ int mpb_plan_bind_sell(mpb_handle *h, mpb_plan *p, const mpb_sell *sell) {
   MPB_CUDA(cudaMemcpy(p->d_td, td.data(), sizeof(TileDesc) * p->ntiles, cudaMemcpyHostToDevice));
   MPB_CUDA(cudaStreamSynchronize(h->user));
   p->bound = sell;
+  // Gather windows: the distinct column offsets of the row patterns,
+  // clustered into <= kMaxWin row intervals [a, b] (a new window where the
+  // gap to the previous offset exceeds a tile); a pass after the first then
+  // stages z_in rows [lo + a, hi + b) of every window with TMA and gathers
+  // from shared memory.  Needs pattern rows only and tiles starting at a
+  // multiple of 4 rows (16-byte aligned fp32 / fp64 windows at a fixed skew).
+  p->win = WinSet{};
+  bool aligned = true;
+  for (auto &d : td) aligned = aligned && (d.lo % 4 == 0);
+  // off by default (MPB_WIN=1): the larger stages made the last pass slower
+  // on C2 (39.2 us against 37.1 without, 37.2 against 33.0 with the full-tile
+  // path; profiles/r02_notes.md)
+  static const bool no_win = !(std::getenv("MPB_WIN") && std::atoi(std::getenv("MPB_WIN")) != 0);
+  if (!p->large && p->ngeneric == 0 && aligned && p->npat > 0 && !no_win) {
+    std::vector<int> pat(static_cast<size_t>(p->npat) * kPatStride);
+    MPB_CUDA(cudaMemcpy(pat.data(), p->d_pat, sizeof(int) * pat.size(), cudaMemcpyDeviceToHost));
+    std::vector<int> offs;
+    for (int q = 0; q < p->npat; q++) {
+      const int *P = &pat[static_cast<size_t>(q) * kPatStride];
+      for (int u = 0; u < (P[0] & 0xFF); u++) offs.push_back(P[1 + u]);
+    }
+    offs.push_back(0);
+    std::sort(offs.begin(), offs.end());
+    offs.erase(std::unique(offs.begin(), offs.end()), offs.end());
+    WinSet w{};
+    int rows = 0;
+    bool ok = true;
+    for (int o : offs) {
+      if (w.n > 0 && o - w.b[w.n - 1] <= kTileRows) {
+        w.b[w.n - 1] = o;
+        continue;
+      }
+      if (w.n == kMaxWin) {
+        ok = false;
+        break;
+      }
+      w.a[w.n] = w.b[w.n] = o;
+      w.n++;
+    }
+    for (int k = 0; k < w.n; k++) rows += kTileRows + w.b[k] - w.a[k];
+    if (ok && rows <= kWinMaxRows) p->win = w;
+    if (std::getenv("MPB_VERBOSE")) {
+      std::fprintf(stderr, "[mpb] gather windows:");
+      for (int k = 0; k < w.n; k++) std::fprintf(stderr, " [%d, %d]", w.a[k], w.b[k]);
+      std::fprintf(stderr, " (%d rows)%s\n", rows, p->win.n ? "" : " -- not used");
+    }
+  }
   return MPB_OK;
 }
 
@@ -1376,7 +1454,7 @@ static SpmvArgs spmv_args(const mpb_handle *h, const mpb_plan *p, const mpb_csr 
   sa.meta = p->d_meta;
   sa.pat = p->d_pat;
   sa.td = p->d_td;
-  sa.ctr = h->d_ctr + 2;
+  sa.ctr = claim_ctr(h, 2);
   sa.g = spmv_geom(p);
   sa.p = w.p;
   sa.z32 = w.z32;
@@ -1946,7 +2024,7 @@ static int profile_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, c
       a.sp = A->sell->d_sp;
       a.scol = A->sell->d_col;
       a.td = plan->d_td;
-      a.ctr = h->d_ctr + 0;
+      a.ctr = claim_ctr(h, 0);
       a.meta = plan->d_meta;
       a.pat = plan->d_pat;
       a.boff = plan->d_boff;
@@ -1958,6 +2036,10 @@ static int profile_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, c
       a.zin = first ? nullptr : ((pass - 1) & 1 ? zB : zA);
       a.zout = last ? zfinal : (pass & 1 ? zB : zA);
       a.part = last ? w.part : nullptr;
+      if (!dist) {
+        a.win = plan->win;
+        a.win.zlen = static_cast<int>(A->n);
+      }
     };
     if (branch == 0) {
       ApplyBufs<double> bb{w.zA64, w.zB64, w.res64, w.dg64, w.wA64, w.wB64};

@@ -70,6 +70,11 @@ constexpr int kMaxPend = 4;  // owned chunks a producer keeps pending
 #define MPB_WS_BOUNDS_SPMV __launch_bounds__(kWsThreads)
 #endif
 constexpr int kBarConsumers = 1;               // named barrier id among consumers
+// full-tile fast path of the passes after the first (bjac_tile_full); MPB_FAST=0 compiles it out
+#ifndef MPB_FAST
+#define MPB_FAST 1
+#endif
+constexpr bool kFastTiles = MPB_FAST != 0;
 constexpr uint16_t kMetaGeneric = 0xFFFFu;
 
 // ---- row patterns ------------------------------------------------------------
@@ -349,11 +354,13 @@ struct TileGeom {
   int ns;      // shared-memory stages (prefetch depth)
   int cols;    // stages carry a column region (the plan has generic rows)
   int npat;    // row patterns in the table
+  int kib;     // most in-block entries of a row
 };
 
 // Byte offsets of one shared-memory stage.
 struct StageLayout {
   uint32_t col, val, sp, meta, v0, v1, v2, v3, bytes;
+  uint32_t win;  // start of the gather windows (bjac_layout with windows), else == bytes
 };
 __host__ __device__ inline uint32_t al16u(uint32_t b) { return (b + 15u) & ~15u; }
 // v*es: element sizes of up to three row-vector slices [lo, hi) (0: absent)
@@ -378,7 +385,33 @@ __host__ __device__ inline StageLayout stage_layout(int cap_e, int es, int max_s
   L.v3 = off;
   off += v3es ? al16u(static_cast<uint32_t>(kTileRows) * v3es + 16u) : 0u;
   L.bytes = off;
+  L.win = off;
   return L;
+}
+
+// ---- z_in gather windows (passes after the first) --------------------------
+// The plan's row patterns use few distinct column offsets (a 7-point stencil:
+// -n^2, -n, -1, 0, 1, n, n^2), clustered into <= kMaxWin intervals [a, b].
+// A stage then also holds z_in rows [lo + a, hi + b) of each window, copied
+// with TMA, so the pass gathers z_in from shared memory instead of global
+// loads.  Window k's region starts at win_off(k) after the stage's other
+// data; global row g sits at byte  (g - lo) es - floor16(a es)  of it (tiles
+// start at a multiple of 4 rows, so the skew is the same for every tile).
+constexpr int kMaxWin = 6;
+constexpr int kWinMaxRows = 2048;
+struct WinSet {
+  int n;              // windows (0: gather from global memory)
+  int zlen;           // rows of z_in (multi-GPU slabs: own rows + ghosts)
+  int a[kMaxWin], b[kMaxWin];
+};
+__host__ __device__ inline int floor16i(int x) { return x & ~15; }
+__host__ __device__ inline uint32_t win_region_bytes(const WinSet &w, int k, int es) {
+  return al16u(static_cast<uint32_t>((kTileRows + w.b[k] - w.a[k]) * es + 32));
+}
+__host__ __device__ inline uint32_t win_off(const WinSet &w, int k, int es) {
+  uint32_t off = 0;
+  for (int j = 0; j < k; j++) off += win_region_bytes(w, j, es);
+  return off;
 }
 
 // Ring of shared-memory stages filled by the producer warp.
@@ -422,12 +455,15 @@ enum { kFillAll = 0, kFillStatic = 1, kFillDynamic = 2 };
 
 // LAST_USE: bit i set = vector slice vi is read for the last time this
 // iteration (streamed evict-first, like the matrix data)
+// win / zwin (passes after the first): the z_in gather windows of the tile,
+// dynamic data like the vector slices (the previous pass wrote z_in).
 template <typename T, typename V0, typename V1, typename V2, bool IB = false, typename V3 = uint8_t,
           unsigned LAST_USE = 0u, class RG>
 __device__ __forceinline__ void produce(RG &R, int st, const TileDesc *td, int tile, const TileGeom &g,
                                         const StageLayout &L, unsigned char *stage, const int *sp, const int *scol,
                                         const T *sval, const uint16_t *meta, const V0 *v0, const V1 *v1,
-                                        const V2 *v2, const V3 *v3 = nullptr, int part = kFillAll) {
+                                        const V2 *v2, const V3 *v3 = nullptr, int part = kFillAll,
+                                        const WinSet *win = nullptr, const T *zwin = nullptr) {
   TileDesc d;
   if (part != kFillDynamic) {
     d = td[tile];
@@ -449,8 +485,16 @@ __device__ __forceinline__ void produce(RG &R, int st, const TileDesc *td, int t
   const bool cols = g.cols && d.ngen > 0;  // pattern rows rebuild their columns
   const uint32_t sbytes = static_cast<uint32_t>(nent) * ((cols ? 4u : 0u) + sizeof(T)) +
                           window_bytes(sp, d.s0, d.s1 + 1) + window_bytes(meta, d.lo, d.hi);
-  const uint32_t dbytes = window_bytes(v0, d.lo, d.hi) + window_bytes(v1, d.lo, d.hi) + window_bytes(v2, d.lo, d.hi) +
-                          window_bytes(v3, d.lo, d.hi);
+  uint32_t dbytes = window_bytes(v0, d.lo, d.hi) + window_bytes(v1, d.lo, d.hi) + window_bytes(v2, d.lo, d.hi) +
+                    window_bytes(v3, d.lo, d.hi);
+  // gather window k: z_in rows [lo + a_k, hi + b_k) clamped to [0, zlen); its
+  // element g lands at byte (g - lo) es - floor16(a_k es) of the window region
+  constexpr int es = sizeof(T);
+  const int nwin = win != nullptr ? win->n : 0;
+  for (int k = 0; k < nwin; k++) {
+    const int gs = max(d.lo + win->a[k], 0), ge = min(d.hi + win->b[k], win->zlen);
+    if (gs < ge) dbytes += static_cast<uint32_t>(((ge * es + 15) & ~15) - floor16i(gs * es));
+  }
   if (part == kFillAll) mbar_arrive_expect_tx(&R.full[st], sbytes + dbytes);
   if (part == kFillStatic) mbar_expect_tx(&R.full[st], sbytes);
   if (part != kFillDynamic) {
@@ -465,6 +509,16 @@ __device__ __forceinline__ void produce(RG &R, int st, const TileDesc *td, int t
   if (v1 != nullptr) tma_window(stage + L.v1, v1, d.lo, d.hi, &R.full[st], LAST_USE & 2u);
   if (v2 != nullptr) tma_window(stage + L.v2, v2, d.lo, d.hi, &R.full[st], LAST_USE & 4u);
   if (v3 != nullptr) tma_window(stage + L.v3, v3, d.lo, d.hi, &R.full[st], LAST_USE & 8u);
+  uint32_t woff = L.win;
+  for (int k = 0; k < nwin; k++) {
+    const int gs = max(d.lo + win->a[k], 0), ge = min(d.hi + win->b[k], win->zlen);
+    if (gs < ge) {
+      const int src0 = floor16i(gs * es), g0 = d.lo * es + floor16i(win->a[k] * es);
+      bulk_g2s(stage + woff + (src0 - g0), reinterpret_cast<const unsigned char *>(zwin) + src0,
+               static_cast<uint32_t>(((ge * es + 15) & ~15) - src0), &R.full[st]);
+    }
+    woff += win_region_bytes(*win, k, es);
+  }
 }
 
 // Producer loop (producer warp, lane 0): claims tiles from the launch's
@@ -487,6 +541,14 @@ __device__ __forceinline__ void produce(RG &R, int st, const TileDesc *td, int t
 // polled while the producer would otherwise wait for a stage to come back,
 // and blocking after the last claim.  (Owners polling from a consumer warp
 // stall their CTA: measured slower.)
+// L1 prefetch of a tile descriptor (48 bytes, may straddle two lines)
+__device__ __forceinline__ void prefetch_desc(const TileDesc *td, int tile) {
+  if (td == nullptr || tile < 0) return;
+  const char *p = reinterpret_cast<const char *>(td + tile);
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p + sizeof(TileDesc) - 1));
+}
+
 // End markers (one thread): stage st (free) and the next nterm - 1 stages
 // get tile -1, so that each of nterm consumer warps sees one (warp-per-tile
 // kernels consume the stages round-robin, stage i by warp i % nterm).
@@ -507,7 +569,8 @@ __device__ __forceinline__ void ring_end(RG &R, int st, int rnd, int ns, int nte
 
 template <typename F, typename G, class RG>
 __device__ __forceinline__ void producer_loop(RG &R, int ntiles, int ns, unsigned int *ctr, bool prefetch,
-                                              G &&gated, F &&fill, const ChunkCtx &ck, int nterm = 1) {
+                                              G &&gated, F &&fill, const ChunkCtx &ck, int nterm = 1,
+                                              const TileDesc *td = nullptr) {
   const int lane = threadIdx.x & 31;
   int next = blockIdx.x;
   auto claim = [&]() -> int {
@@ -565,16 +628,23 @@ __device__ __forceinline__ void producer_loop(RG &R, int ntiles, int ns, unsigne
     for (int i = 0; i < npre; i++) fill(i, R.tile[i], kFillDynamic);
   int st = npre % ns, rnd = npre / ns;  // stage, and how often it has been filled before
   if (!exhausted) {
+    // one claim ahead: the next tile is claimed (and its descriptor
+    // prefetched) after the current stage's copies are issued, so neither
+    // round trip sits between a free stage and its refill
+    int cur = claim();
+    if (lane == 0) prefetch_desc(td, cur);
     for (;;) {
       if (rnd > 0) {
         if (phead != ptail && !mbar_test(&R.empty[st], (rnd - 1) & 1)) poll_oldest(false);
         mbar_wait_sleep(&R.empty[st], (rnd - 1) & 1);
       }
-      const int tile = claim();
+      const int tile = cur;
       if (lane == 0) R.tile[st] = tile;
       if (tile < 0) break;
       if (lane == 0) fill(st, tile, kFillAll);
       own(tile);
+      cur = claim();
+      if (lane == 0) prefetch_desc(td, cur);
       if (++st == ns) {
         st = 0;
         rnd++;
@@ -590,7 +660,7 @@ __device__ __forceinline__ void producer_loop(RG &R, int ntiles, int ns, unsigne
 // chunk owners: the same walk as producer_loop.
 template <typename F, typename G, class RG>
 __device__ __forceinline__ void producer_loop_single(RG &R, int ntiles, int ns, unsigned int *ctr, bool prefetch,
-                                              G &&gated, F &&fill, int nterm = 1) {
+                                              G &&gated, F &&fill, int nterm = 1, const TileDesc *td = nullptr) {
   int next = blockIdx.x;
   auto claim = [&]() -> int {
     if (ctr != nullptr) {
@@ -629,15 +699,19 @@ __device__ __forceinline__ void producer_loop_single(RG &R, int ntiles, int ns, 
     return;
   }
   int st = npre % ns, rnd = npre / ns;  // stage, and how often it has been filled before
+  int cur = claim();  // one claim ahead (producer_loop)
+  prefetch_desc(td, cur);
   for (;;) {
     if (rnd > 0) mbar_wait_sleep(&R.empty[st], (rnd - 1) & 1);
-    const int tile = claim();
+    const int tile = cur;
     R.tile[st] = tile;
     if (tile < 0) {
       ring_end(R, st, rnd, ns, nterm);
       return;
     }
     fill(st, tile, kFillAll);
+    cur = claim();
+    prefetch_desc(td, cur);
     if (++st == ns) {
       st = 0;
       rnd++;
@@ -710,6 +784,7 @@ struct PassArgs {
   int gate;              // 0: st->branch; 1: also skip when the fused update ran this first pass;
                          // 2: st->upd_branch (fused update: the step inside may change st->branch)
   int pdl;               // host side: launch with programmatic serialization
+  WinSet win;            // z_in gather windows (passes after the first; n == 0: none)
 };
 
 template <typename T>
@@ -818,10 +893,13 @@ struct PassRow {
 // A pass up to its first inner sweep for one row: res = r - A z_in (all
 // slots, stored order), d, w = res / d (written to the tile's s_w).
 // GEN: the plan has generic rows (no row pattern); false compiles their path out
-template <typename T, bool FIRST, int KS, bool GEN>
+// zb (windows): the stage base + tid * sizeof(T); z_in of slot u of pattern
+// pid at zb + s_zoff[pid * KS + u], the row's own z_in at zb + s_zoff[kPatMax * KS]
+template <typename T, bool FIRST, int KS, bool GEN, bool WIN = false>
 __device__ __forceinline__ void pass_row_init(PassRow<T> &q, const PassArgs<T> &a, const TileDesc &d, int tid,
                                               const int *col, const T *val, const int *spp, const uint16_t *mt,
-                                              const double *r64t, const T *rTt, const int *s_pat, T *s_w) {
+                                              const double *r64t, const T *rTt, const int *s_pat, T *s_w,
+                                              const unsigned char *zb = nullptr, const int *s_zoff = nullptr) {
   const int row = d.lo + tid;
   q.res = T(0);
   q.dd = T(1);
@@ -839,7 +917,7 @@ __device__ __forceinline__ void pass_row_init(PassRow<T> &q, const PassArgs<T> &
   q.m = mt[tid];
   const T rv = r64t != nullptr ? narrow_checked(a, r64t[tid], row, FIRST) : rTt[tid];
   const T *zr = FIRST ? nullptr : a.zin + row;
-  if (!FIRST) q.zown = __ldg(zr);
+  if (!FIRST) q.zown = (WIN && zb != nullptr) ? *reinterpret_cast<const T *>(zb + s_zoff[kPatMax * KS]) : __ldg(zr);
   if (!GEN || q.m != kMetaGeneric) {
     q.P = s_pat + meta_pid(q.m) * kPatStride;
     const int hdr = q.P[0], len = pat_len(hdr);
@@ -848,10 +926,19 @@ __device__ __forceinline__ void pass_row_init(PassRow<T> &q, const PassArgs<T> &
     T az = T(0);
     if (!FIRST) {
       T v[KS], g[KS];
+      if (WIN && zb != nullptr) {
+        const int *zo = s_zoff + meta_pid(q.m) * KS;
 #pragma unroll
-      for (int u = 0; u < KS; u++) {
-        v[u] = u < len ? val[q.base + 32 * u] : T(0);
-        g[u] = __ldg(zr + q.P[1 + u]);
+        for (int u = 0; u < KS; u++) {
+          v[u] = u < len ? val[q.base + 32 * u] : T(0);
+          g[u] = *reinterpret_cast<const T *>(zb + zo[u]);
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < KS; u++) {
+          v[u] = u < len ? val[q.base + 32 * u] : T(0);
+          g[u] = __ldg(zr + q.P[1 + u]);
+        }
       }
 #pragma unroll
       for (int u = 0; u < KS; u++)
@@ -908,17 +995,21 @@ __device__ __forceinline__ void deferred_tree_finish(DeferredTree &dt, double *p
   dt.tile = -1;
 }
 
-template <typename T, bool FIRST, bool LAST, int KS, bool GEN, int RPT = kRowsPerThread>
+template <typename T, bool FIRST, bool LAST, int KS, bool GEN, int RPT = kRowsPerThread, bool WIN = false>
 __device__ __forceinline__ void bjac_tile_body(const PassArgs<T> &a, int tile, const TileDesc &d, const int *col,
                                                const T *val, const int *spp, const uint16_t *mt, const double *r64t,
                                                const T *rTt, const int *s_pat, T *s_w, double *ws,
-                                               DeferredTree &dt) {
+                                               DeferredTree &dt, const unsigned char *sb = nullptr,
+                                               const int *s_zoff = nullptr) {
   const bool defer = MPB_DEFER_TREE && LAST && a.part != nullptr && a.t >= 2;
   constexpr int NC = kTileThreads / RPT;
   PassRow<T> q[RPT];
 #pragma unroll
-  for (int k = 0; k < RPT; k++)
-    pass_row_init<T, FIRST, KS, GEN>(q[k], a, d, threadIdx.x + k * NC, col, val, spp, mt, r64t, rTt, s_pat, s_w);
+  for (int k = 0; k < RPT; k++) {
+    const int tid = threadIdx.x + k * NC;
+    pass_row_init<T, FIRST, KS, GEN, WIN>(q[k], a, d, tid, col, val, spp, mt, r64t, rTt, s_pat, s_w,
+                                          (WIN && sb != nullptr) ? sb + tid * sizeof(T) : nullptr, s_zoff);
+  }
   for (int s = 1; s < a.t; s++) {  // inner sweeps, the tile's w in shared memory
     named_sync(kBarConsumers, NC);
     if (defer && s == 1) deferred_tree_finish(dt, a.part, ws);
@@ -1036,17 +1127,116 @@ __device__ __forceinline__ void bjac_first_body(const PassArgs<T> &a, const Tile
   }
 }
 
+// Full staged tile of a pass after the first, pattern rows only, one row per
+// consumer thread, tile start a multiple of 32 (so thread tid's row sits in
+// the tile's slice tid / 32 at lane tid % 32): the same arithmetic as
+// bjac_tile_body without its per-row validity branches, with the inner
+// sweep unrolled to KI in-block entries.
+template <typename T, bool LAST, int KS, int KI, bool WIN = false>
+__device__ __forceinline__ void bjac_tile_full(const PassArgs<T> &a, int tile, const TileDesc &d, const T *val,
+                                               const int *spp, const uint16_t *mt, const double *r64t,
+                                               const int *s_pat, T *s_w, double *ws,
+                                               const unsigned char *sb = nullptr, const int *s_zoff = nullptr) {
+  const int tid = threadIdx.x, row = d.lo + tid;
+  const int base = spp[tid >> 5] - d.e0 + (tid & 31);
+  const uint16_t m = mt[tid];
+  const int *P = s_pat + meta_pid(m) * kPatStride;
+  const int hdr = P[0], len = pat_len(hdr);
+  const T *zr = a.zin + row;
+  T v[KS], g[KS], zown;
+  if (WIN) {  // z_in from the stage's gather windows
+    const unsigned char *zb = sb + tid * sizeof(T);
+    const int *zo = s_zoff + meta_pid(m) * KS;
+#pragma unroll
+    for (int u = 0; u < KS; u++) {
+      v[u] = val[base + 32 * u];
+      g[u] = *reinterpret_cast<const T *>(zb + zo[u]);
+    }
+    zown = *reinterpret_cast<const T *>(zb + s_zoff[kPatMax * KS]);
+  } else {
+#pragma unroll
+    for (int u = 0; u < KS; u++) {
+      v[u] = val[base + 32 * u];       // slots past len: never summed (the stage extends past them)
+      g[u] = __ldg(zr + P[1 + u]);     // table offsets past len are 0
+    }
+    zown = __ldg(zr);
+  }
+  T az = T(0);
+#pragma unroll
+  for (int u = 0; u < KS; u++)
+    if (u < len) az = add_rn(az, mul_rn(v[u], g[u]));
+  const T dd = val[base + 32 * pat_dpos(hdr)];
+  const T res = sub_rn(narrow_or_copy<T>(r64t[tid]), az);
+  T w = div_rn(res, dd);
+  s_w[tid] = w;
+  const int i0 = meta_i0(m), i1 = meta_i1(m);
+  for (int s = 1; s < a.t; s++) {
+    named_sync(kBarConsumers, kTileThreads);
+    T acc = T(0);
+#pragma unroll
+    for (int j = 0; j < KI; j++) {
+      const int jj = i0 + j;
+      if (jj < i1) acc = add_rn(acc, mul_rn(val[base + 32 * jj], s_w[tid + P[1 + jj]]));
+    }
+    named_sync(kBarConsumers, kTileThreads);
+    w = add_rn(w, div_rn(sub_rn(res, acc), dd));
+    s_w[tid] = w;
+  }
+  const T zo = add_rn(zown, w);
+  if (a.zout != nullptr) st_keep(a.zout + row, zo);
+  if (a.zout64 != nullptr) a.zout64[row] = static_cast<double>(zo);
+  if (LAST && a.part != nullptr) {
+    double prod[1] = {__dmul_rn(r64t[tid], static_cast<double>(zo))};
+    const double tot = tile_tree_rows<double, 1>(prod, ws, kBarConsumers);
+    if (threadIdx.x == 0) put_part(a.part + tile, tot);
+  }
+}
+
 template <typename T, bool FIRST, bool R64>
 __host__ __device__ inline StageLayout bjac_layout(const TileGeom &g) {
   // v0: the residual slice
   return stage_layout(g.cap_e, sizeof(T), g.max_sl, g.cols != 0, true, R64 ? 8 : sizeof(T), 0, 0);
+}
+// the same plus the z_in gather windows (passes after the first)
+template <typename T, bool FIRST, bool R64>
+__host__ __device__ inline StageLayout bjac_layout_win(const TileGeom &g, const WinSet &w) {
+  StageLayout L = bjac_layout<T, FIRST, R64>(g);
+  L.win = L.bytes;
+  L.bytes += win_off(w, w.n, sizeof(T));
+  return L;
+}
+
+// Per-CTA table of gather byte offsets (relative to stage base + tid * es):
+// s_zoff[pid * KS + u] for slot u of pattern pid (slots past the pattern's
+// length point at the row's own z_in), s_zoff[kPatMax * KS] for the row itself.
+template <typename T, int KS>
+__device__ __forceinline__ void load_zoff(int *s_zoff, const int *pat, int npat, const WinSet &w,
+                                          const StageLayout &L) {
+  constexpr int es = sizeof(T);
+  auto zoff = [&](int o) {
+    int k = 0;
+    while (k + 1 < w.n && o > w.b[k]) k++;
+    return static_cast<int>(L.win + win_off(w, k, es)) - floor16i(w.a[k] * es) + o * es;
+  };
+  for (int idx = threadIdx.x; idx <= npat * KS; idx += blockDim.x) {
+    if (idx == npat * KS) {
+      s_zoff[kPatMax * KS] = zoff(0);
+      continue;
+    }
+    const int q = idx / KS, u = idx % KS;
+    const int hdr = __ldg(pat + q * kPatStride);
+    s_zoff[idx] = zoff(u < pat_len(hdr) ? __ldg(pat + q * kPatStride + 1 + u) : 0);
+  }
 }
 
 // Persistent, warp-specialised fused pass.  TWO: the two-level dot-sum order
 // (chunk owners in the producer warp); false compiles that machinery out.
 // RPT: tile rows per consumer thread (kTileThreads / RPT consumer threads +
 // the producer warp per CTA)
-template <typename T, bool FIRST, bool LAST, bool R64, int KS, bool GEN, bool TWO = false, int RPT = kRowsPerThread>
+// WIN: z_in gathered from the stage's gather windows (passes after the first,
+// plans with windows; a.win.n > 0)
+template <typename T, bool FIRST, bool LAST, bool R64, int KS, bool GEN, bool TWO = false, int RPT = kRowsPerThread,
+          bool WIN = false>
 __global__ void __launch_bounds__(kTileThreads / RPT + 32) k_bjac_tile(const PassArgs<T> a) {
   constexpr int NC = kTileThreads / RPT;
   constexpr int kFinRpt = NC >= kFinThreads ? 1 : kFinThreads / NC;
@@ -1055,13 +1245,16 @@ __global__ void __launch_bounds__(kTileThreads / RPT + 32) k_bjac_tile(const Pas
   __shared__ T s_w[kTileRows];
   __shared__ double ws[32];
   __shared__ int s_pat[kPatMax * kPatStride];
+  __shared__ int s_zoff[WIN ? kPatMax * KS + 1 : 1];
 #ifdef MPB_TIMELINE
   const unsigned long long t_entry = globaltimer_now();
 #endif
   const int ns = a.g.ns;
   constexpr bool kIB = FIRST && !LAST;  // first pass alone: in-block entries only
-  const StageLayout L = bjac_layout<T, FIRST, R64>(a.g);
+  static_assert(!(WIN && FIRST), "gather windows serve the passes after the first");
+  const StageLayout L = WIN ? bjac_layout_win<T, FIRST, R64>(a.g, a.win) : bjac_layout<T, FIRST, R64>(a.g);
   load_patterns(s_pat, a.pat, a.g.npat);
+  if (WIN) load_zoff<T, KS>(s_zoff, a.pat, a.g.npat, a.win, L);
   ring_init(R, ns, NC);
   if (threadIdx.x >= NC) {  // producer warp
     using RT = typename std::conditional<R64, double, T>::type;
@@ -1075,13 +1268,14 @@ __global__ void __launch_bounds__(kTileThreads / RPT + 32) k_bjac_tile(const Pas
                                                static_cast<const uint8_t *>(nullptr), part);
       else
         produce<T, RT, uint8_t, uint8_t>(R, st, a.td, tile, a.g, L, smem + st * L.bytes, a.sp, a.scol, a.sval,
-                                         a.meta, rsrc, nullptr, nullptr, static_cast<const uint8_t *>(nullptr), part);
+                                         a.meta, rsrc, nullptr, nullptr, static_cast<const uint8_t *>(nullptr), part,
+                                         WIN ? &a.win : nullptr, a.zin);
     };
     auto gated = [&]() { return gated_off(a); };
     if (TWO && ck.csum != nullptr && ck.poll)
-      producer_loop(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, gated, fill, ck);
+      producer_loop(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, gated, fill, ck, 1, a.td);
     else if (threadIdx.x == NC)
-      producer_loop_single(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, gated, fill);
+      producer_loop_single(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, gated, fill, 1, a.td);
     else
       pdl_wait();
     if (gated_off(a)) return;
@@ -1126,12 +1320,23 @@ __global__ void __launch_bounds__(kTileThreads / RPT + 32) k_bjac_tile(const Pas
         }
       } else {
         const int *col = scols ? reinterpret_cast<const int *>(sb + L.col) : a.scol + d.e0;
-        if (ok) {
-          bjac_tile_body<T, FIRST, LAST, KS, GEN, RPT>(a, tile, d, col, reinterpret_cast<const T *>(sb + L.val),
+        constexpr bool kFast = !FIRST && !GEN && RPT == 1 && R64 && !MPB_DEFER_TREE;
+        if (kFast && ok && kFastTiles && d.hi - d.lo == kTileRows && (d.lo & 31) == 0 && a.g.kib <= 7) {
+          const T *val = reinterpret_cast<const T *>(sb + L.val);
+          const int *spp = staged(sb + L.sp, a.sp, d.s0, d.s1 + 1);
+          const uint16_t *mt = staged(sb + L.meta, a.meta, d.lo, d.hi);
+          const double *r64t = staged(sb + L.v0, a.r64, d.lo, d.hi);
+          if (a.g.kib <= 3)
+            bjac_tile_full<T, LAST, KS, 3, WIN>(a, tile, d, val, spp, mt, r64t, s_pat, s_w, ws, sb, s_zoff);
+          else
+            bjac_tile_full<T, LAST, KS, 7, WIN>(a, tile, d, val, spp, mt, r64t, s_pat, s_w, ws, sb, s_zoff);
+        } else if (ok) {
+          bjac_tile_body<T, FIRST, LAST, KS, GEN, RPT, WIN>(a, tile, d, col, reinterpret_cast<const T *>(sb + L.val),
                                              staged(sb + L.sp, a.sp, d.s0, d.s1 + 1),
                                              staged(sb + L.meta, a.meta, d.lo, d.hi),
                                              R64 ? staged(sb + L.v0, a.r64, d.lo, d.hi) : nullptr,
-                                             R64 ? nullptr : staged(sb + L.v0, a.rT, d.lo, d.hi), s_pat, s_w, ws, dt);
+                                             R64 ? nullptr : staged(sb + L.v0, a.rT, d.lo, d.hi), s_pat, s_w, ws, dt,
+                                             sb, s_zoff);
         } else {
           bjac_tile_body<T, FIRST, LAST, KS, GEN, RPT>(a, tile, d, col, a.sval + d.e0, a.sp + d.s0, a.meta + d.lo,
                                              R64 ? a.r64 + d.lo : nullptr, R64 ? nullptr : a.rT + d.lo, s_pat, s_w,
@@ -1360,9 +1565,9 @@ __global__ void __launch_bounds__(kWtWarps * 32 + 32) k_bjac_wt(const PassArgs<T
     };
     auto gated = [&]() { return gated_off(a); };
     if (TWO && ck.csum != nullptr && ck.poll)
-      producer_loop(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, gated, fill, ck, kWtWarps);
+      producer_loop(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, gated, fill, ck, kWtWarps, a.td);
     else if (threadIdx.x == NC)
-      producer_loop_single(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, gated, fill, kWtWarps);
+      producer_loop_single(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, gated, fill, kWtWarps, a.td);
     else
       pdl_wait();
     if (gated_off(a)) return;
@@ -1708,9 +1913,9 @@ __global__ void MPB_WS_BOUNDS_SPMV k_spmv_pq(const SpmvArgs a) {
     };
     auto gated = [&]() { return a.st->done != 0; };
     if (TWO && ck.poll)
-      producer_loop(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, gated, fill, ck);
+      producer_loop(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, gated, fill, ck, 1, a.td);
     else if (threadIdx.x == kConsumers)
-      producer_loop_single(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, gated, fill);
+      producer_loop_single(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, gated, fill, 1, a.td);
     else
       pdl_wait();
     if (a.st->done) return;
@@ -1837,9 +2042,9 @@ __device__ __forceinline__ void update_first_body(const PassArgs<T> &a, double *
     };
     auto gated = [&]() { return gated_off(a); };
     if (TWO && ck.poll)
-      producer_loop(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, gated, fill, ck);
+      producer_loop(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, gated, fill, ck, 1, a.td);
     else if (threadIdx.x == kConsumers)
-      producer_loop_single(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, gated, fill);
+      producer_loop_single(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, gated, fill, 1, a.td);
     else
       pdl_wait();
     if (gated_off(a)) return;
@@ -1933,9 +2138,9 @@ __global__ void __launch_bounds__(kWtWarps * 32 + 32)
     };
     auto gated = [&]() { return gated_off(a); };
     if (TWO && ck.poll)
-      producer_loop(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, gated, fill, ck, kWtWarps);
+      producer_loop(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, gated, fill, ck, kWtWarps, a.td);
     else if (threadIdx.x == NC)
-      producer_loop_single(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, gated, fill, kWtWarps);
+      producer_loop_single(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, gated, fill, kWtWarps, a.td);
     else
       pdl_wait();
     if (gated_off(a)) return;
