@@ -1138,11 +1138,13 @@ __device__ __forceinline__ void bjac_tile_full(const PassArgs<T> &a, int tile, c
                                                const int *s_pat, T *s_w, double *ws,
                                                const unsigned char *sb = nullptr, const int *s_zoff = nullptr) {
   const int tid = threadIdx.x, row = d.lo + tid;
-  const int base = spp[tid >> 5] - d.e0 + (tid & 31);
-  const uint16_t m = mt[tid];
+  const bool valid = row < d.hi;  // warp-uniform: tiles of a multiple of 32 rows
+  const int ti = valid ? tid : 0;
+  const int base = spp[ti >> 5] - d.e0 + (ti & 31);
+  const uint16_t m = mt[ti];
   const int *P = s_pat + meta_pid(m) * kPatStride;
   const int hdr = P[0], len = pat_len(hdr);
-  const T *zr = a.zin + row;
+  const T *zr = a.zin + d.lo + ti;
   T v[KS], g[KS], zown;
   if (WIN) {  // z_in from the stage's gather windows
     const unsigned char *zb = sb + tid * sizeof(T);
@@ -1166,9 +1168,9 @@ __device__ __forceinline__ void bjac_tile_full(const PassArgs<T> &a, int tile, c
   for (int u = 0; u < KS; u++)
     if (u < len) az = add_rn(az, mul_rn(v[u], g[u]));
   const T dd = val[base + 32 * pat_dpos(hdr)];
-  const T res = sub_rn(narrow_or_copy<T>(r64t[tid]), az);
+  const T res = sub_rn(narrow_or_copy<T>(r64t[ti]), az);
   T w = div_rn(res, dd);
-  s_w[tid] = w;
+  s_w[tid] = w;  // (rows past the tile: never read by the tile's rows)
   const int i0 = meta_i0(m), i1 = meta_i1(m);
   for (int s = 1; s < a.t; s++) {
     named_sync(kBarConsumers, kTileThreads);
@@ -1183,10 +1185,10 @@ __device__ __forceinline__ void bjac_tile_full(const PassArgs<T> &a, int tile, c
     s_w[tid] = w;
   }
   const T zo = add_rn(zown, w);
-  if (a.zout != nullptr) st_keep(a.zout + row, zo);
-  if (a.zout64 != nullptr) a.zout64[row] = static_cast<double>(zo);
+  if (valid && a.zout != nullptr) st_keep(a.zout + row, zo);
+  if (valid && a.zout64 != nullptr) a.zout64[row] = static_cast<double>(zo);
   if (LAST && a.part != nullptr) {
-    double prod[1] = {__dmul_rn(r64t[tid], static_cast<double>(zo))};
+    double prod[1] = {valid ? __dmul_rn(r64t[ti], static_cast<double>(zo)) : 0.0};
     const double tot = tile_tree_rows<double, 1>(prod, ws, kBarConsumers);
     if (threadIdx.x == 0) put_part(a.part + tile, tot);
   }
@@ -1321,7 +1323,7 @@ __global__ void __launch_bounds__(kTileThreads / RPT + 32) k_bjac_tile(const Pas
       } else {
         const int *col = scols ? reinterpret_cast<const int *>(sb + L.col) : a.scol + d.e0;
         constexpr bool kFast = !FIRST && !GEN && RPT == 1 && R64 && !MPB_DEFER_TREE;
-        if (kFast && ok && kFastTiles && d.hi - d.lo == kTileRows && (d.lo & 31) == 0 && a.g.kib <= 7) {
+        if (kFast && ok && kFastTiles && ((d.hi - d.lo) & 31) == 0 && (d.lo & 31) == 0 && a.g.kib <= 7) {
           const T *val = reinterpret_cast<const T *>(sb + L.val);
           const int *spp = staged(sb + L.sp, a.sp, d.s0, d.s1 + 1);
           const uint16_t *mt = staged(sb + L.meta, a.meta, d.lo, d.hi);
@@ -2021,6 +2023,53 @@ __host__ __device__ inline StageLayout update_first_layout(const TileGeom &g) {
   return stage_layout(g.cap_e, sizeof(T), g.max_sl, g.cols != 0, true, 8, 8, 8, 8);
 }
 
+// Staged tile of the fused update with a multiple of 32 rows at a 32-row-
+// aligned start, pattern rows only (update_first_body's arithmetic without
+// per-row validity branches; the in-block sweep unrolled to KI entries).
+template <typename T, int KI>
+__device__ __forceinline__ void update_first_full(const PassArgs<T> &a, int tile, const TileDesc &d, double alpha,
+                                                  double *x, double *r, const double *xs, const double *ps,
+                                                  const double *qs, const double *rs, const T *val, const int *spp,
+                                                  const uint16_t *mt, const int *s_pat, T *s_w, double *ws) {
+  const int tid = threadIdx.x, row = d.lo + tid;
+  const bool valid = row < d.hi;  // warp-uniform
+  const int ti = valid ? tid : 0;
+  double sq = 0.0;
+  T rv = T(0);
+  if (valid) {
+    st_evict_first(x + row, __dadd_rn(xs[ti], __dmul_rn(alpha, ps[ti])));  // (read again by the next update only)
+    const double rn = __dsub_rn(rs[ti], __dmul_rn(alpha, qs[ti]));
+    r[row] = rn;
+    sq = __dmul_rn(rn, rn);
+    rv = narrow_checked(a, rn, row, true);
+  }
+  const uint16_t m = mt[ti];
+  const int i0 = meta_i0(m), nib = meta_i1(m) - i0;
+  const int *P = s_pat + meta_pid(m) * kPatStride;
+  const int base = spp[ti >> 5] - d.ie0 + (ti & 31);
+  const T dd = val[base + 32 * (pat_dpos(P[0]) - i0)];
+  P += 1 + i0;
+  T w = div_rn(rv, dd);
+  {
+    double v[1] = {sq};
+    const double tot = tile_tree_rows<double, 1>(v, ws, kBarConsumers);  // (its barriers also order s_w)
+    if (threadIdx.x == 0) put_part(a.part + tile, tot);
+  }
+  s_w[tid] = w;
+  for (int s = 1; s < a.t; s++) {
+    named_sync(kBarConsumers, kTileThreads);
+    T acc = T(0);
+#pragma unroll
+    for (int j = 0; j < KI; j++)
+      if (j < nib) acc = add_rn(acc, mul_rn(val[base + 32 * j], s_w[tid + P[j]]));
+    named_sync(kBarConsumers, kTileThreads);
+    w = add_rn(w, div_rn(sub_rn(rv, acc), dd));
+    s_w[tid] = w;
+  }
+  if (valid && a.zout != nullptr) st_keep(a.zout + row, w);
+  if (valid && a.zout64 != nullptr) a.zout64[row] = static_cast<double>(w);
+}
+
 template <typename T, bool GEN, bool TWO>
 __device__ __forceinline__ void update_first_body(const PassArgs<T> &a, double *x, const double *p, const double *q,
                                                   double *r) {
@@ -2061,6 +2110,20 @@ __device__ __forceinline__ void update_first_body(const PassArgs<T> &a, double *
       const TileDesc d = R.desc[st];
       const unsigned char *sb = smem + st * L.bytes;
       const bool ok = R.ok[st] != 0;
+      if (!GEN && kRowsPerThread == 1 && kFastTiles && ok && ((d.hi - d.lo) & 31) == 0 && (d.lo & 31) == 0 &&
+          a.g.kib <= 7) {
+        const double *xs = staged(sb + L.v1, x, d.lo, d.hi), *ps = staged(sb + L.v2, p, d.lo, d.hi);
+        const double *qs = staged(sb + L.v3, q, d.lo, d.hi), *rs = staged(sb + L.v0, r, d.lo, d.hi);
+        const T *val = reinterpret_cast<const T *>(sb + L.val);
+        const int *spp = staged(sb + L.sp, a.ib_sp, d.s0, d.s1 + 1);
+        const uint16_t *mt = staged(sb + L.meta, a.meta, d.lo, d.hi);
+        if (a.g.kib <= 3)
+          update_first_full<T, 3>(a, tile, d, alpha, x, r, xs, ps, qs, rs, val, spp, mt, s_pat, s_w, ws);
+        else
+          update_first_full<T, 7>(a, tile, d, alpha, x, r, xs, ps, qs, rs, val, spp, mt, s_pat, s_w, ws);
+        ring_release(R, st);
+        continue;
+      }
       double sq[kRowsPerThread];
       T rv[kRowsPerThread];
 #pragma unroll
