@@ -294,6 +294,18 @@ int mpb_comm_unique_id(void *h_id);
 int mpb_comm_create(mpb_handle *h, int rank, int nranks, const void *h_id,
                     mpb_comm **out);
 int mpb_comm_destroy(mpb_comm *c);
+/* In-process group of nranks slab ranks on ONE device (tests of the
+ * multi-GPU path with fewer GPUs than ranks): the ranks' host threads call
+ * mpb_pcg_solve_dist concurrently with comms from mpb_comm_create_local;
+ * every rank's work goes to the group's one stream and each halo exchange /
+ * all-reduce is a host barrier at which rank 0 enqueues plain copies and a
+ * rank-ordered sum for all ranks.  No kernel waits on another rank. */
+int mpb_local_group_create(int device, int nranks, void **out);
+int mpb_local_group_destroy(void *group);
+/* the group's stream (cudaStream_t): the ranks' handles and their callers'
+ * copies use it, so nothing orders through the legacy default stream */
+void *mpb_local_group_stream(void *group);
+int mpb_comm_create_local(void *group, int rank, mpb_comm **out);
 int64_t mpb_solve_workspace_bytes_dist(const mpb_plan *plan, int64_t n,
                                        int64_t ghosts);
 /* mpb_pcg_solve on this rank's slab: b has n entries, x has n + ghosts

@@ -44,7 +44,8 @@ EXPORTED = (
     "mpb_profile_iteration_dist", "mpb_plan_layout_info", "mpb_stencil_nnz",
     "mpb_assemble_stencil", "mpb_splitmix64_uniform",
     "mpb_row_features", "mpb_tau_histogram", "mpb_vector_stats",
-    "mpb_first_violations",
+    "mpb_first_violations", "mpb_local_group_create", "mpb_local_group_destroy", "mpb_local_group_stream",
+    "mpb_comm_create_local",
 )
 
 
@@ -153,6 +154,10 @@ def _declare(L):
         "mpb_comm_unique_id": ([_P], C.c_int),
         "mpb_comm_create": ([_P, C.c_int, C.c_int, _P, C.POINTER(_P)], C.c_int),
         "mpb_comm_destroy": ([_P], C.c_int),
+        "mpb_local_group_create": ([C.c_int, C.c_int, C.POINTER(_P)], C.c_int),
+        "mpb_local_group_destroy": ([_P], C.c_int),
+        "mpb_local_group_stream": ([_P], _P),
+        "mpb_comm_create_local": ([_P, C.c_int, C.POINTER(_P)], C.c_int),
         "mpb_solve_workspace_bytes_dist": ([_P, _I64, _I64], C.c_int64),
         "mpb_pcg_solve_dist": ([_P, _P, C.POINTER(MpbHalo), _P, C.POINTER(MpbCsr), C.POINTER(MpbSolveOptions), _P,
                                 _P, _P, _P, _P, _P, _P, _I64, C.POINTER(MpbSolveResult)], C.c_int),
@@ -194,16 +199,27 @@ class Handle:
 
     _per_device: dict = {}
 
-    def __init__(self, device: int):
+    def __init__(self, device: int, stream=None):
+        """stream: a raw cudaStream_t for a private handle (None: torch's
+        current stream, the per-device handle of Handle.get)."""
         import torch
         self.device = device
         self.lib = load()
         h = C.c_void_p()
         with torch.cuda.device(device):
-            stream = torch.cuda.current_stream(device).cuda_stream
+            if stream is None:
+                stream = torch.cuda.current_stream(device).cuda_stream
             check(self.lib.mpb_create(device, C.c_void_p(stream), C.byref(h)),
                   "mpb_create")
         self.ptr = h
+
+    def __del__(self):
+        try:
+            if self.ptr and self not in Handle._per_device.values():
+                self.lib.mpb_destroy(self.ptr)
+                self.ptr = C.c_void_p()
+        except Exception:  # interpreter shutdown
+            pass
 
     @classmethod
     def get(cls, device=None) -> "Handle":

@@ -11,7 +11,9 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <condition_variable>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "../../include/mpbjac.h"
@@ -29,6 +31,14 @@ constexpr int kDefaultGraphIters = 16;  // iterations per while-loop body (measu
 constexpr int kEltThreads = 256;
 
 inline int status_of(cudaError_t e) { return e == cudaSuccess ? MPB_OK : static_cast<int>(e); }
+// MPB_DEBUG_SYNC=1: synchronise the device after every launch and name it
+inline void debug_sync(int line) {
+  static const bool on = std::getenv("MPB_DEBUG_SYNC") != nullptr;
+  if (!on) return;
+  std::fprintf(stderr, "[mpb sync] launch at mpbjac.cu:%d ...", line);
+  const cudaError_t e = cudaDeviceSynchronize();
+  std::fprintf(stderr, " done (%d)\n", static_cast<int>(e));
+}
 
 #define MPB_CUDA(expr)                           \
   do {                                           \
@@ -41,6 +51,7 @@ inline int status_of(cudaError_t e) { return e == cudaSuccess ? MPB_OK : static_
     (h)->launches++;                             \
     cudaError_t e_ = cudaGetLastError();         \
     if (e_ != cudaSuccess) return status_of(e_); \
+    debug_sync(__LINE__);                        \
   } while (0)
 
 struct GraphKey {
@@ -73,9 +84,58 @@ struct mpb_plan {
   WinSet win;               // z_in gather windows of the passes after the first (n == 0: none)
 };
 
+// In-process group of slab ranks on one GPU (mpb_local_group_create): the
+// ranks' host threads enqueue onto ONE shared stream, and every
+// communication point (halo exchange, scalar-step all-reduce) is a host
+// barrier at which rank 0 enqueues the whole exchange -- plain copies
+// between the ranks' buffers, a rank-ordered sum kernel -- for all ranks.
+// Nothing on the device waits on another rank: the stream serialises every
+// rank's kernels.  It runs the multi-GPU code path (slabs, ghosts, halos,
+// all-reduced scalar steps) with more ranks than GPUs, for tests.
+struct LocalGroup {
+  int nranks;
+  cudaStream_t stream;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  long long generation = 0;
+  // per-rank arguments of the current communication point
+  struct Slot {
+    void *buf;
+    int es;
+    int64_t n;
+    mpb_halo halo;
+    mpb::SolverState *st;
+  };
+  std::vector<Slot> slot;
+  bool failed = false;  // a rank returned an error: the others leave their barriers
+  // false: the group failed (the caller returns MPB_ERR_COMM)
+  bool barrier(int rank = -1, const char *what = "") {
+    static const bool dbg = std::getenv("MPB_DEBUG_LOCAL") != nullptr;
+    if (dbg) std::fprintf(stderr, "[mpb local] rank %d barrier %s gen %lld\n", rank, what, generation);
+    std::unique_lock<std::mutex> lk(mu);
+    if (failed) return false;
+    const long long gen = generation;
+    if (++arrived == nranks) {
+      arrived = 0;
+      generation++;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return generation != gen || failed; });
+    }
+    return !failed;
+  }
+  void fail() {
+    std::lock_guard<std::mutex> lk(mu);
+    failed = true;
+    cv.notify_all();
+  }
+};
+
 struct mpb_comm {
   mpb::ncclComm_t comm;
   int rank, nranks;
+  LocalGroup *grp = nullptr;  // in-process group (no NCCL)
 };
 
 struct mpb_sell {
@@ -186,6 +246,28 @@ int num_sms() {
   return g_num_sms;
 }
 
+// Opt a kernel into the largest dynamic shared memory it may use, once.
+// The launch paths never lower the attribute again (probing by setting it
+// per candidate size raced with launches from other host threads: an
+// in-process slab group launches from one thread per rank).
+template <typename K>
+void smem_opt_in(K kernel) {
+  static std::mutex mu;
+  static std::vector<const void *> done;
+  std::lock_guard<std::mutex> lk(mu);
+  const void *key = reinterpret_cast<const void *>(kernel);
+  for (const void *k : done)
+    if (k == key) return;
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaFuncAttributes fa{};
+  cudaFuncGetAttributes(&fa, kernel);
+  const int mx = optin - static_cast<int>(fa.sharedSizeBytes);
+  if (mx > 0) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  done.push_back(key);
+}
+
 // Stage count for a persistent tile kernel: the deepest ring (<= kMaxStages)
 // that keeps the co-resident CTA count registers and threads allow
 // (MPB_STAGES=n forces n; MPB_VERBOSE=1 reports the choice).
@@ -194,7 +276,7 @@ int pick_stages(K kernel, uint32_t stage_bytes, int threads = kWsThreads) {
   auto per_sm = [&](int ns) {
     const uint32_t dyn = ns * stage_bytes;
     if (dyn > 220u * 1024u) return 0;
-    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn));
+    smem_opt_in(kernel);
     int n = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, dyn) != cudaSuccess) n = 0;
     return n;
@@ -214,7 +296,7 @@ int pick_stages(K kernel, uint32_t stage_bytes, int threads = kWsThreads) {
 // shared memory it needs.
 template <typename K>
 int persistent_grid(K kernel, uint32_t dyn_smem, int64_t ntiles, int threads = kCtaThreads) {
-  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn_smem));
+  smem_opt_in(kernel);
   static const int carve = std::getenv("MPB_CARVEOUT") ? std::atoi(std::getenv("MPB_CARVEOUT")) : -1;
   if (carve >= 0) cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
   int per_sm = 0;
@@ -277,7 +359,7 @@ int pick_wt_depth(K kernel, uint32_t stage_bytes, int threads) {
   auto per_sm = [&](int depth) {
     const uint32_t dyn = depth * kWtWarps * stage_bytes;
     if (depth * kWtWarps > kWtMaxStages || dyn > 220u * 1024u) return 0;
-    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn));
+    smem_opt_in(kernel);
     int n = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, dyn) != cudaSuccess) n = 0;
     return n;
@@ -416,10 +498,44 @@ struct DistCtx {
   mpb_halo halo;
 };
 
+// In-process group: rank 0 copies every rank's ghost rows from its
+// neighbours' own rows (what the NCCL path sends and receives).
+int local_halo(const DistCtx *dc, void *buf, int es, int64_t n, cudaStream_t s) {
+  LocalGroup &G = *dc->comm->grp;
+  const int me = dc->comm->rank;
+  G.slot[me].buf = buf;
+  G.slot[me].es = es;
+  G.slot[me].n = n;
+  G.slot[me].halo = dc->halo;
+  if (!G.barrier(me, "halo-in")) return MPB_ERR_COMM;
+  int rc = MPB_OK;
+  if (me == 0) {
+    for (int r = 0; r < G.nranks && rc == MPB_OK; r++) {
+      const LocalGroup::Slot &R = G.slot[r];
+      char *dst = static_cast<char *>(R.buf) + R.n * es;
+      if (R.halo.rank_lo >= 0 && R.halo.recv_lo > 0) {  // rows just below: the lower rank's top rows
+        const LocalGroup::Slot &L = G.slot[R.halo.rank_lo];
+        if (cudaMemcpyAsync(dst, static_cast<const char *>(L.buf) + (L.n - R.halo.recv_lo) * es, R.halo.recv_lo * es,
+                            cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+          rc = MPB_ERR_COMM;
+      }
+      if (R.halo.rank_hi >= 0 && R.halo.recv_hi > 0) {  // rows just above: the upper rank's first rows
+        const LocalGroup::Slot &U = G.slot[R.halo.rank_hi];
+        if (cudaMemcpyAsync(dst + R.halo.recv_lo * es, U.buf, R.halo.recv_hi * es, cudaMemcpyDeviceToDevice, s) !=
+            cudaSuccess)
+          rc = MPB_ERR_COMM;
+      }
+    }
+  }
+  if (!G.barrier(me, "halo-out")) return MPB_ERR_COMM;
+  return rc;
+}
+
 // Fill the ghost rows [n, n+ng) of `buf` from the neighbouring slabs and
 // send ours (NCCL grouped point-to-point, on the solve stream).
 int halo_exchange(const DistCtx *dc, void *buf, int es, int64_t n, cudaStream_t s) {
   if (dc == nullptr) return MPB_OK;
+  if (dc->comm->grp != nullptr) return local_halo(dc, buf, es, n, s);
   NcclApi &N = nccl();
   const mpb_halo &hl = dc->halo;
   const int dt = es == 8 ? kNcclFloat64 : kNcclFloat32;
@@ -441,6 +557,24 @@ int halo_exchange(const DistCtx *dc, void *buf, int es, int64_t n, cudaStream_t 
 // Multi-GPU scalar step: all-reduce this rank's sum, then run the step.
 int dist_step(mpb_handle *h, const DistCtx *dc, SolverState *st, int step, int gate, cudaStream_t s) {
   if (dc == nullptr) return MPB_OK;
+  if (dc->comm->grp != nullptr) {  // in-process group: rank-ordered sum of the ranks' partials
+    LocalGroup &G = *dc->comm->grp;
+    const int me = dc->comm->rank;
+    G.slot[me].st = st;
+    if (!G.barrier(me, "step-in")) return MPB_ERR_COMM;
+    int rc = MPB_OK;
+    if (me == 0) {  // the states travel as kernel arguments (no host-to-device copy)
+      LocalStates sts{};
+      for (int r = 0; r < G.nranks; r++) sts.p[r] = G.slot[r].st;
+      k_local_allreduce<<<1, 32, 0, s>>>(sts, G.nranks);
+      MPB_LAUNCHED(h);
+    }
+    if (!G.barrier(me, "step-out")) return MPB_ERR_COMM;
+    if (rc) return rc;
+    k_apply_step<<<1, 32, 0, s>>>(step, st, gate);
+    MPB_LAUNCHED(h);
+    return MPB_OK;
+  }
   NcclApi &N = nccl();
   if (N.AllReduce(st->red_local, st->red_global, 2, kNcclFloat64, kNcclSum, dc->comm->comm, s) != 0)
     return MPB_ERR_COMM;
@@ -718,6 +852,7 @@ int mpb_destroy(mpb_handle *h) {
   cudaEventDestroy(h->ev_t1);
   cudaStreamDestroy(h->solve);
   delete h;
+  cudaGetLastError();  // (a user stream destroyed first must not leave a stale error behind)
   return MPB_OK;
 }
 
@@ -1613,8 +1748,10 @@ int mpb_pcg_solve_dist(mpb_handle *h, const mpb_comm *comm, const mpb_halo *halo
   if (halo->recv_lo < 0 || halo->recv_hi < 0 || halo->send_lo < 0 || halo->send_hi < 0) return MPB_ERR_ARG;
   if (halo->send_lo > A->n || halo->send_hi > A->n) return MPB_ERR_SHAPE;
   DistCtx dc{comm, *halo};
-  return solve_impl(h, plan, A, opt, b, x, tr_relres, tr_true, tr_branch, tr_time, workspace, workspace_bytes, res,
-                    &dc);
+  const int rc = solve_impl(h, plan, A, opt, b, x, tr_relres, tr_true, tr_branch, tr_time, workspace,
+                            workspace_bytes, res, &dc);
+  if (rc != MPB_OK && comm->grp != nullptr) comm->grp->fail();  // release the other ranks
+  return rc;
 }
 
 int64_t mpb_solve_workspace_bytes_dist(const mpb_plan *plan, int64_t n, int64_t ghosts) {
@@ -1654,9 +1791,54 @@ int mpb_comm_create(mpb_handle *h, int rank, int nranks, const void *h_id, mpb_c
 
 int mpb_comm_destroy(mpb_comm *c) {
   if (!c) return MPB_OK;
-  NcclApi &N = nccl();
-  if (N.ok && c->comm) N.CommDestroy(c->comm);
+  if (c->grp == nullptr) {
+    NcclApi &N = nccl();
+    if (N.ok && c->comm) N.CommDestroy(c->comm);
+  }
   delete c;
+  return MPB_OK;
+}
+
+int mpb_local_group_create(int device, int nranks, void **out) {
+  if (!out || nranks < 1 || nranks > kMaxLocalRanks) return MPB_ERR_ARG;
+  *out = nullptr;
+  MPB_CUDA(cudaSetDevice(device));
+  LocalGroup *g = new LocalGroup();
+  g->nranks = nranks;
+  g->slot.resize(nranks);
+  cudaError_t e = cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete g;
+    return status_of(e);
+  }
+  *out = g;
+  return MPB_OK;
+}
+
+int mpb_local_group_destroy(void *group) {
+  LocalGroup *g = static_cast<LocalGroup *>(group);
+  if (!g) return MPB_OK;
+  cudaStreamSynchronize(g->stream);
+  cudaStreamDestroy(g->stream);
+  delete g;
+  cudaGetLastError();
+  return MPB_OK;
+}
+
+void *mpb_local_group_stream(void *group) {
+  LocalGroup *g = static_cast<LocalGroup *>(group);
+  return g ? static_cast<void *>(g->stream) : nullptr;
+}
+
+int mpb_comm_create_local(void *group, int rank, mpb_comm **out) {
+  LocalGroup *g = static_cast<LocalGroup *>(group);
+  if (!g || !out || rank < 0 || rank >= g->nranks) return MPB_ERR_ARG;
+  mpb_comm *c = new mpb_comm();
+  c->comm = nullptr;
+  c->rank = rank;
+  c->nranks = g->nranks;
+  c->grp = g;
+  *out = c;
   return MPB_OK;
 }
 
@@ -1682,7 +1864,10 @@ static int solve_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, con
   res->overflow_index = -1;
   const int64_t launches0 = h->launches;
   MPB_CUDA(cudaSetDevice(h->device));
-  cudaStream_t s = h->solve;
+  // in-process slab group: every rank enqueues on the group's one stream,
+  // iteration by iteration (no graph: the ranks meet at host barriers)
+  const bool local = dc != nullptr && dc->comm->grp != nullptr;
+  cudaStream_t s = local ? dc->comm->grp->stream : h->solve;
   const unsigned nt = static_cast<unsigned>(plan->ntiles);
   // order after the caller's pending work
   MPB_CUDA(cudaEventRecord(h->ev_in, h->user));
@@ -1771,7 +1956,7 @@ static int solve_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, con
   // done); multi-GPU: host-polled replays
   const bool loop = dc == nullptr && std::getenv("MPB_NO_WHILE") == nullptr;
   key.loop = loop ? 1 : 0;
-  if (!(h->have_graph && h->gkey == key)) {
+  if (!local && !(h->have_graph && h->gkey == key)) {
     if (h->have_graph) {
       cudaGraphExecDestroy(h->gexec);
       h->have_graph = false;
@@ -1827,7 +2012,15 @@ static int solve_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, con
   h->h_state->cond = loop ? static_cast<unsigned long long>(h->cond) : 0ull;
   MPB_CUDA(cudaMemcpyAsync(&w.st->cond, &h->h_state->cond, sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
   for (;;) {
-    MPB_CUDA(cudaGraphLaunch(h->gexec, s));
+    if (local) {
+      const int64_t l0 = h->launches;
+      for (int i = 0; i < G; i++)
+        if ((rc = enqueue_iteration(h, s, plan, A, opt, w, b, x, dc, i))) return rc;
+      h->graph_kernels = h->launches - l0;
+      h->launches = l0;
+    } else {
+      MPB_CUDA(cudaGraphLaunch(h->gexec, s));
+    }
     MPB_CUDA(cudaMemcpyAsync(h->h_state, w.st, sizeof(SolverState), cudaMemcpyDeviceToHost, s));
     MPB_CUDA(cudaStreamSynchronize(s));
     const long long ran = h->h_state->error ? h->h_state->err_it : h->h_state->last_it;

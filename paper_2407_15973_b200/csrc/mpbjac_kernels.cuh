@@ -298,6 +298,20 @@ __device__ __forceinline__ void finish_grid(SolverState *st, int ticket, int ste
   }
 }
 
+// in-process slab group: red_global of every rank = the ranks' red_local
+// summed in rank order (for two ranks the same value as NCCL's sum)
+constexpr int kMaxLocalRanks = 16;
+struct LocalStates {
+  SolverState *p[kMaxLocalRanks];
+};
+__global__ void k_local_allreduce(LocalStates sts, int nranks) {
+  if (threadIdx.x > 1) return;
+  const int i = threadIdx.x;
+  double acc = sts.p[0]->red_local[i];
+  for (int r = 1; r < nranks; r++) acc = __dadd_rn(acc, sts.p[r]->red_local[i]);
+  for (int r = 0; r < nranks; r++) sts.p[r]->red_global[i] = acc;
+}
+
 // multi-GPU: the scalar step on the all-reduced sum (every rank computes the
 // same state from the same global values)
 __global__ void k_apply_step(int step, SolverState *st, int gate) {

@@ -215,3 +215,137 @@ class SlabSolver:
                 self.h.lib.mpb_comm_destroy(self.comm)
         except Exception:  # interpreter shutdown
             pass
+
+
+class LocalSlabGroup:
+    """Every slab of a multi-GPU solve on ONE GPU, in one process: one
+    private handle, one in-process comm (mpb_comm_create_local) and one host
+    thread per slab, each running ``mpb_pcg_solve_dist`` on its slab.  The
+    library's in-process group replaces NCCL: all ranks' work goes to one
+    stream, and at each halo exchange / all-reduce the ranks meet at a host
+    barrier while rank 0 enqueues the copies and a rank-ordered sum.  It runs
+    the multi-GPU code path (slab plans, ghost columns, halos, all-reduced
+    scalar steps) with more ranks than GPUs; the arithmetic is the NCCL
+    path's (a two-rank sum is exact in either order)."""
+
+    def __init__(self, A, partition: BlockPartition, policy, nranks: int, k: int = 2, t: int = 2,
+                 device=None):
+        import threading
+        import torch
+        from . import bjac
+        from .policies import MixedPreconditioner
+        from .sparse import SparseMatrix
+
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        self.nranks = int(nranks)
+        self.n = int(A.n)
+        self.bounds = slab_bounds(partition, self.nranks, A.row_ptr)
+        self.slabs = [extract_slab(A.row_ptr, A.col_idx, A.values, partition, self.bounds, r)
+                      for r in range(self.nranks)]
+        self.A_loc, self.mp = [], []
+        for s in self.slabs:
+            Al = SparseMatrix.trusted(s.m, s.m + s.ghosts, s.row_ptr, s.col_idx, s.values)
+            part = BlockPartition(s.offsets)
+            ph = bjac._setup_impl(Al, k, t, policy.work, part) if policy.needs_high else None
+            pl = bjac._setup_impl(Al, k, t, policy.low, part) if policy.needs_low else None
+            self.A_loc.append(Al)
+            self.mp.append(MixedPreconditioner(policy, ph, pl))
+        L = _lib.load()
+        self._L = L
+        self.group = C.c_void_p()
+        _lib.check(L.mpb_local_group_create(self.device, self.nranks, C.byref(self.group)),
+                   "mpb_local_group_create")
+        # every rank (its handle and its thread's torch copies) works on the
+        # group's one stream: nothing orders through the legacy default stream
+        self.stream_ptr = int(L.mpb_local_group_stream(self.group) or 0)
+        self.stream = torch.cuda.ExternalStream(self.stream_ptr, device=self.device)
+        torch.cuda.current_stream(self.device).synchronize()  # setup work (default stream) done
+        self.comms, self.handles = [], []
+        for r in range(self.nranks):
+            c = C.c_void_p()
+            _lib.check(L.mpb_comm_create_local(self.group, r, C.byref(c)), "mpb_comm_create_local")
+            self.comms.append(c)
+            self.handles.append(_lib.Handle(self.device, stream=self.stream_ptr))
+        self._ovf = {}
+        self._ovf_barrier = threading.Barrier(self.nranks)
+        # the device structures (SELL packing, plan layouts) are built here,
+        # once, on the calling thread: the rank threads only solve
+        from .solver import _dev_struct
+        for Al, m in zip(self.A_loc, self.mp):
+            _dev_struct(Al, m)
+        torch.cuda.current_stream(self.device).synchronize()
+
+    def _overflow_hook(self, rank):
+        def hook(res):
+            # every rank saw the same global count; the first offending row
+            # over all ranks, as global_first_overflow does over NCCL
+            idx = int(res.overflow_index)
+            self._ovf[rank] = (self.slabs[rank].lo + idx if idx >= 0 else None, float(res.err_value))
+            self._ovf_barrier.wait()
+            hits = [v for v in self._ovf.values() if v[0] is not None]
+            g, v = min(hits) if hits else (-1, float("nan"))
+            res.overflow_index = g
+            res.err_value = v
+            self._ovf_barrier.wait()
+        return hook
+
+    def solve(self, b, config=None, x0=None):
+        """Solve with the global right-hand side b (host array); returns
+        (global x as a host array, the per-rank SolveReports)."""
+        import threading
+        import numpy as _np
+        from .solver import SolveConfig, _run_solve
+        config = config or SolveConfig()
+        b = _np.asarray(b, _np.float64)
+        reps, errs = [None] * self.nranks, [None] * self.nranks
+
+        torch = __import__("torch")
+
+        def run(r):
+            s = self.slabs[r]
+            try:
+                with torch.cuda.device(self.device), torch.cuda.stream(self.stream):
+                    reps[r] = _run_solve(
+                    self.A_loc[r], _np.ascontiguousarray(b[s.lo:s.hi]), self.mp[r], config,
+                    None if x0 is None else _np.ascontiguousarray(_np.asarray(x0)[s.lo:s.hi]),
+                    dist=(self.comms[r], s.halo(), s.ghosts, self._overflow_hook(r)),
+                    n_global=self.n, handle=self.handles[r])
+                    self.stream.synchronize()
+            except BaseException as e:  # re-raised in the caller's thread
+                errs[r] = e
+
+        th = [threading.Thread(target=run, args=(r,)) for r in range(self.nranks)]
+        for t_ in th:
+            t_.start()
+        for t_ in th:
+            t_.join()
+        for e in errs:
+            if e is not None:
+                raise e
+        x = _np.concatenate([_np.asarray(rep.x) for rep in reps])
+        return x, reps
+
+    def close(self):
+        """Release the ranks' handles, comms and the group (in that order:
+        the handles use the group's stream)."""
+        try:
+            if not getattr(self, "group", None):
+                return  # closed already (the group's stream no longer exists)
+            if getattr(self, "stream", None) is not None:
+                self.stream.synchronize()
+            for h in getattr(self, "handles", []):
+                if h.ptr:
+                    self._L.mpb_destroy(h.ptr)
+                    h.ptr = C.c_void_p()
+            self.handles = []
+            for c in getattr(self, "comms", []):
+                self._L.mpb_comm_destroy(c)
+            self.comms = []
+            self.stream = None
+            self._L.mpb_local_group_destroy(self.group)
+            self.group = None
+        except Exception:  # interpreter shutdown
+            pass
+
+    def __del__(self):
+        self.close()

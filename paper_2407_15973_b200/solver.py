@@ -202,9 +202,11 @@ def pcg_solve(A: SparseMatrix, b, mp: MixedPreconditioner,
 
 
 def _run_solve(A: SparseMatrix, b, mp: MixedPreconditioner, config: SolveConfig, x0=None,
-               dist=None, n_global=None, graph_iters: int = 0) -> SolveReport:
-    """pcg_solve after the square check.  dist = (comm, halo, ghosts): this
-    rank's slab of a multi-GPU solve (distributed.SlabSolver)."""
+               dist=None, n_global=None, graph_iters: int = 0, handle=None) -> SolveReport:
+    """pcg_solve after the square check.  dist = (comm, halo, ghosts[,
+    overflow hook]): this rank's slab of a multi-GPU solve
+    (distributed.SlabSolver / LocalSlabGroup); handle: a private handle
+    (in-process slab ranks), else the device's."""
     torch = __import__("torch")
     if tuple(b.shape) != (A.n,) or dtype_name(b) != "float64":
         raise ValueError(f"rhs must be float64 of shape ({A.n},)")
@@ -215,7 +217,7 @@ def _run_solve(A: SparseMatrix, b, mp: MixedPreconditioner, config: SolveConfig,
     tensor_io = is_tensor(b)
     D, s = _dev_struct(A, mp)
     P = mp.any
-    h = _lib.Handle.get(D.device.index)
+    h = handle if handle is not None else _lib.Handle.get(D.device.index)
     cap = int(config.iteration_cap(A.n if n_global is None else n_global))
     ghosts = 0 if dist is None else int(dist[2])
     # persistent per-preconditioner buffers keep the device pointers stable,
