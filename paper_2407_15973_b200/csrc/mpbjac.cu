@@ -452,6 +452,27 @@ int launch_pass(mpb_handle *h, cudaStream_t s, const mpb_plan *p, PassArgs<T> a,
   }
   a.resbuf = bufs.res;
   a.dbuf = bufs.dg;
+  static const bool old_big = std::getenv("MPB_OLD_BIG") != nullptr;
+  if (!old_big && a.meta != nullptr && a.pat != nullptr && p->npat > 0) {
+    // row patterns: no column stream, no block search, finish fused into the last sweep
+    k_big_resid_pat<T, F><<<nt, kCtaThreads, 0, s>>>(a, bufs.wA);
+    MPB_LAUNCHED(h);
+    T *cur = bufs.wA, *nxt = bufs.wB;
+    for (int sweep = 1; sweep < a.t; sweep++) {
+      if (sweep + 1 < a.t) {
+        k_big_sweep_pat<T, F, L, false><<<nt, kCtaThreads, 0, s>>>(a, cur, nxt);
+      } else {
+        k_big_sweep_pat<T, F, L, true><<<nt, kCtaThreads, 0, s>>>(a, cur, nxt);
+        MPB_LAUNCHED(h);
+        return MPB_OK;
+      }
+      MPB_LAUNCHED(h);
+      std::swap(cur, nxt);
+    }
+    k_big_finish<T, F, L><<<nt, kCtaThreads, 0, s>>>(a, cur);  // t == 1: no sweep to carry the finish
+    MPB_LAUNCHED(h);
+    return MPB_OK;
+  }
   k_big_resid<T, F><<<nt, kCtaThreads, 0, s>>>(a, bufs.wA);
   MPB_LAUNCHED(h);
   T *cur = bufs.wA, *nxt = bufs.wB;

@@ -1776,6 +1776,97 @@ __global__ void __launch_bounds__(kCtaThreads) k_big_finish(const PassArgs<T> a,
   }
 }
 
+// ---- large blocks, row-pattern versions (plans whose rows have patterns):
+// the row's pattern gives its columns (row + offset, no column stream), its
+// diagonal slot and -- through the plan's row metadata -- its in-block slot
+// range [i0, i1), so no block search; the finish (z_out, r.z) is fused into
+// the last inner sweep.  Generic rows (kMetaGeneric) take the column scans
+// of k_big_resid / k_big_sweep in the same launch.
+template <typename T, bool FIRST>
+__global__ void __launch_bounds__(kCtaThreads) k_big_resid_pat(const PassArgs<T> a, T *w0) {
+  if (gated_off(a)) return;
+  const TileDesc d = a.td[blockIdx.x];
+  const int row = d.lo + threadIdx.x;
+  if (row >= d.hi) return;
+  const T rv = a.r64 != nullptr ? narrow_checked(a, a.r64[row], row, FIRST) : a.rT[row];
+  const int s = row >> 5, sb = __ldg(a.sp + s), base = sb + (row & 31);
+  const uint16_t m = __ldg(a.meta + row);
+  T az = T(0), dd = T(0);
+  if (m != kMetaGeneric) {
+    const int *P = a.pat + meta_pid(m) * kPatStride;
+    const int hdr = __ldg(P), len = pat_len(hdr);
+    dd = __ldg(a.sval + base + 32 * pat_dpos(hdr));
+    if (!FIRST) {
+      T v[kSlots], g[kSlots];
+#pragma unroll
+      for (int u = 0; u < kSlots; u++) {
+        v[u] = u < len ? __ldg(a.sval + base + 32 * u) : T(0);
+        g[u] = u < len ? __ldg(a.zin + row + __ldg(P + 1 + u)) : T(0);
+      }
+#pragma unroll
+      for (int u = 0; u < kSlots; u++)
+        if (u < len) az = add_rn(az, mul_rn(v[u], g[u]));
+    }
+  } else {
+    const int width = (__ldg(a.sp + s + 1) - sb) >> 5;
+    for (int j = 0; j < width; j++) {
+      const int cj = __ldg(a.scol + base + 32 * j);
+      if (cj < 0) continue;
+      const T vj = __ldg(a.sval + base + 32 * j);
+      if (!FIRST) az = add_rn(az, mul_rn(vj, __ldg(a.zin + cj)));
+      if (cj == row) dd = vj;
+    }
+  }
+  const T res = FIRST ? rv : sub_rn(rv, az);
+  a.resbuf[row] = res;
+  a.dbuf[row] = dd;
+  w0[row] = div_rn(res, dd);
+}
+
+// one inner sweep w_new = w + (res - A_b w) / d; FINISH: the pass's last
+// sweep also writes z_out = (z_in +) w_new and the r.z tile partial
+template <typename T, bool FIRST, bool LAST, bool FINISH>
+__global__ void __launch_bounds__(kCtaThreads) k_big_sweep_pat(const PassArgs<T> a, const T *wsrc, T *wdst) {
+  if (gated_off(a)) return;
+  __shared__ double ws[32];
+  const int tile = blockIdx.x;
+  const TileDesc d = a.td[tile];
+  const int row = d.lo + threadIdx.x;
+  double prod = 0.0;
+  if (row < d.hi) {
+    const int s = row >> 5, sb = __ldg(a.sp + s), base = sb + (row & 31);
+    const uint16_t m = __ldg(a.meta + row);
+    T acc = T(0);
+    if (m != kMetaGeneric) {
+      const int *P = a.pat + meta_pid(m) * kPatStride + 1;
+      for (int j = meta_i0(m); j < meta_i1(m); j++)
+        acc = add_rn(acc, mul_rn(__ldg(a.sval + base + 32 * j), wsrc[row + __ldg(P + j)]));
+    } else {
+      int blo, bhi;
+      find_block_abs(a.boff + d.bf, d.nbk, row, blo, bhi);
+      const int width = (__ldg(a.sp + s + 1) - sb) >> 5;
+      for (int j = 0; j < width; j++) {
+        const int cj = __ldg(a.scol + base + 32 * j);
+        if (cj >= blo && cj < bhi) acc = add_rn(acc, mul_rn(__ldg(a.sval + base + 32 * j), wsrc[cj]));
+      }
+    }
+    const T wn = add_rn(wsrc[row], div_rn(sub_rn(a.resbuf[row], acc), a.dbuf[row]));
+    if (!FINISH) {
+      wdst[row] = wn;
+    } else {
+      const T zo = FIRST ? wn : add_rn(a.zin[row], wn);
+      if (a.zout != nullptr) st_keep(a.zout + row, zo);
+      if (a.zout64 != nullptr) a.zout64[row] = static_cast<double>(zo);
+      if (LAST && a.part != nullptr) prod = __dmul_rn(a.r64[row], static_cast<double>(zo));
+    }
+  }
+  if (FINISH && LAST && a.part != nullptr) {
+    const double tot = block_tree<kTileThreads>(prod, ws);
+    if (threadIdx.x == 0) put_part(a.part + tile, tot);
+    finish_grid(a.st, 0, kStepRho, ChunkCtx{a.st != nullptr ? a.csum : nullptr, a.part, a.g.ntiles, a.g.poll}, ws, true);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // p = z (first iteration) | z + beta * p_old   (solver.py:150-153)
 // Streaming, persistent; z is the fp32 (low) or fp64 (high) branch output.
