@@ -340,6 +340,15 @@ int64_t mpb_stencil_nnz(int64_t n);
 int mpb_assemble_stencil(mpb_handle *h, int64_t n, const double *kappa,
                          double wx, double wy, double wz, double scale,
                          int32_t *row_ptr, int32_t *col_idx, double *values);
+/* Config 4's 3-temperature operator (problems.py three_temperature) from
+ * the 7-point operator of its D field (rp1/col1/val1, mpb_assemble_stencil)
+ * and the per-cell exchange rates w_re / w_ei (device, ncell each): rows
+ * 3p+c with the cell's coupling block between the lower and upper stencil
+ * entries (3 * nnz1 + 4 ncell entries; row_ptr 3 ncell + 1).  Bit-identical
+ * to the host generator. */
+int mpb_expand_3t(mpb_handle *h, int64_t ncell, const int32_t *rp1, const int32_t *col1,
+                  const double *val1, const double *w_re, const double *w_ei,
+                  double time_term, int32_t *row_ptr, int32_t *col_idx, double *values);
 /* a * u_i + b for the first count SplitMix64 uniforms of seed
  * (problems.py splitmix64_stream; a = 1, b = 0: the stream itself). */
 int mpb_splitmix64_uniform(mpb_handle *h, uint64_t seed, int64_t count,

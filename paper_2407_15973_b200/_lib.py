@@ -42,7 +42,7 @@ EXPORTED = (
     "mpb_plan_pack_inblock_f32", "mpb_comm_unique_id", "mpb_comm_create",
     "mpb_comm_destroy", "mpb_solve_workspace_bytes_dist", "mpb_pcg_solve_dist",
     "mpb_profile_iteration_dist", "mpb_plan_layout_info", "mpb_stencil_nnz",
-    "mpb_assemble_stencil", "mpb_splitmix64_uniform",
+    "mpb_assemble_stencil", "mpb_splitmix64_uniform", "mpb_expand_3t",
     "mpb_row_features", "mpb_tau_histogram", "mpb_vector_stats",
     "mpb_first_violations", "mpb_local_group_create", "mpb_local_group_destroy", "mpb_local_group_stream",
     "mpb_comm_create_local",
@@ -110,6 +110,7 @@ def _declare(L):
         "mpb_assemble_stencil": ([_P, _I64, _P, C.c_double, C.c_double, C.c_double, C.c_double, _P, _P, _P],
                                  C.c_int),
         "mpb_splitmix64_uniform": ([_P, C.c_uint64, _I64, C.c_double, C.c_double, _P], C.c_int),
+        "mpb_expand_3t": ([_P, _I64, _P, _P, _P, _P, _P, C.c_double, _P, _P, _P], C.c_int),
         "mpb_row_features": ([_P, _I64, _P, _P, _P, _P, _P, _P, _P, _P, _P], C.c_int),
         "mpb_tau_histogram": ([_P, _I64, _P, C.POINTER(C.c_double), C.c_int, C.POINTER(C.c_int64),
                                C.POINTER(C.c_int64)], C.c_int),

@@ -1146,6 +1146,19 @@ int mpb_assemble_stencil(mpb_handle *h, int64_t n, const double *kappa, double w
   return MPB_OK;
 }
 
+int mpb_expand_3t(mpb_handle *h, int64_t ncell, const int32_t *rp1, const int32_t *col1, const double *val1,
+                  const double *w_re, const double *w_ei, double time_term, int32_t *row_ptr, int32_t *col_idx,
+                  double *values) {
+  if (!h || ncell < 1 || !rp1 || !col1 || !val1 || !w_re || !w_ei || !row_ptr || !col_idx || !values)
+    return MPB_ERR_ARG;
+  if (3 * ncell >= (int64_t(1) << 31) - 1) return MPB_ERR_INDEX32;
+  MPB_CUDA(cudaSetDevice(h->device));
+  k_expand_3t<<<elt_blocks(ncell), kEltThreads, 0, h->user>>>(ncell, rp1, col1, val1, w_re, w_ei, time_term, row_ptr,
+                                                              col_idx, values);
+  MPB_LAUNCHED(h);
+  return MPB_OK;
+}
+
 int mpb_splitmix64_uniform(mpb_handle *h, uint64_t seed, int64_t count, double a, double b, double *out) {
   if (!h || count < 0 || (count > 0 && !out)) return MPB_ERR_ARG;
   if (count == 0) return MPB_OK;

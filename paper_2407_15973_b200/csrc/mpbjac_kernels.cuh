@@ -2641,6 +2641,60 @@ __device__ __forceinline__ double harmonic_face(double w, double a, double b) {
 
 // Row p: entries zm, ym, xm, diag, xp, yp, zp (ascending column), the
 // off-diagonals -(face*scale), the diagonal ((((xm+xp)+ym)+yp)+zm)+zp)*scale.
+// Config 4 (3-temperature system, problems.py three_temperature): cell p's
+// 7-point row (rp1/col1/val1 of the D field) becomes rows 3p+c, c = 0..2:
+// [lower stencil entries] [cell block] [upper stencil entries], the cell
+// block  c=0: diag, (3p+1, -w_re);  c=1: (3p, -w_re), diag, (3p+2, -w_ei);
+// c=2: (3p+1, -w_ei), diag; diagonal = ((stencil diag + tt) [+ w_re]) [+ w_ei]
+// in that order.  Row offsets are closed-form: cell p's rows start at
+// 3 rp1[p] + 4 p (4 coupling entries per cell).
+__global__ void k_expand_3t(long long ncell, const int *rp1, const int *col1, const double *val1, const double *wre,
+                            const double *wei, double tt, int *rp3, int *col3, double *val3) {
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < ncell;
+       p += (long long)gridDim.x * blockDim.x) {
+    const int b1 = rp1[p], cnt = rp1[p + 1] - b1;
+    int nlo = 0;
+    while (col1[b1 + nlo] != static_cast<int>(p)) nlo++;
+    const long long R = 3LL * b1 + 4LL * p;
+    const double wr = wre[p], we = wei[p];
+    for (int c = 0; c < 3; c++) {
+      const long long start = R + static_cast<long long>(c) * cnt + (c == 0 ? 0 : (c == 1 ? 1 : 3));
+      const int cpl = c == 1 ? 2 : 1;
+      rp3[3 * p + c] = static_cast<int>(start);
+      for (int j = 0; j < cnt; j++) {
+        if (j == nlo) continue;
+        const long long dst = start + j + (j > nlo ? cpl : 0);
+        col3[dst] = 3 * col1[b1 + j] + c;
+        val3[dst] = val1[b1 + j];
+      }
+      const long long blk = start + nlo;
+      double dd = __dadd_rn(val1[b1 + nlo], tt);
+      if (c <= 1) dd = __dadd_rn(dd, wr);
+      if (c >= 1) dd = __dadd_rn(dd, we);
+      const int cell3 = static_cast<int>(3 * p);
+      if (c == 0) {
+        col3[blk] = cell3;
+        val3[blk] = dd;
+        col3[blk + 1] = cell3 + 1;
+        val3[blk + 1] = -wr;
+      } else if (c == 1) {
+        col3[blk] = cell3;
+        val3[blk] = -wr;
+        col3[blk + 1] = cell3 + 1;
+        val3[blk + 1] = dd;
+        col3[blk + 2] = cell3 + 2;
+        val3[blk + 2] = -we;
+      } else {
+        col3[blk] = cell3 + 1;
+        val3[blk] = -we;
+        col3[blk + 1] = cell3 + 2;
+        val3[blk + 1] = dd;
+      }
+    }
+    if (p == ncell - 1) rp3[3 * ncell] = static_cast<int>(3LL * rp1[ncell] + 4LL * ncell);
+  }
+}
+
 __global__ void k_stencil(long long n, const double *kap, double wx, double wy, double wz, double scale, int *rp,
                           int *col, double *val) {
   const long long N = n * n * n, n2 = n * n;

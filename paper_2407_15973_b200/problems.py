@@ -22,9 +22,10 @@ Grid ordering everywhere: node (i, j, k) -> row p = i + j n + k n^2, cell
 arrays C-ordered [k, j, i]; h = 1/(n+1); face coefficient = harmonic mean
 (2a)b/(a+b) of the two cells, a boundary face takes the cell's own value.
 
-``device=True`` (make_config, diffusion_matrix, splitmix64_stream) assembles
-the 7-point operator and draws the uniform streams on the GPU
-(mpb_assemble_stencil / mpb_splitmix64_uniform: same IEEE operations, same
+``device=True`` (make_config, diffusion_matrix, three_temperature,
+splitmix64_stream) assembles the 7-point and 3-T operators and draws the
+uniform streams on the GPU (mpb_assemble_stencil / mpb_expand_3t /
+mpb_splitmix64_uniform: same IEEE operations, same
 order, bit-identical; tests/test_gpu_parity.py pins it), which turns the
 512^3 setup from minutes of numpy into a fraction of a second plus one
 device-to-host copy.  Cell fields (kappa: exp/log/cos/pow) stay on the host,
@@ -282,10 +283,9 @@ def kappa_c5(n: int) -> np.ndarray:
     return base * np.exp(normal_stream(4, n ** 3))
 
 
-def three_temperature(n: int, validate: bool = True) -> SparseMatrix:
-    """Config 4: per-component 7-point diffusion with D = T^3 plus per-cell
-    radiation-electron (w_RE) and electron-ion (w_EI) exchange; unknown
-    3 p + c (c = 0 radiation, 1 electron, 2 ion), cell-major."""
+def three_temperature_fields(n: int):
+    """Config 4's cell fields (host: libm's exp/sin/pow define them):
+    D = T^3 and the exchange rates w_RE, w_EI."""
     N = n ** 3
     x = (np.arange(n) + 1.0) / (n + 1)
     sx = np.sin(2.0 * np.pi * x)
@@ -296,6 +296,52 @@ def three_temperature(n: int, validate: bool = True) -> SparseMatrix:
     u = splitmix64_stream(103, 2 * N)
     w_re = 10.0 ** (-4.0 + 8.0 * u[:N])
     w_ei = 10.0 ** (-4.0 + 8.0 * u[N:])
+    return D, w_re, w_ei
+
+
+def _three_temperature_gpu(n: int) -> SparseMatrix:
+    """three_temperature assembled on the GPU (mpb_assemble_stencil for the
+    D operator, then mpb_expand_3t); the host copy is fetched once and the
+    device CSR is kept as the matrix's GPU copy."""
+    import torch
+    from . import _lib
+    from .device import DeviceCSR, default_device
+    h = _gpu()
+    dev = default_device()
+    N = n ** 3
+    D, w_re, w_ei = three_temperature_fields(n)
+    scale = float((n + 1) ** 2)
+    nnz1 = int(h.lib.mpb_stencil_nnz(n))
+    f = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float64)).to(dev)  # noqa: E731
+    Dd, wr, we = f(D), f(w_re), f(w_ei)
+    rp1 = torch.empty(N + 1, dtype=torch.int32, device=dev)
+    c1 = torch.empty(nnz1, dtype=torch.int32, device=dev)
+    v1 = torch.empty(nnz1, dtype=torch.float64, device=dev)
+    _lib.check(h.lib.mpb_assemble_stencil(h.ptr, n, _lib.ptr(Dd), 1.0, 1.0, 1.0, scale, _lib.ptr(rp1),
+                                          _lib.ptr(c1), _lib.ptr(v1)), "assemble_stencil")
+    nnz = 3 * nnz1 + 4 * N
+    rp = torch.empty(3 * N + 1, dtype=torch.int32, device=dev)
+    col = torch.empty(nnz, dtype=torch.int32, device=dev)
+    val = torch.empty(nnz, dtype=torch.float64, device=dev)
+    _lib.check(h.lib.mpb_expand_3t(h.ptr, N, _lib.ptr(rp1), _lib.ptr(c1), _lib.ptr(v1), _lib.ptr(wr),
+                                   _lib.ptr(we), 0.01 * scale, _lib.ptr(rp), _lib.ptr(col), _lib.ptr(val)),
+               "expand_3t")
+    del rp1, c1, v1
+    rp_h = rp.cpu().numpy().astype(np.int64)
+    A = SparseMatrix.trusted(3 * N, 3 * N, rp_h, col.cpu().numpy(), val.cpu().numpy())
+    A._dev[str(dev)] = DeviceCSR(3 * N, 3 * N, rp, col, val64=val, host_row_ptr=rp_h)
+    return A
+
+
+def three_temperature(n: int, validate: bool = True, device: bool = False) -> SparseMatrix:
+    """Config 4: per-component 7-point diffusion with D = T^3 plus per-cell
+    radiation-electron (w_RE) and electron-ion (w_EI) exchange; unknown
+    3 p + c (c = 0 radiation, 1 electron, 2 ion), cell-major.  device=True:
+    assembled on the GPU (bit-identical)."""
+    if device and n >= 2:
+        return _three_temperature_gpu(n)
+    N = n ** 3
+    D, w_re, w_ei = three_temperature_fields(n)
     scale = float((n + 1) ** 2)
     rp1, col1, val1 = stencil_csr(n, face_arrays(D.reshape(n, n, n)), scale)
     cnt1 = np.diff(rp1)
@@ -357,8 +403,8 @@ def make_config(name: str, n: int | None = None, validate: bool | None = None,
                 device: bool = False) -> ConfigSystem:
     """Config name 'c1'..'c5' at its BASELINE.json size, or at grid size n
     (same recipe, for parity tests).  Same seeds, fields, blocks, policies.
-    device=True: 7-point operators and right-hand sides built on the GPU
-    (bit-identical; C4's 3-T coupling is assembled on the host)."""
+    device=True: the operators (7-point and C4's 3-T) and right-hand
+    sides built on the GPU (bit-identical)."""
     name = name.lower()
     n = FULL_N[name] if n is None else int(n)
     N = n ** 3
@@ -380,7 +426,7 @@ def make_config(name: str, n: int | None = None, validate: bool | None = None,
         return ConfigSystem("c3", A, splitmix64_stream(2, N, device), 64, ("adaptive-lh:1e-6",),
                             2, 2, 1e-10, n, "8^3-cell blocks, kappa 1e-3..1e3")
     if name == "c4":
-        A = three_temperature(n, validate=validate)
+        A = three_temperature(n, validate=validate, device=device)
         return ConfigSystem("c4", A, splitmix64_stream(3, 3 * N, device), 96,
                             ("fixed-low", "adaptive-hl:10"), 2, 2, 1e-10, n,
                             "3-temperature radiation-diffusion stand-in")

@@ -54,7 +54,7 @@ def _system(cfg):
         A = problems.family_matrix(128, fam, 1.0 if fam is problems.Family.CONST else 1000.0)
         sysm = (A, np.ones(A.n), BlockPartition.equal_split(A.n, 32), 2, 2, 1e-10)
     else:
-        cs = problems.make_config(cfg, device=cfg != "c4")
+        cs = problems.make_config(cfg, device=True)   # (GPU assembly: bit-identical to the host generators)
         sysm = (cs.A, cs.b, BlockPartition.fixed_size(cs.A.n, cs.block_rows), cs.k, cs.t, cs.res_tol)
     _SYSTEMS[cfg] = sysm
     return sysm

@@ -381,11 +381,11 @@ def test_row_patterns_and_generic_rows_bitwise(cuda, oracle):
 
 
 def test_gpu_assembly_bitwise_vs_host(cuda):
-    """The 7-point operators and right-hand sides built on the GPU
-    (mpb_assemble_stencil, mpb_splitmix64_uniform) equal the host
-    generators bit for bit, boundary rows and weights included."""
+    """The 7-point and 3-T operators and right-hand sides built on the GPU
+    (mpb_assemble_stencil, mpb_expand_3t, mpb_splitmix64_uniform) equal the
+    host generators bit for bit, boundary rows and weights included."""
     from paper_2407_15973_b200 import problems
-    for name, n in (("c1", 12), ("c2", 16), ("c3", 24), ("c4", 8), ("c5", 20)):
+    for name, n in (("c1", 12), ("c2", 16), ("c3", 24), ("c4", 8), ("c4", 3), ("c4", 2), ("c5", 20)):
         h = problems.make_config(name, n)
         d = problems.make_config(name, n, device=True)
         np.testing.assert_array_equal(d.A.row_ptr, h.A.row_ptr, err_msg=name)
