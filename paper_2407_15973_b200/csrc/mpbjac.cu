@@ -82,6 +82,15 @@ struct mpb_plan {
   int ks;                   // compile-time slot count of the hot kernels (7 or 9)
   int64_t ngeneric;         // rows without a usable pattern (kMetaGeneric)
   WinSet win;               // z_in gather windows of the passes after the first (n == 0: none)
+  // symmetric offset-slot SpMV (k_spmv_sym): the pattern offsets' nonnegative
+  // half d[0..S) (S = 0: not eligible), per-pattern presence masks, and the
+  // U layout built for one operator value array (sym_key)
+  int sym_S = 0;
+  int sym_d[8] = {};
+  uint16_t *d_pmask = nullptr;
+  double *d_U = nullptr;
+  const void *sym_key = nullptr;
+  bool sym_ok = false;
 };
 
 // In-process group of slab ranks on one GPU (mpb_local_group_create): the
@@ -982,6 +991,8 @@ int mpb_plan_destroy(mpb_plan *p) {
   cudaFree(p->d_meta);
   cudaFree(p->d_ib_sp);
   cudaFree(p->d_ib_col);
+  cudaFree(p->d_pmask);
+  cudaFree(p->d_U);
   delete p;
   return MPB_OK;
 }
@@ -1053,6 +1064,48 @@ int mpb_plan_bind_sell(mpb_handle *h, mpb_plan *p, const mpb_sell *sell) {
   MPB_CUDA(cudaMemcpy(p->d_td, td.data(), sizeof(TileDesc) * p->ntiles, cudaMemcpyHostToDevice));
   MPB_CUDA(cudaStreamSynchronize(h->user));
   p->bound = sell;
+  // Symmetric offset-slot SpMV: the offsets must be a symmetric set with at
+  // most kSymMax nonnegative members (the values are checked per operator)
+  p->sym_S = 0;
+  p->sym_key = nullptr;
+  p->sym_ok = false;
+  // off by default (MPB_SYM=1): on C2 it moves 50 MB less per SpMV (ncu:
+  // 97 MB against 147 MB) but runs 41 us against 32.7 us for the SELL kernel
+  // (profiles/r02_notes.md)
+  static const bool no_sym = !(std::getenv("MPB_SYM") && std::atoi(std::getenv("MPB_SYM")) != 0);
+  if (!no_sym && !p->large && p->ngeneric == 0 && p->npat > 0) {
+    std::vector<int> pat(static_cast<size_t>(p->npat) * kPatStride);
+    MPB_CUDA(cudaMemcpy(pat.data(), p->d_pat, sizeof(int) * pat.size(), cudaMemcpyDeviceToHost));
+    std::vector<int> offs;
+    for (int q = 0; q < p->npat; q++) {
+      const int *P = &pat[static_cast<size_t>(q) * kPatStride];
+      for (int u = 0; u < (P[0] & 0xFF); u++) offs.push_back(P[1 + u]);
+    }
+    std::sort(offs.begin(), offs.end());
+    offs.erase(std::unique(offs.begin(), offs.end()), offs.end());
+    bool symset = !offs.empty();
+    for (int o : offs) symset = symset && std::binary_search(offs.begin(), offs.end(), -o);
+    std::vector<int> pos;
+    for (int o : offs)
+      if (o >= 0) pos.push_back(o);
+    if (symset && !pos.empty() && pos[0] == 0 && (static_cast<int>(pos.size()) == 4 || static_cast<int>(pos.size()) == 6)) {
+      const int S = static_cast<int>(pos.size());
+      std::vector<uint16_t> mask(p->npat, 0);
+      for (int q = 0; q < p->npat; q++) {
+        const int *P = &pat[static_cast<size_t>(q) * kPatStride];
+        for (int u = 0; u < (P[0] & 0xFF); u++) {
+          const int j = static_cast<int>(std::lower_bound(offs.begin(), offs.end(), P[1 + u]) - offs.begin());
+          mask[q] |= static_cast<uint16_t>(1u << j);
+        }
+      }
+      cudaFree(p->d_pmask);
+      p->d_pmask = nullptr;
+      MPB_CUDA(cudaMalloc(&p->d_pmask, sizeof(uint16_t) * p->npat));
+      MPB_CUDA(cudaMemcpy(p->d_pmask, mask.data(), sizeof(uint16_t) * p->npat, cudaMemcpyHostToDevice));
+      p->sym_S = S;
+      for (int k = 0; k < S; k++) p->sym_d[k] = pos[k];
+    }
+  }
   // Gather windows: the distinct column offsets of the row patterns,
   // clustered into <= kMaxWin row intervals [a, b] (a new window where the
   // gap to the previous offset exceeds a tile); a pass after the first then
@@ -1095,7 +1148,7 @@ int mpb_plan_bind_sell(mpb_handle *h, mpb_plan *p, const mpb_sell *sell) {
     for (int k = 0; k < w.n; k++) rows += kTileRows + w.b[k] - w.a[k];
     if (ok && rows <= kWinMaxRows) p->win = w;
     if (std::getenv("MPB_VERBOSE")) {
-      std::fprintf(stderr, "[mpb] gather windows:");
+      std::fprintf(stderr, "[mpb] gather windows (off by default):");
       for (int k = 0; k < w.n; k++) std::fprintf(stderr, " [%d, %d]", w.a[k], w.b[k]);
       std::fprintf(stderr, " (%d rows)%s\n", rows, p->win.n ? "" : " -- not used");
     }
@@ -1613,6 +1666,45 @@ static uint32_t spmv_dyn_smem(const mpb_plan *p) {
   return g.ns * spmv_layout(g).bytes;
 }
 
+// The symmetric offset-slot layout of the operator's values (k_spmv_sym):
+// built once per operator value array when the plan's offsets allow it and
+// the values are symmetric bit for bit (one-GPU solves only: a slab's ghost
+// rows are not row + offset).  Returns whether it is usable.
+static bool ensure_sym(mpb_handle *h, mpb_plan *p, const mpb_csr *A, cudaStream_t s) {
+  if (p->sym_S == 0) return false;
+  const double *vals = op_vals(A);
+  if (p->sym_key == vals) return p->sym_ok;
+  p->sym_key = vals;
+  p->sym_ok = false;
+  unsigned long long *d_bad = nullptr, bad = 1;
+  if (cudaMalloc(&d_bad, sizeof(unsigned long long)) != cudaSuccess) return false;
+  cudaMemsetAsync(d_bad, 0, sizeof(unsigned long long), s);
+  k_sym_check<<<elt_blocks(A->n), kEltThreads, 0, s>>>(A->n, A->sell->d_sp, vals, p->d_meta, p->d_pat, d_bad);
+  cudaMemcpyAsync(&bad, d_bad, sizeof(bad), cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  cudaFree(d_bad);
+  if (cudaGetLastError() != cudaSuccess || bad != 0) return false;
+  cudaFree(p->d_U);
+  p->d_U = nullptr;
+  if (cudaMalloc(&p->d_U, sizeof(double) * p->sym_S * A->n) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  SpmvArgs da{};
+  for (int k = 0; k < p->sym_S; k++) da.d[k] = p->sym_d[k];
+  k_sym_build<<<elt_blocks(A->n), kEltThreads, 0, s>>>(A->n, A->sell->d_sp, vals, p->d_meta, p->d_pat, p->sym_S, da,
+                                                       p->d_U);
+  h->launches += 2;
+  p->sym_ok = cudaGetLastError() == cudaSuccess;
+  return p->sym_ok;
+}
+
+static void (*spmv_sym_kernel(const mpb_plan *p))(SpmvArgs) {
+  const bool two = two_level(p->ntiles);
+  if (p->sym_S == 4) return two ? k_spmv_sym<4, true> : k_spmv_sym<4, false>;
+  return two ? k_spmv_sym<6, true> : k_spmv_sym<6, false>;
+}
+
 // pnew != null: p rebuilt from z and pold inside the SpMV (fused mode)
 static SpmvArgs spmv_args(const mpb_handle *h, const mpb_plan *p, const mpb_csr *A, const SolveWs &w,
                           const double *pold = nullptr, double *pnew = nullptr) {
@@ -1634,7 +1726,31 @@ static SpmvArgs spmv_args(const mpb_handle *h, const mpb_plan *p, const mpb_csr 
   sa.part = w.part;
   sa.st = w.st;
   sa.csum = w.csum;
+  if (p->sym_ok && p->sym_key == op_vals(A) && p->d_U != nullptr) {
+    sa.U = p->d_U;
+    sa.pmask = p->d_pmask;
+    sa.n = static_cast<int>(A->n);
+    sa.S = p->sym_S;
+    for (int k = 0; k < p->sym_S; k++) sa.d[k] = p->sym_d[k];
+    sa.g.ns = pick_stages(spmv_sym_kernel(p), spmv_sym_layout(p->sym_S, p->sym_d).bytes);
+  }
   return sa;
+}
+
+// the SpMV of an iteration: the symmetric offset-slot kernel when spmv_args
+// bound a U layout, else the SELL kernel
+static int launch_spmv(mpb_handle *h, cudaStream_t s, const mpb_plan *p, const SpmvArgs &sa, bool pdl) {
+  if (sa.U != nullptr) {
+    auto kern = spmv_sym_kernel(p);
+    const uint32_t dyn = sa.g.ns * spmv_sym_layout(sa.S, sa.d).bytes;
+    MPB_CUDA(launch_k(pdl, kern, persistent_grid(kern, dyn, p->ntiles, kWsThreads), kWsThreads, dyn, s, sa));
+  } else {
+    const uint32_t dyn = spmv_dyn_smem(p);
+    MPB_CUDA(launch_k(pdl, spmv_kernel(p), persistent_grid(spmv_kernel(p), dyn, p->ntiles, kWsThreads), kWsThreads,
+                      dyn, s, sa));
+  }
+  MPB_LAUNCHED(h);
+  return MPB_OK;
 }
 
 // One PCG iteration (solver.py:140-177): preconditioner of the branch(es)
@@ -1717,6 +1833,7 @@ static int enqueue_iteration(mpb_handle *h, cudaStream_t s, const mpb_plan *p, c
     pcur = (it & 1) ? w.p : w.p2;
     sa = spmv_args(h, p, A, w, pold, pcur);
     sa.prefetch = pre;
+    if (dc) sa.U = nullptr;  // (slabs: the ghost columns are not row + offset)
   } else {
     MPB_CUDA(launch_k(pdl, k_pupdate, persistent_grid(k_pupdate, 0, p->ntiles), kCtaThreads, 0, s,
                       static_cast<const TileDesc *>(p->d_td), static_cast<int>(nt), static_cast<const float *>(w.z32),
@@ -1724,13 +1841,9 @@ static int enqueue_iteration(mpb_handle *h, cudaStream_t s, const mpb_plan *p, c
     MPB_LAUNCHED(h);
     if ((rc = halo_exchange(dc, w.p, 8, A->n, s))) return rc;
     sa = spmv_args(h, p, A, w);
+    if (dc) sa.U = nullptr;
   }
-  {
-    const uint32_t dyn = spmv_dyn_smem(p);
-    MPB_CUDA(launch_k(pdl, spmv_kernel(p), persistent_grid(spmv_kernel(p), dyn, p->ntiles, kWsThreads), kWsThreads,
-                      dyn, s, sa));
-  }
-  MPB_LAUNCHED(h);
+  if ((rc = launch_spmv(h, s, p, sa, pdl))) return rc;
   if (fused && (rc = halo_exchange(dc, pcur, 8, A->n, s))) return rc;  // next iteration's p_old ghosts
   if ((rc = dist_step(h, dc, w.st, kStepPq, 2, s))) return rc;
   if (fused) {
@@ -1960,6 +2073,8 @@ static int solve_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, con
     return MPB_OK;
   }
 
+  // the symmetric offset-slot SpMV layout of the operator (one GPU; built once per value array)
+  if (dc == nullptr) ensure_sym(h, const_cast<mpb_plan *>(plan), A, s);
   // capture G iterations once (cached across solves with the same buffers)
   int G = opt->graph_iters > 0 ? opt->graph_iters : kDefaultGraphIters;
   if (fused_mode(plan, opt, dc) && (G & 1)) G++;  // the two p buffers alternate per iteration
@@ -2302,9 +2417,9 @@ static int profile_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, c
   // rebuilds p from z (no p-update kernel), the x/r update carries the next
   // first pass
   const bool fused = !dist && opt->k >= 2 && !plan->large && std::getenv("MPB_NO_FUSE") == nullptr;
-  const SpmvArgs sa = fused ? spmv_args(h, plan, A, w, w.p, w.p2) : spmv_args(h, plan, A, w);
-  const uint32_t sdyn = spmv_dyn_smem(plan);
-  const int sgrid = persistent_grid(spmv_kernel(plan), sdyn, plan->ntiles, kWsThreads);
+  if (!dist) ensure_sym(h, const_cast<mpb_plan *>(plan), A, s);
+  SpmvArgs sa = fused ? spmv_args(h, plan, A, w, w.p, w.p2) : spmv_args(h, plan, A, w);
+  if (dist) sa.U = nullptr;
   const int ugrid = persistent_grid(k_update, 0, plan->ntiles);
   const int pgrid = persistent_grid(k_pupdate, 0, plan->ntiles);
   if (!fused) {
@@ -2315,11 +2430,7 @@ static int profile_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, c
     });
     if (rc) return rc;
   }
-  rc = timed(3, [&]() -> int {
-    MPB_CUDA(launch_k(!dist, spmv_kernel(plan), sgrid, kWsThreads, sdyn, s, sa));
-    MPB_LAUNCHED(h);
-    return MPB_OK;
-  });
+  rc = timed(3, [&]() -> int { return launch_spmv(h, s, plan, sa, !dist); });
   if (rc) return rc;
   rc = timed(4, [&]() -> int {
     k_update<<<ugrid, kCtaThreads, 0, s>>>(plan->d_td, static_cast<int>(nt), x, w.p, w.q, w.r, w.part,

@@ -376,7 +376,7 @@ struct StageLayout {
   uint32_t col, val, sp, meta, v0, v1, v2, v3, bytes;
   uint32_t win;  // start of the gather windows (bjac_layout with windows), else == bytes
 };
-__host__ __device__ inline uint32_t al16u(uint32_t b) { return (b + 15u) & ~15u; }
+__host__ __device__ constexpr uint32_t al16u(uint32_t b) { return (b + 15u) & ~15u; }
 // v*es: element sizes of up to three row-vector slices [lo, hi) (0: absent)
 __host__ __device__ inline StageLayout stage_layout(int cap_e, int es, int max_sl, bool cols, bool meta, int v0es,
                                                     int v1es, int v2es, int v3es = 0) {
@@ -1251,9 +1251,15 @@ __device__ __forceinline__ void load_zoff(int *s_zoff, const int *pat, int npat,
 // the producer warp per CTA)
 // WIN: z_in gathered from the stage's gather windows (passes after the first,
 // plans with windows; a.win.n > 0)
+// MPB_MINB_LAST=n (experiment): compile the BJAC tile kernels for n co-resident CTAs per SM
+#ifdef MPB_MINB_LAST
+#define MPB_TILE_BOUNDS(RPT) __launch_bounds__(kTileThreads / RPT + 32, MPB_MINB_LAST)
+#else
+#define MPB_TILE_BOUNDS(RPT) __launch_bounds__(kTileThreads / RPT + 32)
+#endif
 template <typename T, bool FIRST, bool LAST, bool R64, int KS, bool GEN, bool TWO = false, int RPT = kRowsPerThread,
           bool WIN = false>
-__global__ void __launch_bounds__(kTileThreads / RPT + 32) k_bjac_tile(const PassArgs<T> a) {
+__global__ void MPB_TILE_BOUNDS(RPT) k_bjac_tile(const PassArgs<T> a) {
   constexpr int NC = kTileThreads / RPT;
   constexpr int kFinRpt = NC >= kFinThreads ? 1 : kFinThreads / NC;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -1929,6 +1935,14 @@ struct SpmvArgs {
   SolverState *st;
   double *csum;        // chunk sums of the two-level p.q sum (ChunkCtx)
   int prefetch;     // see PassArgs::prefetch
+  // symmetric offset-slot layout (k_spmv_sym): U + s n holds each row's value
+  // at column offset d[s] >= 0 (d[0] = 0, 0 where absent); the value at
+  // offset -d[s] is row (i - d[s])'s U_s entry (A symmetric, checked at build)
+  const double *U;
+  const uint16_t *pmask;  // per row pattern: bit j = signed offset j (ascending) present
+  int n;
+  int S;
+  int d[8];
 };
 
 // p_j as the SpMV reads it: stored (ZT = void) or rebuilt from z (ZT = the
@@ -2057,6 +2071,242 @@ __global__ void MPB_WS_BOUNDS_SPMV k_spmv_pq(const SpmvArgs a) {
   finish_grid<16, kFinRptWs>(a.st, 1, kStepPq, ChunkCtx{a.csum, a.part, a.g.ntiles, TWO ? a.g.poll : 0}, ws);
 }
 
+// ---- SpMV on the symmetric offset-slot layout --------------------------------
+// A symmetric pattern-row matrix whose distinct column offsets are
+// {-d[S-1] .. -d[1], 0, d[1] .. d[S-1]} stores only the S nonnegative-offset
+// values of each row (U_s, slot-major): the stage carries the tile's U rows
+// and its row metadata, and row i takes its lower entries (offset -d[s]) from
+// row i - d[s]'s U_s through global memory (L2: those rows were streamed a
+// few tiles earlier).  Ascending column order and one rounding per product
+// and per add, as the SELL kernel: bit-identical.  8 (S = 4) or 12 bytes of
+// values per row less than the SELL layout's 7 (9) slots.
+constexpr int kSymMax = 6;
+
+// Stage regions: U_0 rows [lo, hi); for s >= 1 with d[s] < kTileRows one
+// window [lo - d[s], hi) (upper and lower entries), else two: [lo, hi) and
+// the mirror rows [lo - d[s], hi - d[s]) -- every value the tile's rows use
+// comes from shared memory.  Windows start clamped at row 0.
+struct SymLayout {
+  uint32_t meta, up[kSymMax], lo[kSymMax], bytes;  // lo[s] == up[s] for merged windows
+};
+__host__ __device__ inline uint32_t sym_win_bytes(int rows) {
+  return al16u(static_cast<uint32_t>(rows) * 8u + 32u);
+}
+__host__ __device__ inline SymLayout spmv_sym_layout(int S, const int *d) {
+  SymLayout L{};
+  uint32_t off = 0;
+  L.meta = off;
+  off += al16u(static_cast<uint32_t>(kTileRows) * 2u + 16u);
+  for (int s = 0; s < S; s++) {
+    if (s == 0) {
+      L.up[0] = L.lo[0] = off;
+      off += sym_win_bytes(kTileRows);
+    } else if (d[s] < kTileRows) {
+      L.up[s] = L.lo[s] = off;
+      off += sym_win_bytes(kTileRows + d[s]);
+    } else {
+      L.up[s] = off;
+      off += sym_win_bytes(kTileRows);
+      L.lo[s] = off;
+      off += sym_win_bytes(kTileRows);
+    }
+  }
+  L.bytes = off;
+  return L;
+}
+// the window rows of slot s's lower region [a, b) and upper region [c, e)
+__device__ __forceinline__ void sym_rows(const TileDesc &d, int ds, int s, int &a, int &b, int &c, int &e) {
+  c = d.lo;
+  e = d.hi;
+  if (s == 0) {
+    a = c;
+    b = e;
+  } else if (ds < kTileRows) {
+    a = max(d.lo - ds, 0);
+    b = d.hi;
+  } else {
+    a = max(d.lo - ds, 0);
+    b = max(d.hi - ds, 0);
+  }
+}
+
+__device__ __forceinline__ int mask_of(const uint16_t *s_mask, uint16_t m) { return s_mask[meta_pid(m)]; }
+
+// soff[s]: byte offset (from the stage base) of the tile's row lo - d[s] + tid
+// in slot s's lower window, soff[S + s] of row lo + tid in its upper window
+// (the producer computes them per stage: one shared-memory read per slot here)
+template <int S, typename ZT>
+__device__ __forceinline__ void spmv_sym_tile_body(const SpmvArgs &a, int tile, const TileDesc &d,
+                                                   const unsigned char *sb, const SymLayout &L, const int *soff,
+                                                   const uint16_t *s_mask, double *ws, bool first, double beta) {
+  const int tid = threadIdx.x, row = d.lo + tid;
+  double prod[1] = {0.0};
+  if (row < d.hi) {
+    const uint16_t *mt = staged(sb + L.meta, a.meta, d.lo, d.hi);
+    const int m = mask_of(s_mask, mt[tid]);
+    const unsigned char *sbt = sb + tid * 8;
+    double acc = 0.0;
+#pragma unroll
+    for (int s = S - 1; s >= 1; s--) {  // lower entries, most negative offset first
+      if ((m >> (S - 1 - s)) & 1) {
+        const int c = row - a.d[s];
+        acc = __dadd_rn(acc, __dmul_rn(*reinterpret_cast<const double *>(sbt + soff[s]), p_at<ZT>(a, c, first, beta)));
+      }
+    }
+    const double pown = p_at<ZT>(a, row, first, beta);
+    acc = __dadd_rn(acc, __dmul_rn(*reinterpret_cast<const double *>(sbt + soff[S]), pown));  // diagonal
+#pragma unroll
+    for (int s = 1; s < S; s++) {
+      if ((m >> (S - 1 + s)) & 1)
+        acc = __dadd_rn(acc, __dmul_rn(*reinterpret_cast<const double *>(sbt + soff[S + s]),
+                                       p_at<ZT>(a, row + a.d[s], first, beta)));
+    }
+    a.q[row] = acc;
+    if (!std::is_same<ZT, void>::value) st_keep(a.pnew + row, pown);
+    prod[0] = __dmul_rn(pown, acc);
+  }
+  const double tot = tile_tree_rows<double, 1>(prod, ws, kBarConsumers);
+  if (threadIdx.x == 0) put_part(a.part + tile, tot);
+}
+
+template <int S, bool TWO = false>
+__global__ void MPB_WS_BOUNDS_SPMV k_spmv_sym(const SpmvArgs a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ Ring R;
+  __shared__ double ws[32];
+  __shared__ uint16_t s_mask[kPatMax];
+  __shared__ int s_soff[kMaxStages][2 * kSymMax];
+  const int ns = a.g.ns;
+  const SymLayout L = spmv_sym_layout(S, a.d);
+  for (int i = threadIdx.x; i < a.g.npat; i += blockDim.x) s_mask[i] = __ldg(a.pmask + i);
+  ring_init(R, ns);
+  if (threadIdx.x >= kConsumers) {
+    const ChunkCtx ck{a.csum, a.part, a.g.ntiles, TWO ? a.g.poll : 0};
+    // every staged byte is static (U, row metadata): all of it may stream
+    // before the grid dependency wait; the dynamic part only arrives
+    auto fill = [&](int st, int tile, int part) {
+      unsigned char *stage = smem + st * L.bytes;
+      if (part != kFillDynamic) {
+        const TileDesc d = a.td[tile];
+        R.desc[st] = d;
+        R.ok[st] = 1;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        uint32_t bytes = window_bytes(a.meta, d.lo, d.hi);
+        for (int s = 0; s < S; s++) {
+          const double *us = a.U + static_cast<long long>(s) * a.n;
+          int wa, wb, wc, we;
+          sym_rows(d, a.d[s], s, wa, wb, wc, we);
+          if (wb > wa) bytes += window_bytes(us, wa, wb);
+          if (s > 0 && a.d[s] >= kTileRows) bytes += window_bytes(us, wc, we);
+        }
+        if (part == kFillAll) mbar_arrive_expect_tx(&R.full[st], bytes);
+        else mbar_expect_tx(&R.full[st], bytes);
+        tma_window(stage + L.meta, a.meta, d.lo, d.hi, &R.full[st], true);
+        for (int s = 0; s < S; s++) {
+          const double *us = a.U + static_cast<long long>(s) * a.n;
+          int wa, wb, wc, we;
+          sym_rows(d, a.d[s], s, wa, wb, wc, we);
+          if (wb > wa) tma_window(stage + L.lo[s], us, wa, wb, &R.full[st]);
+          if (s > 0 && a.d[s] >= kTileRows) tma_window(stage + L.up[s], us, wc, we, &R.full[st]);
+          // byte offsets of row (lo - d[s]) and row lo in the windows (may
+          // point before a clamped window start: those rows are never read)
+          const int skew_lo = static_cast<int>(window_of(us, wa, wb).skew);
+          s_soff[st][s] = static_cast<int>(L.lo[s]) + skew_lo + 8 * (d.lo - a.d[s] - wa);
+          if (s == 0 || a.d[s] < kTileRows) s_soff[st][S + s] = static_cast<int>(L.lo[s]) + skew_lo + 8 * (d.lo - wa);
+          else s_soff[st][S + s] = static_cast<int>(L.up[s]) + static_cast<int>(window_of(us, wc, we).skew);
+        }
+      } else {
+        mbar_arrive(&R.full[st]);
+      }
+    };
+    auto gated = [&]() { return a.st->done != 0; };
+    if (TWO && ck.poll)
+      producer_loop(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, gated, fill, ck, 1, a.td);
+    else if (threadIdx.x == kConsumers)
+      producer_loop_single(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, gated, fill, 1, a.td);
+    else
+      pdl_wait();
+    if (a.st->done) return;
+  } else {
+    pdl_wait();
+    if (a.st->done) return;
+    const int mode = a.pnew == nullptr ? 0 : (a.st->branch == 1 ? 1 : 2);
+    const bool first = a.st->first != 0;
+    const double beta = a.st->beta;
+    for (RingCursor cur;; cur.advance(ns)) {
+      const int st = cur.st;
+      mbar_wait(&R.full[st], cur.phase);
+      const int tile = R.tile[st];
+      if (tile < 0) break;
+      const TileDesc d = R.desc[st];
+      const unsigned char *sb = smem + st * L.bytes;
+      const int *soff = s_soff[st];
+      if (mode == 0) spmv_sym_tile_body<S, void>(a, tile, d, sb, L, soff, s_mask, ws, first, beta);
+      else if (mode == 1) spmv_sym_tile_body<S, float>(a, tile, d, sb, L, soff, s_mask, ws, first, beta);
+      else spmv_sym_tile_body<S, double>(a, tile, d, sb, L, soff, s_mask, ws, first, beta);
+      ring_release(R, st);
+    }
+  }
+  pdl_trigger();
+  finish_grid<16, kFinRptWs>(a.st, 1, kStepPq, ChunkCtx{a.csum, a.part, a.g.ntiles, TWO ? a.g.poll : 0}, ws);
+}
+
+// Symmetry check of pattern rows against the offset set d (S entries >= 0):
+// counts entries (row i, offset o > 0) whose value differs bitwise from row
+// i + o's value at offset -o, or whose mirror entry is missing.
+__global__ void k_sym_check(long long n, const int *sp, const double *sval, const uint16_t *meta, const int *pat,
+                            unsigned long long *bad) {
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x) {
+    const int row = static_cast<int>(r);
+    const uint16_t m = meta[row];
+    if (m == kMetaGeneric) {
+      atomicAdd(bad, 1ull);
+      continue;
+    }
+    const int *P = pat + meta_pid(m) * kPatStride;
+    const int len = pat_len(P[0]);
+    const int base = sp[row >> 5] + (row & 31);
+    for (int u = 0; u < len; u++) {
+      const int o = P[1 + u];
+      if (o == 0) continue;
+      const int c = row + o;
+      const uint16_t mc = meta[c];
+      bool found = false;
+      if (mc != kMetaGeneric) {
+        const int *Q = pat + meta_pid(mc) * kPatStride;
+        const int lc = pat_len(Q[0]);
+        const int bc = sp[c >> 5] + (c & 31);
+        for (int v = 0; v < lc; v++)
+          if (Q[1 + v] == -o) {
+            found = __double_as_longlong(sval[bc + 32 * v]) == __double_as_longlong(sval[base + 32 * u]);
+            break;
+          }
+      }
+      if (!found) atomicAdd(bad, 1ull);
+    }
+  }
+}
+
+// U_s[i] = row i's value at offset d[s] (0 where absent)
+__global__ void k_sym_build(long long n, const int *sp, const double *sval, const uint16_t *meta, const int *pat,
+                            int S, SpmvArgs da, double *U) {
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x) {
+    const int row = static_cast<int>(r);
+    const uint16_t m = meta[row];
+    for (int s = 0; s < S; s++) U[s * n + r] = 0.0;
+    if (m == kMetaGeneric) continue;
+    const int *P = pat + meta_pid(m) * kPatStride;
+    const int len = pat_len(P[0]);
+    const int base = sp[row >> 5] + (row & 31);
+    for (int u = 0; u < len; u++) {
+      const int o = P[1 + u];
+      if (o < 0) continue;
+      for (int s = 0; s < S; s++)
+        if (da.d[s] == o) U[s * n + r] = sval[base + 32 * u];
+    }
+  }
+}
+
 // x += alpha p ; r -= alpha q ; r.r partial   (solver.py:160-165)
 // Persistent; each CTA iteration streams kStreamTiles tiles with every load
 // issued up front and one barrier pair for their tile sums.
@@ -2122,10 +2372,16 @@ __global__ void __launch_bounds__(kCtaThreads)
 // the overflow count) and runs the in-block sweeps into z1.  The last CTA
 // runs kStepRrZ; if the step changes the branch, z1 is discarded and the
 // standalone first pass of the new branch runs instead (z1_gate).
+// MPB_UF_DIRECT=1 (experiment): x and q are read by the consumers straight
+// from global memory instead of being staged (two bulk copies fewer per stage)
+#ifndef MPB_UF_DIRECT
+#define MPB_UF_DIRECT 0
+#endif
+constexpr bool kUfDirect = MPB_UF_DIRECT != 0;
 template <typename T>
 __host__ __device__ inline StageLayout update_first_layout(const TileGeom &g) {
   // v0 r, v1 x, v2 p, v3 q (fp64 slices)
-  return stage_layout(g.cap_e, sizeof(T), g.max_sl, g.cols != 0, true, 8, 8, 8, 8);
+  return stage_layout(g.cap_e, sizeof(T), g.max_sl, g.cols != 0, true, 8, kUfDirect ? 0 : 8, 8, kUfDirect ? 0 : 8);
 }
 
 // Staged tile of the fused update with a multiple of 32 rows at a 32-row-
@@ -2192,7 +2448,9 @@ __device__ __forceinline__ void update_first_body(const PassArgs<T> &a, double *
     auto fill = [&](int st, int tile, int part) {
       // x (v1) and q (v3) are not read again before the next x/r update
       produce<T, double, double, double, true, double, 0xAu>(R, st, a.td, tile, a.g, L, smem + st * L.bytes,
-                                                             a.ib_sp, a.ib_col, a.ib_val, a.meta, r, x, p, q, part);
+                                                             a.ib_sp, a.ib_col, a.ib_val, a.meta, r,
+                                                             kUfDirect ? nullptr : x, p, kUfDirect ? nullptr : q,
+                                                             part);
     };
     auto gated = [&]() { return gated_off(a); };
     if (TWO && ck.poll)
@@ -2217,8 +2475,10 @@ __device__ __forceinline__ void update_first_body(const PassArgs<T> &a, double *
       const bool ok = R.ok[st] != 0;
       if (!GEN && kRowsPerThread == 1 && kFastTiles && ok && ((d.hi - d.lo) & 31) == 0 && (d.lo & 31) == 0 &&
           a.g.kib <= 7) {
-        const double *xs = staged(sb + L.v1, x, d.lo, d.hi), *ps = staged(sb + L.v2, p, d.lo, d.hi);
-        const double *qs = staged(sb + L.v3, q, d.lo, d.hi), *rs = staged(sb + L.v0, r, d.lo, d.hi);
+        const double *xs = kUfDirect ? x + d.lo : staged(sb + L.v1, x, d.lo, d.hi);
+        const double *ps = staged(sb + L.v2, p, d.lo, d.hi);
+        const double *qs = kUfDirect ? q + d.lo : staged(sb + L.v3, q, d.lo, d.hi);
+        const double *rs = staged(sb + L.v0, r, d.lo, d.hi);
         const T *val = reinterpret_cast<const T *>(sb + L.val);
         const int *spp = staged(sb + L.sp, a.ib_sp, d.s0, d.s1 + 1);
         const uint16_t *mt = staged(sb + L.meta, a.meta, d.lo, d.hi);
@@ -2237,9 +2497,9 @@ __device__ __forceinline__ void update_first_body(const PassArgs<T> &a, double *
         sq[k] = 0.0;
         rv[k] = T(0);
         if (row >= d.hi) continue;
-        const double xv = ok ? staged(sb + L.v1, x, d.lo, d.hi)[i] : x[row];
+        const double xv = (ok && !kUfDirect) ? staged(sb + L.v1, x, d.lo, d.hi)[i] : x[row];
         const double pv = ok ? staged(sb + L.v2, p, d.lo, d.hi)[i] : p[row];
-        const double qv = ok ? staged(sb + L.v3, q, d.lo, d.hi)[i] : q[row];
+        const double qv = (ok && !kUfDirect) ? staged(sb + L.v3, q, d.lo, d.hi)[i] : q[row];
         const double ro = ok ? staged(sb + L.v0, r, d.lo, d.hi)[i] : r[row];
         st_evict_first(x + row, __dadd_rn(xv, __dmul_rn(alpha, pv)));  // (read again by the next update only)
         const double rn = __dsub_rn(ro, __dmul_rn(alpha, qv));
@@ -2302,7 +2562,9 @@ __global__ void __launch_bounds__(kWtWarps * 32 + 32)
     auto fill = [&](int st, int tile, int part) {
       // x (v1) and q (v3) are not read again before the next x/r update
       produce<T, double, double, double, true, double, 0xAu>(R, st, a.td, tile, a.g, L, smem + st * L.bytes,
-                                                             a.ib_sp, a.ib_col, a.ib_val, a.meta, r, x, p, q, part);
+                                                             a.ib_sp, a.ib_col, a.ib_val, a.meta, r,
+                                                             kUfDirect ? nullptr : x, p, kUfDirect ? nullptr : q,
+                                                             part);
     };
     auto gated = [&]() { return gated_off(a); };
     if (TWO && ck.poll)
@@ -2326,9 +2588,9 @@ __global__ void __launch_bounds__(kWtWarps * 32 + 32)
       const TileDesc d = R.desc[st];
       const unsigned char *sb = smem + st * L.bytes;
       const bool ok = R.ok[st] != 0;
-      const double *xs = ok ? staged(sb + L.v1, x, d.lo, d.hi) : x + d.lo;
+      const double *xs = (ok && !kUfDirect) ? staged(sb + L.v1, x, d.lo, d.hi) : x + d.lo;
       const double *ps = ok ? staged(sb + L.v2, p, d.lo, d.hi) : p + d.lo;
-      const double *qs = ok ? staged(sb + L.v3, q, d.lo, d.hi) : q + d.lo;
+      const double *qs = (ok && !kUfDirect) ? staged(sb + L.v3, q, d.lo, d.hi) : q + d.lo;
       const double *rs = ok ? staged(sb + L.v0, r, d.lo, d.hi) : r + d.lo;
       double sq[kWtRows];
       T rv[kWtRows];

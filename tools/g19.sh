@@ -1,0 +1,8 @@
+set -u
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize.py -x -q -k "not acceptance" > gpurun_out/g19_pytest.log 2>&1; echo "pytest rc=$?"
+for v in "MPB_X=0" "MPB_NO_SYM=1"; do
+  tag=$(echo $v | tr ' =' '__')
+  env $v timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/g19_bench_$tag.json 2> gpurun_out/g19_bench_$tag.err
+  echo "$v rc=$?"
+done
