@@ -17,6 +17,7 @@ OUT = os.path.join(ROOT, "gpurun_out")
 PROF = os.path.join(ROOT, "profiles")
 
 SHORT = {"k_update_first": "update_first", "k_bjac_tile<float, 1, 0": "bjac_first", "k_bjac_tile<float, 0, 1": "bjac_last",
+         "k_bjac_tileIfLb0ELb1E": "bjac_last", "k_bjac_tileIdLb0ELb1E": "bjac_last", "k_update_firstI": "update_first",
          "k_bjac_tile<double, 1, 0": "bjac_first", "k_bjac_tile<double, 0, 1": "bjac_last",
          "k_spmv_pq": "spmv_pq", "k_update": "update", "k_pupdate": "pupdate"}
 
@@ -45,8 +46,20 @@ def launches(tag, cfg):
 
 def full(tag, cfg):
     rep = os.path.join(OUT, f"prof_{tag}_{cfg}.ncu-rep")
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-    rows = list(csv.reader(raw.splitlines()))
+    if os.path.exists(rep):
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+        rows = list(csv.reader(raw.splitlines()))
+    else:  # tools/gpu_profile2.sh: one raw CSV per hot kernel, exported on the box
+        rows = []
+        for nm in ("last", "spmv", "update_first"):
+            path = os.path.join(OUT, f"full_{tag}_{cfg}_{nm}.csv")
+            if not os.path.exists(path) or os.path.getsize(path) == 0:
+                continue
+            part = list(csv.reader(open(path)))
+            if not rows:
+                rows = part
+            else:
+                rows += part[2:]
     hdr, units = rows[0], rows[1]
 
     def get(r, k):
