@@ -263,7 +263,7 @@ int mpb_pcg_solve(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A,
  * bracketing every launch with CUDA events, using the buffers of a prior
  * mpb_pcg_solve with the same arguments (the solver state is reset to a
  * mid-solve state before each launch).  branch: 0 fp64 / 1 fp32 instance.
- * h_ms[16] receives the mean ms per launch of: 0 first BJAC pass,
+ * h_ms[18] receives the mean ms per launch of: 0 first BJAC pass,
  * 1 middle passes (all of them, 0 when k < 3), 2 last BJAC pass,
  * 3 SpMV q = A p with the fused p.q step, 4 x/r update (fused relres
  * step), 5 x/r update fused with the next iteration's first pass (what the
@@ -271,7 +271,10 @@ int mpb_pcg_solve(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A,
  * the kernels the solve runs), 7 p-update p = z + beta p; each launched
  * alone between two events ("cold").  h_ms[8 + i]: the same kernels, `reps`
  * launches back to back with programmatic dependent launch as the solve
- * graph chains them ("chained"). */
+ * graph chains them ("chained").  h_ms[16] / h_ms[17]: the wave kernel
+ * (x/r update + first pass + the next iteration's last pass, what the solve
+ * runs for fixed-branch policies with k = 2 on one GPU; 0 otherwise), cold /
+ * chained; the whole iteration (6 / 14) is then the SpMV plus the wave. */
 int mpb_profile_iteration(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A,
                           const mpb_solve_options *opt, const double *b, double *x,
                           void *workspace, int64_t workspace_bytes, int branch,

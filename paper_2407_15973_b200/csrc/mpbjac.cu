@@ -91,6 +91,11 @@ struct mpb_plan {
   double *d_U = nullptr;
   const void *sym_key = nullptr;
   bool sym_ok = false;
+  // wave kernel (k_wave): eligibility, item lag, tile-group size and each
+  // tile's dependency range in groups (mpb_plan_bind_sell)
+  bool wave_ok = false;
+  int wave_lag = 0, wave_gshift = 5, wave_ngroups = 0;
+  int2 *d_wdep = nullptr;
 };
 
 // In-process group of slab ranks on one GPU (mpb_local_group_create): the
@@ -717,6 +722,65 @@ int launch_update_first(mpb_handle *h, cudaStream_t s, const mpb_plan *p, const 
   return MPB_OK;
 }
 
+// The wave kernel (k_wave) of one fixed branch: x/r update + first pass of
+// iteration i and the last pass of iteration i+1.  z1: the first pass's
+// output (the last pass's z_in); zout: the last pass's output.
+template <typename T>
+int launch_wave(mpb_handle *h, cudaStream_t s, const mpb_plan *p, const mpb_csr *A, int t, T *z1, T *zout,
+                double *x, const double *pv, const double *q, double *r, double *part_rr, double *part_rz,
+                unsigned int *gcnt, unsigned long long *ovf_count, long long *ovf_first, SolverState *st,
+                int want_branch, bool pdl = true) {
+  if (!p->wave_ok) return MPB_ERR_LAYOUT;
+  PassArgs<T> au{};
+  au.sp = A->sell->d_sp;
+  au.sval = sell_vals<T>(A);
+  au.ib_val = ib_vals<T>(A);
+  au.ib_sp = p->d_ib_sp;
+  au.ib_col = p->d_ib_col;
+  if (au.ib_val == nullptr || au.sval == nullptr) return MPB_ERR_LAYOUT;
+  au.meta = p->d_meta;
+  au.pat = p->d_pat;
+  au.td = p->d_td;
+  au.ctr = claim_ctr(h, 1);
+  au.boff = p->d_boff;
+  au.g = geom_for<T>(p);
+  au.g.cap_e = p->max_tile_ib;
+  au.t = t;
+  au.zout = z1;
+  au.part = part_rr;
+  au.ovf_count = ovf_count;
+  au.ovf_first = ovf_first;
+  au.st = st;
+  au.want_branch = want_branch;
+  au.gate = 2;
+  PassArgs<T> al = au;
+  al.ib_sp = nullptr;
+  al.ib_col = nullptr;
+  al.ib_val = nullptr;
+  al.g = geom_for<T>(p);
+  al.g.cap_e = static_cast<int>(p->max_tile_sell);
+  al.r64 = r;
+  al.zin = z1;
+  al.zout = zout;
+  al.part = part_rz;
+  al.ovf_count = nullptr;
+  al.ovf_first = nullptr;
+  const uint32_t sb = std::max(update_first_layout<T>(au.g).bytes,
+                               stage_layout(al.g.cap_e, sizeof(T), al.g.max_sl, false, true, 0, 0, 0).bytes);
+  void (*kern)(const PassArgs<T>, const PassArgs<T>, double *, const double *, const double *, double *,
+               const WaveCtl) = nullptr;
+  if (p->ks == 7) kern = p->max_ib_row <= 3 ? k_wave<T, 7, 3> : k_wave<T, 7, 7>;
+  else kern = k_wave<T, kSlots, 7>;
+  au.g.ns = al.g.ns = pick_stages(kern, sb, kTileThreads + 32);
+  const uint32_t dyn = au.g.ns * sb;
+  const int grid = persistent_grid(kern, dyn, 2 * p->ntiles, kTileThreads + 32);
+  static const int dbg = std::getenv("MPB_WAVE_DBG") ? std::atoi(std::getenv("MPB_WAVE_DBG")) : 0;
+  const WaveCtl wc{gcnt, p->d_wdep, p->wave_lag, p->wave_gshift, dbg, static_cast<int>(p->ntiles / 32 + 4)};
+  MPB_CUDA(launch_k(pdl, kern, grid, kTileThreads + 32, dyn, s, au, al, x, pv, q, r, wc));
+  MPB_LAUNCHED(h);
+  return MPB_OK;
+}
+
 int check_csr(const mpb_csr *A) {
   if (!A || !A->row_ptr || !A->col_idx || A->n < 1) return MPB_ERR_ARG;
   if (A->n >= (int64_t(1) << 31) - 1 || A->nnz >= (int64_t(1) << 31)) return MPB_ERR_INDEX32;
@@ -772,6 +836,8 @@ struct SolveWs {
   double *res64, *dg64, *wA64, *wB64;
   float *res32, *dg32, *wA32, *wB32;
   double *part;
+  double *part2;       // wave kernel: the r.z tile partials of its last-pass items (part: r.r)
+  unsigned int *gcnt;  // wave kernel: per tile group, update items published this solve
   double *csum;        // chunk sums of the two-level dot sums (part: all slots kPartEmpty between kernels)
   SolverState *st;
   size_t bytes;
@@ -810,6 +876,8 @@ SolveWs carve(const mpb_plan *p, int64_t n, char *base, int64_t ng = 0) {
     w.wB32 = (float *)take(f);
   }
   w.part = (double *)take(sizeof(double) * (p->ntiles + 1));
+  w.part2 = (double *)take(sizeof(double) * (p->ntiles + 1));
+  w.gcnt = (unsigned int *)take(sizeof(unsigned int) * (p->ntiles / 32 + 8));
   w.csum = (double *)take(sizeof(double) * ((p->ntiles + kChunkTiles - 1) / kChunkTiles + 1));
   w.st = (SolverState *)take(sizeof(SolverState));
   w.bytes = off;
@@ -993,7 +1061,68 @@ int mpb_plan_destroy(mpb_plan *p) {
   cudaFree(p->d_ib_col);
   cudaFree(p->d_pmask);
   cudaFree(p->d_U);
+  cudaFree(p->d_wdep);
   delete p;
+  return MPB_OK;
+}
+
+// Wave kernel eligibility and dependencies (k_wave): pattern rows only,
+// every tile a multiple of 32 rows at a 32-row-aligned start (the full-tile
+// bodies), stages that hold every tile, one-level sums.  A tile's last pass
+// reads rows [lo + omin, hi - 1 + omax] (the patterns' extreme offsets); its
+// dependency range is the tile groups covering them, and the item lag
+// exceeds the farthest tile such a group reaches (plus slack for the items
+// in flight, MPB_WAVE_SLACK, default 1536 tiles).  Off by default (MPB_WAVE=1
+// enables it): on C2 the wave kernel takes 67.1 us against 64.5 us for the
+// last pass + fused update it replaces -- each publication's gpu-scope
+// release (MEMBAR.ALL.GPU) costs the SM more than the kernel boundary it
+// saves (61.2 us with an unfenced, unsafe publication; profiles/r02_notes.md).
+static int plan_wave(mpb_handle *h, mpb_plan *p, const std::vector<TileDesc> &td) {
+  p->wave_ok = false;
+  static const bool off = !(std::getenv("MPB_WAVE") && std::atoi(std::getenv("MPB_WAVE")) != 0);
+  if (off || p->large || p->ngeneric != 0 || p->npat <= 0 || two_level(p->ntiles) || p->max_ib_row > 7 ||
+      p->max_tile_sell > kStageCap || p->max_tile_ib > kStageCap)
+    return MPB_OK;
+  for (const auto &d : td)
+    if ((d.lo & 31) != 0 || ((d.hi - d.lo) & 31) != 0) return MPB_OK;
+  std::vector<int> pat(static_cast<size_t>(p->npat) * kPatStride);
+  MPB_CUDA(cudaMemcpy(pat.data(), p->d_pat, sizeof(int) * pat.size(), cudaMemcpyDeviceToHost));
+  int omin = 0, omax = 0;
+  for (int q = 0; q < p->npat; q++) {
+    const int *P = &pat[static_cast<size_t>(q) * kPatStride];
+    for (int u = 0; u < (P[0] & 0xFF); u++) {
+      omin = std::min(omin, P[1 + u]);
+      omax = std::max(omax, P[1 + u]);
+    }
+  }
+  const int64_t nt = p->ntiles, n = p->n;
+  const int gs = p->wave_gshift;
+  std::vector<int> lo(nt);
+  for (int64_t i = 0; i < nt; i++) lo[i] = td[i].lo;
+  auto tile_of = [&](int64_t row) {
+    return static_cast<int>(std::upper_bound(lo.begin(), lo.end(), static_cast<int>(row)) - lo.begin()) - 1;
+  };
+  std::vector<int2> dep(nt);
+  int64_t reach = 0;
+  for (int64_t i = 0; i < nt; i++) {
+    const int t0 = tile_of(std::max<int64_t>(0, td[i].lo + int64_t(omin)));
+    const int t1 = tile_of(std::min<int64_t>(n - 1, td[i].hi - 1 + int64_t(omax)));
+    dep[i] = make_int2(t0 >> gs, t1 >> gs);
+    const int64_t far = std::min<int64_t>(nt - 1, ((int64_t(t1 >> gs) + 1) << gs) - 1);
+    reach = std::max(reach, far - i);
+  }
+  static const int slack = std::getenv("MPB_WAVE_SLACK") ? std::atoi(std::getenv("MPB_WAVE_SLACK")) : 1536;
+  p->wave_lag = static_cast<int>(std::min<int64_t>(nt, reach + 1 + std::max(slack, 0)));
+  p->wave_ngroups = static_cast<int>((nt + (1 << gs) - 1) >> gs);
+  cudaFree(p->d_wdep);
+  p->d_wdep = nullptr;
+  MPB_CUDA(cudaMalloc(&p->d_wdep, sizeof(int2) * nt));
+  MPB_CUDA(cudaMemcpy(p->d_wdep, dep.data(), sizeof(int2) * nt, cudaMemcpyHostToDevice));
+  p->wave_ok = true;
+  if (std::getenv("MPB_VERBOSE"))
+    std::fprintf(stderr, "[mpb] wave: offsets [%d, %d], reach %lld tiles, lag %d of %lld tiles, %d groups\n", omin,
+                 omax, static_cast<long long>(reach), p->wave_lag, static_cast<long long>(nt), p->wave_ngroups);
+  (void)h;
   return MPB_OK;
 }
 
@@ -1153,7 +1282,7 @@ int mpb_plan_bind_sell(mpb_handle *h, mpb_plan *p, const mpb_sell *sell) {
       std::fprintf(stderr, " (%d rows)%s\n", rows, p->win.n ? "" : " -- not used");
     }
   }
-  return MPB_OK;
+  return plan_wave(h, p, td);
 }
 
 int64_t mpb_plan_inblock_nnz(const mpb_plan *p) { return (p && p->bound) ? p->ib_nnz : MPB_ERR_LAYOUT; }
@@ -1767,6 +1896,12 @@ static bool fused_mode(const mpb_plan *p, const mpb_solve_options *o, const Dist
   static const bool off = std::getenv("MPB_NO_FUSE") != nullptr;
   return !off && o->k >= 2 && !p->large;
 }
+// wave mode (one GPU, fixed branch, k = 2): the iteration is the SpMV and
+// the wave kernel (x/r update + first pass + the next last pass)
+static bool wave_mode(const mpb_plan *p, const mpb_solve_options *o, const DistCtx *dc) {
+  return dc == nullptr && fused_mode(p, o, dc) && o->k == 2 && p->wave_ok &&
+         (o->kind == MPB_FIXED_LOW || o->kind == MPB_UNIFORM);
+}
 
 // Standalone first passes of the policy's branches (gated on st->branch and,
 // z1_gate, on the fused update not having produced z1 already).
@@ -1806,13 +1941,14 @@ static int enqueue_iteration(mpb_handle *h, cudaStream_t s, const mpb_plan *p, c
   // adaptive policies: the branch may have changed, invalidating the fused z1
   if (fused && high && low && (rc = enqueue_first_passes(h, s, p, A, o, w, dc))) return rc;
   const int from = fused ? 1 : 0;
-  if (high) {
+  const bool wave = wave_mode(p, o, dc);  // the last pass ran in the previous wave kernel (or the prologue)
+  if (high && !wave) {
     ApplyBufs<double> bb{w.zA64, w.zB64, w.res64, w.dg64, w.wA64, w.wB64};
     rc = launch_apply<double>(h, s, p, A, o->k, o->t, w.r, nullptr, w.z64, nullptr, w.part, nullptr, nullptr, w.st,
                               0, bb, dc, from, 1 << 30, 0, pre);
     if (rc) return rc;
   }
-  if (low) {
+  if (low && !wave) {
     ApplyBufs<float> bb{w.zA32, w.zB32, w.res32, w.dg32, w.wA32, w.wB32};
     rc = launch_apply<float>(h, s, p, A, o->k, o->t, w.r, nullptr, w.z32, nullptr, w.part, &w.st->ovf_count,
                              &w.st->ovf_first, w.st, 1, bb, dc, from, 1 << 30, 0, pre);
@@ -1846,7 +1982,14 @@ static int enqueue_iteration(mpb_handle *h, cudaStream_t s, const mpb_plan *p, c
   if ((rc = launch_spmv(h, s, p, sa, pdl))) return rc;
   if (fused && (rc = halo_exchange(dc, pcur, 8, A->n, s))) return rc;  // next iteration's p_old ghosts
   if ((rc = dist_step(h, dc, w.st, kStepPq, 2, s))) return rc;
-  if (fused) {
+  if (wave) {
+    if (high && (rc = launch_wave<double>(h, s, p, A, o->t, w.zA64, w.z64, x, pcur, w.q, w.r, w.part, w.part2, w.gcnt,
+                                          nullptr, nullptr, w.st, 0, pdl)))
+      return rc;
+    if (low && (rc = launch_wave<float>(h, s, p, A, o->t, w.zA32, w.z32, x, pcur, w.q, w.r, w.part, w.part2, w.gcnt,
+                                        &w.st->ovf_count, &w.st->ovf_first, w.st, 1, pdl)))
+      return rc;
+  } else if (fused) {
     if (high && (rc = launch_update_first<double>(h, s, p, A, o->t, w.zA64, x, pcur, w.q, w.r, w.part, nullptr,
                                                   nullptr, w.st, 0, pre, pdl)))
       return rc;
@@ -2156,8 +2299,23 @@ static int solve_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, con
   k_scalar_start<<<1, 32, 0, s>>>(w.st);
   MPB_LAUNCHED(h);
   MPB_CUDA(cudaEventRecord(h->ev_t0, s));
-  // fused mode: the first iteration's first pass runs ahead of the graph
-  if (fused_mode(plan, opt, dc) && (rc = enqueue_first_passes(h, s, plan, A, opt, w, dc))) return rc;
+  // fused mode: the first iteration's first pass runs ahead of the graph;
+  // wave mode: both its passes (the wave kernels run the later ones)
+  if (wave_mode(plan, opt, dc)) {
+    MPB_CUDA(cudaMemsetAsync(w.gcnt, 0, sizeof(unsigned int) * (plan->ntiles / 32 + 8), s));
+    if (opt->kind == MPB_UNIFORM) {
+      ApplyBufs<double> bb{w.zA64, w.zB64, w.res64, w.dg64, w.wA64, w.wB64};
+      rc = launch_apply<double>(h, s, plan, A, opt->k, opt->t, w.r, nullptr, w.z64, nullptr, w.part, nullptr,
+                                nullptr, w.st, 0, bb, dc);
+    } else {
+      ApplyBufs<float> bb{w.zA32, w.zB32, w.res32, w.dg32, w.wA32, w.wB32};
+      rc = launch_apply<float>(h, s, plan, A, opt->k, opt->t, w.r, nullptr, w.z32, nullptr, w.part,
+                               &w.st->ovf_count, &w.st->ovf_first, w.st, 1, bb, dc);
+    }
+    if (rc) return rc;
+  } else if (fused_mode(plan, opt, dc) && (rc = enqueue_first_passes(h, s, plan, A, opt, w, dc))) {
+    return rc;
+  }
   h->h_state->cond = loop ? static_cast<unsigned long long>(h->cond) : 0ull;
   MPB_CUDA(cudaMemcpyAsync(&w.st->cond, &h->h_state->cond, sizeof(unsigned long long), cudaMemcpyHostToDevice, s));
   for (;;) {
@@ -2227,6 +2385,11 @@ static int solve_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, con
                    nm[k], acc[k][0] / cnt, gaps[k][gaps[k].size() / 2], gaps[k].back(), acc[k][1] / cnt,
                    acc[k][2] / cnt, acc[k][3] / cnt, cnt);
     }
+  }
+  if (wave_mode(plan, opt, dc) && std::getenv("MPB_VERBOSE")) {
+    unsigned int spins = 0;
+    MPB_CUDA(cudaMemcpy(&spins, w.gcnt + plan->ntiles / 32 + 4, sizeof(unsigned int), cudaMemcpyDeviceToHost));
+    std::fprintf(stderr, "[mpb] wave: %u dependency polls in this solve\n", spins);
   }
   const SolverState st = *h->h_state;
   if (st.error == kOk) {  // final true residual (solver.py:179-182)
@@ -2321,9 +2484,12 @@ static int profile_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, c
   *h->h_state = mid;
   MPB_CUDA(cudaMemsetAsync(w.part, 0xFF, sizeof(double) * plan->ntiles, s));  // every slot kPartEmpty
   auto reset = [&]() -> cudaError_t {
-    return cudaMemcpyAsync(w.st, h->h_state, sizeof(SolverState), cudaMemcpyHostToDevice, s);
+    cudaError_t e = cudaMemcpyAsync(w.st, h->h_state, sizeof(SolverState), cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess && plan->wave_ok)  // wave kernels: group counters match the state's epoch
+      e = cudaMemsetAsync(w.gcnt, 0, sizeof(unsigned int) * (plan->ntiles / 32 + 8), s);
+    return e;
   };
-  for (int i = 0; i < 16; i++) h_ms[i] = 0.0;  // 7: p-update; 8..15: the same, chained
+  for (int i = 0; i < 18; i++) h_ms[i] = 0.0;  // 7: p-update; 8..15: the same, chained; 16/17: wave
   const unsigned nt = static_cast<unsigned>(plan->ntiles);
   // h_ms[slot]: one launch between two events (cold: launch latency, ramp
   // and drain included); h_ms[8 + slot]: `reps` launches back to back with
@@ -2345,6 +2511,7 @@ static int profile_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, c
       total += ms;
     }
     h_ms[slot] += total / reps;
+    const int chained = slot < 8 ? 8 + slot : slot + 1;
     MPB_CUDA(reset());
     MPB_CUDA(cudaEventRecord(h->ev_t0, s));
     for (int r = 0; r < reps; r++) {
@@ -2355,7 +2522,7 @@ static int profile_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, c
     MPB_CUDA(cudaEventSynchronize(h->ev_t1));
     float ms = 0.f;
     MPB_CUDA(cudaEventElapsedTime(&ms, h->ev_t0, h->ev_t1));
-    h_ms[8 + slot] += ms / reps;
+    h_ms[chained] += ms / reps;
     return MPB_OK;
   };
   // BJAC passes of the requested instance, one pass at a time
@@ -2451,10 +2618,25 @@ static int profile_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, c
     });
     if (rc) return rc;
   }
+  // the wave kernel (x/r update + first pass + the next last pass), when the solve uses it
+  mpb_solve_options fo = *opt;
+  fo.kind = branch == 0 ? MPB_UNIFORM : MPB_FIXED_LOW;
+  const bool wave = !dist && wave_mode(plan, &fo, nullptr);
+  if (wave) {
+    rc = timed(16, [&]() -> int {
+      if (branch == 0)
+        return launch_wave<double>(h, s, plan, A, opt->t, w.zA64, w.z64, x, w.p2, w.q, w.r, w.part, w.part2, w.gcnt,
+                                   nullptr, nullptr, w.st, 0);
+      return launch_wave<float>(h, s, plan, A, opt->t, w.zA32, w.z32, x, w.p2, w.q, w.r, w.part, w.part2, w.gcnt,
+                                &w.st->ovf_count, &w.st->ovf_first, w.st, 1);
+    });
+    if (rc) return rc;
+  }
   for (int c = 0; c < 16; c += 8) {
     double *m = h_ms + c;
     const double passes = m[1] * (opt->k > 2 ? opt->k - 2 : 0) + m[2];
-    m[6] = fused ? passes + m[3] + m[5] + m[7] : m[0] + passes + m[3] + m[4] + m[7];
+    m[6] = wave ? m[3] + h_ms[16 + c / 8]
+                : (fused ? passes + m[3] + m[5] + m[7] : m[0] + passes + m[3] + m[4] + m[7]);
   }
   MPB_CUDA(cudaEventRecord(h->ev_out, s));
   MPB_CUDA(cudaStreamWaitEvent(h->user, h->ev_out, 0));

@@ -62,7 +62,7 @@ struct SolverState {
   int true_pending;
   int z1_ok;       // the fused update already ran the next first pass for `branch`
   int upd_branch;  // branch of the iteration whose x/r update is pending (set at kStepPq)
-  int pad;
+  int wave_epoch;  // wave kernels completed in this solve (their group counters' target)
   unsigned long long cond;  // while-node handle of the solve graph (0: host-polled loop)
   unsigned long long *tl;   // diagnostics (MPB_TIMELINE): per-iteration kernel timestamps, or null
 };

@@ -1146,7 +1146,9 @@ __device__ __forceinline__ void bjac_first_body(const PassArgs<T> &a, const Tile
 // the tile's slice tid / 32 at lane tid % 32): the same arithmetic as
 // bjac_tile_body without its per-row validity branches, with the inner
 // sweep unrolled to KI in-block entries.
-template <typename T, bool LAST, int KS, int KI, bool WIN = false>
+// COH: z_in was written earlier in the same kernel (the wave kernel's update
+// items): plain coherent loads instead of the read-only path.
+template <typename T, bool LAST, int KS, int KI, bool WIN = false, bool COH = false>
 __device__ __forceinline__ void bjac_tile_full(const PassArgs<T> &a, int tile, const TileDesc &d, const T *val,
                                                const int *spp, const uint16_t *mt, const double *r64t,
                                                const int *s_pat, T *s_w, double *ws,
@@ -1173,9 +1175,9 @@ __device__ __forceinline__ void bjac_tile_full(const PassArgs<T> &a, int tile, c
 #pragma unroll
     for (int u = 0; u < KS; u++) {
       v[u] = val[base + 32 * u];       // slots past len: never summed (the stage extends past them)
-      g[u] = __ldg(zr + P[1 + u]);     // table offsets past len are 0
+      g[u] = COH ? zr[P[1 + u]] : __ldg(zr + P[1 + u]);  // table offsets past len are 0
     }
-    zown = __ldg(zr);
+    zown = COH ? *zr : __ldg(zr);
   }
   T az = T(0);
 #pragma unroll
@@ -2622,6 +2624,196 @@ __global__ void __launch_bounds__(kWtWarps * 32 + 32)
   }
   pdl_trigger();
   finish_grid<8, kFinRpt>(a.st, 2, kStepRrZ, ChunkCtx{a.csum, a.part, a.g.ntiles, TWO ? a.g.poll : 0}, ws);
+}
+
+// ---------------------------------------------------------------------------
+// Wave kernel (fixed-branch policies, k = 2): the x/r update + next first
+// pass of iteration i and the last pass of iteration i+1 in ONE kernel.
+// No global reduction sits between them: the last pass of tile m needs r of
+// its own rows and z1 of the rows its pattern offsets reach (tiles within
+// `reach` of m).  Work items are claimed in the order
+//   U(0) .. U(lag-1), then U(lag) L(0) U(lag+1) L(1) ..., then the last L's
+// (U = update + first pass of a tile, L = last pass), so with lag > reach
+// every item an L item depends on was claimed before it; U items never wait,
+// hence the walk cannot deadlock (only CTAs that claimed an item hold one).
+// A U item is published when its producer recycles the stage (the consumers'
+// mbarrier release, the producer's acquire, then a gpu-scope release
+// increment of the item's tile-group counter); an L item's consumers wait
+// (acquire) until every group it reaches is complete for this launch, then
+// read r and z1 with coherent loads.  The r.r and r.z sums keep their tile
+// order; the final CTA runs the relres step of iteration i and, unless the
+// solve stopped there, the rho step of iteration i+1 -- the same steps the
+// separate kernels ran, so the solve is bit-identical.
+// ---------------------------------------------------------------------------
+struct WaveCtl {
+  unsigned int *gcnt;  // per tile group: U items published (cumulative over the solve)
+  const int2 *dep;     // per tile: first and last tile group its last pass reads
+  int lag;             // U items ahead of the L items
+  int gshift;          // tile group = tile >> gshift
+  int dbg;             // experiments (MPB_WAVE_DBG): 1 no dependency waits (unsafe), 2 relaxed publish
+                       // (unsafe), 4 count the wait polls in gcnt[spin_slot]
+  int spin_slot;
+};
+
+__device__ __forceinline__ int2 wave_item(int j, int nt, int lag) {  // (kind 0 U / 1 L, tile)
+  if (j < lag) return make_int2(0, j);
+  const int k = j - lag, nb = 2 * (nt - lag);
+  if (k < nb) return (k & 1) ? make_int2(1, k >> 1) : make_int2(0, lag + (k >> 1));
+  return make_int2(1, nt - lag + (k - nb));
+}
+
+__device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int *p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <typename T, int KS, int KI>
+__global__ void __launch_bounds__(kTileThreads + 32)
+    k_wave(const PassArgs<T> au, const PassArgs<T> al, double *x, const double *p, const double *q, double *r,
+           const WaveCtl wc) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ Ring R;
+  __shared__ int s_kind[kMaxStages];
+  __shared__ T s_w[kTileRows];
+  __shared__ double ws[32];
+  __shared__ int s_pat[kPatMax * kPatStride];
+  const int ns = au.g.ns, nt = au.g.ntiles;
+  const StageLayout Lu = update_first_layout<T>(au.g);
+  const StageLayout Ll = stage_layout(al.g.cap_e, sizeof(T), al.g.max_sl, false, true, 0, 0, 0);
+  const uint32_t sbytes = max(Lu.bytes, Ll.bytes);
+  load_patterns(s_pat, au.pat, au.g.npat);
+  ring_init(R, ns);
+  if (threadIdx.x >= kTileThreads) {  // producer warp (lane 0 walks the items)
+    pdl_wait();
+    if (gated_off(au)) return;
+    if (threadIdx.x != kTileThreads) return;
+    const unsigned int total = 2u * static_cast<unsigned int>(nt);
+    auto claim = [&]() -> int {
+      const unsigned int v = atomicAdd(au.ctr, 1u);
+      if (v == total + gridDim.x - 1u) atomicExch(au.ctr, 0u);
+      return v < total ? static_cast<int>(v) : -1;
+    };
+    auto publish_tile = [&](int tile) {  // a finished U item (its stage's empty barrier acquired)
+      if (wc.dbg & 2)
+        asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(wc.gcnt + (tile >> wc.gshift)) : "memory");
+      else
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(wc.gcnt + (tile >> wc.gshift)) : "memory");
+    };
+    auto publish = [&](int s) {
+      if (s_kind[s] == 0 && R.tile[s] >= 0) publish_tile(R.tile[s]);
+    };
+    auto fill = [&](int s, int2 it) {
+      unsigned char *stage = smem + s * sbytes;
+      R.tile[s] = it.y;
+      s_kind[s] = it.x;
+      if (it.x == 0)
+        produce<T, double, double, double, true, double, 0xAu>(R, s, au.td, it.y, au.g, Lu, stage, au.ib_sp,
+                                                               au.ib_col, au.ib_val, au.meta, r, x, p, q);
+      else
+        produce<T, double, double, double>(R, s, al.td, it.y, al.g, Ll, stage, al.sp, al.scol, al.sval, al.meta,
+                                           static_cast<const double *>(nullptr), static_cast<const double *>(nullptr),
+                                           static_cast<const double *>(nullptr));
+    };
+    int st = 0, rnd = 0;
+    int cur = claim();
+    for (;;) {
+      int done_tile = -1;  // U item the consumers just finished in stage st
+      if (rnd > 0) {
+        mbar_wait_sleep(&R.empty[st], (rnd - 1) & 1);
+        if (s_kind[st] == 0) done_tile = R.tile[st];
+      }
+      if (cur < 0) {
+        if (done_tile >= 0) publish_tile(done_tile);
+        break;
+      }
+      const int2 it = wave_item(cur, nt, wc.lag);
+      fill(st, it);  // the refill's copies first, then the (fenced) publication
+      if (done_tile >= 0) publish_tile(done_tile);
+      cur = claim();
+      if (cur >= 0) prefetch_desc(au.td, wave_item(cur, nt, wc.lag).y);
+      if (++st == ns) {
+        st = 0;
+        rnd++;
+      }
+    }
+    R.tile[st] = -1;  // end marker (stage st is free)
+    mbar_arrive(&R.full[st]);
+    // publish the items still in flight, in the consumers' order
+    for (int k = 1; k < ns; k++) {
+      const int s = (st + k) % ns;
+      const int fills = s > st ? rnd : rnd + 1;  // times stage s was filled
+      if (fills == 0) continue;
+      mbar_wait_sleep(&R.empty[s], (fills - 1) & 1);
+      publish(s);
+    }
+  } else {
+    pdl_wait();
+    if (gated_off(au)) return;
+    const double alpha = au.st->alpha;
+    const unsigned int epoch1 = static_cast<unsigned int>(au.st->wave_epoch) + 1u;
+    for (RingCursor cur;; cur.advance(ns)) {
+      const int st = cur.st;
+      mbar_wait(&R.full[st], cur.phase);
+      const int tile = R.tile[st];
+      if (tile < 0) break;
+      const TileDesc d = R.desc[st];
+      const unsigned char *sb = smem + st * sbytes;
+      if (s_kind[st] == 0) {
+        update_first_full<T, KI>(au, tile, d, alpha, x, r, staged(sb + Lu.v1, x, d.lo, d.hi),
+                                 staged(sb + Lu.v2, p, d.lo, d.hi), staged(sb + Lu.v3, q, d.lo, d.hi),
+                                 staged(sb + Lu.v0, r, d.lo, d.hi), reinterpret_cast<const T *>(sb + Lu.val),
+                                 staged(sb + Lu.sp, au.ib_sp, d.s0, d.s1 + 1), staged(sb + Lu.meta, au.meta, d.lo, d.hi),
+                                 s_pat, s_w, ws);
+      } else {
+        if (threadIdx.x < 32 && !(wc.dbg & 1)) {  // every tile group the pass reads: complete for this launch
+          const int2 dg = wc.dep[tile];
+          for (int g = dg.x + static_cast<int>(threadIdx.x); g <= dg.y; g += 32) {
+            const unsigned int gsz = static_cast<unsigned int>(min(1 << wc.gshift, nt - (g << wc.gshift)));
+            const unsigned int target = epoch1 * gsz;
+            while (ld_acquire_u32(wc.gcnt + g) < target) {
+              if (wc.dbg & 4) atomicAdd(wc.gcnt + wc.spin_slot, 1u);
+              __nanosleep(64);
+            }
+          }
+        }
+        named_sync(kBarConsumers, kTileThreads);
+        bjac_tile_full<T, true, KS, KI, false, true>(al, tile, d, reinterpret_cast<const T *>(sb + Ll.val),
+                                                    staged(sb + Ll.sp, al.sp, d.s0, d.s1 + 1),
+                                                    staged(sb + Ll.meta, al.meta, d.lo, d.hi), al.r64 + d.lo,
+                                                    s_pat, s_w, ws);
+      }
+      ring_release(R, st);
+    }
+  }
+  pdl_trigger();
+  // final CTA: relres step of iteration i, then (unless the solve stopped) rho of i+1
+  SolverState *gst = au.st;
+  if (!grid_last(&gst->ticket[2])) return;
+  __shared__ __align__(16) unsigned long long s_state[kStWords];
+  if (threadIdx.x < kStWords) s_state[threadIdx.x] = __ldcg(reinterpret_cast<const unsigned long long *>(gst) + threadIdx.x);
+  SolverState *L = reinterpret_cast<SolverState *>(s_state);
+  const double rr = fin_sum<8, 1>(au.part, nt, ws);  // (its barriers publish s_state)
+  if (threadIdx.x == 0) scalar_step_body(kStepRrZ, rr, L);
+  __syncthreads();
+  if (!L->done) {
+    const double rz = fin_sum<8, 1>(al.part, nt, ws);
+    if (threadIdx.x == 0) scalar_step_body(kStepRho, rz, L);
+  }
+  if (threadIdx.x == 0) {
+    L->wave_epoch++;
+    gst->ticket[2] = 0u;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {  // the changed state back (state_store's ranges)
+    unsigned long long *dst = reinterpret_cast<unsigned long long *>(gst);
+    constexpr int a1 = static_cast<int>(offsetof(SolverState, tr_relres) / 8);
+    constexpr int b0 = static_cast<int>(offsetof(SolverState, dist) / 8), b1 = static_cast<int>(offsetof(SolverState, cond) / 8);
+    for (int i = threadIdx.x; i < a1 + (b1 - b0); i += 32) {
+      const int w = i < a1 ? i : b0 + (i - a1);
+      dst[w] = s_state[w];
+    }
+  }
 }
 
 // res = b - A x (or b), optionally stored; res.res partial; the last CTA runs

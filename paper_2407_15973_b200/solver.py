@@ -388,7 +388,7 @@ def profile_iteration(A: SparseMatrix, mp: MixedPreconditioner, *,
     opt.k, opt.t = P.k, P.t
     opt.res_tol = float(config.res_tol)
     opt.max_iter = cap
-    out = (C.c_double * 16)()
+    out = (C.c_double * 18)()
     if n_global is None:    # one GPU: the kernels pcg_solve runs (fused iteration)
         _lib.check(h.lib.mpb_profile_iteration(
             h.ptr, P.plan.ptr, C.byref(s), C.byref(opt), _lib.ptr(bd), _lib.ptr(x),
@@ -403,4 +403,5 @@ def profile_iteration(A: SparseMatrix, mp: MixedPreconditioner, *,
              "update_first", "iteration", "pupdate")
     res = {k: float(out[i]) for i, k in enumerate(names)}
     res.update({k + "_chained": float(out[8 + i]) for i, k in enumerate(names)})
+    res["wave"], res["wave_chained"] = float(out[16]), float(out[17])
     return res
