@@ -38,6 +38,14 @@
 namespace mpb {
 
 constexpr int kSlots = 9;                      // register-resident row entries (stencils, 3-T rows)
+// Offset-slot ("DIA") layout of 7-point stencil plans: every row pattern's
+// column offsets are a subset of the same kDiaSlots ascending offsets, so
+// slot k of EVERY row is the entry at column row + doff[k] (absent entries:
+// value 0 and a cleared bit in the row's presence mask).  Stored order =
+// ascending column = ascending slot, so a row sum over the present slots is
+// the same sequence of roundings as over the stored entries.
+constexpr int kDiaSlots = 7;
+constexpr int kDiaDiag = 3;                    // the diagonal's slot (offset 0)
 #ifndef MPB_ROWS_PER_THREAD
 #define MPB_ROWS_PER_THREAD 1
 #endif
@@ -369,6 +377,7 @@ struct TileGeom {
   int cols;    // stages carry a column region (the plan has generic rows)
   int npat;    // row patterns in the table
   int kib;     // most in-block entries of a row
+  int ub;      // every block has this many rows (0: blocks differ)
 };
 
 // Byte offsets of one shared-memory stage.
@@ -799,6 +808,11 @@ struct PassArgs {
                          // 2: st->upd_branch (fused update: the step inside may change st->branch)
   int pdl;               // host side: launch with programmatic serialization
   WinSet win;            // z_in gather windows (passes after the first; n == 0: none)
+  // offset-slot ("DIA") layout of stencil plans (k_bjac_dia; null: not available)
+  const T *dval;             // values, slot k of row r at (r / 32) * 32 kDiaSlots + 32 k + r % 32
+  const uint16_t *dmeta;     // per row: present slots | in-block slots << 8
+  int doff[8];               // column offset of slot k (doff[kDiaDiag] == 0), ascending
+  int ibany;                 // slots that are in-block in at least one row
 };
 
 template <typename T>
@@ -1210,6 +1224,111 @@ __device__ __forceinline__ void bjac_tile_full(const PassArgs<T> &a, int tile, c
   }
 }
 
+// Warp-per-block tile of a pass after the first (kernels with 4 consumer
+// warps, RPT = 2): the partition's blocks all have 64 rows, so block w of the
+// tile is rows [lo + 64 w, lo + 64 w + 64) and consumer warp w owns it, two
+// rows per lane (tile rows 64 w + lane and 64 w + 32 + lane: SELL slices 2 w
+// and 2 w + 1).  In-block neighbours never leave the warp's rows, so the inner
+// sweeps synchronise with __syncwarp only and the consumer warps of a CTA run
+// their blocks independently -- no CTA-wide barrier per sweep or per tile sum.
+// The tile's r.z sum keeps the order of include/mpbjac_order.h: virtual warp
+// 2 w + k butterflies rows 64 w + 32 k .. + 31 into wsum[2 w + k]; the warp
+// that arrives last on the stage's counter butterflies the 8 warp sums padded
+// with +0.  Same arithmetic per row as bjac_tile_full.
+template <typename T, bool LAST, int KS, int KI>
+__device__ __forceinline__ void bjac_tile_wb(const PassArgs<T> &a, int tile, const TileDesc &d, const T *val,
+                                             const int *spp, const uint16_t *mt, const double *r64t,
+                                             const int *s_pat, T *s_w, double *wsum, unsigned int *wcnt) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool active = 64 * warp < d.hi - d.lo;  // warp-uniform: the tile holds (hi - lo) / 64 blocks
+  double s[2] = {0.0, 0.0};
+  if (active) {
+    int ti[2], base[2], i0[2], i1[2];
+    const int *P[2];
+    T v[2][KS], g[2][KS], zown[2], res[2], dd[2], w[2];
+    int len[2];
+#pragma unroll
+    for (int k = 0; k < 2; k++) {
+      ti[k] = 64 * warp + 32 * k + lane;
+      base[k] = spp[2 * warp + k] - d.e0 + lane;
+      const uint16_t m = mt[ti[k]];
+      P[k] = s_pat + meta_pid(m) * kPatStride;
+      i0[k] = meta_i0(m);
+      i1[k] = meta_i1(m);
+    }
+#pragma unroll
+    for (int k = 0; k < 2; k++) {
+      const T *zr = a.zin + d.lo + ti[k];
+#pragma unroll
+      for (int u = 0; u < KS; u++) {
+        v[k][u] = val[base[k] + 32 * u];       // slots past len: never summed
+        g[k][u] = __ldg(zr + P[k][1 + u]);     // table offsets past len are 0
+      }
+      zown[k] = __ldg(zr);
+    }
+#pragma unroll
+    for (int k = 0; k < 2; k++) {
+      const int hdr = P[k][0];
+      len[k] = pat_len(hdr);
+      T az = T(0);
+#pragma unroll
+      for (int u = 0; u < KS; u++)
+        if (u < len[k]) az = add_rn(az, mul_rn(v[k][u], g[k][u]));
+      dd[k] = val[base[k] + 32 * pat_dpos(hdr)];
+      res[k] = sub_rn(narrow_or_copy<T>(r64t[ti[k]]), az);
+      w[k] = div_rn(res[k], dd[k]);
+      s_w[ti[k]] = w[k];
+    }
+    for (int sw = 1; sw < a.t; sw++) {
+      __syncwarp();
+      T acc[2];
+#pragma unroll
+      for (int k = 0; k < 2; k++) {
+        acc[k] = T(0);
+#pragma unroll
+        for (int j = 0; j < KI; j++) {
+          const int jj = i0[k] + j;
+          if (jj < i1[k]) acc[k] = add_rn(acc[k], mul_rn(val[base[k] + 32 * jj], s_w[ti[k] + P[k][1 + jj]]));
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < 2; k++) {
+        w[k] = add_rn(w[k], div_rn(sub_rn(res[k], acc[k]), dd[k]));
+        s_w[ti[k]] = w[k];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 2; k++) {
+      const int row = d.lo + ti[k];
+      const T zo = add_rn(zown[k], w[k]);
+      if (a.zout != nullptr) st_keep(a.zout + row, zo);
+      if (a.zout64 != nullptr) a.zout64[row] = static_cast<double>(zo);
+      if (LAST && a.part != nullptr) s[k] = __dmul_rn(r64t[ti[k]], static_cast<double>(zo));
+    }
+  }
+  if (LAST && a.part != nullptr) {
+#pragma unroll
+    for (int k = 0; k < 2; k++) {
+      s[k] = warp_bfly(s[k]);
+      if (lane == 0) wsum[2 * warp + k] = s[k];
+    }
+    __syncwarp();
+    unsigned int old = 0;
+    if (lane == 0)
+      asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(smem_u32(wcnt)) : "memory");
+    old = __shfl_sync(0xffffffffu, old, 0);
+    if (old == kTileThreads / 64 - 1) {  // the tile's last warp: every warp sum is stored
+      double r = lane < kTileThreads / 32 ? wsum[lane] : 0.0;
+      r = warp_bfly(r);
+      if (lane == 0) {
+        *wcnt = 0u;
+        put_part(a.part + tile, r);
+      }
+    }
+  }
+}
+
 template <typename T, bool FIRST, bool R64>
 __host__ __device__ inline StageLayout bjac_layout(const TileGeom &g) {
   // v0: the residual slice
@@ -1270,6 +1389,11 @@ __global__ void MPB_TILE_BOUNDS(RPT) k_bjac_tile(const PassArgs<T> a) {
   __shared__ double ws[32];
   __shared__ int s_pat[kPatMax * kPatStride];
   __shared__ int s_zoff[WIN ? kPatMax * KS + 1 : 1];
+  // warp-per-block tiles (bjac_tile_wb): per-stage warp sums and arrival counters
+  constexpr bool kWb = !FIRST && !GEN && RPT == 2 && R64 && !WIN && !MPB_DEFER_TREE;
+  __shared__ double s_wsum[kWb ? kMaxStages * (kTileThreads / 32) : 1];
+  __shared__ unsigned int s_wcnt[kMaxStages];
+  if (threadIdx.x < kMaxStages) s_wcnt[threadIdx.x] = 0u;  // (published by ring_init's barrier)
 #ifdef MPB_TIMELINE
   const unsigned long long t_entry = globaltimer_now();
 #endif
@@ -1345,7 +1469,18 @@ __global__ void MPB_TILE_BOUNDS(RPT) k_bjac_tile(const PassArgs<T> a) {
       } else {
         const int *col = scols ? reinterpret_cast<const int *>(sb + L.col) : a.scol + d.e0;
         constexpr bool kFast = !FIRST && !GEN && RPT == 1 && R64 && !MPB_DEFER_TREE;
-        if (kFast && ok && kFastTiles && ((d.hi - d.lo) & 31) == 0 && (d.lo & 31) == 0 && a.g.kib <= 7) {
+        if (kWb && ok && a.g.ub == 64 && ((d.hi - d.lo) & 63) == 0 && (d.lo & 63) == 0 && a.g.kib <= 7) {
+          const T *val = reinterpret_cast<const T *>(sb + L.val);
+          const int *spp = staged(sb + L.sp, a.sp, d.s0, d.s1 + 1);
+          const uint16_t *mt = staged(sb + L.meta, a.meta, d.lo, d.hi);
+          const double *r64t = staged(sb + L.v0, a.r64, d.lo, d.hi);
+          if (a.g.kib <= 3)
+            bjac_tile_wb<T, LAST, KS, 3>(a, tile, d, val, spp, mt, r64t, s_pat, s_w, s_wsum + st * (kTileThreads / 32),
+                                         s_wcnt + st);
+          else
+            bjac_tile_wb<T, LAST, KS, 7>(a, tile, d, val, spp, mt, r64t, s_pat, s_w, s_wsum + st * (kTileThreads / 32),
+                                         s_wcnt + st);
+        } else if (kFast && ok && kFastTiles && ((d.hi - d.lo) & 31) == 0 && (d.lo & 31) == 0 && a.g.kib <= 7) {
           const T *val = reinterpret_cast<const T *>(sb + L.val);
           const int *spp = staged(sb + L.sp, a.sp, d.s0, d.s1 + 1);
           const uint16_t *mt = staged(sb + L.meta, a.meta, d.lo, d.hi);
@@ -1378,6 +1513,237 @@ __global__ void MPB_TILE_BOUNDS(RPT) k_bjac_tile(const PassArgs<T> a) {
   pdl_trigger();  // dependents may launch into the SMs this grid drains
   if (LAST && a.part != nullptr)
     finish_grid<16, kFinRpt>(a.st, 0, kStepRho, ChunkCtx{a.csum, a.part, a.g.ntiles, TWO ? a.g.poll : 0}, ws);
+}
+
+// ---------------------------------------------------------------------------
+// Offset-slot pass after the first, warp per 64-row block (k_bjac_dia).
+//
+// For plans whose row patterns all draw their column offsets from the same
+// kDiaSlots offsets (7-point stencils) and whose blocks all have 64 rows.
+// The pass streams the offset-slot value array (PassArgs::dval) instead of
+// the SELL values: no slice pointers, no pattern ids, no pattern-table
+// lookups and no dynamic slot indices -- a row's slot k is at a fixed
+// shared-memory offset, its column is row + doff[k] (kernel constants), its
+// diagonal is slot kDiaDiag, and what the row has / which of it is in-block
+// is one 16-bit mask.  Consumer warp w owns block w of the tile, two rows
+// per lane (bjac_tile_wb's mapping and tile-sum order); the arithmetic per
+// row is bjac_tile_full's: res = r - sum over present slots in ascending
+// slot (= stored) order, w = res / d, t - 1 masked sweeps, z = z_in + w.
+// IBM: slots that may be in-block (compile time; others are never tested).
+// ---------------------------------------------------------------------------
+// v is "defined" without an instruction: its value is whatever the register
+// held.  For operands that are only used under the same predicate as their
+// real definition (saves the zero-initialising move per predicated load).
+__device__ __forceinline__ void undefined_value(float &v) { asm volatile("" : "=f"(v)); }
+__device__ __forceinline__ void undefined_value(double &v) { asm volatile("" : "=d"(v)); }
+
+template <typename T>
+__host__ __device__ constexpr uint32_t dia_stage_bytes() {
+  return kTileRows * kDiaSlots * sizeof(T) + kTileRows * 2u + kTileRows * 8u;  // values, masks, fp64 residual
+}
+
+template <typename T, bool LAST, int IBM>
+__device__ __forceinline__ void dia_tile_wb(const PassArgs<T> &a, const int (&off)[kDiaSlots], int tile, int lo,
+                                            int nrows, const T *val, const uint16_t *dm, const double *r64t,
+                                            T *s_w, double *wsum, unsigned int *wcnt) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool active = 64 * warp < nrows;  // warp-uniform: the tile holds nrows / 64 blocks
+  double s[2] = {0.0, 0.0};
+  if (active) {
+    T v[2][kDiaSlots], g[2][kDiaSlots], res[2], w[2];
+    unsigned int m[2];
+    int ti[2];
+#pragma unroll
+    for (int k = 0; k < 2; k++) {
+      ti[k] = 64 * warp + 32 * k + lane;
+      m[k] = dm[ti[k]];
+    }
+#pragma unroll
+    for (int k = 0; k < 2; k++) {
+      const T *vb = val + (2 * warp + k) * (32 * kDiaSlots) + lane;
+      const T *zr = a.zin + lo + ti[k];
+#pragma unroll
+      for (int u = 0; u < kDiaSlots; u++) {
+        v[k][u] = vb[32 * u];
+        undefined_value(g[k][u]);  // (an absent slot's product is computed and never added)
+        if ((m[k] >> u) & 1u) g[k][u] = __ldg(zr + off[u]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 2; k++) {
+      T az = T(0);
+#pragma unroll
+      for (int u = 0; u < kDiaSlots; u++)
+        if ((m[k] >> u) & 1u) az = add_rn(az, mul_rn(v[k][u], g[k][u]));
+      res[k] = sub_rn(narrow_or_copy<T>(r64t[ti[k]]), az);
+      w[k] = div_rn(res[k], v[k][kDiaDiag]);
+      s_w[ti[k]] = w[k];
+    }
+    for (int sw = 1; sw < a.t; sw++) {
+      __syncwarp();
+      T acc[2];
+#pragma unroll
+      for (int k = 0; k < 2; k++) {
+        acc[k] = T(0);
+#pragma unroll
+        for (int u = 0; u < kDiaSlots; u++)
+          if ((IBM >> u) & 1) {
+            // acc is never -0 (it starts at +0), so adding +0 for a slot that is not in-block changes nothing
+            const bool in = (m[k] >> (8 + u)) & 1u;
+            T sv;
+            undefined_value(sv);
+            if (in) sv = s_w[ti[k] + off[u]];
+            acc[k] = add_rn(acc[k], in ? mul_rn(v[k][u], sv) : T(0));
+          }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < 2; k++) {
+        w[k] = add_rn(w[k], div_rn(sub_rn(res[k], acc[k]), v[k][kDiaDiag]));
+        s_w[ti[k]] = w[k];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 2; k++) {
+      const int row = lo + ti[k];
+      const T zo = add_rn(g[k][kDiaDiag], w[k]);  // (the diagonal's gather is the row's own z_in)
+      if (a.zout != nullptr) st_keep(a.zout + row, zo);
+      if (a.zout64 != nullptr) a.zout64[row] = static_cast<double>(zo);
+      if (LAST && a.part != nullptr) s[k] = __dmul_rn(r64t[ti[k]], static_cast<double>(zo));
+    }
+  }
+  if (LAST && a.part != nullptr) {
+#pragma unroll
+    for (int k = 0; k < 2; k++) {
+      s[k] = warp_bfly(s[k]);
+      if (lane == 0) wsum[2 * warp + k] = s[k];
+    }
+    __syncwarp();
+    unsigned int old = 0;
+    if (lane == 0)
+      asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(smem_u32(wcnt)) : "memory");
+    old = __shfl_sync(0xffffffffu, old, 0);
+    if (old == kTileThreads / 64 - 1) {  // the tile's last warp: every warp sum is stored
+      double r = lane < kTileThreads / 32 ? wsum[lane] : 0.0;
+      r = warp_bfly(r);
+      if (lane == 0) {
+        *wcnt = 0u;
+        put_part(a.part + tile, r);
+      }
+    }
+  }
+}
+
+template <typename T, bool LAST, bool TWO, int IBM>
+__global__ void __launch_bounds__(kTileThreads / 2 + 32) k_bjac_dia(const PassArgs<T> a) {
+  constexpr int NC = kTileThreads / 2;
+  constexpr int kFinRpt = NC >= kFinThreads ? 1 : kFinThreads / NC;
+  constexpr uint32_t kVal = kTileRows * kDiaSlots * sizeof(T), kMeta = kTileRows * 2u;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ Ring R;
+  __shared__ T s_w[kTileRows];
+  __shared__ double ws[32];
+  __shared__ double s_wsum[kMaxStages * (kTileThreads / 32)];
+  __shared__ unsigned int s_wcnt[kMaxStages];
+  if (threadIdx.x < kMaxStages) s_wcnt[threadIdx.x] = 0u;  // (published by ring_init's barrier)
+  const int ns = a.g.ns;
+  ring_init(R, ns, NC);
+  if (threadIdx.x >= NC) {  // producer warp
+    const ChunkCtx ck{(TWO && LAST && a.part != nullptr && a.st != nullptr) ? a.csum : nullptr, a.part, a.g.ntiles,
+                      TWO ? a.g.poll : 0};
+    auto fill = [&](int st, int tile, int part) {
+      TileDesc d;
+      if (part != kFillDynamic) {
+        d = a.td[tile];
+        R.desc[st] = d;
+        R.ok[st] = 1;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      } else {
+        d = R.desc[st];
+      }
+      const uint32_t rows = static_cast<uint32_t>(d.hi - d.lo);  // a multiple of 64
+      const uint32_t sbytes = rows * (kDiaSlots * static_cast<uint32_t>(sizeof(T)) + 2u), dbytes = rows * 8u;
+      unsigned char *stage = smem + st * dia_stage_bytes<T>();
+      if (part == kFillAll) mbar_arrive_expect_tx(&R.full[st], sbytes + dbytes);
+      if (part == kFillStatic) mbar_expect_tx(&R.full[st], sbytes);
+      if (part != kFillDynamic) {
+        bulk_g2s_stream(stage, a.dval + static_cast<long long>(kDiaSlots) * d.lo,
+                        rows * kDiaSlots * static_cast<uint32_t>(sizeof(T)), &R.full[st]);
+        bulk_g2s(stage + kVal, a.dmeta + d.lo, rows * 2u, &R.full[st]);
+      }
+      if (part == kFillStatic) return;
+      if (part == kFillDynamic) mbar_arrive_expect_tx(&R.full[st], dbytes);
+      bulk_g2s(stage + kVal + kMeta, a.r64 + d.lo, dbytes, &R.full[st]);
+    };
+    auto gated = [&]() { return gated_off(a); };
+    if (TWO && ck.csum != nullptr && ck.poll)
+      producer_loop(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, gated, fill, ck, 1, a.td);
+    else if (threadIdx.x == NC)
+      producer_loop_single(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, gated, fill, 1, a.td);
+    else
+      pdl_wait();
+    if (gated_off(a)) return;
+  } else {
+    pdl_wait();
+    if (gated_off(a)) return;
+    if (LAST && threadIdx.x == 0) tl_mark(a.st, 0, 0, false);
+    int off[kDiaSlots];  // the slot offsets, register-resident (not re-read from the parameter bank per gather)
+#pragma unroll
+    for (int u = 0; u < kDiaSlots; u++) {
+      off[u] = a.doff[u];
+      asm volatile("" : "+r"(off[u]));
+    }
+    for (RingCursor cur;; cur.advance(ns)) {
+      const int st = cur.st;
+      mbar_wait(&R.full[st], cur.phase);
+      const int tile = R.tile[st];
+      if (tile < 0) break;
+      const int lo = R.desc[st].lo, nrows = R.desc[st].hi - lo;
+      const unsigned char *sb = smem + st * dia_stage_bytes<T>();
+      dia_tile_wb<T, LAST, IBM>(a, off, tile, lo, nrows, reinterpret_cast<const T *>(sb),
+                                reinterpret_cast<const uint16_t *>(sb + kVal),
+                                reinterpret_cast<const double *>(sb + kVal + kMeta), s_w,
+                                s_wsum + st * (kTileThreads / 32), s_wcnt + st);
+      ring_release(R, st);
+    }
+    if (LAST && threadIdx.x == 0) tl_mark(a.st, 0, 1, true);
+  }
+  pdl_trigger();  // dependents may launch into the SMs this grid drains
+  if (LAST && a.part != nullptr)
+    finish_grid<16, kFinRpt>(a.st, 0, kStepRho, ChunkCtx{a.csum, a.part, a.g.ntiles, TWO ? a.g.poll : 0}, ws);
+}
+
+// Setup: per-row masks of the offset-slot layout from the row metadata
+// (pattern id, in-block slot range) and pslot[pid * kSlots + j] = the
+// offset slot of the pattern's j-th stored entry; any[0] collects the slots
+// that are in-block somewhere.
+__global__ void k_dia_meta(long long n, const uint16_t *meta, const int *pat, const signed char *pslot,
+                           uint16_t *dmeta, unsigned int *any) {
+  unsigned int seen = 0u;
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x) {
+    const uint16_t m = meta[r];
+    const int pid = meta_pid(m), len = pat_len(pat[pid * kPatStride]);
+    unsigned int have = 0u, inb = 0u;
+    for (int j = 0; j < len; j++) {
+      const unsigned int bit = 1u << pslot[pid * kSlots + j];
+      have |= bit;
+      if (j >= meta_i0(m) && j < meta_i1(m)) inb |= bit;
+    }
+    dmeta[r] = static_cast<uint16_t>(have | (inb << 8));
+    seen |= inb;
+  }
+  if (seen) atomicOr(any, seen);
+}
+
+// Setup: SELL-32 values into the offset-slot layout (out zeroed before)
+template <typename E>
+__global__ void k_dia_pack(long long n, const int *sp, const E *sval, const uint16_t *meta, const int *pat,
+                           const signed char *pslot, E *out) {
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x) {
+    const int pid = meta_pid(meta[r]), len = pat_len(pat[pid * kPatStride]);
+    const long long src = sp[r >> 5] + (r & 31), dst = (r >> 5) * (32 * kDiaSlots) + (r & 31);
+    for (int j = 0; j < len; j++) out[dst + 32 * pslot[pid * kSlots + j]] = sval[src + 32 * j];
+  }
 }
 
 // ---------------------------------------------------------------------------
