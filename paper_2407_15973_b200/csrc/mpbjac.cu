@@ -102,6 +102,7 @@ struct mpb_plan {
   uint16_t *d_dmeta = nullptr;
   signed char *d_pslot = nullptr;
   int64_t dia_at = 0, dia_entries = 0;
+  int64_t near_at = 0, near_entries = 0;  // the near slots alone (0 entries: some in-block entry sits elsewhere)
   // wave kernel (k_wave): eligibility, item lag, tile-group size and each
   // tile's dependency range in groups (mpb_plan_bind_sell)
   bool wave_ok = false;
@@ -669,6 +670,7 @@ template <typename T>
 void bind_dia(PassArgs<T> &a, const mpb_plan *p) {
   if (!p->dia_ok || a.ib_val == nullptr) return;
   a.dval = a.ib_val + p->dia_at;
+  a.dnear = p->near_entries > 0 ? a.ib_val + p->near_at : nullptr;
   a.dmeta = p->d_dmeta;
   for (int u = 0; u < kDiaSlots; u++) a.doff[u] = p->dia_off[u];
   a.ibany = p->dia_ibany;
@@ -758,6 +760,18 @@ int launch_update_first(mpb_handle *h, cudaStream_t s, const mpb_plan *p, const 
   a.want_branch = want_branch;
   a.gate = 2;
   a.prefetch = prefetch;
+  bind_dia(a, p);
+  if (a.dnear != nullptr && a.part != nullptr && st != nullptr) {  // offset-slot layout, warp per block
+    constexpr int threads = kTileThreads / 2 + 32;
+    constexpr uint32_t sb = dia_uf_stage_bytes<T>();
+    auto kern = two_level(p->ntiles) ? k_update_first_dia<T, true> : k_update_first_dia<T, false>;
+    a.g.ns = pick_stages(kern, sb, threads);
+    const uint32_t dyn = a.g.ns * sb;
+    const int grid = persistent_grid(kern, dyn, p->ntiles, threads);
+    MPB_CUDA(launch_k(pdl, kern, grid, threads, dyn, s, a, x, pv, q, r));
+    MPB_LAUNCHED(h);
+    return MPB_OK;
+  }
   const StageLayout L = update_first_layout<T>(a.g);
   if (p->ngeneric == 0 && use_wt()) {
     constexpr int threads = kWtWarps * 32 + 32;
@@ -1240,6 +1254,9 @@ static int plan_dia(mpb_handle *h, mpb_plan *p) {
   p->dia_ibany = static_cast<int>(any);
   p->dia_at = (p->ib_nnz + 63) & ~int64_t(63);  // (256-byte aligned for either precision)
   p->dia_entries = p->n * kDiaSlots;            // (n is a multiple of 64)
+  constexpr unsigned int kNear = (1u << (kDiaDiag - 1)) | (1u << kDiaDiag) | (1u << (kDiaDiag + 1));
+  p->near_at = p->dia_at + p->dia_entries;      // (a multiple of 64 entries again)
+  p->near_entries = (any & ~kNear) == 0u ? p->n * kNearSlots : 0;
   p->dia_ok = true;
   return MPB_OK;
 }
@@ -1411,7 +1428,7 @@ int mpb_plan_bind_sell(mpb_handle *h, mpb_plan *p, const mpb_sell *sell) {
 // (stencil plans, dia_ok) the offset-slot values at entry dia_at
 int64_t mpb_plan_inblock_nnz(const mpb_plan *p) {
   if (!p || !p->bound) return MPB_ERR_LAYOUT;
-  return p->dia_ok ? p->dia_at + p->dia_entries : p->ib_nnz;
+  return p->dia_ok ? p->near_at + p->near_entries : p->ib_nnz;
 }
 
 template <typename T>
@@ -1427,6 +1444,10 @@ static int pack_ib_impl(mpb_handle *h, const mpb_plan *p, const T *sell_val, T *
     k_dia_pack<T><<<elt_blocks(p->n), kEltThreads, 0, h->user>>>(p->n, p->bound->d_sp, sell_val, p->d_meta, p->d_pat,
                                                                 p->d_pslot, ib_val + p->dia_at);
     MPB_LAUNCHED(h);
+    if (p->near_entries > 0) {
+      k_dia_near<T><<<elt_blocks(p->n), kEltThreads, 0, h->user>>>(p->n, ib_val + p->dia_at, ib_val + p->near_at);
+      MPB_LAUNCHED(h);
+    }
   }
   return MPB_OK;
 }

@@ -811,6 +811,8 @@ struct PassArgs {
   // offset-slot ("DIA") layout of stencil plans (k_bjac_dia; null: not available)
   const T *dval;             // values, slot k of row r at (r / 32) * 32 kDiaSlots + 32 k + r % 32
   const uint16_t *dmeta;     // per row: present slots | in-block slots << 8
+  const T *dnear;            // slots kDiaDiag - 1 .. + 1 only, 3 per row in the same slice layout (null: some
+                             // in-block entry sits elsewhere); read by the fused update's first pass
   int doff[8];               // column offset of slot k (doff[kDiaDiag] == 0), ascending
   int ibany;                 // slots that are in-block in at least one row
 };
@@ -1713,6 +1715,177 @@ __global__ void __launch_bounds__(kTileThreads / 2 + 32) k_bjac_dia(const PassAr
     finish_grid<16, kFinRpt>(a.st, 0, kStepRho, ChunkCtx{a.csum, a.part, a.g.ntiles, TWO ? a.g.poll : 0}, ws);
 }
 
+// ---------------------------------------------------------------------------
+// Fused x/r update + next first pass in the offset-slot layout, warp per
+// 64-row block (k_update_first's arithmetic; dia_tile_wb's mapping).  The
+// first pass reads only in-block entries, here slots kDiaDiag - 1 .. + 1
+// (PassArgs::dnear, 3 values per row): plans whose in-block entries are the
+// diagonal and its two neighbours in the offset list.  No CTA barrier: the
+// r.r tile sum uses the stage's arrival counter, the sweeps __syncwarp.
+// ---------------------------------------------------------------------------
+constexpr int kNearSlots = 3;
+template <typename T>
+__host__ __device__ constexpr uint32_t dia_uf_stage_bytes() {
+  return kTileRows * kNearSlots * sizeof(T) + kTileRows * 2u + 4u * kTileRows * 8u;  // values, masks, r x p q
+}
+
+template <typename T>
+__device__ __forceinline__ void dia_update_first_wb(const PassArgs<T> &a, int offm, int offp, int tile, int lo,
+                                                    int nrows, double alpha, double *x, double *r, const T *val,
+                                                    const uint16_t *dm, const double *rs, const double *xs,
+                                                    const double *ps, const double *qs, T *s_w, double *wsum,
+                                                    unsigned int *wcnt) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool active = 64 * warp < nrows;
+  double sq[2] = {0.0, 0.0};
+  if (active) {
+    T v[2][kNearSlots], rv[2], w[2];
+    unsigned int m[2];
+    int ti[2];
+#pragma unroll
+    for (int k = 0; k < 2; k++) {
+      ti[k] = 64 * warp + 32 * k + lane;
+      const int row = lo + ti[k];
+      m[k] = dm[ti[k]] >> (8 + kDiaDiag - 1);  // in-block bits of the three near slots
+      const T *vb = val + (2 * warp + k) * (32 * kNearSlots) + lane;
+#pragma unroll
+      for (int u = 0; u < kNearSlots; u++) v[k][u] = vb[32 * u];
+      st_evict_first(x + row, __dadd_rn(xs[ti[k]], __dmul_rn(alpha, ps[ti[k]])));  // (read again by the next update only)
+      const double rn = __dsub_rn(rs[ti[k]], __dmul_rn(alpha, qs[ti[k]]));
+      r[row] = rn;
+      sq[k] = __dmul_rn(rn, rn);
+      rv[k] = narrow_checked(a, rn, row, true);
+      w[k] = div_rn(rv[k], v[k][1]);
+      s_w[ti[k]] = w[k];
+    }
+    for (int sw = 1; sw < a.t; sw++) {
+      __syncwarp();
+      T acc[2];
+#pragma unroll
+      for (int k = 0; k < 2; k++) {
+        // acc is never -0 (it starts at +0), so adding +0 for a slot that is not in-block changes nothing
+        T sm, sp;
+        undefined_value(sm);
+        undefined_value(sp);
+        if (m[k] & 1u) sm = s_w[ti[k] + offm];
+        if (m[k] & 4u) sp = s_w[ti[k] + offp];
+        acc[k] = add_rn(T(0), (m[k] & 1u) ? mul_rn(v[k][0], sm) : T(0));
+        acc[k] = add_rn(acc[k], (m[k] & 2u) ? mul_rn(v[k][1], w[k]) : T(0));  // (the row's own w)
+        acc[k] = add_rn(acc[k], (m[k] & 4u) ? mul_rn(v[k][2], sp) : T(0));
+      }
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < 2; k++) {
+        w[k] = add_rn(w[k], div_rn(sub_rn(rv[k], acc[k]), v[k][1]));
+        s_w[ti[k]] = w[k];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 2; k++) {
+      const int row = lo + ti[k];
+      if (a.zout != nullptr) st_keep(a.zout + row, w[k]);
+      if (a.zout64 != nullptr) a.zout64[row] = static_cast<double>(w[k]);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 2; k++) {
+    sq[k] = warp_bfly(sq[k]);
+    if (lane == 0) wsum[2 * warp + k] = sq[k];
+  }
+  __syncwarp();
+  unsigned int old = 0;
+  if (lane == 0)
+    asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(smem_u32(wcnt)) : "memory");
+  old = __shfl_sync(0xffffffffu, old, 0);
+  if (old == kTileThreads / 64 - 1) {  // the tile's last warp: every warp sum is stored
+    double t = lane < kTileThreads / 32 ? wsum[lane] : 0.0;
+    t = warp_bfly(t);
+    if (lane == 0) {
+      *wcnt = 0u;
+      put_part(a.part + tile, t);
+    }
+  }
+}
+
+template <typename T, bool TWO>
+__global__ void __launch_bounds__(kTileThreads / 2 + 32)
+    k_update_first_dia(const PassArgs<T> a, double *x, const double *p, const double *q, double *r) {
+  constexpr int NC = kTileThreads / 2;
+  constexpr int kFinRpt = NC >= kFinThreads ? 1 : kFinThreads / NC;
+  constexpr uint32_t kVal = kTileRows * kNearSlots * sizeof(T), kMeta = kTileRows * 2u, kVec = kTileRows * 8u;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ Ring R;
+  __shared__ T s_w[kTileRows];
+  __shared__ double ws[32];
+  __shared__ double s_wsum[kMaxStages * (kTileThreads / 32)];
+  __shared__ unsigned int s_wcnt[kMaxStages];
+  if (threadIdx.x < kMaxStages) s_wcnt[threadIdx.x] = 0u;  // (published by ring_init's barrier)
+  const int ns = a.g.ns;
+  ring_init(R, ns, NC);
+  if (threadIdx.x >= NC) {  // producer warp
+    const ChunkCtx ck{a.csum, a.part, a.g.ntiles, TWO ? a.g.poll : 0};
+    auto fill = [&](int st, int tile, int part) {
+      TileDesc d;
+      if (part != kFillDynamic) {
+        d = a.td[tile];
+        R.desc[st] = d;
+        R.ok[st] = 1;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      } else {
+        d = R.desc[st];
+      }
+      const uint32_t rows = static_cast<uint32_t>(d.hi - d.lo);  // a multiple of 64
+      const uint32_t vb = rows * kNearSlots * static_cast<uint32_t>(sizeof(T));
+      const uint32_t sbytes = vb + rows * 2u, dbytes = 4u * rows * 8u;
+      unsigned char *stage = smem + st * dia_uf_stage_bytes<T>();
+      if (part == kFillAll) mbar_arrive_expect_tx(&R.full[st], sbytes + dbytes);
+      if (part == kFillStatic) mbar_expect_tx(&R.full[st], sbytes);
+      if (part != kFillDynamic) {
+        bulk_g2s_stream(stage, a.dnear + static_cast<long long>(kNearSlots) * d.lo, vb, &R.full[st]);
+        bulk_g2s(stage + kVal, a.dmeta + d.lo, rows * 2u, &R.full[st]);
+      }
+      if (part == kFillStatic) return;
+      if (part == kFillDynamic) mbar_arrive_expect_tx(&R.full[st], dbytes);
+      unsigned char *vec = stage + kVal + kMeta;
+      bulk_g2s(vec, r + d.lo, rows * 8u, &R.full[st]);
+      bulk_g2s_stream(vec + kVec, x + d.lo, rows * 8u, &R.full[st]);  // x and q: not read again before the next update
+      bulk_g2s(vec + 2 * kVec, p + d.lo, rows * 8u, &R.full[st]);
+      bulk_g2s_stream(vec + 3 * kVec, q + d.lo, rows * 8u, &R.full[st]);
+    };
+    auto gated = [&]() { return gated_off(a); };
+    if (TWO && ck.poll)
+      producer_loop(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, gated, fill, ck, 1, a.td);
+    else if (threadIdx.x == NC)
+      producer_loop_single(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, gated, fill, 1, a.td);
+    else
+      pdl_wait();
+    if (gated_off(a)) return;
+  } else {
+    pdl_wait();
+    if (gated_off(a)) return;
+    if (threadIdx.x == 0) tl_mark(a.st, 2, 0, false);
+    const double alpha = a.st->alpha;
+    const int offm = a.doff[kDiaDiag - 1], offp = a.doff[kDiaDiag + 1];
+    for (RingCursor cur;; cur.advance(ns)) {
+      const int st = cur.st;
+      mbar_wait(&R.full[st], cur.phase);
+      const int tile = R.tile[st];
+      if (tile < 0) break;
+      const int lo = R.desc[st].lo, nrows = R.desc[st].hi - lo;
+      const unsigned char *sb = smem + st * dia_uf_stage_bytes<T>();
+      const double *vec = reinterpret_cast<const double *>(sb + kVal + kMeta);
+      dia_update_first_wb<T>(a, offm, offp, tile, lo, nrows, alpha, x, r, reinterpret_cast<const T *>(sb),
+                             reinterpret_cast<const uint16_t *>(sb + kVal), vec, vec + kTileRows,
+                             vec + 2 * kTileRows, vec + 3 * kTileRows, s_w, s_wsum + st * (kTileThreads / 32),
+                             s_wcnt + st);
+      ring_release(R, st);
+    }
+    if (threadIdx.x == 0) tl_mark(a.st, 2, 1, true);
+  }
+  pdl_trigger();
+  finish_grid<8, kFinRpt>(a.st, 2, kStepRrZ, ChunkCtx{a.csum, a.part, a.g.ntiles, TWO ? a.g.poll : 0}, ws);
+}
+
 // Setup: per-row masks of the offset-slot layout from the row metadata
 // (pattern id, in-block slot range) and pslot[pid * kSlots + j] = the
 // offset slot of the pattern's j-th stored entry; any[0] collects the slots
@@ -1733,6 +1906,16 @@ __global__ void k_dia_meta(long long n, const uint16_t *meta, const int *pat, co
     seen |= inb;
   }
   if (seen) atomicOr(any, seen);
+}
+
+// Setup: the near slots (kDiaDiag - 1 .. + 1) of the offset-slot values, 3 per row
+template <typename E>
+__global__ void k_dia_near(long long n, const E *dval, E *out) {
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < n; r += (long long)gridDim.x * blockDim.x) {
+    const long long src = (r >> 5) * (32 * kDiaSlots) + (r & 31), dst = (r >> 5) * (32 * kNearSlots) + (r & 31);
+#pragma unroll
+    for (int u = 0; u < kNearSlots; u++) out[dst + 32 * u] = dval[src + 32 * (kDiaDiag - 1 + u)];
+  }
 }
 
 // Setup: SELL-32 values into the offset-slot layout (out zeroed before)
