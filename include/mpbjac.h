@@ -101,6 +101,11 @@ typedef struct mpb_csr {
    * and the true residuals read these (solver.py:154, 93-98).  NULL: the
    * operator is sell_val64. */
   const double *op_sell_val64;
+  /* op_sell_val64 in the plan-packed layout (mpb_plan_pack_inblock_f64), so
+   * that the outer SpMV can use the plan's offset-slot layout; NULL: the
+   * SELL kernel runs.  Ignored when op_sell_val64 is NULL (ib_val64 is the
+   * operator's then). */
+  const double *op_ib_val64;
 } mpb_csr;
 
 typedef struct mpb_solve_options {

@@ -59,7 +59,8 @@ class MpbCsr(C.Structure):
                 ("val64", C.c_void_p), ("val32", C.c_void_p),
                 ("sell", C.c_void_p), ("sell_val64", C.c_void_p),
                 ("sell_val32", C.c_void_p), ("ib_val64", C.c_void_p),
-                ("ib_val32", C.c_void_p), ("op_sell_val64", C.c_void_p)]
+                ("ib_val32", C.c_void_p), ("op_sell_val64", C.c_void_p),
+                ("op_ib_val64", C.c_void_p)]
 
 
 class MpbHalo(C.Structure):

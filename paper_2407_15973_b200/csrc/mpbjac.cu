@@ -2009,6 +2009,16 @@ static SpmvArgs spmv_args(const mpb_handle *h, const mpb_plan *p, const mpb_csr 
   sa.part = w.part;
   sa.st = w.st;
   sa.csum = w.csum;
+  // offset-slot layout of the operator: its plan-packed values (the
+  // preconditioner's fp64 buffer when the operator is the preconditioner's matrix)
+  const double *op_packed = A->op_sell_val64 ? A->op_ib_val64 : A->ib_val64;
+  if (p->dia_ok && op_packed != nullptr) {
+    sa.dval = op_packed + p->dia_at;
+    sa.dmeta = p->d_dmeta;
+    for (int u = 0; u < kDiaSlots; u++) sa.doff[u] = p->dia_off[u];
+    auto kern = two_level(p->ntiles) ? k_spmv_dia<true> : k_spmv_dia<false>;
+    sa.g.ns = pick_stages(kern, kDiaSpmvStage);
+  }
   if (p->sym_ok && p->sym_key == op_vals(A) && p->d_U != nullptr) {
     sa.U = p->d_U;
     sa.pmask = p->d_pmask;
@@ -2023,7 +2033,11 @@ static SpmvArgs spmv_args(const mpb_handle *h, const mpb_plan *p, const mpb_csr 
 // the SpMV of an iteration: the symmetric offset-slot kernel when spmv_args
 // bound a U layout, else the SELL kernel
 static int launch_spmv(mpb_handle *h, cudaStream_t s, const mpb_plan *p, const SpmvArgs &sa, bool pdl) {
-  if (sa.U != nullptr) {
+  if (sa.dval != nullptr && sa.U == nullptr) {
+    auto kern = two_level(p->ntiles) ? k_spmv_dia<true> : k_spmv_dia<false>;
+    const uint32_t dyn = sa.g.ns * kDiaSpmvStage;
+    MPB_CUDA(launch_k(pdl, kern, persistent_grid(kern, dyn, p->ntiles, kWsThreads), kWsThreads, dyn, s, sa));
+  } else if (sa.U != nullptr) {
     auto kern = spmv_sym_kernel(p);
     const uint32_t dyn = sa.g.ns * spmv_sym_layout(sa.S, sa.d).bytes;
     MPB_CUDA(launch_k(pdl, kern, persistent_grid(kern, dyn, p->ntiles, kWsThreads), kWsThreads, dyn, s, sa));

@@ -2489,6 +2489,10 @@ struct SpmvArgs {
   // symmetric offset-slot layout (k_spmv_sym): U + s n holds each row's value
   // at column offset d[s] >= 0 (d[0] = 0, 0 where absent); the value at
   // offset -d[s] is row (i - d[s])'s U_s entry (A symmetric, checked at build)
+  // offset-slot layout of the operator (k_spmv_dia; PassArgs::dval's layout in fp64)
+  const double *dval;
+  const uint16_t *dmeta;
+  int doff[8];
   const double *U;
   const uint16_t *pmask;  // per row pattern: bit j = signed offset j (ascending) present
   int n;
@@ -2614,6 +2618,125 @@ __global__ void MPB_WS_BOUNDS_SPMV k_spmv_pq(const SpmvArgs a) {
         spmv_tile<KS, GEN>(a, tile, d, a.scol + d.e0, a.sval + d.e0, a.sp + d.s0, a.meta + d.lo, s_pat, ws, mode, first,
                       beta);
       }
+      ring_release(R, st);
+    }
+    if (threadIdx.x == 0) tl_mark(a.st, 1, 1, true);
+  }
+  pdl_trigger();
+  finish_grid<16, kFinRptWs>(a.st, 1, kStepPq, ChunkCtx{a.csum, a.part, a.g.ntiles, TWO ? a.g.poll : 0}, ws);
+}
+
+// ---- SpMV on the offset-slot layout ------------------------------------------
+// q = A p with p rebuilt where it is gathered (k_spmv_pq's arithmetic) on the
+// offset-slot values of the operator: slot k of a row at a fixed shared-memory
+// offset, column row + doff[k], the row's own p from the diagonal slot's
+// gather.  One row per thread, 8 consumer warps that never meet at a CTA
+// barrier: the tile's p.q sum is finished by the warp that arrives last on
+// the stage's counter (the order of include/mpbjac_order.h).
+constexpr uint32_t kDiaSpmvStage = kTileRows * kDiaSlots * 8u + kTileRows * 2u;
+
+template <typename ZT>
+__device__ __forceinline__ void dia_spmv_tile(const SpmvArgs &a, int tile, int lo, int nrows, const double *val,
+                                              const uint16_t *dm, double *wsum, unsigned int *wcnt, bool first,
+                                              double beta) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, ti = threadIdx.x;
+  double prod = 0.0;
+  if (32 * warp < nrows) {  // warp-uniform (tiles hold a multiple of 64 rows)
+    const int row = lo + ti;
+    const unsigned int m = dm[ti];
+    const double *vb = val + warp * (32 * kDiaSlots) + lane;
+    double v[kDiaSlots], pv[kDiaSlots];
+#pragma unroll
+    for (int u = 0; u < kDiaSlots; u++) {
+      v[u] = vb[32 * u];
+      // (an absent slot gathers the row's own p: its product is never added)
+      pv[u] = p_at<ZT>(a, row + (((m >> u) & 1u) ? a.doff[u] : 0), first, beta);
+    }
+    double acc = 0.0;
+#pragma unroll
+    for (int u = 0; u < kDiaSlots; u++)
+      if ((m >> u) & 1u) acc = __dadd_rn(acc, __dmul_rn(v[u], pv[u]));
+    a.q[row] = acc;
+    const double pown = pv[kDiaDiag];
+    if (!std::is_same<ZT, void>::value) st_keep(a.pnew + row, pown);
+    prod = __dmul_rn(pown, acc);
+  }
+  prod = warp_bfly(prod);
+  if (lane == 0) wsum[warp] = prod;
+  __syncwarp();
+  unsigned int old = 0;
+  if (lane == 0)
+    asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(smem_u32(wcnt)) : "memory");
+  old = __shfl_sync(0xffffffffu, old, 0);
+  if (old == kTileThreads / 32 - 1) {  // the tile's last warp: every warp sum is stored
+    double t = lane < kTileThreads / 32 ? wsum[lane] : 0.0;
+    t = warp_bfly(t);
+    if (lane == 0) {
+      *wcnt = 0u;
+      put_part(a.part + tile, t);
+    }
+  }
+}
+
+template <bool TWO>
+__global__ void __launch_bounds__(kWsThreads, 4) k_spmv_dia(const SpmvArgs a) {
+  static_assert(kConsumers == kTileThreads, "one row per consumer thread");
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ Ring R;
+  __shared__ double ws[32];
+  __shared__ double s_wsum[kMaxStages * (kTileThreads / 32)];
+  __shared__ unsigned int s_wcnt[kMaxStages];
+  if (threadIdx.x < kMaxStages) s_wcnt[threadIdx.x] = 0u;  // (published by ring_init's barrier)
+  const int ns = a.g.ns;
+  ring_init(R, ns);
+  if (threadIdx.x >= kConsumers) {
+    const ChunkCtx ck{a.csum, a.part, a.g.ntiles, TWO ? a.g.poll : 0};
+    // every staged byte is static (values, masks): all of it may stream
+    // before the grid dependency wait; the dynamic part only arrives
+    auto fill = [&](int st, int tile, int part) {
+      if (part != kFillDynamic) {
+        const TileDesc d = a.td[tile];
+        R.desc[st] = d;
+        R.ok[st] = 1;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        const uint32_t rows = static_cast<uint32_t>(d.hi - d.lo);  // a multiple of 64
+        unsigned char *stage = smem + st * kDiaSpmvStage;
+        if (part == kFillAll) mbar_arrive_expect_tx(&R.full[st], rows * (kDiaSlots * 8u + 2u));
+        else mbar_expect_tx(&R.full[st], rows * (kDiaSlots * 8u + 2u));
+        bulk_g2s_stream(stage, a.dval + static_cast<long long>(kDiaSlots) * d.lo, rows * kDiaSlots * 8u, &R.full[st]);
+        bulk_g2s(stage + kTileRows * kDiaSlots * 8u, a.dmeta + d.lo, rows * 2u, &R.full[st]);
+      } else {
+        mbar_arrive(&R.full[st]);
+      }
+    };
+    auto gated = [&]() { return a.st->done != 0; };
+    if (TWO && ck.poll)
+      producer_loop(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, gated, fill, ck, 1, a.td);
+    else if (threadIdx.x == kConsumers)
+      producer_loop_single(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, gated, fill, 1, a.td);
+    else
+      pdl_wait();
+    if (a.st->done) return;
+  } else {
+    pdl_wait();
+    if (a.st->done) return;
+    if (threadIdx.x == 0) tl_mark(a.st, 1, 0, false);
+    const int mode = a.pnew == nullptr ? 0 : (a.st->branch == 1 ? 1 : 2);
+    const bool first = a.st->first != 0;
+    const double beta = a.st->beta;
+    for (RingCursor cur;; cur.advance(ns)) {
+      const int st = cur.st;
+      mbar_wait(&R.full[st], cur.phase);
+      const int tile = R.tile[st];
+      if (tile < 0) break;
+      const int lo = R.desc[st].lo, nrows = R.desc[st].hi - lo;
+      const unsigned char *sb = smem + st * kDiaSpmvStage;
+      const double *val = reinterpret_cast<const double *>(sb);
+      const uint16_t *dm = reinterpret_cast<const uint16_t *>(sb + kTileRows * kDiaSlots * 8u);
+      double *wsum = s_wsum + st * (kTileThreads / 32);
+      if (mode == 0) dia_spmv_tile<void>(a, tile, lo, nrows, val, dm, wsum, s_wcnt + st, first, beta);
+      else if (mode == 1) dia_spmv_tile<float>(a, tile, lo, nrows, val, dm, wsum, s_wcnt + st, first, beta);
+      else dia_spmv_tile<double>(a, tile, lo, nrows, val, dm, wsum, s_wcnt + st, first, beta);
       ring_release(R, st);
     }
     if (threadIdx.x == 0) tl_mark(a.st, 1, 1, true);

@@ -133,6 +133,8 @@ def _dev_struct(A: SparseMatrix, mp: MixedPreconditioner):
     val32 = mp.p_low.dvalues if mp.p_low is not None else None
     s = D.c_struct(val64=val64, val32=val32, plan=P.plan)
     s.op_sell_val64 = op.data_ptr() if op is not None else None
+    if op is not None:  # the operator's values in the plan's packed layout (offset-slot SpMV)
+        s.op_ib_val64 = P.plan.inblock_values(op).data_ptr()
     return D, s
 
 
