@@ -450,7 +450,10 @@ int launch_tile_kernel(mpb_handle *h, cudaStream_t s, const mpb_plan *p, PassArg
   }
   // Offset-slot passes (k_bjac_dia): stencil plans with 64-row blocks
   if constexpr (!F && !GEN && R64 && KS == 7) {
-    if (a.dval != nullptr && p->dia_ok) {
+    // (fp64 instances: two fp64 rows per lane need 90 registers; measured against the SELL
+    // kernel in the same run, the C3 solve is 0.8 % faster with it; MPB_DIA_F64=0 turns it off)
+    static const bool dia64 = !(std::getenv("MPB_DIA_F64") && std::atoi(std::getenv("MPB_DIA_F64")) == 0);
+    if (a.dval != nullptr && p->dia_ok && (sizeof(T) == 4 || dia64)) {
       constexpr int threads = kTileThreads / 2 + 32;
       constexpr uint32_t sb = dia_stage_bytes<T>();
       constexpr int kNear = (1 << (kDiaDiag - 1)) | (1 << kDiaDiag) | (1 << (kDiaDiag + 1));
@@ -507,7 +510,12 @@ int launch_pass(mpb_handle *h, cudaStream_t s, const mpb_plan *p, PassArgs<T> a,
       if (a.r64 != nullptr) return launch_tile_kernel<T, F, L, true, 7, false>(h, s, p, a);
       return launch_tile_kernel<T, F, L, false, 7, false>(h, s, p, a);
     }
-    if (a.r64 != nullptr) return launch_tile_kernel<T, F, L, true, kSlots, true>(h, s, p, a);
+    // longer rows (3-T systems): without generic rows the passes that read an fp64
+    // residual take the kernels with the full-tile fast path compiled in
+    if (a.r64 != nullptr) {
+      if (p->ngeneric == 0) return launch_tile_kernel<T, F, L, true, kSlots, false>(h, s, p, a);
+      return launch_tile_kernel<T, F, L, true, kSlots, true>(h, s, p, a);
+    }
     return launch_tile_kernel<T, F, L, false, kSlots, true>(h, s, p, a);
   }
   a.resbuf = bufs.res;
