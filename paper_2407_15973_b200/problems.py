@@ -406,6 +406,16 @@ def make_config(name: str, n: int | None = None, validate: bool | None = None,
     device=True: the operators (7-point and C4's 3-T) and right-hand
     sides built on the GPU (bit-identical)."""
     name = name.lower()
+    if name in ("const128_nb32", "ani128_nb32"):
+        # the reference's own acceptance problems (pkg/tests/test_acceptance.py:226-274) on its
+        # default partition nb = 32 (bjac.py:152): 65,536-row blocks at n = 128, b = ones
+        n = 128 if n is None else int(n)
+        fam, scale = (Family.CONST, 1.0) if name.startswith("const") else (Family.ANI, 1000.0)
+        A = family_matrix(n, fam, scale)
+        if A.n % 32:
+            raise ValueError("nb = 32 needs n^3 divisible by 32")
+        return ConfigSystem(name, A, np.ones(A.n), A.n // 32, ("fixed-low", "uniform"), 2, 2, 1e-10, n,
+                            f"{fam.value} family, b = ones, the reference's default partition nb = 32")
     n = FULL_N[name] if n is None else int(n)
     N = n ** 3
     if validate is None:
