@@ -157,9 +157,13 @@ int mpb_plan_destroy(mpb_plan *p);
  * in-block slot range) against a SELL-32 layout of the matrix; required
  * before the plan is used with that matrix by the preconditioner / solve. */
 int mpb_plan_bind_sell(mpb_handle *h, mpb_plan *p, const mpb_sell *sell);
-/* The bound plan's in-block SELL-32 layout (each row's entries inside its
- * own block, ascending column): padded entry count, and value packing from
- * SELL-32 values of the bound structure. */
+/* The bound plan's packed value buffer: each row's entries inside its own
+ * block in an in-block SELL-32 layout (ascending column; read by the first
+ * BJAC pass), followed -- for plans with an offset-slot layout, see
+ * mpb_plan_offset_slot_info -- by the values in that layout (and its near
+ * slots alone).  mpb_plan_inblock_nnz: the entry count of the whole buffer
+ * (the caller allocates it in the values' precision); mpb_plan_pack_inblock_*:
+ * fill it from SELL-32 values of the bound structure. */
 int64_t mpb_plan_inblock_nnz(const mpb_plan *p);
 int mpb_plan_pack_inblock_f64(mpb_handle *h, const mpb_plan *p,
                               const double *sell_val, double *ib_val);
@@ -171,6 +175,15 @@ int mpb_plan_info(const mpb_plan *p, int64_t *h_ntiles, int *h_large,
  * whose column offsets match one of *h_npat (<= 128) patterns carry no column
  * index on the hot path; *h_ngeneric rows read their SELL columns. */
 int mpb_plan_layout_info(const mpb_plan *p, int *h_npat, int64_t *h_ngeneric);
+/* Offset-slot layout of the bound plan: when every row pattern draws its
+ * column offsets from the same 7 ascending values with 0 in the middle (a
+ * 7-point stencil on any grid) and every block has 64 rows, the hot kernels
+ * read slot k of every row as the entry at column row + offset[k] (no
+ * pattern lookups; absent entries masked).  *h_slots: 7, or 0 without the
+ * layout; *h_inblock_slots: bit k set = slot k is in-block in some row;
+ * *h_near: the fused x/r update + first pass also runs on it (in-block
+ * entries only at the diagonal and its two neighbouring offsets). */
+int mpb_plan_offset_slot_info(const mpb_plan *p, int *h_slots, int *h_inblock_slots, int *h_near);
 
 /* ---- SELL-32 layout (hot-path matrix format) ----------------------------- */
 /* Builds slice pointers (from the host row_ptr) and packs the column array on

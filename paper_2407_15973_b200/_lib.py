@@ -41,7 +41,7 @@ EXPORTED = (
     "mpb_plan_bind_sell", "mpb_plan_inblock_nnz", "mpb_plan_pack_inblock_f64",
     "mpb_plan_pack_inblock_f32", "mpb_comm_unique_id", "mpb_comm_create",
     "mpb_comm_destroy", "mpb_solve_workspace_bytes_dist", "mpb_pcg_solve_dist",
-    "mpb_profile_iteration_dist", "mpb_plan_layout_info", "mpb_stencil_nnz",
+    "mpb_profile_iteration_dist", "mpb_plan_layout_info", "mpb_plan_offset_slot_info", "mpb_stencil_nnz",
     "mpb_assemble_stencil", "mpb_splitmix64_uniform", "mpb_expand_3t",
     "mpb_row_features", "mpb_tau_histogram", "mpb_vector_stats",
     "mpb_first_violations", "mpb_local_group_create", "mpb_local_group_destroy", "mpb_local_group_stream",
@@ -107,6 +107,7 @@ def _declare(L):
         "mpb_plan_destroy": ([_P], C.c_int),
         "mpb_plan_info": ([_P, _I64P, C.POINTER(C.c_int), _I64P], C.c_int),
         "mpb_plan_layout_info": ([_P, C.POINTER(C.c_int), _I64P], C.c_int),
+        "mpb_plan_offset_slot_info": ([_P, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)], C.c_int),
         "mpb_stencil_nnz": ([_I64], C.c_int64),
         "mpb_assemble_stencil": ([_P, _I64, _P, C.c_double, C.c_double, C.c_double, C.c_double, _P, _P, _P],
                                  C.c_int),

@@ -129,11 +129,18 @@ class DevicePlan:
         return self
 
     def layout_info(self) -> dict:
-        """Row patterns of the bound structure: {"patterns", "generic_rows"}."""
+        """Row patterns of the bound structure ({"patterns", "generic_rows"}) and its
+        offset-slot layout ("offset_slots": 7 or 0, "inblock_slots" mask,
+        "offset_slot_update": the fused update runs on it too)."""
         npat, ngen = C.c_int(), C.c_int64()
         _lib.check(self.h.lib.mpb_plan_layout_info(self.ptr, C.byref(npat), C.byref(ngen)),
                    "mpb_plan_layout_info")
-        return {"patterns": int(npat.value), "generic_rows": int(ngen.value)}
+        slots, inb, near = C.c_int(), C.c_int(), C.c_int()
+        _lib.check(self.h.lib.mpb_plan_offset_slot_info(self.ptr, C.byref(slots), C.byref(inb), C.byref(near)),
+                   "mpb_plan_offset_slot_info")
+        return {"patterns": int(npat.value), "generic_rows": int(ngen.value),
+                "offset_slots": int(slots.value), "inblock_slots": int(inb.value),
+                "offset_slot_update": bool(near.value)}
 
     def __del__(self):
         try:

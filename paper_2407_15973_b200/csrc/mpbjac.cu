@@ -1519,6 +1519,14 @@ int mpb_plan_layout_info(const mpb_plan *p, int *h_npat, int64_t *h_ngeneric) {
   return MPB_OK;
 }
 
+int mpb_plan_offset_slot_info(const mpb_plan *p, int *h_slots, int *h_inblock_slots, int *h_near) {
+  if (!p || !p->bound) return MPB_ERR_ARG;
+  if (h_slots) *h_slots = p->dia_ok ? kDiaSlots : 0;
+  if (h_inblock_slots) *h_inblock_slots = p->dia_ok ? p->dia_ibany : 0;
+  if (h_near) *h_near = (p->dia_ok && p->near_entries > 0) ? 1 : 0;
+  return MPB_OK;
+}
+
 // ---- backend kernels -------------------------------------------------------
 int mpb_csr_matvec_f64(mpb_handle *h, int64_t n, const int32_t *row_ptr, const int32_t *col_idx, const double *val,
                        const double *x, double *y) {

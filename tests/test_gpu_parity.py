@@ -355,7 +355,8 @@ def test_row_patterns_and_generic_rows_bitwise(cuda, oracle):
     cs = problems.make_config("c2", 16)
     P = setup(cs.A, k=2, t=2, partition=BlockPartition.fixed_size(cs.A.n, 64))
     info = P.plan.layout_info()
-    assert info == {"patterns": 27, "generic_rows": 0}       # 7-point stencil, all boundary cases
+    assert (info["patterns"], info["generic_rows"]) == (27, 0)   # 7-point stencil, all boundary cases
+    assert info["offset_slots"] == 7 and not info["offset_slot_update"]   # (+-16 is in-block at n = 16)
     rng = np.random.default_rng(91)
     A = random_spd_csr(3000, 0.0012, rng)                    # thousands of distinct patterns
     r = rng.standard_normal(A.n)
@@ -442,3 +443,47 @@ def test_pcg_preconditioner_from_other_matrix(cuda, oracle, pol):
                                     adp_tol=pp.adp_tol, k=int(k), t=int(t), res_tol=float(tol),
                                     stride=4, order="device")
             np.testing.assert_array_equal(rep2.x, orc2["x"], err_msg=name)
+
+
+@pytest.mark.parametrize("n,pol", ((64, "fixed-low"), (64, "uniform"), (64, "adaptive-hl:1e-3"),
+                                   (32, "fixed-low"), (32, "adaptive-lh:1e-4")))
+def test_offset_slot_layout_bitwise(cuda, oracle, n, pol):
+    """7-point stencil plans with 64-row blocks run the offset-slot kernels
+    (k_bjac_dia, k_spmv_dia, k_update_first_dia: warp per block, no pattern
+    lookups, masked absent slots).  n = 64: in-block entries at the diagonal
+    and +-1 only (the fused update runs on the layout too); n = 32: +-32 is
+    in-block as well (generic in-block mask).  Whole solves, bit for bit
+    against the oracle, repeated (the tile sums are finished by whichever
+    warp arrives last: any race there would show as a differing rerun), and
+    with the preconditioner set up from another matrix of the same structure
+    (the operator's own offset-slot values, mpb_csr.op_ib_val64)."""
+    from paper_2407_15973_b200 import problems
+    from paper_2407_15973_b200.bjac import BlockPartition
+    from paper_2407_15973_b200.policies import PrecisionPolicy, build_mixed
+    from paper_2407_15973_b200.problems import diag_augment
+    from paper_2407_15973_b200.solver import SolveConfig, pcg_solve
+    cs = problems.make_config("c2", n)
+    A = cs.A
+    part = BlockPartition.fixed_size(A.n, 64)
+    pp = PrecisionPolicy.parse(pol)
+    mp = build_mixed(A, pp, k=2, t=3, partition=part)
+    info = mp.any.plan.layout_info()
+    assert info["offset_slots"] == 7 and info["generic_rows"] == 0
+    assert info["offset_slot_update"] == (n >= 64)
+    assert info["inblock_slots"] == (0b0011100 if n >= 64 else 0b0111110)
+    cfg = SolveConfig(res_tol=1e-9, record_true_residual_every=5)
+    kw = dict(kind=pp.kind.value, adp_tol=pp.adp_tol, k=2, t=3, res_tol=1e-9, stride=5, order="device")
+    orc = oracle.pcg_solve(A.row_ptr, A.col_idx, A.values, cs.b, part.offsets, **kw)
+    for _ in range(6):
+        rep = pcg_solve(A, cs.b, mp, cfg)
+        assert rep.iterations == orc["iterations"]
+        np.testing.assert_array_equal(rep.x, orc["x"])
+        np.testing.assert_array_equal([r.implicit_relres for r in rep.trace], orc["relres"])
+        assert rep.final_true_relres == orc["final_true_relres"]
+    A2 = diag_augment(A, 0.25)
+    mp2 = build_mixed(A2, pp, k=2, t=3, partition=part)
+    rep = pcg_solve(A, cs.b, mp2, cfg)
+    orc = oracle.pcg_solve(A.row_ptr, A.col_idx, A.values, cs.b, part.offsets, prec_values=A2.values, **kw)
+    assert rep.iterations == orc["iterations"]
+    np.testing.assert_array_equal(rep.x, orc["x"])
+    assert rep.final_true_relres == orc["final_true_relres"]
