@@ -18,7 +18,7 @@ timeout 900 $CMD > gpurun_out/plain_${TAG}_${CFG}.log 2>&1; echo "plain rc=$?"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k "regex:k_bjac|k_spmv|k_update|k_pupdate|k_big" --csv \
     --log-file gpurun_out/launches_${TAG}_${CFG}.csv $CMD > gpurun_out/ncu_launch_${TAG}_${CFG}.log 2>&1
 echo "ncu launch rc=$?"
-for pair in "last:k_bjac_diaI[fd]Lb1E|k_bjac_tileI[fd]Lb0ELb1E" "spmv:k_spmv_pq" "update_first:k_update_first"; do
+for pair in "last:k_bjac_diaI[fd]Lb1E|k_bjac_tileI[fd]Lb0ELb1E" "spmv:k_spmv_dia|k_spmv_pq" "update_first:k_update_first"; do
   nm=${pair%%:*}; rx=${pair#*:}
   timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base mangled -k "regex:$rx" -c 1 \
       -o /tmp/prof_${TAG}_${CFG}_$nm $CMD > gpurun_out/ncu_full_${TAG}_${CFG}_$nm.log 2>&1

@@ -16,7 +16,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "gpurun_out")
 PROF = os.path.join(ROOT, "profiles")
 
-SHORT = {"k_update_first": "update_first", "k_bjac_tile<float, 1, 0": "bjac_first", "k_bjac_tile<float, 0, 1": "bjac_last",
+SHORT = {"k_bjac_dia": "bjac_last", "k_spmv_dia": "spmv_pq", "k_update_first": "update_first", "k_bjac_tile<float, 1, 0": "bjac_first", "k_bjac_tile<float, 0, 1": "bjac_last",
          "k_bjac_tileIfLb0ELb1E": "bjac_last", "k_bjac_tileIdLb0ELb1E": "bjac_last", "k_update_firstI": "update_first",
          "k_bjac_tile<double, 1, 0": "bjac_first", "k_bjac_tile<double, 0, 1": "bjac_last",
          "k_spmv_pq": "spmv_pq", "k_update": "update", "k_pupdate": "pupdate"}
