@@ -96,7 +96,9 @@ struct mpb_plan {
   // (k_bjac_dia): eligibility, the slot offsets, the slots that are in-block
   // somewhere, per-row masks, per-pattern slot maps, and where the DIA
   // values sit in the plan-packed value buffer (mpb_plan_pack_inblock_*)
-  bool dia_ok = false;
+  bool dia_layout = false;  // the arrays below exist (tile plans: dia_ok; large blocks: dia_big)
+  bool dia_ok = false;      // tile kernels (blocks of 64 rows)
+  bool dia_big = false;     // large-block kernels (k_big_dia_*)
   int dia_off[8] = {};
   int dia_ibany = 0;
   uint16_t *d_dmeta = nullptr;
@@ -521,6 +523,26 @@ int launch_pass(mpb_handle *h, cudaStream_t s, const mpb_plan *p, PassArgs<T> a,
   a.resbuf = bufs.res;
   a.dbuf = bufs.dg;
   static const bool old_big = std::getenv("MPB_OLD_BIG") != nullptr;
+  if (!old_big && p->dia_big && a.dval != nullptr) {
+    // offset-slot layout: coalesced slot loads, no pattern-table reads
+    k_big_dia_resid<T, F><<<nt, kCtaThreads, 0, s>>>(a, bufs.wA);
+    MPB_LAUNCHED(h);
+    T *cur = bufs.wA, *nxt = bufs.wB;
+    for (int sweep = 1; sweep < a.t; sweep++) {
+      if (sweep + 1 < a.t) {
+        k_big_dia_sweep<T, F, L, false><<<nt, kCtaThreads, 0, s>>>(a, cur, nxt);
+      } else {
+        k_big_dia_sweep<T, F, L, true><<<nt, kCtaThreads, 0, s>>>(a, cur, nxt);
+        MPB_LAUNCHED(h);
+        return MPB_OK;
+      }
+      MPB_LAUNCHED(h);
+      std::swap(cur, nxt);
+    }
+    k_big_finish<T, F, L><<<nt, kCtaThreads, 0, s>>>(a, cur);  // t == 1: no sweep to carry the finish
+    MPB_LAUNCHED(h);
+    return MPB_OK;
+  }
   if (!old_big && a.meta != nullptr && a.pat != nullptr && p->npat > 0) {
     // row patterns: no column stream, no block search, finish fused into the last sweep
     k_big_resid_pat<T, F><<<nt, kCtaThreads, 0, s>>>(a, bufs.wA);
@@ -676,7 +698,7 @@ int dist_step(mpb_handle *h, const DistCtx *dc, SolverState *st, int step, int g
 // the plan-packed buffer a.ib_val)
 template <typename T>
 void bind_dia(PassArgs<T> &a, const mpb_plan *p) {
-  if (!p->dia_ok || a.ib_val == nullptr) return;
+  if (!p->dia_layout || a.ib_val == nullptr) return;
   a.dval = a.ib_val + p->dia_at;
   a.dnear = p->near_entries > 0 ? a.ib_val + p->near_at : nullptr;
   a.dmeta = p->d_dmeta;
@@ -1216,11 +1238,21 @@ static int plan_wave(mpb_handle *h, mpb_plan *p, const std::vector<TileDesc> &td
 // stencil in any grid size), and every block has 64 rows.  MPB_DIA=0 turns
 // it off (the SELL kernels then run).
 static int plan_dia(mpb_handle *h, mpb_plan *p) {
-  p->dia_ok = false;
+  p->dia_layout = p->dia_ok = p->dia_big = false;
   p->dia_entries = 0;
   p->dia_at = 0;
+  p->near_entries = 0;
   static const bool off = std::getenv("MPB_DIA") && std::atoi(std::getenv("MPB_DIA")) == 0;
-  if (off || p->large || p->ngeneric != 0 || p->npat <= 0 || p->ub != 64 || p->max_ib_row > kDiaSlots) return MPB_OK;
+  if (off || p->ngeneric != 0 || p->npat <= 0 || p->max_ib_row > kDiaSlots) return MPB_OK;
+  if (!p->large && p->ub != 64) return MPB_OK;  // (tile kernels: a warp per 64-row block)
+  if (p->large) {  // every row must have row metadata (large plans do not count generic rows per tile)
+    static const bool big_off = std::getenv("MPB_DIA_BIG") && std::atoi(std::getenv("MPB_DIA_BIG")) == 0;
+    if (big_off) return MPB_OK;
+    std::vector<uint16_t> meta(p->n);
+    MPB_CUDA(cudaMemcpy(meta.data(), p->d_meta, sizeof(uint16_t) * p->n, cudaMemcpyDeviceToHost));
+    for (int64_t r = 0; r < p->n; r++)
+      if (meta[r] == kMetaGeneric) return MPB_OK;
+  }
   std::vector<int> pat(static_cast<size_t>(p->npat) * kPatStride);
   MPB_CUDA(cudaMemcpy(pat.data(), p->d_pat, sizeof(int) * pat.size(), cudaMemcpyDeviceToHost));
   std::vector<int> offs;
@@ -1261,11 +1293,13 @@ static int plan_dia(mpb_handle *h, mpb_plan *p) {
   for (int k = 0; k < kDiaSlots; k++) p->dia_off[k] = offs[k];
   p->dia_ibany = static_cast<int>(any);
   p->dia_at = (p->ib_nnz + 63) & ~int64_t(63);  // (256-byte aligned for either precision)
-  p->dia_entries = p->n * kDiaSlots;            // (n is a multiple of 64)
+  p->dia_entries = ((p->n + 31) / 32) * 32 * kDiaSlots;  // (whole 32-row slices)
   constexpr unsigned int kNear = (1u << (kDiaDiag - 1)) | (1u << kDiaDiag) | (1u << (kDiaDiag + 1));
   p->near_at = p->dia_at + p->dia_entries;      // (a multiple of 64 entries again)
-  p->near_entries = (any & ~kNear) == 0u ? p->n * kNearSlots : 0;
-  p->dia_ok = true;
+  p->near_entries = (!p->large && (any & ~kNear) == 0u) ? p->n * kNearSlots : 0;
+  p->dia_layout = true;
+  p->dia_ok = !p->large;
+  p->dia_big = p->large != 0;
   return MPB_OK;
 }
 
@@ -1436,7 +1470,7 @@ int mpb_plan_bind_sell(mpb_handle *h, mpb_plan *p, const mpb_sell *sell) {
 // (stencil plans, dia_ok) the offset-slot values at entry dia_at
 int64_t mpb_plan_inblock_nnz(const mpb_plan *p) {
   if (!p || !p->bound) return MPB_ERR_LAYOUT;
-  return p->dia_ok ? p->near_at + p->near_entries : p->ib_nnz;
+  return p->dia_layout ? p->near_at + p->near_entries : p->ib_nnz;
 }
 
 template <typename T>
@@ -1447,7 +1481,7 @@ static int pack_ib_impl(mpb_handle *h, const mpb_plan *p, const T *sell_val, T *
   k_ib_pack<T><<<elt_blocks(p->n), kEltThreads, 0, h->user>>>(p->n, p->bound->d_sp, p->bound->d_col, p->d_boff,
                                                              static_cast<int>(p->nb), p->d_ib_sp, sell_val, ib_val);
   MPB_LAUNCHED(h);
-  if (p->dia_ok) {  // the offset-slot values follow at entry dia_at
+  if (p->dia_layout) {  // the offset-slot values follow at entry dia_at
     MPB_CUDA(cudaMemsetAsync(ib_val + p->ib_nnz, 0, sizeof(T) * (p->dia_at + p->dia_entries - p->ib_nnz), h->user));
     k_dia_pack<T><<<elt_blocks(p->n), kEltThreads, 0, h->user>>>(p->n, p->bound->d_sp, sell_val, p->d_meta, p->d_pat,
                                                                 p->d_pslot, ib_val + p->dia_at);
@@ -1521,8 +1555,8 @@ int mpb_plan_layout_info(const mpb_plan *p, int *h_npat, int64_t *h_ngeneric) {
 
 int mpb_plan_offset_slot_info(const mpb_plan *p, int *h_slots, int *h_inblock_slots, int *h_near) {
   if (!p || !p->bound) return MPB_ERR_ARG;
-  if (h_slots) *h_slots = p->dia_ok ? kDiaSlots : 0;
-  if (h_inblock_slots) *h_inblock_slots = p->dia_ok ? p->dia_ibany : 0;
+  if (h_slots) *h_slots = p->dia_layout ? kDiaSlots : 0;
+  if (h_inblock_slots) *h_inblock_slots = p->dia_layout ? p->dia_ibany : 0;
   if (h_near) *h_near = (p->dia_ok && p->near_entries > 0) ? 1 : 0;
   return MPB_OK;
 }

@@ -1888,6 +1888,79 @@ __global__ void __launch_bounds__(kTileThreads / 2 + 32)
   finish_grid<8, kFinRpt>(a.st, 2, kStepRrZ, ChunkCtx{a.csum, a.part, a.g.ntiles, TWO ? a.g.poll : 0}, ws);
 }
 
+// ---------------------------------------------------------------------------
+// Large blocks (a block spans several tiles, e.g. the reference's default
+// nb = 32) on the offset-slot layout: k_big_resid_pat / k_big_sweep_pat's
+// arithmetic with slot k of every row at column row + doff[k] -- coalesced
+// value loads, no pattern-table reads.  One CTA per 256-row tile, a row per
+// thread; the in-block sweeps gather w from global memory (other tiles).
+// ---------------------------------------------------------------------------
+template <typename T, bool FIRST>
+__global__ void __launch_bounds__(kCtaThreads) k_big_dia_resid(const PassArgs<T> a, T *w0) {
+  if (gated_off(a)) return;
+  const TileDesc d = a.td[blockIdx.x];
+  const int row = d.lo + threadIdx.x;
+  if (row >= d.hi) return;
+  const T rv = a.r64 != nullptr ? narrow_checked(a, a.r64[row], row, FIRST) : a.rT[row];
+  const T *vb = a.dval + static_cast<long long>(row >> 5) * (32 * kDiaSlots) + (row & 31);
+  T az = T(0);
+  if (!FIRST) {
+    const unsigned int m = __ldg(a.dmeta + row);
+    const T *zr = a.zin + row;
+    T v[kDiaSlots], g[kDiaSlots];
+#pragma unroll
+    for (int u = 0; u < kDiaSlots; u++) {
+      v[u] = __ldg(vb + 32 * u);
+      g[u] = __ldg(zr + (((m >> u) & 1u) ? a.doff[u] : 0));  // (an absent slot's product is never added)
+    }
+#pragma unroll
+    for (int u = 0; u < kDiaSlots; u++)
+      if ((m >> u) & 1u) az = add_rn(az, mul_rn(v[u], g[u]));
+  }
+  const T res = FIRST ? rv : sub_rn(rv, az);
+  a.resbuf[row] = res;
+  w0[row] = div_rn(res, __ldg(vb + 32 * kDiaDiag));
+}
+
+template <typename T, bool FIRST, bool LAST, bool FINISH>
+__global__ void __launch_bounds__(kCtaThreads) k_big_dia_sweep(const PassArgs<T> a, const T *wsrc, T *wdst) {
+  if (gated_off(a)) return;
+  __shared__ double ws[32];
+  const int tile = blockIdx.x;
+  const TileDesc d = a.td[tile];
+  const int row = d.lo + threadIdx.x;
+  double prod = 0.0;
+  if (row < d.hi) {
+    const unsigned int m = __ldg(a.dmeta + row) >> 8;  // in-block slots
+    const T *vb = a.dval + static_cast<long long>(row >> 5) * (32 * kDiaSlots) + (row & 31);
+    const T *wr = wsrc + row;
+    T v[kDiaSlots], g[kDiaSlots];
+#pragma unroll
+    for (int u = 0; u < kDiaSlots; u++) {
+      v[u] = __ldg(vb + 32 * u);
+      g[u] = wr[((m >> u) & 1u) ? a.doff[u] : 0];
+    }
+    T acc = T(0);
+#pragma unroll
+    for (int u = 0; u < kDiaSlots; u++)
+      if ((m >> u) & 1u) acc = add_rn(acc, mul_rn(v[u], g[u]));
+    const T wn = add_rn(g[kDiaDiag], div_rn(sub_rn(a.resbuf[row], acc), v[kDiaDiag]));  // (the diagonal is in-block)
+    if (!FINISH) {
+      wdst[row] = wn;
+    } else {
+      const T zo = FIRST ? wn : add_rn(a.zin[row], wn);
+      if (a.zout != nullptr) st_keep(a.zout + row, zo);
+      if (a.zout64 != nullptr) a.zout64[row] = static_cast<double>(zo);
+      if (LAST && a.part != nullptr) prod = __dmul_rn(a.r64[row], static_cast<double>(zo));
+    }
+  }
+  if (FINISH && LAST && a.part != nullptr) {
+    const double tot = block_tree<kTileThreads>(prod, ws);
+    if (threadIdx.x == 0) put_part(a.part + tile, tot);
+    finish_grid(a.st, 0, kStepRho, ChunkCtx{a.st != nullptr ? a.csum : nullptr, a.part, a.g.ntiles, a.g.poll}, ws, true);
+  }
+}
+
 // Setup: per-row masks of the offset-slot layout from the row metadata
 // (pattern id, in-block slot range) and pslot[pid * kSlots + j] = the
 // offset slot of the pattern's j-th stored entry; any[0] collects the slots
