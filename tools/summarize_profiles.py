@@ -58,8 +58,25 @@ def full(tag, cfg):
             part = list(csv.reader(open(path)))
             if not rows:
                 rows = part
-            else:
-                rows += part[2:]
+            else:  # ncu picks units per report: rescale this file's byte / time columns to the first file's
+                scale = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3, "ns": 1e-3, "us": 1.0, "ms": 1e3,
+                         "usecond": 1.0, "nsecond": 1e-3, "msecond": 1e3}
+                h0, u0 = rows[0], rows[1]
+                for r in part[2:]:
+                    out = []
+                    for k, u_first in zip(h0, u0):
+                        if k not in part[0]:
+                            out.append("")
+                            continue
+                        i = part[0].index(k)
+                        v, u = r[i], part[1][i]
+                        if u != u_first and u in scale and u_first in scale:
+                            try:
+                                v = repr(float(v.replace(",", "")) * scale[u] / scale[u_first])
+                            except ValueError:
+                                pass
+                        out.append(v)
+                    rows.append(out)
     hdr, units = rows[0], rows[1]
 
     def get(r, k):
