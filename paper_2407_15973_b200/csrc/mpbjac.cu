@@ -938,6 +938,7 @@ struct SolveWs {
   float *res32, *dg32, *wA32, *wB32;
   double *part;
   double *part2;       // wave kernel: the r.z tile partials of its last-pass items (part: r.r)
+  double *part3;       // k_solve_small: one array per dot product (part r.z, part2 p.q, part3 r.r)
   unsigned int *gcnt;  // wave kernel: per tile group, update items published this solve
   double *csum;        // chunk sums of the two-level dot sums (part: all slots kPartEmpty between kernels)
   SolverState *st;
@@ -978,6 +979,7 @@ SolveWs carve(const mpb_plan *p, int64_t n, char *base, int64_t ng = 0) {
   }
   w.part = (double *)take(sizeof(double) * (p->ntiles + 1));
   w.part2 = (double *)take(sizeof(double) * (p->ntiles + 1));
+  w.part3 = (double *)take(sizeof(double) * (p->ntiles + 1));
   w.gcnt = (unsigned int *)take(sizeof(unsigned int) * (p->ntiles / 32 + 8));
   w.csum = (double *)take(sizeof(double) * ((p->ntiles + kChunkTiles - 1) / kChunkTiles + 1));
   w.st = (SolverState *)take(sizeof(SolverState));
@@ -2350,6 +2352,105 @@ int mpb_comm_create_local(void *group, int rank, mpb_comm **out) {
   return MPB_OK;
 }
 
+// The end of a solve (the state is in h->h_state, the loop's events are
+// recorded): final true residual, result struct, hand-over to the caller's
+// stream.
+static int finish_solve(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, const double *b, double *x,
+                        const SolveWs &w, mpb_solve_result *res, const DistCtx *dc, cudaStream_t s,
+                        int64_t launches0) {
+  int rc = MPB_OK;
+  const unsigned nt = static_cast<unsigned>(plan->ntiles);
+  const SolverState st = *h->h_state;
+  if (st.error == kOk) {  // final true residual (solver.py:179-182)
+    if ((rc = halo_exchange(dc, x, 8, A->n, s))) return rc;
+    k_resid<true><<<persistent_grid(k_resid<true>, 0, plan->ntiles), kCtaThreads, 0, s>>>(
+                                              A->sell->d_sp, A->sell->d_col, op_vals(A), plan->d_td, static_cast<int>(nt), b, x, nullptr, w.part, w.st, 0,
+                                              kStepFinal, w.csum, owners_poll(plan->ntiles) ? 1 : 0);
+    MPB_LAUNCHED(h);
+    if ((rc = dist_step(h, dc, w.st, kStepFinal, 0, s))) return rc;
+    MPB_CUDA(cudaMemcpyAsync(h->h_state, w.st, sizeof(SolverState), cudaMemcpyDeviceToHost, s));
+  }
+  MPB_CUDA(cudaStreamSynchronize(s));
+  float ms = 0.f;
+  MPB_CUDA(cudaEventElapsedTime(&ms, h->ev_t0, h->ev_t1));
+  const SolverState fin = *h->h_state;
+  res->converged = fin.converged;
+  res->error = fin.error;
+  res->iterations = fin.error ? fin.err_it : fin.last_it;
+  res->err_iteration = fin.error ? fin.err_it : 0;
+  res->err_value = fin.err_val;
+  res->final_true_relres = fin.error ? NAN : fin.final_true;
+  // ovf_count is global (all-reduced on the multi-GPU path); ovf_first is
+  // this rank's own first local row, INT64_MAX when the overflow happened on
+  // another rank (the caller all-reduces the global first index,
+  // distributed.SlabSolver).  Only a row this rank owns is dereferenced.
+  const bool local_ovf = fin.ovf_count && fin.ovf_first >= 0 && fin.ovf_first < A->n;
+  res->overflow_count = static_cast<int64_t>(fin.ovf_count);
+  res->overflow_index = local_ovf ? fin.ovf_first : -1;
+  if (fin.error == kNarrowOverflow) {  // the offending r entry
+    res->err_value = NAN;
+    if (local_ovf)
+      MPB_CUDA(cudaMemcpy(&res->err_value, w.r + fin.ovf_first, sizeof(double), cudaMemcpyDeviceToHost));
+  }
+  res->device_seconds = 1e-3 * ms;
+  res->kernel_launches = h->launches - launches0;
+  MPB_CUDA(cudaEventRecord(h->ev_out, s));
+  MPB_CUDA(cudaStreamWaitEvent(h->user, h->ev_out, 0));
+  return MPB_OK;
+}
+
+// ---- small problems: the whole loop in k_solve_small ------------------------
+static bool small_mode(const mpb_handle *h, const mpb_plan *p, const mpb_csr *A, const mpb_solve_options *o,
+                       const DistCtx *dc) {
+  static const bool off = std::getenv("MPB_SMALL") && std::atoi(std::getenv("MPB_SMALL")) == 0;
+  if (off || dc != nullptr || !p->dia_ok || o->true_stride != 0 || std::getenv("MPB_TIMELINE")) return false;
+  if (p->ntiles > num_sms()) return false;
+  if (o->kind != MPB_UNIFORM && A->ib_val32 == nullptr) return false;
+  if (o->kind != MPB_FIXED_LOW && A->ib_val64 == nullptr) return false;
+  if ((A->op_sell_val64 ? A->op_ib_val64 : A->ib_val64) == nullptr) return false;
+  (void)h;
+  return true;
+}
+
+static int launch_small(mpb_handle *h, cudaStream_t s, const mpb_plan *p, const mpb_csr *A,
+                        const mpb_solve_options *o, const SolveWs &w, double *x) {
+  SmallArgs a{};
+  a.dval32 = o->kind != MPB_UNIFORM ? A->ib_val32 + p->dia_at : nullptr;
+  a.dval64 = o->kind != MPB_FIXED_LOW ? A->ib_val64 + p->dia_at : nullptr;
+  a.dvalop = (A->op_sell_val64 ? A->op_ib_val64 : A->ib_val64) + p->dia_at;
+  a.dmeta = p->d_dmeta;
+  a.td = p->d_td;
+  for (int u = 0; u < kDiaSlots; u++) a.doff[u] = p->dia_off[u];
+  a.ntiles = static_cast<int>(p->ntiles);
+  a.k = o->k;
+  a.t = o->t;
+  a.x = x;
+  a.r = w.r;
+  a.z = w.z64;
+  a.pA = w.p;
+  a.pB = w.p2;
+  a.zA32 = w.zA32;
+  a.zB32 = w.zB32;
+  a.zA64 = w.zA64;
+  a.zB64 = w.zB64;
+  a.part_rz = w.part;
+  a.part_pq = w.part2;
+  a.part_rr = w.part3;
+  a.bar = w.gcnt;
+  a.st = w.st;
+  MPB_CUDA(cudaMemsetAsync(w.gcnt, 0, sizeof(unsigned int), s));
+  const bool two64 = a.dval64 != nullptr && a.dval64 != a.dvalop;
+  const size_t dyn = sizeof(double) * kTileRows * kDiaSlots * (two64 ? 2 : 1) + sizeof(float) * kTileRows * kDiaSlots;
+  int per_sm = 0;
+  MPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve_small, kCtaThreads, dyn));
+  if (per_sm < 1 || p->ntiles > int64_t(per_sm) * num_sms()) return MPB_ERR_WORKSPACE;
+  void *args[] = {&a};
+  MPB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void *>(k_solve_small), dim3(static_cast<unsigned>(p->ntiles)),
+                                       dim3(kCtaThreads), args, dyn, s));
+  MPB_LAUNCHED(h);
+  return MPB_OK;
+}
+
 static int solve_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, const mpb_solve_options *opt,
                       const double *b, double *x, double *tr_relres, double *tr_true, int32_t *tr_branch,
                       double *tr_time, void *workspace, int64_t workspace_bytes, mpb_solve_result *res,
@@ -2434,6 +2535,18 @@ static int solve_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, con
     return MPB_OK;
   }
 
+  // Small problems (at most one tile per SM, offset-slot layout, no strided
+  // true residuals): the whole loop in one persistent cooperative kernel
+  if (small_mode(h, plan, A, opt, dc)) {
+    k_scalar_start<<<1, 32, 0, s>>>(w.st);
+    MPB_LAUNCHED(h);
+    MPB_CUDA(cudaEventRecord(h->ev_t0, s));
+    if ((rc = launch_small(h, s, plan, A, opt, w, x))) return rc;
+    MPB_CUDA(cudaEventRecord(h->ev_t1, s));
+    MPB_CUDA(cudaMemcpyAsync(h->h_state, w.st, sizeof(SolverState), cudaMemcpyDeviceToHost, s));
+    MPB_CUDA(cudaStreamSynchronize(s));
+    return finish_solve(h, plan, A, b, x, w, res, dc, s, launches0);
+  }
   // the symmetric offset-slot SpMV layout of the operator (one GPU; built once per value array)
   if (dc == nullptr) ensure_sym(h, const_cast<mpb_plan *>(plan), A, s);
   // capture G iterations once (cached across solves with the same buffers)
@@ -2609,43 +2722,7 @@ static int solve_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, con
     MPB_CUDA(cudaMemcpy(&spins, w.gcnt + plan->ntiles / 32 + 4, sizeof(unsigned int), cudaMemcpyDeviceToHost));
     std::fprintf(stderr, "[mpb] wave: %u dependency polls in this solve\n", spins);
   }
-  const SolverState st = *h->h_state;
-  if (st.error == kOk) {  // final true residual (solver.py:179-182)
-    if ((rc = halo_exchange(dc, x, 8, A->n, s))) return rc;
-    k_resid<true><<<persistent_grid(k_resid<true>, 0, plan->ntiles), kCtaThreads, 0, s>>>(
-                                              A->sell->d_sp, A->sell->d_col, op_vals(A), plan->d_td, static_cast<int>(nt), b, x, nullptr, w.part, w.st, 0,
-                                              kStepFinal, w.csum, owners_poll(plan->ntiles) ? 1 : 0);
-    MPB_LAUNCHED(h);
-    if ((rc = dist_step(h, dc, w.st, kStepFinal, 0, s))) return rc;
-    MPB_CUDA(cudaMemcpyAsync(h->h_state, w.st, sizeof(SolverState), cudaMemcpyDeviceToHost, s));
-  }
-  MPB_CUDA(cudaStreamSynchronize(s));
-  float ms = 0.f;
-  MPB_CUDA(cudaEventElapsedTime(&ms, h->ev_t0, h->ev_t1));
-  const SolverState fin = *h->h_state;
-  res->converged = fin.converged;
-  res->error = fin.error;
-  res->iterations = fin.error ? fin.err_it : fin.last_it;
-  res->err_iteration = fin.error ? fin.err_it : 0;
-  res->err_value = fin.err_val;
-  res->final_true_relres = fin.error ? NAN : fin.final_true;
-  // ovf_count is global (all-reduced on the multi-GPU path); ovf_first is
-  // this rank's own first local row, INT64_MAX when the overflow happened on
-  // another rank (the caller all-reduces the global first index,
-  // distributed.SlabSolver).  Only a row this rank owns is dereferenced.
-  const bool local_ovf = fin.ovf_count && fin.ovf_first >= 0 && fin.ovf_first < A->n;
-  res->overflow_count = static_cast<int64_t>(fin.ovf_count);
-  res->overflow_index = local_ovf ? fin.ovf_first : -1;
-  if (fin.error == kNarrowOverflow) {  // the offending r entry
-    res->err_value = NAN;
-    if (local_ovf)
-      MPB_CUDA(cudaMemcpy(&res->err_value, w.r + fin.ovf_first, sizeof(double), cudaMemcpyDeviceToHost));
-  }
-  res->device_seconds = 1e-3 * ms;
-  res->kernel_launches = h->launches - launches0;
-  MPB_CUDA(cudaEventRecord(h->ev_out, s));
-  MPB_CUDA(cudaStreamWaitEvent(h->user, h->ev_out, 0));
-  return MPB_OK;
+  return finish_solve(h, plan, A, b, x, w, res, dc, s, launches0);
 }
 
 static int profile_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, const mpb_solve_options *opt,

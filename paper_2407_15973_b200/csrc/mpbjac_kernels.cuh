@@ -144,7 +144,9 @@ __device__ __forceinline__ void fail(SolverState *st, int code, double val) {
 // Executed by one thread once the global sum `tot` of a step is known.
 // Inlined where the step is a constant (the switch folds), on a state copy
 // in shared memory (finish_grid) or registers.
-__device__ __forceinline__ void scalar_step_body(int step, double tot, SolverState *st) {
+// trace: false skips the trace-array writes (k_solve_small: every CTA runs
+// the steps on its own state copy, CTA 0 alone writes the trace)
+__device__ __forceinline__ void scalar_step_body(int step, double tot, SolverState *st, bool trace = true) {
   switch (step) {
     case kStepR0: {
       st->r0 = sqrt(tot);
@@ -190,9 +192,11 @@ __device__ __forceinline__ void scalar_step_body(int step, double tot, SolverSta
       const double relres = rnorm / st->r0;
       st->relres = relres;
       const long long it = st->it;
-      st->tr_relres[it - 1] = relres;
-      st->tr_branch[it - 1] = st->branch;
-      st->tr_time[it - 1] = 1e-9 * static_cast<double>(globaltimer_ns() - st->t0_ns);
+      if (trace) {
+        st->tr_relres[it - 1] = relres;
+        st->tr_branch[it - 1] = st->branch;
+        st->tr_time[it - 1] = 1e-9 * static_cast<double>(globaltimer_ns() - st->t0_ns);
+      }
       st->last_it = it;
       st->true_pending = (st->stride > 0 && it % st->stride == 0) ? 1 : 0;
       if (relres <= st->res_tol) {
@@ -1958,6 +1962,271 @@ __global__ void __launch_bounds__(kCtaThreads) k_big_dia_sweep(const PassArgs<T>
     const double tot = block_tree<kTileThreads>(prod, ws);
     if (threadIdx.x == 0) put_part(a.part + tile, tot);
     finish_grid(a.st, 0, kStepRho, ChunkCtx{a.st != nullptr ? a.csum : nullptr, a.part, a.g.ntiles, a.g.poll}, ws, true);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Whole solve in ONE persistent cooperative kernel, for problems of at most
+// one tile per SM on the offset-slot layout (C1: 128 tiles).  Such a problem
+// is L2-resident and each of the three kernels of an iteration is almost all
+// fixed cost (launch, TMA round trip, grid ticket, final-CTA sum, drain):
+// ~7 us per kernel against < 1 us of work.  Here CTA t owns tile t for the
+// whole solve: its rows' x, r, p stay in registers, its matrix values (fp32
+// and fp64 instance, operator) in shared memory; the three dependent global
+// sums of an iteration are three grid barriers (release add + acquire spin on
+// one counter), after which EVERY CTA sums the tile partials in the fixed
+// order and runs the scalar step on its own copy of the solver state -- all
+// copies stay identical, CTA 0 writes the trace.  Vectors other CTAs gather
+// (pass outputs, z, p) go through global memory (L2: __ldcg).  Arithmetic,
+// sum orders and the policy logic are those of the three-kernel iteration,
+// so the solve is bit-identical to it (and to the oracle's device order).
+// ---------------------------------------------------------------------------
+struct SmallArgs {
+  const float *dval32;    // offset-slot values: fp32 instance (null: uniform policy)
+  const double *dval64;   // fp64 instance (null: fixed-low policy)
+  const double *dvalop;   // the operator
+  const uint16_t *dmeta;
+  const TileDesc *td;
+  int doff[8];
+  int ntiles, k, t;
+  double *x, *r;          // in: x0 and r0 = b - A x0; out: the solution (and final r)
+  double *z;              // final z of the iteration, widened (gathered by the p rebuild)
+  double *pA, *pB;        // search direction, alternating
+  float *zA32, *zB32;     // pass outputs (fp32 instance)
+  double *zA64, *zB64;    //              (fp64 instance)
+  double *part_rz, *part_pq, *part_rr;
+  unsigned int *bar;      // grid barrier counter (zero at launch)
+  SolverState *st;
+};
+
+__device__ __forceinline__ void grid_bar(unsigned int *bar, unsigned int &target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    target += gridDim.x;
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+    unsigned int v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+    } while (v < target);
+  }
+  __syncthreads();
+}
+
+// in-block sweeps of one row (w in, w out) against the tile's s_w
+template <typename T>
+__device__ __forceinline__ T small_sweeps(const SmallArgs &a, const T *v, unsigned int inb, int ti, bool valid,
+                                          T res, T w, T *s_w) {
+  s_w[ti] = w;
+  for (int sw = 1; sw < a.t; sw++) {
+    __syncthreads();
+    T acc = T(0);
+#pragma unroll
+    for (int u = 0; u < kDiaSlots; u++)
+      if (valid && ((inb >> u) & 1u)) acc = add_rn(acc, mul_rn(v[32 * u], s_w[ti + a.doff[u]]));
+    __syncthreads();
+    w = add_rn(w, div_rn(sub_rn(res, acc), v[32 * kDiaDiag]));
+    s_w[ti] = w;
+  }
+  __syncthreads();  // (s_w is rewritten by the next pass)
+  return w;
+}
+
+// first pass z1 = D_b^{-1} r of the row (bjac_first_body's arithmetic), stored for the other tiles
+template <typename T>
+__device__ __forceinline__ T small_first(const SmallArgs &a, const T *v, unsigned int m, int ti, int row, bool valid,
+                                         double ri, T *s_w, T *zout, T &rv) {
+  rv = T(0);
+  if (valid) {
+    rv = narrow_or_copy<T>(ri);
+    if (sizeof(T) == 4 && isinf(rv) && isfinite(ri)) {
+      atomicAdd(&a.st->ovf_count, 1ull);
+      atomicMin(&a.st->ovf_first, static_cast<long long>(row));
+    }
+  }
+  T w = valid ? div_rn(rv, v[32 * kDiaDiag]) : T(0);
+  w = small_sweeps<T>(a, v, m >> 8, ti, valid, rv, w, s_w);
+  if (valid) zout[row] = w;
+  return w;
+}
+
+// a pass after the first: z_out = z_in + D_b^{-1}(r - A z_in)
+template <typename T>
+__device__ __forceinline__ T small_pass(const SmallArgs &a, const T *v, unsigned int m, int ti, int row, bool valid,
+                                        T rv, const T *zin, T *s_w) {
+  T zown = T(0), res = T(0), w = T(0);
+  if (valid) {
+    T g[kDiaSlots];
+#pragma unroll
+    for (int u = 0; u < kDiaSlots; u++) g[u] = __ldcg(zin + row + (((m >> u) & 1u) ? a.doff[u] : 0));
+    T az = T(0);
+#pragma unroll
+    for (int u = 0; u < kDiaSlots; u++)
+      if ((m >> u) & 1u) az = add_rn(az, mul_rn(v[32 * u], g[u]));
+    zown = g[kDiaDiag];
+    res = sub_rn(rv, az);
+    w = div_rn(res, v[32 * kDiaDiag]);
+  }
+  w = small_sweeps<T>(a, v, m >> 8, ti, valid, res, w, s_w);
+  return add_rn(zown, w);
+}
+
+// the preconditioner of the iteration from its first pass on (z1 in zA): returns z widened
+template <typename T>
+__device__ __forceinline__ double small_rest(const SmallArgs &a, const T *v, unsigned int m, int ti, int row,
+                                             bool valid, T rv, T z1, T *zA, T *zB, T *s_w, unsigned int &target,
+                                             bool synced) {
+  T z = z1;
+  for (int pass = 1; pass < a.k; pass++) {
+    // the previous pass's output of every tile must be stored (synced: z1 was, before the r.r barrier)
+    if (pass > 1 || !synced) grid_bar(a.bar, target);
+    const T *zin = (pass - 1) & 1 ? zB : zA;
+    z = small_pass<T>(a, v, m, ti, row, valid, rv, zin, s_w);
+    if (valid && pass + 1 < a.k) (pass & 1 ? zB : zA)[row] = z;
+  }
+  return static_cast<double>(z);
+}
+
+__global__ void __launch_bounds__(kCtaThreads) k_solve_small(const SmallArgs a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(16) unsigned long long s_state[kStWords];
+  __shared__ double ws[32];
+  __shared__ float s_w32[kTileRows];
+  __shared__ double s_w64[kTileRows];
+  constexpr int kSlab = kTileRows * kDiaSlots;  // entries of a tile's value slab
+  double *s_op = reinterpret_cast<double *>(smem);
+  double *s_v64 = a.dval64 == nullptr ? nullptr : (a.dval64 == a.dvalop ? s_op : s_op + kSlab);
+  float *s_v32 = reinterpret_cast<float *>(s_op + ((a.dval64 != nullptr && a.dval64 != a.dvalop) ? 2 : 1) * kSlab);
+  const int tile = blockIdx.x, ti = threadIdx.x;
+  const TileDesc d = a.td[tile];
+  const int row = d.lo + ti;
+  const bool valid = row < d.hi;
+  SolverState *L = reinterpret_cast<SolverState *>(s_state);
+  if (ti < kStWords) s_state[ti] = __ldcg(reinterpret_cast<const unsigned long long *>(a.st) + ti);
+  {  // the tile's value slabs (rows past the tile: zero)
+    const long long g0 = static_cast<long long>(kDiaSlots) * d.lo;
+    const int cnt = kDiaSlots * (((d.hi - d.lo) + 31) & ~31);
+    for (int i = ti; i < kSlab; i += kCtaThreads) {
+      s_op[i] = i < cnt ? a.dvalop[g0 + i] : 0.0;
+      if (s_v64 != nullptr && s_v64 != s_op) s_v64[i] = i < cnt ? a.dval64[g0 + i] : 0.0;
+      if (a.dval32 != nullptr) s_v32[i] = i < cnt ? a.dval32[g0 + i] : 0.f;
+    }
+  }
+  const unsigned int m = valid ? a.dmeta[row] : 0u;
+  const int vo = (ti >> 5) * (32 * kDiaSlots) + (ti & 31);  // slot u of the row at vo + 32 u
+  const double *vop = s_op + vo;
+  const double *v64 = s_v64 != nullptr ? s_v64 + vo : nullptr;
+  const float *v32 = s_v32 + vo;
+  double xi = valid ? a.x[row] : 0.0, ri = valid ? a.r[row] : 0.0, pi = 0.0;
+  unsigned int target = 0;
+  int cur = 0;  // pold = cur ? pB : pA
+  __syncthreads();
+  const bool lead = blockIdx.x == 0;
+  float rv32 = 0.f, z1_32 = 0.f;
+  double rv64 = 0.0, z1_64 = 0.0;
+  // the first iteration's first pass
+  if (L->branch == 1) z1_32 = small_first<float>(a, v32, m, ti, row, valid, ri, s_w32, a.zA32, rv32);
+  else z1_64 = small_first<double>(a, v64, m, ti, row, valid, ri, s_w64, a.zA64, rv64);
+  bool synced = false;  // every tile's z1 is stored and a grid barrier has passed since
+  for (;;) {
+    // ---- z = M^{-1} r (remaining passes), rho = r.z --------------------------
+    const double zi = L->branch == 1
+                          ? small_rest<float>(a, v32, m, ti, row, valid, rv32, z1_32, a.zA32, a.zB32, s_w32, target, synced)
+                          : small_rest<double>(a, v64, m, ti, row, valid, rv64, z1_64, a.zA64, a.zB64, s_w64, target, synced);
+    if (valid) a.z[row] = zi;
+    {
+      const double tot = block_tree<kTileThreads>(valid ? __dmul_rn(ri, zi) : 0.0, ws);
+      if (ti == 0) a.part_rz[tile] = tot;
+    }
+    grid_bar(a.bar, target);
+    {
+      const double rho = fin_sum<8, 1>(a.part_rz, a.ntiles, ws);
+      if (ti == 0) {
+        L->ovf_count = __ldcg(&a.st->ovf_count);
+        L->ovf_first = __ldcg(&a.st->ovf_first);
+        scalar_step_body(kStepRho, rho, L, lead);
+      }
+      __syncthreads();
+    }
+    if (L->done) break;
+    // ---- p = z + beta p, q = A p, pq = p.q ------------------------------------
+    const bool first = L->first != 0;
+    const double beta = L->beta;
+    const double *pold = cur ? a.pB : a.pA;
+    double q = 0.0;
+    if (valid) {
+      double pv[kDiaSlots];
+#pragma unroll
+      for (int u = 0; u < kDiaSlots; u++) {
+        const int c = row + (((m >> u) & 1u) ? a.doff[u] : 0);
+        const double zv = __ldcg(a.z + c);
+        pv[u] = first ? zv : __dadd_rn(zv, __dmul_rn(beta, __ldcg(pold + c)));
+      }
+#pragma unroll
+      for (int u = 0; u < kDiaSlots; u++)
+        if ((m >> u) & 1u) q = __dadd_rn(q, __dmul_rn(vop[32 * u], pv[u]));
+      pi = pv[kDiaDiag];
+      (cur ? a.pA : a.pB)[row] = pi;
+    }
+    cur ^= 1;
+    {
+      const double tot = block_tree<kTileThreads>(valid ? __dmul_rn(pi, q) : 0.0, ws);
+      if (ti == 0) a.part_pq[tile] = tot;
+    }
+    grid_bar(a.bar, target);
+    {
+      const double pq = fin_sum<8, 1>(a.part_pq, a.ntiles, ws);
+      if (ti == 0) scalar_step_body(kStepPq, pq, L, lead);
+      __syncthreads();
+    }
+    if (L->done) break;
+    // ---- x += alpha p, r -= alpha q, rr = r.r, the next first pass -------------
+    const double alpha = L->alpha;
+    if (valid) {
+      xi = __dadd_rn(xi, __dmul_rn(alpha, pi));
+      ri = __dsub_rn(ri, __dmul_rn(alpha, q));
+    }
+    {
+      const double tot = block_tree<kTileThreads>(valid ? __dmul_rn(ri, ri) : 0.0, ws);
+      if (ti == 0) a.part_rr[tile] = tot;
+    }
+    if (L->branch == 1) z1_32 = small_first<float>(a, v32, m, ti, row, valid, ri, s_w32, a.zA32, rv32);
+    else z1_64 = small_first<double>(a, v64, m, ti, row, valid, ri, s_w64, a.zA64, rv64);
+    grid_bar(a.bar, target);
+    {
+      const double rr = fin_sum<8, 1>(a.part_rr, a.ntiles, ws);
+      if (ti == 0) scalar_step_body(kStepRrZ, rr, L, lead);
+      __syncthreads();
+    }
+    if (L->done) break;
+    synced = true;
+    if (!L->z1_ok) {  // the aMP branch changed: the speculative first pass (and its narrowing count) is void
+      synced = false;
+      if (lead && ti == 0) {
+        a.st->ovf_count = 0ull;
+        a.st->ovf_first = 0x7fffffffffffffffLL;
+      }
+      grid_bar(a.bar, target);
+      if (L->branch == 1) z1_32 = small_first<float>(a, v32, m, ti, row, valid, ri, s_w32, a.zA32, rv32);
+      else z1_64 = small_first<double>(a, v64, m, ti, row, valid, ri, s_w64, a.zA64, rv64);
+    }
+  }
+  if (valid) {
+    a.x[row] = xi;
+    a.r[row] = ri;
+  }
+  if (lead && ti < 32) {  // the final state (state_store's ranges; the narrowing counters stay as counted)
+    if (ti == 0) {
+      L->ovf_count = __ldcg(&a.st->ovf_count);
+      L->ovf_first = __ldcg(&a.st->ovf_first);
+    }
+    __syncwarp();
+    unsigned long long *dst = reinterpret_cast<unsigned long long *>(a.st);
+    constexpr int a1 = static_cast<int>(offsetof(SolverState, tr_relres) / 8);
+    constexpr int b0 = static_cast<int>(offsetof(SolverState, dist) / 8), b1 = static_cast<int>(offsetof(SolverState, cond) / 8);
+    for (int i = ti; i < a1 + (b1 - b0); i += 32) {
+      const int wd = i < a1 ? i : b0 + (i - a1);
+      dst[wd] = s_state[wd];
+    }
   }
 }
 

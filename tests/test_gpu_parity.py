@@ -480,8 +480,21 @@ def test_offset_slot_layout_bitwise(cuda, oracle, n, pol):
         np.testing.assert_array_equal(rep.x, orc["x"])
         np.testing.assert_array_equal([r.implicit_relres for r in rep.trace], orc["relres"])
         assert rep.final_true_relres == orc["final_true_relres"]
+    # without strided true residuals a problem of at most one tile per SM (n = 32: 128 tiles)
+    # runs the whole loop in one persistent cooperative kernel (k_solve_small)
+    for _ in range(3):
+        rep = pcg_solve(A, cs.b, mp, SolveConfig(res_tol=1e-9))
+        assert rep.iterations == orc["iterations"]
+        np.testing.assert_array_equal(rep.x, orc["x"])
+        np.testing.assert_array_equal([r.implicit_relres for r in rep.trace], orc["relres"])
+        assert [r.branch for r in rep.trace] == list(orc["branch"])
+        assert rep.final_true_relres == orc["final_true_relres"]
     A2 = diag_augment(A, 0.25)
     mp2 = build_mixed(A2, pp, k=2, t=3, partition=part)
+    rep = pcg_solve(A, cs.b, mp2, SolveConfig(res_tol=1e-9))
+    orc2 = oracle.pcg_solve(A.row_ptr, A.col_idx, A.values, cs.b, part.offsets, prec_values=A2.values, **kw)
+    assert rep.iterations == orc2["iterations"]
+    np.testing.assert_array_equal(rep.x, orc2["x"])
     rep = pcg_solve(A, cs.b, mp2, cfg)
     orc = oracle.pcg_solve(A.row_ptr, A.col_idx, A.values, cs.b, part.offsets, prec_values=A2.values, **kw)
     assert rep.iterations == orc["iterations"]
