@@ -474,7 +474,10 @@ def run_b200(args, world, rank, local):
             "config": config_dict(cs, part, policy, {
                 "parallelism": (f"z-slabs over {world} GPU(s), NCCL halos + fp64 all-reduce"
                                 if sharded else "1 GPU"),
-                "graph": "one CUDA graph per solve: a device-side while loop over 16-iteration bodies",
+                "graph": ("one persistent cooperative kernel per solve (k_solve_small: at most one tile "
+                          "per SM); kernels.* below time the three-kernel iteration it replaces"
+                          if launches / max(args.steps, 1) < 16 and not sharded else
+                          "one CUDA graph per solve: a device-side while loop over 16-iteration bodies"),
                 "row_patterns": plan.layout_info()}),
             "iterations": it_med, "time_to_solution_ms": ms_per_step,
             "converged": bool(rep.converged), "final_true_relres": rep.final_true_relres,
