@@ -112,6 +112,22 @@ __device__ __forceinline__ float warp_bfly(float v) {
   return v;
 }
 
+// Two butterflies at once (a lane's values of two 32-row groups): after the
+// xor-16 level lanes 0-15 carry the first value's partial sums and lanes
+// 16-31 the second's (a + b computed by one of the two lanes that would both
+// compute it -- IEEE addition commutes), and the remaining levels stay inside
+// the 16-lane halves.  Every sum is formed from the same operands as in
+// warp_bfly, so the totals are bit-identical: lanes 0-15 return v0's, lanes
+// 16-31 v1's.  One shuffle per level instead of two.
+__device__ __forceinline__ double warp_bfly2(double v0, double v1) {
+  const bool hi = (threadIdx.x & 16) != 0;
+  const double send = hi ? v0 : v1, keep = hi ? v1 : v0;
+  double v = __dadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, 16));
+#pragma unroll
+  for (int o = 8; o >= 1; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
 // Steps 2-3: per-warp butterfly then warp 0 butterflies the warp sums padded
 // with +0 to 32 lanes.  Result valid in thread 0.  ws: 32 entries of smem.
 template <int NT, typename R>
