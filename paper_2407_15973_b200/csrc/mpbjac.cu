@@ -2404,12 +2404,19 @@ static bool small_mode(const mpb_handle *h, const mpb_plan *p, const mpb_csr *A,
                        const DistCtx *dc) {
   static const bool off = std::getenv("MPB_SMALL") && std::atoi(std::getenv("MPB_SMALL")) == 0;
   if (off || dc != nullptr || !p->dia_ok || o->true_stride != 0 || std::getenv("MPB_TIMELINE")) return false;
-  if (p->ntiles > num_sms()) return false;
   if (o->kind != MPB_UNIFORM && A->ib_val32 == nullptr) return false;
   if (o->kind != MPB_FIXED_LOW && A->ib_val64 == nullptr) return false;
   if ((A->op_sell_val64 ? A->op_ib_val64 : A->ib_val64) == nullptr) return false;
   (void)h;
-  return true;
+  // every CTA of the grid must be resident at once (cooperative launch)
+  int per_sm = 0, coop = 0, dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev) != cudaSuccess || !coop)
+    return false;
+  const size_t dyn = sizeof(double) * kTileRows * kDiaSlots * 2 + sizeof(float) * kTileRows * kDiaSlots;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve_small, kCtaThreads, dyn) != cudaSuccess)
+    return false;
+  return per_sm >= 1 && p->ntiles <= int64_t(per_sm) * num_sms();
 }
 
 static int launch_small(mpb_handle *h, cudaStream_t s, const mpb_plan *p, const mpb_csr *A,
@@ -2535,7 +2542,7 @@ static int solve_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, con
     return MPB_OK;
   }
 
-  // Small problems (at most one tile per SM, offset-slot layout, no strided
+  // Small problems (every tile's CTA co-resident, offset-slot layout, no strided
   // true residuals): the whole loop in one persistent cooperative kernel
   if (small_mode(h, plan, A, opt, dc)) {
     k_scalar_start<<<1, 32, 0, s>>>(w.st);

@@ -446,7 +446,8 @@ def test_pcg_preconditioner_from_other_matrix(cuda, oracle, pol):
 
 
 @pytest.mark.parametrize("n,pol", ((64, "fixed-low"), (64, "uniform"), (64, "adaptive-hl:1e-3"),
-                                   (32, "fixed-low"), (32, "adaptive-lh:1e-4")))
+                                   (32, "fixed-low"), (32, "adaptive-lh:1e-4"),
+                                   (48, "fixed-low"), (48, "adaptive-hl:1e-3")))
 def test_offset_slot_layout_bitwise(cuda, oracle, n, pol):
     """7-point stencil plans with 64-row blocks run the offset-slot kernels
     (k_bjac_dia, k_spmv_dia, k_update_first_dia: warp per block, no pattern
@@ -480,8 +481,9 @@ def test_offset_slot_layout_bitwise(cuda, oracle, n, pol):
         np.testing.assert_array_equal(rep.x, orc["x"])
         np.testing.assert_array_equal([r.implicit_relres for r in rep.trace], orc["relres"])
         assert rep.final_true_relres == orc["final_true_relres"]
-    # without strided true residuals a problem of at most one tile per SM (n = 32: 128 tiles)
-    # runs the whole loop in one persistent cooperative kernel (k_solve_small)
+    # without strided true residuals a problem whose tiles' CTAs are all co-resident (n = 32: 128
+    # tiles, one per SM; n = 48: 432 tiles, three per SM) runs the whole loop in one persistent
+    # cooperative kernel (k_solve_small)
     for _ in range(3):
         rep = pcg_solve(A, cs.b, mp, SolveConfig(res_tol=1e-9))
         assert rep.iterations == orc["iterations"]
