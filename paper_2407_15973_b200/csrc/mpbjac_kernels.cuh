@@ -1884,7 +1884,7 @@ __global__ void __launch_bounds__(kTileThreads / 2 + 32)
     if (threadIdx.x == 0) tl_mark(a.st, 2, 1, true);
   }
   pdl_trigger();
-  finish_grid<8, kFinRpt>(a.st, 2, kStepRrZ, ChunkCtx{a.csum, a.part, a.g.ntiles, TWO ? a.g.poll : 0}, ws);
+  finish_grid<16, kFinRpt>(a.st, 2, kStepRrZ, ChunkCtx{a.csum, a.part, a.g.ntiles, TWO ? a.g.poll : 0}, ws);
 }
 
 // ---------------------------------------------------------------------------
