@@ -502,3 +502,46 @@ def test_offset_slot_layout_bitwise(cuda, oracle, n, pol):
     assert rep.iterations == orc["iterations"]
     np.testing.assert_array_equal(rep.x, orc["x"])
     assert rep.final_true_relres == orc["final_true_relres"]
+
+
+def test_offset_slot_error_paths_both_solve_paths(cuda):
+    """The reference's exceptions through the offset-slot kernels, on both
+    solve paths of a small stencil problem (record_true_residual_every=0: the
+    one persistent kernel; 3: the three-kernel graph iteration): narrowing
+    overflow of the right-hand side (first index and count), a negative
+    definite operator (indefinite preconditioner at iteration 1), the
+    iteration cap, and a zero right-hand side."""
+    from paper_2407_15973_b200 import NarrowingOverflowError, SparseMatrix, problems
+    from paper_2407_15973_b200.bjac import BlockPartition
+    from paper_2407_15973_b200.policies import PrecisionPolicy, build_mixed
+    from paper_2407_15973_b200.solver import IndefiniteOperatorError, SolveConfig, pcg_solve
+    cs = problems.make_config("c2", 20)
+    A = cs.A
+    part = BlockPartition.fixed_size(A.n, 64)
+    low = build_mixed(A, PrecisionPolicy.parse("fixed-low"), k=2, t=2, partition=part)
+    assert low.any.plan.layout_info()["offset_slots"] == 7
+    b = cs.b.copy()
+    b[[777, 4242]] = 1e39
+    seen = []
+    for stride in (0, 3):
+        with pytest.raises(NarrowingOverflowError, match="first at index 777") as ei:
+            pcg_solve(A, b, low, SolveConfig(record_true_residual_every=stride))
+        seen.append(str(ei.value))
+    assert seen[0] == seen[1]
+    Aneg = SparseMatrix(A.n, A.m, A.row_ptr, A.col_idx, -A.values)
+    for pol in ("uniform", "fixed-low"):
+        mp = build_mixed(Aneg, PrecisionPolicy.parse(pol), k=2, t=2, partition=part)
+        seen = []
+        for stride in (0, 3):
+            with pytest.raises(IndefiniteOperatorError, match="iteration 1: r'z") as ei:
+                pcg_solve(Aneg, cs.b, mp, SolveConfig(record_true_residual_every=stride))
+            seen.append(str(ei.value))
+        assert seen[0] == seen[1]
+    reps = [pcg_solve(A, cs.b, low, SolveConfig(max_iter=7, record_true_residual_every=s)) for s in (0, 3)]
+    for rep in reps:
+        assert not rep.converged and rep.iterations == 7
+    np.testing.assert_array_equal(reps[0].x, reps[1].x)
+    assert reps[0].final_true_relres == reps[1].final_true_relres
+    assert reps[0].stats["kernel_launches"] < reps[1].stats["kernel_launches"]
+    rep = pcg_solve(A, np.zeros(A.n), low)
+    assert rep.converged and rep.iterations == 0
