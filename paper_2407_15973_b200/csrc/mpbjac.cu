@@ -2450,7 +2450,7 @@ static int launch_small(mpb_handle *h, cudaStream_t s, const mpb_plan *p, const 
   const size_t dyn = sizeof(double) * kTileRows * kDiaSlots * (two64 ? 2 : 1) + sizeof(float) * kTileRows * kDiaSlots;
   int per_sm = 0;
   MPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_solve_small, kCtaThreads, dyn));
-  if (per_sm < 1 || p->ntiles > int64_t(per_sm) * num_sms()) return MPB_ERR_WORKSPACE;
+  if (per_sm < 1 || p->ntiles > int64_t(per_sm) * num_sms()) return static_cast<int>(cudaErrorCooperativeLaunchTooLarge);
   void *args[] = {&a};
   MPB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void *>(k_solve_small), dim3(static_cast<unsigned>(p->ntiles)),
                                        dim3(kCtaThreads), args, dyn, s));
@@ -2548,11 +2548,17 @@ static int solve_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, con
     k_scalar_start<<<1, 32, 0, s>>>(w.st);
     MPB_LAUNCHED(h);
     MPB_CUDA(cudaEventRecord(h->ev_t0, s));
-    if ((rc = launch_small(h, s, plan, A, opt, w, x))) return rc;
-    MPB_CUDA(cudaEventRecord(h->ev_t1, s));
-    MPB_CUDA(cudaMemcpyAsync(h->h_state, w.st, sizeof(SolverState), cudaMemcpyDeviceToHost, s));
-    MPB_CUDA(cudaStreamSynchronize(s));
-    return finish_solve(h, plan, A, b, x, w, res, dc, s, launches0);
+    rc = launch_small(h, s, plan, A, opt, w, x);
+    if (rc == MPB_OK) {
+      MPB_CUDA(cudaEventRecord(h->ev_t1, s));
+      MPB_CUDA(cudaMemcpyAsync(h->h_state, w.st, sizeof(SolverState), cudaMemcpyDeviceToHost, s));
+      MPB_CUDA(cudaStreamSynchronize(s));
+      return finish_solve(h, plan, A, b, x, w, res, dc, s, launches0);
+    }
+    // the device cannot hold the whole grid right now (e.g. SMs taken by another client):
+    // nothing ran, the graph iteration below takes over; any other error is the caller's
+    if (rc != static_cast<int>(cudaErrorCooperativeLaunchTooLarge)) return rc;
+    cudaGetLastError();
   }
   // the symmetric offset-slot SpMV layout of the operator (one GPU; built once per value array)
   if (dc == nullptr) ensure_sym(h, const_cast<mpb_plan *>(plan), A, s);
