@@ -241,6 +241,9 @@ constexpr int kStageCap = 4096;  // staged SELL entries per tile (2 stages per C
 // the two-level sum order applies (and chunk owners poll) above
 // MPB_ONE_LEVEL_TILES tiles
 bool owners_poll(int64_t ntiles) { return two_level(ntiles); }
+// streamed one-level sums of the offset-slot kernels (defined with the workspace layout)
+bool red_mode(const mpb_plan *p);
+double *red_part(const mpb_plan *p, int64_t n, double *part);
 
 template <typename T>
 TileGeom geom_for(const mpb_plan *p) {
@@ -254,6 +257,7 @@ TileGeom geom_for(const mpb_plan *p) {
   g.poll = owners_poll(p->ntiles) ? 1 : 0;
   g.kib = p->max_ib_row;
   g.ub = p->ub;
+  g.red = 0;
   return g;
 }
 
@@ -460,6 +464,10 @@ int launch_tile_kernel(mpb_handle *h, cudaStream_t s, const mpb_plan *p, PassArg
       constexpr uint32_t sb = dia_stage_bytes<T>();
       constexpr int kNear = (1 << (kDiaDiag - 1)) | (1 << kDiaDiag) | (1 << (kDiaDiag + 1));
       const bool near = (a.ibany & ~kNear) == 0;  // in-block entries only at the diagonal and its two neighbours
+      if (L && a.part != nullptr && a.st != nullptr && red_mode(p)) {  // streamed one-level sum
+        a.part = red_part(p, p->n, a.part);
+        a.g.red = 1;
+      }
       auto kern = near ? ((L && a.g.poll) ? k_bjac_dia<T, L, L, kNear> : k_bjac_dia<T, L, false, kNear>)
                        : ((L && a.g.poll) ? k_bjac_dia<T, L, L, 0x7f> : k_bjac_dia<T, L, false, 0x7f>);
       a.g.ns = pick_stages(kern, sb, threads);
@@ -794,6 +802,10 @@ int launch_update_first(mpb_handle *h, cudaStream_t s, const mpb_plan *p, const 
   if (a.dnear != nullptr && a.part != nullptr && st != nullptr) {  // offset-slot layout, warp per block
     constexpr int threads = kTileThreads / 2 + 32;
     constexpr uint32_t sb = dia_uf_stage_bytes<T>();
+    if (red_mode(p)) {  // streamed one-level sum
+      a.part = red_part(p, p->n, a.part);
+      a.g.red = 1;
+    }
     auto kern = two_level(p->ntiles) ? k_update_first_dia<T, true> : k_update_first_dia<T, false>;
     a.g.ns = pick_stages(kern, sb, threads);
     const uint32_t dyn = a.g.ns * sb;
@@ -939,6 +951,7 @@ struct SolveWs {
   double *part;
   double *part2;       // wave kernel: the r.z tile partials of its last-pass items (part: r.r)
   double *part3;       // k_solve_small: one array per dot product (part r.z, part2 p.q, part3 r.r)
+  double *ppart;       // streamed one-level sums of the offset-slot kernels (red_mode)
   unsigned int *gcnt;  // wave kernel: per tile group, update items published this solve
   double *csum;        // chunk sums of the two-level dot sums (part: all slots kPartEmpty between kernels)
   SolverState *st;
@@ -982,9 +995,27 @@ SolveWs carve(const mpb_plan *p, int64_t n, char *base, int64_t ng = 0) {
   w.part3 = (double *)take(sizeof(double) * (p->ntiles + 1));
   w.gcnt = (unsigned int *)take(sizeof(unsigned int) * (p->ntiles / 32 + 8));
   w.csum = (double *)take(sizeof(double) * ((p->ntiles + kChunkTiles - 1) / kChunkTiles + 1));
+  // streamed one-level sums (reduce_stream): their own tile partials, all slots kPartEmpty between kernels
+  w.ppart = (double *)take(sizeof(double) * (p->ntiles + 1));
   w.st = (SolverState *)take(sizeof(SolverState));
   w.bytes = off;
   return w;
+}
+
+// Streamed one-level sums (reduce_stream) for the offset-slot kernels: plans
+// of 4 .. 32 rows of 256 tiles (above, the two-level order has its chunk
+// owners; below, the final CTA's sum is short).  MPB_RED=0 turns it off.
+// The kernels get their own partials array (every slot kPartEmpty between
+// kernels), found from the solve's partials pointer (carve's layout).
+bool red_mode(const mpb_plan *p) {
+  static const bool off = std::getenv("MPB_RED") && std::atoi(std::getenv("MPB_RED")) == 0;
+  return !off && p->dia_ok && !two_level(p->ntiles) && p->ntiles >= 4 * kChunkTiles;
+}
+double *red_part(const mpb_plan *p, int64_t n, double *part) {
+  char *const fake = reinterpret_cast<char *>(uintptr_t(1) << 20);
+  const SolveWs f = carve(p, n, fake);
+  return reinterpret_cast<double *>(reinterpret_cast<char *>(part) +
+                                    (reinterpret_cast<char *>(f.ppart) - reinterpret_cast<char *>(f.part)));
 }
 
 
@@ -2068,6 +2099,10 @@ static SpmvArgs spmv_args(const mpb_handle *h, const mpb_plan *p, const mpb_csr 
     sa.dval = op_packed + p->dia_at;
     sa.dmeta = p->d_dmeta;
     for (int u = 0; u < kDiaSlots; u++) sa.doff[u] = p->dia_off[u];
+    if (red_mode(p)) {  // streamed one-level sum
+      sa.part = red_part(p, p->n, sa.part);
+      sa.g.red = 1;
+    }
     auto kern = two_level(p->ntiles) ? k_spmv_dia<true> : k_spmv_dia<false>;
     sa.g.ns = pick_stages(kern, kDiaSpmvStage);
   }
@@ -2515,6 +2550,7 @@ static int solve_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, con
   // claims leaves its counter dirty; only the end of a solve gates so)
   MPB_CUDA(cudaMemsetAsync(h->d_ctr, 0, 16 * sizeof(unsigned int), s));
   MPB_CUDA(cudaMemsetAsync(w.part, 0xFF, sizeof(double) * plan->ntiles, s));  // every slot kPartEmpty
+  MPB_CUDA(cudaMemsetAsync(w.ppart, 0xFF, sizeof(double) * (plan->ntiles + 1), s));
   k_fill<<<elt_blocks(opt->max_iter), kEltThreads, 0, s>>>(tr_true, opt->max_iter, NAN);
   MPB_LAUNCHED(h);
   if (!opt->has_x0) MPB_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * A->n, s));
@@ -2791,6 +2827,7 @@ static int profile_impl(mpb_handle *h, const mpb_plan *plan, const mpb_csr *A, c
   mid.tr_time = reinterpret_cast<double *>(w.zB64) + 8;
   *h->h_state = mid;
   MPB_CUDA(cudaMemsetAsync(w.part, 0xFF, sizeof(double) * plan->ntiles, s));  // every slot kPartEmpty
+  MPB_CUDA(cudaMemsetAsync(w.ppart, 0xFF, sizeof(double) * (plan->ntiles + 1), s));
   auto reset = [&]() -> cudaError_t {
     cudaError_t e = cudaMemcpyAsync(w.st, h->h_state, sizeof(SolverState), cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess && plan->wave_ok)  // wave kernels: group counters match the state's epoch

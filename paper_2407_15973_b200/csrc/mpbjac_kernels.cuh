@@ -315,6 +315,96 @@ __device__ __forceinline__ void finish_grid(SolverState *st, int ticket, int ste
   }
 }
 
+// One-level sums, streamed: instead of the kernel's last CTA summing every
+// tile partial after the last tile (C2: 8,192 partials, 2-4 us on the
+// critical path between two kernels, after a grid ticket), ONE warp of the
+// grid (CTA 0, which takes no tiles) carries the 256 lane sums of the
+// one-level order while the kernel runs: row c of the partials (tiles
+// 256 c .. 256 c + 255) completes roughly in order of c; the warp polls the
+// rows in order (each slot its own completion flag, kPartEmpty), lane l adding
+// slots l, l + 32, .. of each row to its 8 lane sums -- lane j of 256 still
+// adds partials j, j + 256, .. in ascending order from +0 -- and empties
+// them.  After the last row: the 256-lane tree (8 virtual warps' butterflies,
+// then the butterfly of their sums) and the scalar step, one L2 round trip
+// after the last tile's partial lands.  Same additions in the same order as
+// fin_sum: bit-identical.  The state snapshot is taken once at the start
+// (only this step changes it during the kernel).  Called by one warp.
+__device__ __forceinline__ void reduce_stream(SolverState *st, int step, double *part, int ntiles) {
+  __shared__ __align__(16) unsigned long long s_rstate[kStWords];
+  const int lane = threadIdx.x & 31;
+  for (int i = lane; i < kStWords; i += 32) s_rstate[i] = __ldcg(reinterpret_cast<const unsigned long long *>(st) + i);
+  constexpr int W = kChunkTiles / 32;
+  double acc[W];
+#pragma unroll
+  for (int w = 0; w < W; w++) acc[w] = 0.0;
+  const int nrows = (ntiles + kChunkTiles - 1) / kChunkTiles;
+  for (int c = 0; c < nrows;) {
+    unsigned long long b0[W], b1[W];
+    const bool two = c + 1 < nrows;
+    bool f0 = true, f1 = true;
+#pragma unroll
+    for (int w = 0; w < W; w++) {
+      const int i0 = c * kChunkTiles + 32 * w + lane, i1 = i0 + kChunkTiles;
+      b0[w] = i0 < ntiles ? get_part_bits(part + i0) : 0ull;
+      b1[w] = (two && i1 < ntiles) ? get_part_bits(part + i1) : 0ull;
+      f0 = f0 && b0[w] != kPartEmpty;
+      f1 = f1 && b1[w] != kPartEmpty;
+    }
+    f0 = __all_sync(0xffffffffu, f0);
+    f1 = __all_sync(0xffffffffu, f1) && f0 && two;
+    if (!f0) continue;
+#pragma unroll
+    for (int w = 0; w < W; w++) {
+      const int i0 = c * kChunkTiles + 32 * w + lane;
+      if (i0 < ntiles) {
+        acc[w] = __dadd_rn(acc[w], __longlong_as_double(static_cast<long long>(b0[w])));
+        reinterpret_cast<unsigned long long *>(part)[i0] = kPartEmpty;
+      }
+    }
+    c++;
+    if (f1) {
+#pragma unroll
+      for (int w = 0; w < W; w++) {
+        const int i1 = c * kChunkTiles + 32 * w + lane;
+        if (i1 < ntiles) {
+          acc[w] = __dadd_rn(acc[w], __longlong_as_double(static_cast<long long>(b1[w])));
+          reinterpret_cast<unsigned long long *>(part)[i1] = kPartEmpty;
+        }
+      }
+      c++;
+    }
+  }
+  // block_tree<256>: virtual warp w = slots 32 w + lane
+  double r = 0.0;
+#pragma unroll
+  for (int w = 0; w < W; w++) {
+    const double v = warp_bfly(acc[w]);
+    if (lane == w) r = v;
+  }
+  const double tot = warp_bfly(r);
+  SolverState *L = reinterpret_cast<SolverState *>(s_rstate);
+  __syncwarp();
+  const bool dist = L->dist != 0;
+  if (lane == 0) {
+    if (dist) {  // multi-GPU: all-reduce first, k_apply_step runs the step
+      st->red_local[0] = tot;
+      st->red_local[1] = static_cast<double>(L->ovf_count);
+    } else {
+      scalar_step_body(step, tot, L);
+    }
+  }
+  __syncwarp();
+  if (!dist) {  // the changed state words (state_store's ranges)
+    unsigned long long *d = reinterpret_cast<unsigned long long *>(st);
+    constexpr int a1 = static_cast<int>(offsetof(SolverState, tr_relres) / 8);
+    constexpr int b0 = static_cast<int>(offsetof(SolverState, dist) / 8), b1 = static_cast<int>(offsetof(SolverState, cond) / 8);
+    for (int i = lane; i < a1 + (b1 - b0); i += 32) {
+      const int wd = i < a1 ? i : b0 + (i - a1);
+      d[wd] = s_rstate[wd];
+    }
+  }
+}
+
 // in-process slab group: red_global of every rank = the ranks' red_local
 // summed in rank order (for two ranks the same value as NCCL's sum)
 constexpr int kMaxLocalRanks = 16;
@@ -387,6 +477,7 @@ struct TileGeom {
   int npat;    // row patterns in the table
   int kib;     // most in-block entries of a row
   int ub;      // every block has this many rows (0: blocks differ)
+  int red;     // one-level sums streamed by CTA 0's first warp (reduce_stream); CTA 0 takes no tiles
 };
 
 // Byte offsets of one shared-memory stage.
@@ -690,14 +781,17 @@ __device__ __forceinline__ void producer_loop(RG &R, int ntiles, int ns, unsigne
 
 // Single-lane producer (lane 0 of the producer warp) for kernels without
 // chunk owners: the same walk as producer_loop.
+// nclaim: CTAs that claim tiles (each makes exactly one failing claim; 0: the whole grid)
 template <typename F, typename G, class RG>
 __device__ __forceinline__ void producer_loop_single(RG &R, int ntiles, int ns, unsigned int *ctr, bool prefetch,
-                                              G &&gated, F &&fill, int nterm = 1, const TileDesc *td = nullptr) {
+                                              G &&gated, F &&fill, int nterm = 1, const TileDesc *td = nullptr,
+                                              unsigned int nclaim = 0u) {
   int next = blockIdx.x;
+  if (nclaim == 0u) nclaim = gridDim.x;
   auto claim = [&]() -> int {
     if (ctr != nullptr) {
       const unsigned int v = atomicAdd(ctr, 1u);
-      if (v == static_cast<unsigned int>(ntiles) + gridDim.x - 1u) atomicExch(ctr, 0u);
+      if (v == static_cast<unsigned int>(ntiles) + nclaim - 1u) atomicExch(ctr, 0u);
       return v < static_cast<unsigned int>(ntiles) ? static_cast<int>(v) : -1;
     }
     const int t = next < ntiles ? next : -1;
@@ -1657,6 +1751,13 @@ __global__ void __launch_bounds__(kTileThreads / 2 + 32) k_bjac_dia(const PassAr
   if (threadIdx.x < kMaxStages) s_wcnt[threadIdx.x] = 0u;  // (published by ring_init's barrier)
   const int ns = a.g.ns;
   ring_init(R, ns, NC);
+  const bool red = LAST && a.g.red != 0 && a.part != nullptr && a.st != nullptr;
+  if (red && blockIdx.x == 0) {  // this CTA takes no tiles: its first warp streams the r.z sum
+    pdl_wait();
+    if (!gated_off(a) && threadIdx.x < 32) reduce_stream(a.st, kStepRho, a.part, a.g.ntiles);
+    pdl_trigger();
+    return;
+  }
   if (threadIdx.x >= NC) {  // producer warp
     const ChunkCtx ck{(TWO && LAST && a.part != nullptr && a.st != nullptr) ? a.csum : nullptr, a.part, a.g.ntiles,
                       TWO ? a.g.poll : 0};
@@ -1688,7 +1789,7 @@ __global__ void __launch_bounds__(kTileThreads / 2 + 32) k_bjac_dia(const PassAr
     if (TWO && ck.csum != nullptr && ck.poll)
       producer_loop(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, gated, fill, ck, 1, a.td);
     else if (threadIdx.x == NC)
-      producer_loop_single(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, gated, fill, 1, a.td);
+      producer_loop_single(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, gated, fill, 1, a.td, gridDim.x - (red ? 1u : 0u));
     else
       pdl_wait();
     if (gated_off(a)) return;
@@ -1718,7 +1819,7 @@ __global__ void __launch_bounds__(kTileThreads / 2 + 32) k_bjac_dia(const PassAr
     if (LAST && threadIdx.x == 0) tl_mark(a.st, 0, 1, true);
   }
   pdl_trigger();  // dependents may launch into the SMs this grid drains
-  if (LAST && a.part != nullptr)
+  if (LAST && a.part != nullptr && !red)
     finish_grid<16, kFinRpt>(a.st, 0, kStepRho, ChunkCtx{a.csum, a.part, a.g.ntiles, TWO ? a.g.poll : 0}, ws);
 }
 
@@ -1828,6 +1929,13 @@ __global__ void __launch_bounds__(kTileThreads / 2 + 32)
   if (threadIdx.x < kMaxStages) s_wcnt[threadIdx.x] = 0u;  // (published by ring_init's barrier)
   const int ns = a.g.ns;
   ring_init(R, ns, NC);
+  const bool red = a.g.red != 0;
+  if (red && blockIdx.x == 0) {  // this CTA takes no tiles: its first warp streams the r.r sum
+    pdl_wait();
+    if (!gated_off(a) && threadIdx.x < 32) reduce_stream(a.st, kStepRrZ, a.part, a.g.ntiles);
+    pdl_trigger();
+    return;
+  }
   if (threadIdx.x >= NC) {  // producer warp
     const ChunkCtx ck{a.csum, a.part, a.g.ntiles, TWO ? a.g.poll : 0};
     auto fill = [&](int st, int tile, int part) {
@@ -1862,7 +1970,7 @@ __global__ void __launch_bounds__(kTileThreads / 2 + 32)
     if (TWO && ck.poll)
       producer_loop(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, gated, fill, ck, 1, a.td);
     else if (threadIdx.x == NC)
-      producer_loop_single(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, gated, fill, 1, a.td);
+      producer_loop_single(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, gated, fill, 1, a.td, gridDim.x - (red ? 1u : 0u));
     else
       pdl_wait();
     if (gated_off(a)) return;
@@ -1889,7 +1997,7 @@ __global__ void __launch_bounds__(kTileThreads / 2 + 32)
     if (threadIdx.x == 0) tl_mark(a.st, 2, 1, true);
   }
   pdl_trigger();
-  finish_grid<16, kFinRpt>(a.st, 2, kStepRrZ, ChunkCtx{a.csum, a.part, a.g.ntiles, TWO ? a.g.poll : 0}, ws);
+  if (!red) finish_grid<16, kFinRpt>(a.st, 2, kStepRrZ, ChunkCtx{a.csum, a.part, a.g.ntiles, TWO ? a.g.poll : 0}, ws);
 }
 
 // ---------------------------------------------------------------------------
@@ -3033,6 +3141,13 @@ __global__ void __launch_bounds__(kWsThreads, 4) k_spmv_dia(const SpmvArgs a) {
   if (threadIdx.x < kMaxStages) s_wcnt[threadIdx.x] = 0u;  // (published by ring_init's barrier)
   const int ns = a.g.ns;
   ring_init(R, ns);
+  const bool red = a.g.red != 0;
+  if (red && blockIdx.x == 0) {  // this CTA takes no tiles: its first warp streams the p.q sum
+    pdl_wait();
+    if (!a.st->done && threadIdx.x < 32) reduce_stream(a.st, kStepPq, a.part, a.g.ntiles);
+    pdl_trigger();
+    return;
+  }
   if (threadIdx.x >= kConsumers) {
     const ChunkCtx ck{a.csum, a.part, a.g.ntiles, TWO ? a.g.poll : 0};
     // every staged byte is static (values, masks): all of it may stream
@@ -3057,7 +3172,7 @@ __global__ void __launch_bounds__(kWsThreads, 4) k_spmv_dia(const SpmvArgs a) {
     if (TWO && ck.poll)
       producer_loop(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, gated, fill, ck, 1, a.td);
     else if (threadIdx.x == kConsumers)
-      producer_loop_single(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, gated, fill, 1, a.td);
+      producer_loop_single(R, a.g.ntiles, ns, a.ctr, a.prefetch != 0, gated, fill, 1, a.td, gridDim.x - (red ? 1u : 0u));
     else
       pdl_wait();
     if (a.st->done) return;
@@ -3086,7 +3201,7 @@ __global__ void __launch_bounds__(kWsThreads, 4) k_spmv_dia(const SpmvArgs a) {
     if (threadIdx.x == 0) tl_mark(a.st, 1, 1, true);
   }
   pdl_trigger();
-  finish_grid<16, kFinRptWs>(a.st, 1, kStepPq, ChunkCtx{a.csum, a.part, a.g.ntiles, TWO ? a.g.poll : 0}, ws);
+  if (!red) finish_grid<16, kFinRptWs>(a.st, 1, kStepPq, ChunkCtx{a.csum, a.part, a.g.ntiles, TWO ? a.g.poll : 0}, ws);
 }
 
 // ---- SpMV on the symmetric offset-slot layout --------------------------------
