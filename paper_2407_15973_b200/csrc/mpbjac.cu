@@ -1003,13 +1003,13 @@ SolveWs carve(const mpb_plan *p, int64_t n, char *base, int64_t ng = 0) {
 }
 
 // Streamed one-level sums (reduce_stream) for the offset-slot kernels: plans
-// of 4 .. 32 rows of 256 tiles (above, the two-level order has its chunk
-// owners; below, the final CTA's sum is short).  MPB_RED=0 turns it off.
+// of 64 to 8,192 tiles (above, the two-level order has its chunk owners).
+// MPB_RED=0 turns it off.
 // The kernels get their own partials array (every slot kPartEmpty between
 // kernels), found from the solve's partials pointer (carve's layout).
 bool red_mode(const mpb_plan *p) {
   static const bool off = std::getenv("MPB_RED") && std::atoi(std::getenv("MPB_RED")) == 0;
-  return !off && p->dia_ok && !two_level(p->ntiles) && p->ntiles >= 4 * kChunkTiles;
+  return !off && p->dia_ok && !two_level(p->ntiles) && p->ntiles >= 64;  // (CTA 0 takes no tiles: the grid needs more)
 }
 double *red_part(const mpb_plan *p, int64_t n, double *part) {
   char *const fake = reinterpret_cast<char *>(uintptr_t(1) << 20);
