@@ -1008,7 +1008,9 @@ SolveWs carve(const mpb_plan *p, int64_t n, char *base, int64_t ng = 0) {
 // The kernels get their own partials array (every slot kPartEmpty between
 // kernels), found from the solve's partials pointer (carve's layout).
 bool red_mode(const mpb_plan *p) {
-  static const bool off = std::getenv("MPB_RED") && std::atoi(std::getenv("MPB_RED")) == 0;
+  // (the static tile walk of MPB_STATIC=1 assumes every CTA takes tiles)
+  static const bool off = (std::getenv("MPB_RED") && std::atoi(std::getenv("MPB_RED")) == 0) ||
+                          (std::getenv("MPB_STATIC") && std::atoi(std::getenv("MPB_STATIC")) != 0);
   return !off && p->dia_ok && !two_level(p->ntiles) && p->ntiles >= 64;  // (CTA 0 takes no tiles: the grid needs more)
 }
 double *red_part(const mpb_plan *p, int64_t n, double *part) {
