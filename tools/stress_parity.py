@@ -56,6 +56,32 @@ def main():
                     print(f"MISMATCH n={n} {pol} k={k} t={t} stride={stride}: it {rep.iterations} vs "
                           f"{orc['iterations']}, launches {rep.stats['kernel_launches']}, layout {info}", flush=True)
         print(f"n={n}: N={A.n} tiles={mp.any.plan.ntiles} layout={info} ({time.time() - t0:.0f}s)", flush=True)
+    # 3-T systems (96-row blocks, 81 patterns: the SELL + row-pattern kernels) and a 7-point grid
+    # whose row count is not a multiple of 64 (no offset-slot layout): the same checks
+    for name, n, rows in (("c4", 20, 96), ("c4", 28, 96), ("c2", 50, 64), ("c2", 30, 64)):
+        cs = problems.make_config(name, n)
+        A = cs.A
+        part = BlockPartition.fixed_size(A.n, rows)
+        for pol, (k, t) in itertools.product(pols, ((1, 2), (2, 2), (3, 1))):
+            pp = PrecisionPolicy.parse(pol)
+            mp = build_mixed(A, pp, k=k, t=t, partition=part)
+            info = mp.any.plan.layout_info()
+            for stride in (0, 4):
+                kw = dict(kind=pp.kind.value, adp_tol=pp.adp_tol, k=k, t=t, res_tol=1e-9, stride=stride,
+                          order="device", max_iter=300)
+                orc = O.pcg_solve(A.row_ptr, A.col_idx, A.values, cs.b, part.offsets, **kw)
+                rep = pcg_solve(A, cs.b, mp, SolveConfig(res_tol=1e-9, max_iter=300,
+                                                         record_true_residual_every=stride))
+                ok = (rep.iterations == orc["iterations"] and np.array_equal(rep.x, orc["x"])
+                      and np.array_equal([r.implicit_relres for r in rep.trace], orc["relres"])
+                      and [r.branch for r in rep.trace] == list(orc["branch"])
+                      and rep.final_true_relres == orc["final_true_relres"])
+                cases += 1
+                if not ok:
+                    bad += 1
+                    print(f"MISMATCH {name} n={n} {pol} k={k} t={t} stride={stride}: it {rep.iterations} vs "
+                          f"{orc['iterations']}, layout {info}", flush=True)
+        print(f"{name} n={n}: N={A.n} tiles={mp.any.plan.ntiles} layout={info} ({time.time() - t0:.0f}s)", flush=True)
     print(f"{cases} cases, {bad} mismatches")
     return 1 if bad else 0
 
