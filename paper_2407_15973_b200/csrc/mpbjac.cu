@@ -533,14 +533,17 @@ int launch_pass(mpb_handle *h, cudaStream_t s, const mpb_plan *p, PassArgs<T> a,
   static const bool old_big = std::getenv("MPB_OLD_BIG") != nullptr;
   if (!old_big && p->dia_big && a.dval != nullptr) {
     // offset-slot layout: coalesced slot loads, no pattern-table reads
-    k_big_dia_resid<T, F><<<nt, kCtaThreads, 0, s>>>(a, bufs.wA);
+    const bool pdl = a.pdl != 0;  // chained inside a solve: the next grid is scheduled while this one drains
+    MPB_CUDA(launch_k(pdl, k_big_dia_resid<T, F>, static_cast<unsigned>(nt), kCtaThreads, 0, s, a, bufs.wA));
     MPB_LAUNCHED(h);
     T *cur = bufs.wA, *nxt = bufs.wB;
     for (int sweep = 1; sweep < a.t; sweep++) {
       if (sweep + 1 < a.t) {
-        k_big_dia_sweep<T, F, L, false><<<nt, kCtaThreads, 0, s>>>(a, cur, nxt);
+        MPB_CUDA(launch_k(pdl, k_big_dia_sweep<T, F, L, false>, static_cast<unsigned>(nt), kCtaThreads, 0, s, a,
+                          static_cast<const T *>(cur), nxt));
       } else {
-        k_big_dia_sweep<T, F, L, true><<<nt, kCtaThreads, 0, s>>>(a, cur, nxt);
+        MPB_CUDA(launch_k(pdl, k_big_dia_sweep<T, F, L, true>, static_cast<unsigned>(nt), kCtaThreads, 0, s, a,
+                          static_cast<const T *>(cur), nxt));
         MPB_LAUNCHED(h);
         return MPB_OK;
       }

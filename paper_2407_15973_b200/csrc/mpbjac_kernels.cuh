@@ -2009,6 +2009,7 @@ __global__ void __launch_bounds__(kTileThreads / 2 + 32)
 // ---------------------------------------------------------------------------
 template <typename T, bool FIRST>
 __global__ void __launch_bounds__(kCtaThreads) k_big_dia_resid(const PassArgs<T> a, T *w0) {
+  pdl_wait();  // (launched with programmatic dependent launch inside a solve: everything read below is the predecessor's)
   if (gated_off(a)) return;
   const TileDesc d = a.td[blockIdx.x];
   const int row = d.lo + threadIdx.x;
@@ -2036,6 +2037,7 @@ __global__ void __launch_bounds__(kCtaThreads) k_big_dia_resid(const PassArgs<T>
 
 template <typename T, bool FIRST, bool LAST, bool FINISH>
 __global__ void __launch_bounds__(kCtaThreads) k_big_dia_sweep(const PassArgs<T> a, const T *wsrc, T *wdst) {
+  pdl_wait();
   if (gated_off(a)) return;
   __shared__ double ws[32];
   const int tile = blockIdx.x;
